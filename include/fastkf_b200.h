@@ -1,0 +1,130 @@
+/* fastkf_b200.h — C ABI of the B200-native fast Kalman filter hot path (sm_100a).
+ *
+ * Drop-in boundary for the reference's header-only C++ API in
+ * /root/reference/proj/include/fastkf (namespace fastkf).  The reference has no FFI;
+ * each entry point below names the reference function it replaces (file:line).
+ * The C++ shim include/fastkf_b200.hpp restores the reference's class/function
+ * names and exception types on top of this ABI.
+ *
+ * Conventions:
+ *  - status codes: 0 ok, 1 invalid argument (std::invalid_argument),
+ *    2 runtime error (std::runtime_error), 3 CUDA error; fkb_last_error() has the text.
+ *  - dense blocks are column-major FP64 with explicit leading dimensions (Eigen MatrixXd);
+ *    fields are flat x-major vectors, index ix*ny + iy (grid.hpp:48).
+ *  - CSR: int32 rowptr/col, FP64 values (SparseRowMatrix, grid.hpp:15).
+ *  - one CUDA stream per covariance operator; calls on one operator/filter are
+ *    serialized; host-buffer calls are synchronous; *_device calls take device pointers
+ *    and are stream-ordered.
+ */
+#ifndef FASTKF_B200_H
+#define FASTKF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FKB_OK 0
+#define FKB_INVALID_ARGUMENT 1
+#define FKB_RUNTIME_ERROR 2
+#define FKB_CUDA_ERROR 3
+
+typedef struct fkb_cov fkb_cov;
+typedef struct fkb_filter fkb_filter;
+
+const char* fkb_last_error(void);
+unsigned long long fkb_launch_count(void); /* kernels launched by this library so far */
+int fkb_version(void);
+int fkb_device_count(void); /* CUDA devices visible (0 on a CPU-only host) */
+
+/* ---- host-side setup (no GPU needed) ------------------------------------------ */
+/* kernel_eval, kernel.hpp:51-63 (family 0 powered-exponential, 1 Matérn) */
+int fkb_kernel_eval(int family, double theta, double length, double power, double nu, double alpha_scale, double r,
+                    double* out);
+/* detail::next_smooth, covariance.hpp:35-43 */
+int fkb_next_smooth(int n);
+/* trace_ray, tomography.hpp:29-86: segments in traversal order; *count = total segments */
+int fkb_trace_ray(int nx, int ny, double lx, double ly, double sx, double sy, double rx, double ry, int cap,
+                  long long* cells, double* lengths, int* count);
+/* build_H, tomography.hpp:130-146 (rows source-major, columns ascending).  Call with
+ * cap = 0 to query *nnz; rowptr needs n_src*n_rec+1 entries. */
+int fkb_build_H(int nx, int ny, double lx, double ly, int n_src, const double* src_xy, int n_rec,
+                const double* rec_xy, int* rows, long long* nnz, int* rowptr, int* col, double* val, long long cap);
+/* small symmetric eigensolver used by the GHEP (stand-in for SelfAdjointEigenSolver,
+ * lowrank.hpp:193): ascending eigenvalues w, eigenvectors Z (n×n column-major) */
+int fkb_sym_eig(int n, const double* A, double* w, double* Z);
+
+/* ---- covariance operator Γ (CovarianceOperator FFT mode, covariance.hpp:69-353) ---- */
+/* constructor covariance.hpp:71-79 + build_fft :238-260 (padding loop, acceptance) */
+int fkb_cov_create(int nx, int ny, double lx, double ly, int family, double theta, double length, double power,
+                   double nu, double alpha_scale, fkb_cov** out);
+void fkb_cov_destroy(fkb_cov* c);
+int fkb_cov_dims(const fkb_cov* c, int* mx, int* my);
+/* spectrum(), covariance.hpp:207-211: mx*my row-major, clipped at 0 */
+int fkb_cov_spectrum(fkb_cov* c, double* out);
+/* apply_matrix, covariance.hpp:111-115 (host buffers; Y may equal X) */
+int fkb_cov_apply(fkb_cov* c, const double* X, long long ldx, int ncols, double* Y, long long ldy);
+int fkb_cov_apply_device(fkb_cov* c, const double* dX, long long ldx, int ncols, double* dY, long long ldy);
+/* sample_pair, covariance.hpp:190-197,332-353 (host outputs, length nx*ny each) */
+int fkb_cov_sample_pair(fkb_cov* c, uint64_t seed, uint64_t stream, double* a, double* b);
+long long fkb_cov_apply_count(const fkb_cov* c); /* apply_count(), covariance.hpp:213 */
+void* fkb_cov_stream(fkb_cov* c);                 /* the operator's cudaStream_t */
+
+/* gaussian_matrix, rng.hpp:79-86, generated on the device (host output, column-major) */
+int fkb_gaussian_matrix(long long rows, int cols, uint64_t seed, uint64_t base_stream, double* out);
+
+/* ---- constant-H fast filter (FkfContext + LowRankState, fast_filter.hpp:21-125) ---- */
+/* fkf_init, fast_filter.hpp:51-75: GHEP (lowrank.hpp:141-213, two-pass) with
+ * a_apply = HᵀH/σ², G = HΓHᵀ, B = HU; the state starts at zero_start (:30-36). */
+int fkb_fkf_init(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,
+                 long long k_rank, long long p_oversample, uint64_t seed, fkb_filter** out);
+void fkb_filter_destroy(fkb_filter* f);
+int fkb_filter_rank(const fkb_filter* f, int* rank, int* kept_cols);
+int fkb_filter_lambda(fkb_filter* f, double* out); /* GepResult::lambda, descending */
+/* which: 0 U (N×r), 1 Ū = Γ⁻¹U (N×r), 2 G = HΓHᵀ (m×m), 3 B = HU (m×r) — host copies */
+int fkb_filter_get(fkb_filter* f, int which, double* out);
+/* fkf_step, fast_filter.hpp:84-125, advancing the device-resident state */
+int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen);
+int fkb_fkf_step_device(fkb_filter* f, const double* d_y);
+/* nsteps device-resident observations (column k at d_ys + k*ldy) without host syncs;
+ * fkb_fkf_sync performs the deferred singularity check and commits the state. */
+int fkb_fkf_steps_async(fkb_filter* f, const double* d_ys, int nsteps, long long ldy);
+int fkb_fkf_sync(fkb_filter* f, int nsteps);
+/* LowRankState download / upload (d has `rank` entries, mean N) */
+int fkb_filter_state(fkb_filter* f, double* alpha, int* step, int* rank, double* d, double* mean);
+int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const double* d, const double* mean);
+int fkb_filter_reset(fkb_filter* f);
+int fkb_filter_mean_device(fkb_filter* f, const double** d_mean);
+
+/* ---- UQ (uq.hpp:16-112) ---------------------------------------------------------- */
+int fkb_variance(fkb_filter* f, double* out);              /* variance, uq.hpp:16-23 */
+int fkb_variance_device(fkb_filter* f, double* d_out);
+int fkb_trace_criterion(fkb_filter* f, double* out);       /* uq.hpp:27-34 */
+int fkb_relative_entropy(fkb_filter* f, double* out);      /* uq.hpp:39-53 */
+/* conditional realizations in FFT mode (uq.hpp:70-112 with the circulant root, SURVEY
+ * App. A.4): draw s uses sample_pair(seed, s/2), Re for even s, Im for odd; count ≤ 8.
+ * out: N×count column-major; var (optional) receives diag Σ from the same pass. */
+int fkb_realizations(fkb_filter* f, uint64_t seed, int count, double* out);
+int fkb_realizations_device(fkb_filter* f, uint64_t seed, int count, double* d_out, double* d_var);
+
+/* ---- kernels exposed for parity tests / benchmarks (device pointers) ------------- */
+/* Y = H X (trans = 0) or Hᵀ X (trans = 1) with the filter's uploaded operator */
+int fkb_filter_spmm(fkb_filter* f, int trans, const double* dX, long long ldx, int ncols, double* dY,
+                    long long ldy);
+void* fkb_filter_stream(fkb_filter* f);
+int fkb_filter_launches_per_step(fkb_filter* f);
+
+/* device memory helpers (so bindings need no CUDA runtime of their own) */
+int fkb_dmalloc(void** p, size_t bytes);
+int fkb_dfree(void* p);
+int fkb_h2d(void* dst, const void* src, size_t bytes);
+int fkb_d2h(void* dst, const void* src, size_t bytes);
+int fkb_dsync(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTKF_B200_H */

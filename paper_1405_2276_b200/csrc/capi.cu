@@ -1,0 +1,367 @@
+// capi.cu — extern "C" boundary (include/fastkf_b200.h) over the device runtime.
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+
+#include "../../include/fastkf_b200.h"
+#include "filter.cuh"
+#include "host_linalg.h"
+
+namespace fkb {
+unsigned long long g_launches = 0;
+}
+
+struct fkb_cov {
+    cudaStream_t stream = nullptr;
+    std::unique_ptr<fkb::Cov> cov;
+    ~fkb_cov() {
+        cov.reset();
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+struct fkb_filter {
+    fkb_cov* owner = nullptr;
+    std::unique_ptr<fkb::Filter> f;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return FKB_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return FKB_INVALID_ARGUMENT;
+    } catch (const fkb::CudaError& e) {
+        g_err = e.what();
+        return FKB_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FKB_RUNTIME_ERROR;
+    }
+}
+void need(const void* p, const char* what) {
+    if (!p) throw std::invalid_argument(std::string("null pointer: ") + what);
+}
+}  // namespace
+
+extern "C" {
+
+const char* fkb_last_error(void) { return g_err.c_str(); }
+unsigned long long fkb_launch_count(void) { return fkb::g_launches; }
+int fkb_version(void) { return 1; }
+int fkb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int fkb_kernel_eval(int family, double theta, double length, double power, double nu, double alpha_scale, double r,
+                    double* out) {
+    return guarded([&] {
+        fkb::KernelSpec s;
+        s.family = family; s.theta = theta; s.length = length; s.power = power; s.nu = nu; s.alpha_scale = alpha_scale;
+        *out = fkb::kernel_eval(s, r);
+    });
+}
+int fkb_next_smooth(int n) { return fkb::next_smooth(n); }
+
+int fkb_trace_ray(int nx, int ny, double lx, double ly, double sx, double sy, double rx, double ry, int cap,
+                  long long* cells, double* lengths, int* count) {
+    return guarded([&] {
+        if (nx < 1 || ny < 1) throw std::invalid_argument("grid: nx and ny must be positive");
+        *count = fkb::trace_ray_into(nx, ny, lx, ly, sx, sy, rx, ry, cap, cells, lengths);
+    });
+}
+
+int fkb_build_H(int nx, int ny, double lx, double ly, int n_src, const double* src_xy, int n_rec,
+                const double* rec_xy, int* rows, long long* nnz, int* rowptr, int* col, double* val, long long cap) {
+    return guarded([&] {
+        std::vector<int> rp, ci;
+        std::vector<double> v;
+        fkb::build_H(nx, ny, lx, ly, n_src, src_xy, n_rec, rec_xy, rp, ci, v);
+        *rows = n_src * n_rec;
+        *nnz = (long long)v.size();
+        if (cap >= (long long)v.size()) {
+            std::memcpy(rowptr, rp.data(), rp.size() * sizeof(int));
+            std::memcpy(col, ci.data(), ci.size() * sizeof(int));
+            std::memcpy(val, v.data(), v.size() * sizeof(double));
+        }
+    });
+}
+
+int fkb_sym_eig(int n, const double* A, double* w, double* Z) {
+    return guarded([&] { fkb::sym_eig_small(n, A, w, Z); });
+}
+
+int fkb_cov_create(int nx, int ny, double lx, double ly, int family, double theta, double length, double power,
+                   double nu, double alpha_scale, fkb_cov** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        auto h = std::make_unique<fkb_cov>();
+        FKB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        fkb::KernelSpec s;
+        s.family = family; s.theta = theta; s.length = length; s.power = power; s.nu = nu; s.alpha_scale = alpha_scale;
+        h->cov = std::make_unique<fkb::Cov>(nx, ny, lx, ly, s, h->stream);
+        *out = h.release();
+    });
+}
+void fkb_cov_destroy(fkb_cov* c) { delete c; }
+int fkb_cov_dims(const fkb_cov* c, int* mx, int* my) {
+    return guarded([&] {
+        need(c, "cov");
+        *mx = c->cov->mx;
+        *my = c->cov->my;
+    });
+}
+int fkb_cov_spectrum(fkb_cov* c, double* out) {
+    return guarded([&] {
+        need(c, "cov");
+        auto v = c->cov->spectrum_host();
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+int fkb_cov_apply_device(fkb_cov* c, const double* dX, long long ldx, int ncols, double* dY, long long ldy) {
+    return guarded([&] {
+        need(c, "cov");
+        if (ncols < 0 || ldx < c->cov->size() || ldy < c->cov->size())
+            throw std::invalid_argument("cov_apply: expected vector of length " + std::to_string(c->cov->size()));
+        c->cov->apply(dX, ldx, ncols, dY, ldy);
+    });
+}
+int fkb_cov_apply(fkb_cov* c, const double* X, long long ldx, int ncols, double* Y, long long ldy) {
+    return guarded([&] {
+        need(c, "cov");
+        const long long n = c->cov->size();
+        if (ncols < 0 || ldx < n || ldy < n)
+            throw std::invalid_argument("cov_apply: expected vector of length " + std::to_string(n));
+        if (ncols == 0) return;
+        fkb::DBuf<double> d(size_t(n) * ncols);
+        cudaStream_t s = c->stream;
+        for (int j = 0; j < ncols; ++j)
+            FKB_CUDA(cudaMemcpyAsync(d.p + (long long)j * n, X + (long long)j * ldx, n * sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+        c->cov->apply(d.p, n, ncols, d.p, n);
+        for (int j = 0; j < ncols; ++j)
+            FKB_CUDA(cudaMemcpyAsync(Y + (long long)j * ldy, d.p + (long long)j * n, n * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+int fkb_cov_sample_pair(fkb_cov* c, uint64_t seed, uint64_t stream, double* a, double* b) {
+    return guarded([&] {
+        need(c, "cov");
+        const long long n = c->cov->size();
+        fkb::DBuf<double> d(size_t(2 * n));
+        c->cov->sample_pair(seed, stream, d.p, d.p + n);
+        FKB_CUDA(cudaMemcpyAsync(a, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        FKB_CUDA(cudaMemcpyAsync(b, d.p + n, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        FKB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+long long fkb_cov_apply_count(const fkb_cov* c) { return c ? c->cov->applies : 0; }
+void* fkb_cov_stream(fkb_cov* c) { return c ? (void*)c->stream : nullptr; }
+
+int fkb_gaussian_matrix(long long rows, int cols, uint64_t seed, uint64_t base_stream, double* out) {
+    return guarded([&] {
+        if (rows < 0 || cols < 0) throw std::invalid_argument("gaussian_matrix: negative size");
+        fkb::DBuf<double> d(size_t(rows) * cols);
+        fkb::gaussian_matrix(rows, cols, seed, base_stream, d.p, rows, nullptr);
+        FKB_CUDA(cudaMemcpy(out, d.p, d.bytes(), cudaMemcpyDeviceToHost));
+    });
+}
+
+int fkb_fkf_init(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,
+                 long long k_rank, long long p_oversample, uint64_t seed, fkb_filter** out) {
+    return guarded([&] {
+        need(c, "cov");
+        need(out, "out");
+        need(rowptr, "rowptr");
+        *out = nullptr;
+        auto h = std::make_unique<fkb_filter>();
+        h->owner = c;
+        h->f = std::make_unique<fkb::Filter>(c->cov.get(), m, h_cols, rowptr, col, val, sigma2, k_rank, p_oversample,
+                                             seed);
+        *out = h.release();
+    });
+}
+void fkb_filter_destroy(fkb_filter* f) { delete f; }
+int fkb_filter_rank(const fkb_filter* f, int* rank, int* kept_cols) {
+    return guarded([&] {
+        need(f, "filter");
+        if (rank) *rank = f->f->r;
+        if (kept_cols) *kept_cols = f->f->kept_cols;
+    });
+}
+int fkb_filter_lambda(fkb_filter* f, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        std::memcpy(out, f->f->lambda_h.data(), f->f->lambda_h.size() * sizeof(double));
+    });
+}
+int fkb_filter_get(fkb_filter* f, int which, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        const double* src = nullptr;
+        size_t count = 0;
+        switch (which) {
+            case 0: src = F.U.p; count = size_t(F.n) * F.r; break;
+            case 1: src = F.Ubar.p; count = size_t(F.n) * F.r; break;
+            case 2: src = F.G.p; count = size_t(F.m) * F.m; break;
+            case 3: src = F.B.p; count = size_t(F.m) * F.r; break;
+            default: throw std::invalid_argument("filter_get: unknown product");
+        }
+        if (count) {
+            FKB_CUDA(cudaMemcpyAsync(out, src, count * sizeof(double), cudaMemcpyDeviceToHost, F.s));
+            FKB_CUDA(cudaStreamSynchronize(F.s));
+        }
+    });
+}
+int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (ylen != F.m)
+            throw std::invalid_argument("fkf_step: observation length " + std::to_string(ylen) + " does not match " +
+                                        std::to_string(F.m) + " measurements");
+        F.step_host(y);
+    });
+}
+int fkb_fkf_step_device(fkb_filter* f, const double* d_y) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->step(d_y);
+    });
+}
+int fkb_fkf_steps_async(fkb_filter* f, const double* d_ys, int nsteps, long long ldy) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->steps_async(d_ys, nsteps, ldy);
+    });
+}
+int fkb_fkf_sync(fkb_filter* f, int nsteps) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->finish_async(nsteps);
+    });
+}
+int fkb_filter_state(fkb_filter* f, double* alpha, int* step, int* rank, double* d, double* mean) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (alpha) *alpha = F.alpha;
+        if (step) *step = F.step_no;
+        if (rank) *rank = F.state_rank;
+        if (d && F.state_rank) FKB_CUDA(cudaMemcpyAsync(d, F.d.p, sizeof(double) * F.r, cudaMemcpyDeviceToHost, F.s));
+        if (mean) FKB_CUDA(cudaMemcpyAsync(mean, F.mean.p, sizeof(double) * F.n, cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const double* d, const double* mean) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (rank != 0 && rank != F.r)  // fast_filter.hpp:92-95
+            throw std::invalid_argument(
+                "fkf_step: state rank does not match the eigendecomposition (constant-H regime requires W = U)");
+        const double a2[2] = {alpha, alpha};
+        FKB_CUDA(cudaMemcpyAsync(F.alpha_dev.p, a2, sizeof(a2), cudaMemcpyHostToDevice, F.s));
+        if (rank) FKB_CUDA(cudaMemcpyAsync(F.d.p, d, sizeof(double) * F.r, cudaMemcpyHostToDevice, F.s));
+        else FKB_CUDA(cudaMemsetAsync(F.d.p, 0, F.d.bytes(), F.s));
+        if (mean) FKB_CUDA(cudaMemcpyAsync(F.mean.p, mean, sizeof(double) * F.n, cudaMemcpyHostToDevice, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+        F.alpha = alpha;
+        F.step_no = step;
+        F.state_rank = rank;
+    });
+}
+int fkb_filter_reset(fkb_filter* f) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->reset();
+    });
+}
+int fkb_filter_mean_device(fkb_filter* f, const double** d_mean) {
+    return guarded([&] {
+        need(f, "filter");
+        *d_mean = f->f->mean.p;
+    });
+}
+
+int fkb_variance_device(fkb_filter* f, double* d_out) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->variance(d_out);
+    });
+}
+int fkb_variance(fkb_filter* f, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        fkb::DBuf<double> d(static_cast<size_t>(F.n));
+        F.variance(d.p);
+        FKB_CUDA(cudaMemcpyAsync(out, d.p, d.bytes(), cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+int fkb_trace_criterion(fkb_filter* f, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        *out = f->f->trace_criterion();
+    });
+}
+int fkb_relative_entropy(fkb_filter* f, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        *out = f->f->relative_entropy();
+    });
+}
+int fkb_realizations_device(fkb_filter* f, uint64_t seed, int count, double* d_out, double* d_var) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->realizations(seed, count, d_out, d_var);
+    });
+}
+int fkb_realizations(fkb_filter* f, uint64_t seed, int count, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
+        if (count == 0) return;
+        fkb::DBuf<double> d(size_t(F.n) * count);
+        F.realizations(seed, count, d.p, nullptr);
+        FKB_CUDA(cudaMemcpyAsync(out, d.p, d.bytes(), cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+
+int fkb_filter_spmm(fkb_filter* f, int trans, const double* dX, long long ldx, int ncols, double* dY, long long ldy) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        fkb::spmm(trans ? F.HT : F.H, dX, ldx, ncols, dY, ldy, 1.0, 0.0, F.s);
+    });
+}
+void* fkb_filter_stream(fkb_filter* f) { return f ? (void*)f->f->s : nullptr; }
+int fkb_filter_launches_per_step(fkb_filter* f) { return f ? f->f->launches_per_step : 0; }
+
+int fkb_dmalloc(void** p, size_t bytes) { return guarded([&] { FKB_CUDA(cudaMalloc(p, bytes)); }); }
+int fkb_dfree(void* p) { return guarded([&] { FKB_CUDA(cudaFree(p)); }); }
+int fkb_h2d(void* dst, const void* src, size_t bytes) {
+    return guarded([&] { FKB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+int fkb_d2h(void* dst, const void* src, size_t bytes) {
+    return guarded([&] { FKB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+}
+int fkb_dsync(void) { return guarded([&] { FKB_CUDA(cudaDeviceSynchronize()); }); }
+
+}  // extern "C"

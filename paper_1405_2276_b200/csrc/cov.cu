@@ -1,0 +1,425 @@
+// cov.cu — K1: batched FP64 FFT circulant-embedding Γ·X on sm_100a.
+//
+// Reference: CovarianceOperator FFT mode, /root/reference/proj/include/fastkf/
+// covariance.hpp:238-353.  The reference applies Γ one column at a time with
+// two full mx×my complex FFTs (apply_fft :309-330).  Here a block of columns is
+// transformed at once, and the zero padding is exploited:
+//   pass A  rows:    real length-my rows ix < nx → Hermitian half (two rows per
+//                    complex transform), stored transposed as W[col][ky][ix];
+//   pass B  columns: per ky, zero-pad ix to mx, forward FFT, × spectrum,
+//                    inverse FFT, keep ix < nx (in place in W);
+//   pass C  rows:    Hermitian half → real rows, ×1/M, crop iy < ny.
+// The intermediate W for a batch is sized to stay L2-resident.
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numbers>
+#include <sstream>
+
+#include "cov.cuh"
+#include "fft_device.cuh"
+#include "rng_device.cuh"
+
+namespace fkb {
+
+static bool g_odd_ready = false;
+
+static void init_odd_tables() {
+    if (g_odd_ready) return;
+    OddRadixTables t;
+    for (int j = 0; j < 3; ++j) { t.c3[j] = double(cosl(2.0L * std::numbers::pi_v<long double> * j / 3)); t.s3[j] = double(sinl(2.0L * std::numbers::pi_v<long double> * j / 3)); }
+    for (int j = 0; j < 5; ++j) { t.c5[j] = double(cosl(2.0L * std::numbers::pi_v<long double> * j / 5)); t.s5[j] = double(sinl(2.0L * std::numbers::pi_v<long double> * j / 5)); }
+    for (int j = 0; j < 7; ++j) { t.c7[j] = double(cosl(2.0L * std::numbers::pi_v<long double> * j / 7)); t.s7[j] = double(sinl(2.0L * std::numbers::pi_v<long double> * j / 7)); }
+    FKB_CUDA(cudaMemcpyToSymbol(c_odd, &t, sizeof(t)));
+    g_odd_ready = true;
+}
+
+// --------------------------------------------------------------------------- host math
+void KernelSpec::validate() const {  // kernel.hpp:27-43
+    if (!(theta > 0.0)) throw std::invalid_argument("kernel: theta must be positive, got " + std::to_string(theta));
+    if (!(length > 0.0)) throw std::invalid_argument("kernel: length must be positive, got " + std::to_string(length));
+    if (family == 0) {
+        if (!(power > 0.0) || power > 2.0)
+            throw std::invalid_argument("kernel: power must lie in (0, 2], got " + std::to_string(power));
+    } else if (!(nu > 0.0)) {
+        throw std::invalid_argument("kernel: nu must be positive, got " + std::to_string(nu));
+    }
+}
+
+double kernel_eval(const KernelSpec& s, double r) {  // kernel.hpp:51-63 (host: symbol only)
+    s.validate();
+    if (r < 0.0) throw std::invalid_argument("kernel: distance must be nonnegative");
+    if (r == 0.0) return s.theta;
+    if (s.family == 0) return s.theta * std::exp(-std::pow(r / s.length, s.power));
+    const double arg = std::sqrt(2.0 * s.nu) * s.scale() * r;
+    if (arg > 700.0) return 0.0;
+    const double pref = std::exp((1.0 - s.nu) * std::numbers::ln2 - std::lgamma(s.nu));
+    return s.theta * pref * std::pow(arg, s.nu) * std::cyl_bessel_k(s.nu, arg);
+}
+
+int next_smooth(int n) {  // covariance.hpp:35-43
+    if (n <= 1) return 1;
+    for (int m = n;; ++m) {
+        int v = m;
+        for (int f : {2, 3, 5, 7})
+            while (v % f == 0) v /= f;
+        if (v == 1) return m;
+    }
+}
+
+// --------------------------------------------------------------------------- kernels
+constexpr int kThreads = 256;
+
+// Pass A: rows → Hermitian half along y.  Block = (row group, column).
+// Each complex transform packs two real rows (two-for-one).  Rows ≥ nx_in are zero.
+// Output W[col][ky][ix] for ix < nx_out (ld_w per column, ld_ky = nx_out).
+__global__ void __launch_bounds__(kThreads) k_rows_fwd(const double* __restrict__ X, long long ldx, int nx_in,
+                                                      int ny, int nx_out, FftLen fy, double2* __restrict__ W,
+                                                      long long ldw, int pairs) {
+    extern __shared__ double2 sm[];
+    const int my = fy.n, nky = my / 2 + 1;
+    double2* a = sm;
+    double2* b = sm + pairs * my;
+    const int ix0 = blockIdx.x * pairs * 2;
+    const double* x = X + (long long)blockIdx.y * ldx;
+    for (int e = threadIdx.x; e < pairs * my; e += blockDim.x) {
+        const int t = e / my, iy = e - t * my;
+        const int r0 = ix0 + 2 * t, r1 = r0 + 1;
+        double v0 = 0.0, v1 = 0.0;
+        if (iy < ny) {
+            if (r0 < nx_in) v0 = x[(long long)r0 * ny + iy];
+            if (r1 < nx_in) v1 = x[(long long)r1 * ny + iy];
+        }
+        a[e] = make_double2(v0, v1);
+    }
+    __syncthreads();
+    const double2* z = fft_smem<-1>(a, b, fy, pairs);
+    double2* w = W + (long long)blockIdx.y * ldw;
+    const int rows = pairs * 2;
+    for (int e = threadIdx.x; e < rows * nky; e += blockDim.x) {
+        const int ky = e / rows, rl = e - ky * rows;
+        const int ix = ix0 + rl;
+        if (ix >= nx_out) continue;
+        const int t = rl >> 1;
+        const double2 p = z[t * my + ky];
+        const double2 q = cconj(z[t * my + (ky == 0 ? 0 : my - ky)]);
+        double2 o;
+        if ((rl & 1) == 0) o = make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));  // (Z + conj Z−)/2
+        else o = make_double2(0.5 * (p.y - q.y), -0.5 * (p.x - q.x));              // (Z − conj Z−)/(2i)
+        w[(long long)ky * nx_out + ix] = o;
+    }
+}
+
+// Pass B: along x per ky column.  mode 0: zero-pad nx→mx, FFT, × spectrum, iFFT, keep nx.
+// mode 1 (spectrum build): forward only over the full mx, write mx entries.
+__global__ void __launch_bounds__(kThreads) k_cols(double2* __restrict__ W, long long ldw, int nx, FftLen fx,
+                                                  int nky, const double* __restrict__ spec_half, int kt,
+                                                  int mode) {
+    extern __shared__ double2 sm[];
+    const int mx = fx.n;
+    double2* a = sm;
+    double2* b = sm + kt * mx;
+    const int ky0 = blockIdx.x * kt;
+    double2* w = W + (long long)blockIdx.y * ldw;
+    const int ld = (mode == 0) ? nx : mx;
+    for (int e = threadIdx.x; e < kt * mx; e += blockDim.x) {
+        const int t = e / mx, ix = e - t * mx;
+        const int ky = ky0 + t;
+        double2 v = make_double2(0.0, 0.0);
+        if (ky < nky && ix < ld) v = w[(long long)ky * ld + ix];
+        a[e] = v;
+    }
+    __syncthreads();
+    double2* f = fft_smem<-1>(a, b, fx, kt);
+    double2* g = (f == a) ? b : a;
+    if (mode == 0) {
+        for (int e = threadIdx.x; e < kt * mx; e += blockDim.x) {
+            const int t = e / mx, kx = e - t * mx;
+            const int ky = min(ky0 + t, nky - 1);
+            f[e] = cscale(f[e], __ldg(spec_half + (long long)ky * mx + kx));
+        }
+        __syncthreads();
+        f = fft_smem<+1>(f, g, fx, kt);
+    }
+    const int keep = (mode == 0) ? nx : mx;
+    for (int e = threadIdx.x; e < kt * keep; e += blockDim.x) {
+        const int t = e / keep, ix = e - t * keep;
+        const int ky = ky0 + t;
+        if (ky < nky) w[(long long)ky * ld + ix] = f[t * mx + ix];
+    }
+}
+
+// Pass C: Hermitian half → real rows (two rows per complex transform), ×scale, crop.
+__global__ void __launch_bounds__(kThreads) k_rows_inv(const double2* __restrict__ W, long long ldw, int nx,
+                                                      int ny, FftLen fy, double* __restrict__ Y, long long ldy,
+                                                      int pairs, double scale) {
+    extern __shared__ double2 sm[];
+    const int my = fy.n;
+    double2* a = sm;
+    double2* b = sm + pairs * my;
+    const int ix0 = blockIdx.x * pairs * 2;
+    const double2* w = W + (long long)blockIdx.y * ldw;
+    for (int e = threadIdx.x; e < pairs * my; e += blockDim.x) {
+        const int t = e / my, ky = e - t * my;
+        const int r0 = ix0 + 2 * t, r1 = r0 + 1;
+        const bool hi = ky > my / 2;
+        const int kk = hi ? my - ky : ky;
+        double2 x1 = make_double2(0.0, 0.0), x2 = make_double2(0.0, 0.0);
+        if (r0 < nx) x1 = w[(long long)kk * nx + r0];
+        if (r1 < nx) x2 = w[(long long)kk * nx + r1];
+        if (hi) { x1 = cconj(x1); x2 = cconj(x2); }
+        a[e] = make_double2(x1.x - x2.y, x1.y + x2.x);  // X1 + i·X2
+    }
+    __syncthreads();
+    const double2* z = fft_smem<+1>(a, b, fy, pairs);
+    double* y = Y + (long long)blockIdx.y * ldy;
+    for (int e = threadIdx.x; e < pairs * 2 * ny; e += blockDim.x) {
+        const int rl = e / ny, iy = e - rl * ny;
+        const int ix = ix0 + rl;
+        if (ix >= nx) continue;
+        const double2 v = z[(rl >> 1) * my + iy];
+        y[(long long)ix * ny + iy] = ((rl & 1) ? v.y : v.x) * scale;
+    }
+}
+
+// Sampler pass 1: draw amp·(n_re + i n_im) on the torus for a tile of ky columns,
+// inverse FFT along x, keep ix < nx → T[ky][ix] (full ky range).
+__global__ void __launch_bounds__(kThreads) k_sampler_cols(const double* __restrict__ amp, int my, int nx,
+                                                          FftLen fx, uint64_t st_re, uint64_t st_im,
+                                                          double2* __restrict__ T, int kt) {
+    extern __shared__ double2 sm[];
+    const int mx = fx.n;
+    double2* a = sm;
+    double2* b = sm + kt * mx;
+    const int ky0 = blockIdx.x * kt;
+    for (int e = threadIdx.x; e < kt * mx; e += blockDim.x) {
+        const int t = e / mx, kx = e - t * mx;
+        const int ky = ky0 + t;
+        double2 v = make_double2(0.0, 0.0);
+        if (ky < my) {
+            const unsigned long long idx = (unsigned long long)kx * my + ky;  // covariance.hpp:338-342
+            const double am = __ldg(amp + idx);
+            v = make_double2(am * rng_normal_at(st_re, idx), am * rng_normal_at(st_im, idx));
+        }
+        a[e] = v;
+    }
+    __syncthreads();
+    const double2* f = fft_smem<+1>(a, b, fx, kt);
+    for (int e = threadIdx.x; e < kt * nx; e += blockDim.x) {
+        const int t = e / nx, ix = e - t * nx;
+        const int ky = ky0 + t;
+        if (ky < my) T[(long long)ky * nx + ix] = f[t * mx + ix];
+    }
+}
+
+// Sampler pass 2: per row ix, inverse c2c FFT along y, crop, Re → a, Im → b (×1/√M).
+__global__ void __launch_bounds__(kThreads) k_sampler_rows(const double2* __restrict__ T, int nx, int ny,
+                                                          FftLen fy, double* __restrict__ da,
+                                                          double* __restrict__ db, int rows, double scale) {
+    extern __shared__ double2 sm[];
+    const int my = fy.n;
+    double2* a = sm;
+    double2* b = sm + rows * my;
+    const int ix0 = blockIdx.x * rows;
+    for (int e = threadIdx.x; e < rows * my; e += blockDim.x) {
+        const int t = e / my, ky = e - t * my;
+        const int ix = ix0 + t;
+        a[e] = ix < nx ? T[(long long)ky * nx + ix] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const double2* f = fft_smem<+1>(a, b, fy, rows);
+    for (int e = threadIdx.x; e < rows * ny; e += blockDim.x) {
+        const int t = e / ny, iy = e - t * ny;
+        const int ix = ix0 + t;
+        if (ix < nx) {
+            const double2 v = f[t * my + iy];
+            da[(long long)ix * ny + iy] = v.x * scale;
+            db[(long long)ix * ny + iy] = v.y * scale;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- host orchestration
+static void plan_radices(FftLen& L, int n) {
+    L.n = n;
+    L.npass = 0;
+    int v = n;
+    auto push = [&](int r) {
+        if (L.npass >= kMaxPasses) throw std::runtime_error("fft: too many passes");
+        L.radix[L.npass++] = r;
+    };
+    while (v % 16 == 0) { push(16); v /= 16; }
+    if (v % 8 == 0) { push(8); v /= 8; }
+    if (v % 4 == 0) { push(4); v /= 4; }
+    if (v % 2 == 0) { push(2); v /= 2; }
+    for (int f : {3, 5, 7})
+        while (v % f == 0) { push(f); v /= f; }
+    if (v != 1) throw std::invalid_argument("fft: length " + std::to_string(n) + " is not {2,3,5,7}-smooth");
+}
+
+void Cov::setup_len(FftLen& L, DBuf<double2>& tw, int n) {
+    plan_radices(L, n);
+    std::vector<double2> h(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+        const long double ang = -2.0L * std::numbers::pi_v<long double> * k / n;
+        h[size_t(k)] = make_double2(double(cosl(ang)), double(sinl(ang)));
+    }
+    tw.alloc(size_t(n));
+    FKB_CUDA(cudaMemcpy(tw.p, h.data(), sizeof(double2) * size_t(n), cudaMemcpyHostToDevice));
+    L.tw = tw.p;
+}
+
+static int pairs_for(int my) { return my >= 1024 ? 2 : (my >= 512 ? 4 : std::max(4, 2048 / std::max(my, 1) / 2)); }
+static int kt_for(int mx) { return mx >= 1024 ? 2 : (mx >= 512 ? 4 : std::max(4, 2048 / std::max(mx, 1))); }
+static size_t smem_bytes(int batch, int n) { return 2 * size_t(batch) * size_t(n) * sizeof(double2); }
+
+static void set_smem(const void* fn, size_t bytes) {
+    if (bytes > 227 * 1024) throw std::invalid_argument("fft: transform too large for shared memory");
+    FKB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+}
+
+Cov::Cov(int nx_, int ny_, double lx_, double ly_, const KernelSpec& s, cudaStream_t st)
+    : nx(nx_), ny(ny_), lx(lx_), ly(ly_), spec(s), stream(st) {
+    if (nx < 1 || ny < 1)
+        throw std::invalid_argument("grid: nx and ny must be positive, got " + std::to_string(nx) + "x" + std::to_string(ny));
+    if (!(lx > 0.0) || !(ly > 0.0)) throw std::invalid_argument("grid: domain lengths must be positive");
+    spec.validate();
+    init_odd_tables();
+    const int base_x = std::max(2 * nx - 1, 1), base_y = std::max(2 * ny - 1, 1);
+    double worst = 0.0;
+    for (int pad = 1; pad <= 8; pad *= 2) {  // covariance.hpp:238-260
+        mx = next_smooth(base_x * pad);
+        my = next_smooth(base_y * pad);
+        if (try_spectrum(worst)) return;
+    }
+    std::ostringstream msg;
+    msg << "covariance: circulant embedding is not nonnegative definite for kernel "
+        << (spec.family == 0 ? "powered-exponential" : "matern") << " (theta=" << spec.theta
+        << ", length=" << spec.length;
+    if (spec.family == 0) msg << ", power=" << spec.power;
+    else msg << ", nu=" << spec.nu;
+    msg << ") on grid " << nx << "x" << ny << " even after 8x padding (worst negative/max spectrum ratio " << worst
+        << "); use dense mode or a shorter correlation length";
+    throw std::runtime_error(msg.str());
+}
+
+void Cov::ensure_work(int ncols) {
+    const size_t need = size_t(ncols) * size_t(nky) * size_t(std::max(nx, mx));
+    if (work.n < need) work.alloc(need);
+}
+
+bool Cov::try_spectrum(double& worst) {  // covariance.hpp:264-298
+    nky = my / 2 + 1;
+    setup_len(fx, twx, mx);
+    setup_len(fy, twy, my);
+    // Symbol on the torus at wrapped distances (:269-277), evaluated on the host with the
+    // reference formula (std::cyl_bessel_k); only the unique quarter is evaluated.
+    const double dx = lx / nx, dy = ly / ny;
+    const int hx = mx / 2 + 1, hy = my / 2 + 1;
+    std::vector<double> quarter(static_cast<size_t>(hx) * hy);
+    for (int i = 0; i < hx; ++i)
+        for (int j = 0; j < hy; ++j)
+            quarter[size_t(i) * hy + j] = kernel_eval(spec, std::hypot(std::min(i, mx - i) * dx, std::min(j, my - j) * dy));
+    std::vector<double> sym(static_cast<size_t>(M()));
+    for (int i = 0; i < mx; ++i)
+        for (int j = 0; j < my; ++j) sym[size_t(i) * my + j] = quarter[size_t(std::min(i, mx - i)) * hy + std::min(j, my - j)];
+    DBuf<double> dsym(sym.size());
+    FKB_CUDA(cudaMemcpyAsync(dsym.p, sym.data(), sym.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+    // Forward 2-D DFT of the real symbol: rows (R2C) then full columns, on the GPU.
+    ensure_work(1);
+    const int pairs = pairs_for(my), kt = kt_for(mx);
+    set_smem((const void*)k_rows_fwd, smem_bytes(pairs, my));
+    set_smem((const void*)k_cols, smem_bytes(kt, mx));
+    set_smem((const void*)k_rows_inv, smem_bytes(pairs, my));
+    k_rows_fwd<<<dim3(ceil_div(mx, 2 * pairs), 1), kThreads, smem_bytes(pairs, my), stream>>>(
+        dsym.p, 0, mx, my, mx, fy, work.p, 0, pairs);
+    FKB_LAUNCH_CHECK();
+    k_cols<<<dim3(ceil_div(nky, kt), 1), kThreads, smem_bytes(kt, mx), stream>>>(work.p, 0, mx, fx, nky, nullptr, kt, 1);
+    FKB_LAUNCH_CHECK();
+    count_launch(2);
+    std::vector<double2> half(static_cast<size_t>(nky) * mx);
+    FKB_CUDA(cudaMemcpyAsync(half.data(), work.p, half.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+    FKB_CUDA(cudaStreamSynchronize(stream));
+    // Full-torus real spectrum: S[kx][ky] = Re(half[ky][kx]) for ky ≤ my/2 and the even
+    // mirror S[kx][ky] = S[−kx][−ky] above (exact for the DFT of a real even symbol).
+    std::vector<double> full(static_cast<size_t>(M()));
+    double mxv = 0.0, mnv = 0.0;
+    for (int kx = 0; kx < mx; ++kx)
+        for (int ky = 0; ky < my; ++ky) {
+            double v;
+            if (ky < nky) v = half[size_t(ky) * mx + kx].x;
+            else v = half[size_t(my - ky) * mx + (kx == 0 ? 0 : mx - kx)].x;
+            full[size_t(kx) * my + ky] = v;
+            mxv = std::max(mxv, v);
+            mnv = std::min(mnv, v);
+        }
+    if (mxv <= 0.0) return false;
+    worst = std::max(worst, -mnv / mxv);
+    if (mnv < -1e-10 * mxv) return false;
+    std::vector<double> sh(static_cast<size_t>(nky) * mx), amp(static_cast<size_t>(M()));
+    for (int ky = 0; ky < nky; ++ky)
+        for (int kx = 0; kx < mx; ++kx) sh[size_t(ky) * mx + kx] = std::max(half[size_t(ky) * mx + kx].x, 0.0);
+    for (size_t i = 0; i < full.size(); ++i) {
+        full[i] = std::max(full[i], 0.0);
+        amp[i] = std::sqrt(full[i]);
+    }
+    spec_half.alloc(sh.size());
+    amp_full.alloc(amp.size());
+    FKB_CUDA(cudaMemcpyAsync(spec_half.p, sh.data(), sh.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+    FKB_CUDA(cudaMemcpyAsync(amp_full.p, amp.data(), amp.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+    FKB_CUDA(cudaStreamSynchronize(stream));
+    // Batch so the intermediate stays well inside the 126 MB L2.
+    const size_t per_col = size_t(nky) * size_t(nx) * sizeof(double2);
+    batch_cap = int(std::max<size_t>(1, std::min<size_t>(256, (48u << 20) / per_col)));
+    // One workspace for the whole lifetime (graph-captured steps hold its address):
+    // batched Γ-apply intermediate or the sampler's my×nx column pass.
+    work.release();
+    work.alloc(std::max(size_t(batch_cap) * nky * nx, size_t(my) * nx));
+    return true;
+}
+
+std::vector<double> Cov::spectrum_host() const {
+    std::vector<double> amp(static_cast<size_t>(M()));
+    FKB_CUDA(cudaMemcpy(amp.data(), amp_full.p, amp.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (auto& v : amp) v = v * v;
+    return amp;
+}
+
+void Cov::apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy) {
+    if (ncols <= 0) return;
+    ++applies;
+    const int pairs = pairs_for(my), kt = kt_for(mx);
+    const long long ldw = (long long)nky * nx;
+    const double scale = 1.0 / double(M());
+    for (int c0 = 0; c0 < ncols; c0 += batch_cap) {
+        const int bc = std::min(batch_cap, ncols - c0);
+        k_rows_fwd<<<dim3(ceil_div(nx, 2 * pairs), bc), kThreads, smem_bytes(pairs, my), stream>>>(
+            dX + (long long)c0 * ldx, ldx, nx, ny, nx, fy, work.p, ldw, pairs);
+        FKB_LAUNCH_CHECK();
+        k_cols<<<dim3(ceil_div(nky, kt), bc), kThreads, smem_bytes(kt, mx), stream>>>(work.p, ldw, nx, fx, nky,
+                                                                                     spec_half.p, kt, 0);
+        FKB_LAUNCH_CHECK();
+        k_rows_inv<<<dim3(ceil_div(nx, 2 * pairs), bc), kThreads, smem_bytes(pairs, my), stream>>>(
+            work.p, ldw, nx, ny, fy, dY + (long long)c0 * ldy, ldy, pairs, scale);
+        FKB_LAUNCH_CHECK();
+        count_launch(3);
+    }
+}
+
+void Cov::sample_pair(uint64_t seed, uint64_t sid, double* da, double* db) {
+    const int kt = kt_for(mx);
+    const int rows = std::max(1, std::min(4, 4096 / my));
+    set_smem((const void*)k_sampler_cols, smem_bytes(kt, mx));
+    set_smem((const void*)k_sampler_rows, smem_bytes(rows, my));
+    const uint64_t st_re = derive_seed_host(seed, 2 * sid), st_im = derive_seed_host(seed, 2 * sid + 1);
+    k_sampler_cols<<<ceil_div(my, kt), kThreads, smem_bytes(kt, mx), stream>>>(amp_full.p, my, nx, fx, st_re, st_im,
+                                                                             work.p, kt);
+    FKB_LAUNCH_CHECK();
+    k_sampler_rows<<<ceil_div(nx, rows), kThreads, smem_bytes(rows, my), stream>>>(work.p, nx, ny, fy, da, db, rows,
+                                                                                   1.0 / std::sqrt(double(M())));
+    FKB_LAUNCH_CHECK();
+    count_launch(2);
+}
+
+}  // namespace fkb

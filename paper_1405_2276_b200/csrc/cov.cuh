@@ -1,0 +1,49 @@
+// cov.cuh — Γ_sys on the device: FFT circulant embedding (reference covariance.hpp FFT mode).
+#pragma once
+
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace fkb {
+
+struct KernelSpec {  // kernel.hpp:19-48
+    int family = 0;  // 0 powered_exponential, 1 matern
+    double theta = 1.0, length = 0.2, power = 1.0, nu = 0.5, alpha_scale = 0.0;
+    void validate() const;
+    double scale() const { return alpha_scale > 0.0 ? alpha_scale : 1.0 / length; }
+};
+double kernel_eval(const KernelSpec& s, double r);  // kernel.hpp:51-63
+int next_smooth(int n);                             // covariance.hpp:35-43
+
+struct Cov {
+    int nx = 0, ny = 0;
+    double lx = 1.0, ly = 1.0;
+    KernelSpec spec;
+    int mx = 0, my = 0, nky = 0;  // nky = my/2 + 1 (Hermitian half along y)
+    cudaStream_t stream = nullptr;
+    FftLen fx, fy;
+    DBuf<double2> twx, twy;
+    DBuf<double> spec_half;  // [ky][kx], clipped ≥ 0 (covariance.hpp:295)
+    DBuf<double> amp_full;   // √spectrum on the full torus, row-major mx×my (sampler :339)
+    DBuf<double2> work;      // intermediate [col][ky][ix]
+    int batch_cap = 0;
+    long long applies = 0;
+
+    Cov(int nx, int ny, double lx, double ly, const KernelSpec& spec, cudaStream_t s);
+    long long size() const { return (long long)nx * ny; }
+    long long M() const { return (long long)mx * my; }
+
+    // Y = Γ X, X/Y column-major device blocks (covariance.hpp:101-115); Y may alias X.
+    void apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy);
+    // Two N(0,Γ) draws (covariance.hpp:332-353) into device vectors.
+    void sample_pair(uint64_t seed, uint64_t stream_id, double* da, double* db);
+    // Host copy of the full clipped spectrum (covariance.hpp:207-211), row-major mx×my.
+    std::vector<double> spectrum_host() const;
+
+  private:
+    bool try_spectrum(double& worst);
+    void setup_len(FftLen& L, DBuf<double2>& tw, int n);
+    void ensure_work(int ncols);
+};
+
+}  // namespace fkb

@@ -1,0 +1,447 @@
+// dense.cu — FP64 dense kernels for sm_100a: DMMA GEMM (K4/K5/K6), blocked Cholesky (K6),
+// flag-chained triangular solves, tall-skinny GEMV (K7/K8).
+//
+// FP64 has no tcgen05 kind; the FP64 tensor path on B200 is mma.sync .f64 (SASS DMMA).
+// Replaces the reference's Eigen products and LLT (fast_filter.hpp:100-108,
+// lowrank.hpp:186-205).
+
+#include <algorithm>
+
+#include "dense.cuh"
+
+namespace fkb {
+
+// --------------------------------------------------------------------------- DMMA GEMM
+constexpr int GBM = 64, GBN = 64, GBK = 16, GLD = GBM + 4, GTHREADS = 128;
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, const double* safe, bool valid) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 8 : 0;  // src-size 0 → zero fill, nothing read
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(valid ? src : safe), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(GTHREADS) k_gemm(GemmArgs g, int kchunk, double* __restrict__ partial) {
+    __shared__ __align__(16) double As[2][GBK][GLD];
+    __shared__ __align__(16) double Bs[2][GBK][GLD];
+    const int i0 = blockIdx.x * GBM, j0 = blockIdx.y * GBN;
+    if (g.lower_only && j0 > i0 + GBM - 1) return;
+    const int kbeg = blockIdx.z * kchunk;
+    const int kend = min(g.K, kbeg + kchunk);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    auto load = [&](int st, int k0) {
+#pragma unroll
+        for (int r = 0; r < (GBK * GBM) / GTHREADS; ++r) {
+            const int e = tid + r * GTHREADS;
+            int ii, kk;
+            if (g.transA == 0) { kk = e / GBM; ii = e - kk * GBM; }
+            else { ii = e / GBK; kk = e - ii * GBK; }
+            const int gi = i0 + ii, gk = k0 + kk;
+            const bool v = gi < g.M && gk < kend;
+            const double* src = g.transA == 0 ? g.A + gi + (long long)gk * g.lda : g.A + gk + (long long)gi * g.lda;
+            cp_async8(&As[st][kk][ii], src, g.A, v);
+        }
+#pragma unroll
+        for (int r = 0; r < (GBK * GBN) / GTHREADS; ++r) {
+            const int e = tid + r * GTHREADS;
+            int jj, kk;
+            if (g.transB == 0) { jj = e / GBK; kk = e - jj * GBK; }
+            else { kk = e / GBN; jj = e - kk * GBN; }
+            const int gj = j0 + jj, gk = k0 + kk;
+            const bool v = gj < g.N && gk < kend;
+            const double* src = g.transB == 0 ? g.B + gk + (long long)gj * g.ldb : g.B + gj + (long long)gk * g.ldb;
+            cp_async8(&Bs[st][kk][jj], src, g.B, v);
+        }
+        cp_async_commit();
+    };
+
+    const int nk = (kend - kbeg + GBK - 1) / GBK;
+    if (nk > 0) load(0, kbeg);
+    for (int it = 0; it < nk; ++it) {
+        const int st = it & 1;
+        if (it + 1 < nk) {
+            load(st ^ 1, kbeg + (it + 1) * GBK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GBK; kk += 4) {
+            double a[4], b[4];
+            double sc = 1.0;
+            if (g.dA) {
+                const int gk = kbeg + it * GBK + kk + tq;
+                sc = gk < kend ? __ldg(g.dA + gk) : 0.0;
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As[st][kk + tq][wm + mi * 8 + gq] * sc;
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[st][kk + tq][wn + ni * 8 + gq];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+
+    const double beta = g.beta_ptr ? *g.beta_ptr : g.beta;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int i = i0 + wm + mi * 8 + gq;
+                const int j = j0 + wn + ni * 8 + tq * 2 + q;
+                if (i >= g.M || j >= g.N) continue;
+                if (partial) {
+                    partial[(long long)blockIdx.z * g.M * g.N + i + (long long)j * g.M] = acc[mi][ni][q];
+                } else {
+                    double out = g.alpha * acc[mi][ni][q];
+                    if (beta != 0.0) out += beta * g.Cin[i + (long long)j * g.ldcin];
+                    if (i == j) out += g.diag_add;
+                    g.C[i + (long long)j * g.ldc] = out;
+                }
+            }
+}
+
+__global__ void k_splitk_reduce(GemmArgs g, const double* __restrict__ partial) {
+    const long long total = (long long)g.M * g.N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int i = int(e % g.M), j = int(e / g.M);
+        if (g.lower_only && (j / GBN) * GBN > (i / GBM) * GBM + GBM - 1) continue;
+        double s = 0.0;
+        for (int z = 0; z < g.splitk; ++z) s += partial[(long long)z * total + e];
+        double out = g.alpha * s;
+        const double beta = g.beta_ptr ? *g.beta_ptr : g.beta;
+        if (beta != 0.0) out += beta * g.Cin[i + (long long)j * g.ldcin];
+        if (i == j) out += g.diag_add;
+        g.C[i + (long long)j * g.ldc] = out;
+    }
+}
+
+int gemm_pick_splitk(int M, int N, int K) {
+    const long long tiles = (long long)ceil_div(M, GBM) * ceil_div(N, GBN);
+    if (tiles >= 296 || K < 512) return 1;
+    const long long want = (296 + tiles - 1) / tiles;
+    return int(std::max<long long>(1, std::min<long long>(want, K / 256)));
+}
+
+size_t gemm_ws_elems(const GemmArgs& g) { return g.splitk > 1 ? size_t(g.splitk) * g.M * g.N : 0; }
+
+void gemm(const GemmArgs& g_in, double* ws, cudaStream_t s) {
+    GemmArgs g = g_in;
+    if (g.M <= 0 || g.N <= 0) return;
+    if (!g.Cin) { g.Cin = g.C; g.ldcin = g.ldc; }
+    if (g.splitk < 1) g.splitk = 1;
+    int kchunk = g.K;
+    if (g.splitk > 1) {
+        kchunk = ((ceil_div(g.K, g.splitk) + GBK - 1) / GBK) * GBK;
+        g.splitk = ceil_div(g.K, kchunk);
+    }
+    dim3 grid(ceil_div(g.M, GBM), ceil_div(g.N, GBN), g.splitk);
+    if (g.K <= 0) {  // pure epilogue
+        g.splitk = 1;
+        grid.z = 1;
+    }
+    k_gemm<<<grid, GTHREADS, 0, s>>>(g, std::max(kchunk, 1), g.splitk > 1 ? ws : nullptr);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    if (g.splitk > 1) {
+        const long long total = (long long)g.M * g.N;
+        k_splitk_reduce<<<std::min<long long>(4096, (total + 255) / 256), 256, 0, s>>>(g, ws);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
+}
+
+// --------------------------------------------------------------------------- GEMV
+__global__ void k_gemv_n(int n, int k, const double* __restrict__ A, long long lda, const double* __restrict__ x,
+                         double alpha, double beta, double* __restrict__ y) {
+    extern __shared__ double xs[];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) xs[c] = x[c];
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        int c = 0;
+        for (; c + 1 < k; c += 2) {
+            s0 = fma(A[i + (long long)c * lda], xs[c], s0);
+            s1 = fma(A[i + (long long)(c + 1) * lda], xs[c + 1], s1);
+        }
+        if (c < k) s0 = fma(A[i + (long long)c * lda], xs[c], s0);
+        const double v = alpha * (s0 + s1);
+        y[i] = beta == 0.0 ? v : v + beta * y[i];
+    }
+}
+
+void gemv_n(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
+            cudaStream_t s) {
+    if (n <= 0) return;
+    if (k <= 0) {
+        if (beta != 1.0) {  // y = beta·y via a K=0 gemm epilogue
+            GemmArgs g;
+            g.M = n; g.N = 1; g.K = 0; g.A = A; g.lda = lda; g.B = x; g.ldb = 1;
+            g.alpha = 0.0; g.beta = beta; g.C = y; g.ldc = n;
+            gemm(g, nullptr, s);
+        }
+        return;
+    }
+    const int blocks = std::min(ceil_div(n, 256), 148 * 8);
+    k_gemv_n<<<blocks, 256, size_t(k) * sizeof(double), s>>>(n, k, A, lda, x, alpha, beta, y);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
+__global__ void k_gemv_t(int n, const double* __restrict__ A, long long lda, const double* __restrict__ x,
+                         double alpha, double beta, double* __restrict__ y) {
+    const int c = blockIdx.x;
+    const double* a = A + (long long)c * lda;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], x[i], s);
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) y[c] = beta == 0.0 ? alpha * s : alpha * s + beta * y[c];
+    }
+}
+
+void gemv_t(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
+            cudaStream_t s) {
+    if (k <= 0) return;
+    k_gemv_t<<<k, 256, 0, s>>>(n, A, lda, x, alpha, beta, y);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
+// --------------------------------------------------------------------------- Cholesky
+constexpr int CNB = 64;
+
+__global__ void __launch_bounds__(256) k_potrf_diag(double* A, long long lda, int kb, int k0, int* info) {
+    __shared__ double s[CNB][CNB + 1];
+    if (*info) return;
+    double* a = A + k0 + (long long)k0 * lda;
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+        const int i = e % kb, j = e / kb;
+        if (i >= j) s[i][j] = a[i + (long long)j * lda];
+    }
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int j = 0; j < kb; ++j) {
+        if (threadIdx.x == 0) {
+            const double d = s[j][j];
+            if (!(d > 0.0)) {
+                bad = 1;
+                atomicCAS(info, 0, k0 + j + 1);
+            } else {
+                s[j][j] = sqrt(d);
+            }
+        }
+        __syncthreads();
+        if (bad) return;
+        const double piv = s[j][j];
+        for (int i = j + 1 + threadIdx.x; i < kb; i += blockDim.x) s[i][j] /= piv;
+        __syncthreads();
+        const int rem = kb - j - 1;
+        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+            const int i = j + 1 + e % rem, c = j + 1 + e / rem;
+            if (i >= c) s[i][c] -= s[i][j] * s[c][j];
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+        const int i = e % kb, j = e / kb;
+        if (i >= j) a[i + (long long)j * lda] = s[i][j];
+    }
+}
+
+// L21 = A21 · L11⁻ᵀ for a 64-row block below the diagonal block at k0.
+__global__ void __launch_bounds__(CNB) k_trsm_panel(double* A, long long lda, int n, int k0, int kb, const int* info) {
+    extern __shared__ double trsm_sm[];
+    double (*L)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(trsm_sm);
+    double (*X)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(trsm_sm + CNB * (CNB + 1));
+    if (*info) return;
+    const int r0 = k0 + kb + blockIdx.x * CNB;
+    const int rb = min(CNB, n - r0);
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+        const int i = e % kb, j = e / kb;
+        L[i][j] = i >= j ? A[(k0 + i) + (long long)(k0 + j) * lda] : 0.0;
+    }
+    for (int e = threadIdx.x; e < rb * kb; e += blockDim.x) {
+        const int i = e % rb, j = e / rb;
+        X[i][j] = A[(r0 + i) + (long long)(k0 + j) * lda];
+    }
+    __syncthreads();
+    const int r = threadIdx.x;
+    if (r < rb) {
+        for (int j = 0; j < kb; ++j) {
+            double v = X[r][j];
+            for (int p = 0; p < j; ++p) v -= X[r][p] * L[j][p];
+            X[r][j] = v / L[j][j];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rb * kb; e += blockDim.x) {
+        const int i = e % rb, j = e / rb;
+        A[(r0 + i) + (long long)(k0 + j) * lda] = X[i][j];
+    }
+}
+
+size_t potrf_ws_elems(int n) {
+    // worst split-K workspace of a trailing update (none: trailing updates have K = 64)
+    (void)n;
+    return 0;
+}
+
+void potrf_lower(int n, double* A, long long lda, int* info, double* ws, size_t ws_elems, cudaStream_t s) {
+    (void)ws;
+    (void)ws_elems;
+    const size_t trsm_smem = 2 * sizeof(double) * CNB * (CNB + 1);
+    static bool attr = false;
+    if (!attr) {
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_trsm_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(trsm_smem)));
+        attr = true;
+    }
+    for (int k0 = 0; k0 < n; k0 += CNB) {
+        const int kb = std::min(CNB, n - k0);
+        k_potrf_diag<<<1, 256, 0, s>>>(A, lda, kb, k0, info);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        const int rest = n - k0 - kb;
+        if (rest <= 0) break;
+        k_trsm_panel<<<ceil_div(rest, CNB), CNB, trsm_smem, s>>>(A, lda, n, k0, kb, info);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        GemmArgs g;  // A22 −= L21 L21ᵀ (lower tiles)
+        g.M = rest; g.N = rest; g.K = kb;
+        g.A = A + (k0 + kb) + (long long)k0 * lda; g.lda = lda; g.transA = 0;
+        g.B = g.A; g.ldb = lda; g.transB = 1;
+        g.alpha = -1.0; g.beta = 1.0;
+        g.C = A + (k0 + kb) + (long long)(k0 + kb) * lda; g.ldc = lda;
+        g.lower_only = 1;
+        gemm(g, nullptr, s);
+    }
+}
+
+// --------------------------------------------------------------------------- triangular solves
+// Flag-chained block substitution: CTA b owns rows [64b, 64b+64); it folds in finished
+// blocks as their flags appear, then solves its diagonal block and publishes.  All CTAs
+// are co-resident (≤ 64 CTAs of 256 threads), and CTAs only wait on lower blockIdx.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(256) k_trsv(const double* __restrict__ L, long long lda, int n,
+                                             double* x, int* flags) {
+    const int nblk = (n + CNB - 1) / CNB;
+    const int b = TRANS ? nblk - 1 - blockIdx.x : blockIdx.x;
+    const int r0 = b * CNB, rb = min(CNB, n - r0);
+    __shared__ double part[4][CNB];
+    __shared__ double ysh[CNB];
+    __shared__ double D[CNB][CNB + 1];
+    const int tid = threadIdx.x;
+    // diagonal block
+    for (int e = tid; e < rb * rb; e += blockDim.x) {
+        const int i = e % rb, j = e / rb;
+        D[i][j] = L[(r0 + i) + (long long)(r0 + j) * lda];
+    }
+    double acc = 0.0;
+    const int r = TRANS ? (tid >> 2) : (tid & 63);
+    const int q = TRANS ? (tid & 3) : (tid >> 6);
+    const int jlo = TRANS ? b + 1 : 0, jhi = TRANS ? nblk : b;
+    for (int jj = jlo; jj < jhi; ++jj) {
+        const int j = TRANS ? (nblk - 1 - (jj - jlo)) : jj;  // consume in publication order
+        if (tid == 0)
+            while (ld_acquire(flags + j) == 0) {
+            }
+        __syncthreads();
+        const int c0 = j * CNB, cb = min(CNB, n - c0);
+        if (tid < cb) ysh[tid] = __ldcg(x + c0 + tid);
+        __syncthreads();
+        if (r < rb) {
+            for (int cc = 0; cc < 16; ++cc) {
+                const int c = q * 16 + cc;
+                if (c < cb) {
+                    const double l = TRANS ? L[(c0 + c) + (long long)(r0 + r) * lda] : L[(r0 + r) + (long long)(c0 + c) * lda];
+                    acc = fma(l, ysh[c], acc);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (r < CNB) part[q][r] = acc;
+    __syncthreads();
+    if (tid < 32) {
+        // rhs for the two rows this lane owns
+        double v0 = 0.0, v1 = 0.0;
+        const int i0 = tid, i1 = tid + 32;
+        if (i0 < rb) v0 = x[r0 + i0] - (part[0][i0] + part[1][i0] + part[2][i0] + part[3][i0]);
+        if (i1 < rb) v1 = x[r0 + i1] - (part[0][i1] + part[1][i1] + part[2][i1] + part[3][i1]);
+        if (!TRANS) {
+            for (int k = 0; k < rb; ++k) {
+                const double vk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+                const double yk = vk / D[k][k];
+                if (i0 == k) v0 = yk;
+                if (i1 == k) v1 = yk;
+                if (i0 > k && i0 < rb) v0 -= D[i0][k] * yk;
+                if (i1 > k && i1 < rb) v1 -= D[i1][k] * yk;
+            }
+        } else {
+            for (int k = rb - 1; k >= 0; --k) {
+                const double vk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+                const double yk = vk / D[k][k];
+                if (i0 == k) v0 = yk;
+                if (i1 == k) v1 = yk;
+                if (i0 < k) v0 -= D[k][i0] * yk;
+                if (i1 < k) v1 -= D[k][i1] * yk;
+            }
+        }
+        if (i0 < rb) x[r0 + i0] = v0;
+        if (i1 < rb) x[r0 + i1] = v1;
+        __threadfence();
+        __syncwarp();
+        if (tid == 0) st_release(flags + b, 1);
+    }
+}
+
+void potrs_lower(int n, const double* L, long long lda, double* x, int* flags, cudaStream_t s) {
+    const int nblk = ceil_div(n, CNB);
+    FKB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 2 * size_t(nblk), s));
+    k_trsv<false><<<nblk, 256, 0, s>>>(L, lda, n, x, flags);
+    FKB_LAUNCH_CHECK();
+    k_trsv<true><<<nblk, 256, 0, s>>>(L, lda, n, x, flags + nblk);
+    FKB_LAUNCH_CHECK();
+    count_launch(2);
+}
+
+}  // namespace fkb

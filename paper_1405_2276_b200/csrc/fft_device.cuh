@@ -1,0 +1,173 @@
+// fft_device.cuh — device-side FP64 Stockham FFT in shared memory (K1 core).
+//
+// Mixed-radix {16, 8, 4, 2, 3, 5, 7} self-sorting Stockham passes; each thread
+// performs whole radix-R butterflies from registers, twiddles come from a
+// per-length table tw[k] = exp(−2πi k/n) read through the read-only path.
+#pragma once
+
+#include "fft.cuh"
+
+namespace fkb {
+
+// defined here: this header is included by exactly one translation unit (cov.cu)
+__constant__ OddRadixTables c_odd;
+
+// W16^q for q in 0..7 (forward sign): cos(2πq/16), −sin(2πq/16)
+__device__ __forceinline__ constexpr double w16c(int q) {
+    return q == 0 ? 1.0
+         : q == 1 ? 0.92387953251128674
+         : q == 2 ? 0.70710678118654757
+         : q == 3 ? 0.38268343236508978
+         : q == 4 ? 0.0
+         : q == 5 ? -0.38268343236508978
+         : q == 6 ? -0.70710678118654757
+                  : -0.92387953251128674;
+}
+__device__ __forceinline__ constexpr double w16s(int q) {
+    return q == 0 ? 0.0
+         : q == 1 ? 0.38268343236508978
+         : q == 2 ? 0.70710678118654757
+         : q == 3 ? 0.92387953251128674
+         : q == 4 ? 1.0
+         : q == 5 ? 0.92387953251128674
+         : q == 6 ? 0.70710678118654757
+                  : 0.38268343236508978;
+}
+
+// b · exp(SIGN·2πi q/16), q compile-time after unrolling
+template <int SIGN>
+__device__ __forceinline__ double2 tw16(double2 b, int q) {
+    if (q == 0) return b;
+    if (q == 4) return cmul_i<SIGN>(b);
+    const double c = w16c(q), s = SIGN < 0 ? -w16s(q) : w16s(q);
+    if (q == 2 || q == 6) {  // |c| = |s| = √2/2
+        const double h = 0.70710678118654757;
+        const double sc = (q == 2) ? 1.0 : -1.0;  // sign of c
+        const double ss = s > 0 ? 1.0 : -1.0;
+        // (bx + i by)(sc·h + i ss·h) = h·(sc·bx − ss·by) + i h·(ss·bx + sc·by)
+        return make_double2(h * (sc * b.x - ss * b.y), h * (ss * b.x + sc * b.y));
+    }
+    return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));
+}
+
+template <int R>
+__device__ __forceinline__ constexpr int brev(int i) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) {
+        r = (r << 1) | (i & 1);
+        i >>= 1;
+    }
+    return r;
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_pow2(double2* v) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int j = brev<R>(i);
+        if (j > i) {
+            const double2 t = v[i];
+            v[i] = v[j];
+            v[j] = t;
+        }
+    }
+#pragma unroll
+    for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+        for (int i = 0; i < R; i += len) {
+#pragma unroll
+            for (int k = 0; k < len / 2; ++k) {
+                const double2 a = v[i + k];
+                const double2 b = tw16<SIGN>(v[i + k + len / 2], k * (16 / len));
+                v[i + k] = cadd(a, b);
+                v[i + k + len / 2] = csub(a, b);
+            }
+        }
+    }
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_odd(double2* v) {
+    const double* cs = R == 3 ? c_odd.c3 : (R == 5 ? c_odd.c5 : c_odd.c7);
+    const double* sn = R == 3 ? c_odd.s3 : (R == 5 ? c_odd.s5 : c_odd.s7);
+    double2 out[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        double2 acc = v[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            const int idx = (r * q) % R;
+            const double2 w = make_double2(cs[idx], SIGN < 0 ? -sn[idx] : sn[idx]);
+            acc = cadd(acc, cmul(v[r], w));
+        }
+        out[q] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = out[q];
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(double2* v) {
+    if constexpr (R == 2 || R == 4 || R == 8 || R == 16)
+        dft_pow2<R, SIGN>(v);
+    else
+        dft_odd<R, SIGN>(v);
+}
+
+// One Stockham pass over `batch` contiguous transforms of length L.n.
+template <int R, int SIGN>
+__device__ __forceinline__ void stockham_pass(const double2* __restrict__ in, double2* __restrict__ out,
+                                              const FftLen& L, int batch, int Ns) {
+    const int n = L.n, nb = n / R, total = nb * batch;
+    const int tws = n / (Ns * R);
+    for (int w = threadIdx.x; w < total; w += blockDim.x) {
+        const int t = w / nb, j = w - t * nb;
+        const double2* src = in + t * n;
+        double2* dst = out + t * n;
+        const int k = j % Ns;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = src[j + r * nb];
+        if (Ns > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 tw = __ldg(L.tw + r * k * tws);
+                if (SIGN > 0) tw.y = -tw.y;
+                v[r] = cmul(v[r], tw);
+            }
+        }
+        dft<R, SIGN>(v);
+        const int d = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[d + r * Ns] = v[r];
+    }
+}
+
+// Transforms `batch` contiguous length-L.n sequences held in `a` (scratch `b`).
+// Returns the buffer holding the result.  Caller must __syncthreads() before.
+template <int SIGN>
+__device__ double2* fft_smem(double2* a, double2* b, const FftLen& L, int batch) {
+    double2* in = a;
+    double2* out = b;
+    int Ns = 1;
+    for (int p = 0; p < L.npass; ++p) {
+        const int R = L.radix[p];
+        switch (R) {
+            case 16: stockham_pass<16, SIGN>(in, out, L, batch, Ns); break;
+            case 8: stockham_pass<8, SIGN>(in, out, L, batch, Ns); break;
+            case 4: stockham_pass<4, SIGN>(in, out, L, batch, Ns); break;
+            case 2: stockham_pass<2, SIGN>(in, out, L, batch, Ns); break;
+            case 3: stockham_pass<3, SIGN>(in, out, L, batch, Ns); break;
+            case 5: stockham_pass<5, SIGN>(in, out, L, batch, Ns); break;
+            default: stockham_pass<7, SIGN>(in, out, L, batch, Ns); break;
+        }
+        __syncthreads();
+        double2* t = in;
+        in = out;
+        out = t;
+        Ns *= R;
+    }
+    return in;
+}
+
+}  // namespace fkb

@@ -1,0 +1,520 @@
+// filter.cu — randomized GHEP, fkf_init, fkf_step and the UQ kernels on sm_100a.
+//
+// Reference: lowrank.hpp:141-213 (randomized_ghep, two-pass), fast_filter.hpp:51-125
+// (fkf_init / fkf_step), uq.hpp:16-112 (variance, trace, entropy, realizations).
+//
+// Γ-metric orthonormalization.  The reference orthonormalizes Ȳ = AΩ column by column
+// (modified Gram–Schmidt, 3 Γ-applies per column, lowrank.hpp:53-106).  Its outputs
+// (λ, U·f(D)·Uᵀ) depend only on span(AΩ), so the device path uses a
+// span-equivalent block method: one batched Γ-apply Z = ΓȲ, then two Gram passes
+// (G₁ = ȲᵀZ, G₂ = Q̄₁ᵀZ₁ on DMMA) each followed by a small host eigensolve, dropping
+// Gram directions below 1e-13·max (the rank-revealing counterpart of the reference's
+// 1e-12 norm-ratio drop).  The second pass needs no new Γ-apply because ΓQ̄₁ = Z·W₁.
+// Two-pass core T = Qᵀ(AQ) = (HQ)ᵀ(HQ)/σ².
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "filter.cuh"
+#include "host_linalg.h"
+
+namespace fkb {
+
+// --------------------------------------------------------------------------- small kernels
+__global__ void k_densify_rows(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                               int row0, int nrows, double* __restrict__ out, long long ld) {
+    const int r = blockIdx.y;
+    if (r >= nrows) return;
+    const int e0 = rp[row0 + r], e1 = rp[row0 + r + 1];
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) out[ci[e] + (long long)r * ld] = v[e];
+}
+
+__global__ void k_symmetrize(double* A, int n, long long lda) {  // A = ½(A + Aᵀ)
+    const long long total = (long long)n * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int i = int(e % n), j = int(e / n);
+        if (i <= j) continue;
+        const double v = 0.5 * (A[i + (long long)j * lda] + A[j + (long long)i * lda]);
+        A[i + (long long)j * lda] = v;
+        A[j + (long long)i * lda] = v;
+    }
+}
+
+__global__ void k_colsq(long long n, const double* __restrict__ U, double* __restrict__ out) {
+    const double* u = U + (long long)blockIdx.x * n;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) s = fma(u[i], u[i], s);
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) out[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_step_begin(double* alpha_dev) { alpha_dev[1] = alpha_dev[0] + 1.0; }  // α ← α + 1 (:97)
+
+// mean ← mean + α·t − U·(d ⊙ c)   (fast_filter.hpp:114-116), skipped if the LLT failed
+__global__ void __launch_bounds__(256) k_mean_update(long long n, int r, const double* __restrict__ U,
+                                                    const double* __restrict__ d, const double* __restrict__ c,
+                                                    const double* __restrict__ t, const double* __restrict__ alpha_dev,
+                                                    double* __restrict__ mean, const int* __restrict__ info) {
+    extern __shared__ double dc[];
+    if (*info) return;
+    for (int j = threadIdx.x; j < r; j += blockDim.x) dc[j] = d[j] * c[j];
+    __syncthreads();
+    const double alpha = alpha_dev[1];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        int j = 0;
+        for (; j + 1 < r; j += 2) {
+            s0 = fma(U[i + (long long)j * n], dc[j], s0);
+            s1 = fma(U[i + (long long)(j + 1) * n], dc[j + 1], s1);
+        }
+        if (j < r) s0 = fma(U[i + (long long)j * n], dc[j], s0);
+        mean[i] = (mean[i] + alpha * t[i]) - (s0 + s1);
+    }
+}
+
+// d'_i = (d_i + αλ_i(α − d_i)) / (1 + λ_i(α − d_i))  (fast_filter.hpp:118-123); commits α
+__global__ void k_d_update(int r, double* __restrict__ d, const double* __restrict__ lam, double* alpha_dev,
+                           const int* __restrict__ info) {
+    if (*info) return;
+    const double alpha = alpha_dev[1];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
+        const double c = alpha - d[i];
+        const double l = lam[i];
+        d[i] = (d[i] + alpha * l * c) / (1.0 + l * c);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) alpha_dev[0] = alpha;
+}
+
+// diag Σ and conditional realizations from one pass over U (uq.hpp:16-23, App. A.4):
+//   var_i = αθ − Σ_j d_j U_ij²;  x_s,i = mean_i + (√α z_s,i − √α Σ_j U_ij Σ₋_j (Ūᵀz_s)_j)
+__global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __restrict__ U,
+                                           const double* __restrict__ d, const double* __restrict__ alpha_dev,
+                                           double theta, const double* __restrict__ mean, int count,
+                                           const double* __restrict__ Z, const double* __restrict__ proj,
+                                           double* __restrict__ X, double* __restrict__ var) {
+    extern __shared__ double sh[];
+    double* ds = sh;          // r
+    double* P = sh + r;       // r × count
+    const double alpha = alpha_dev[0];
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        ds[j] = d[j];
+        const double sm = alpha == 0.0 ? 0.0 : 1.0 - sqrt(fmax(1.0 - d[j] / alpha, 0.0));  // uq.hpp:59-64
+        for (int s = 0; s < count; ++s) P[j * count + s] = sm * proj[j + (long long)s * r];
+    }
+    __syncthreads();
+    const double ra = sqrt(alpha);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double vs = 0.0;
+        double acc[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[s] = 0.0;
+        for (int j = 0; j < r; ++j) {
+            const double u = U[i + (long long)j * n];
+            vs = fma(u * u, ds[j], vs);
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+                if (s < count) acc[s] = fma(u, P[j * count + s], acc[s]);
+        }
+        if (var) var[i] = alpha * theta - vs;
+        const double mi = mean[i];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if (s < count) {
+                const double z = Z[i + (long long)s * n];
+                X[i + (long long)s * n] = alpha == 0.0 ? mi : mi + (ra * z - ra * acc[s]);
+            }
+    }
+}
+
+// --------------------------------------------------------------------------- host side
+static void check_nonneg_args(long long k, long long p, long long n) {  // lowrank.hpp:145-151
+    if (k < 0 || p < 0) throw std::invalid_argument("randomized_ghep: k and oversampling must be nonnegative");
+    if (k + p > n)
+        throw std::invalid_argument("randomized_ghep: k + oversampling = " + std::to_string(k + p) +
+                                    " exceeds problem size " + std::to_string(n));
+}
+
+static std::vector<double> download(const double* p, size_t count, cudaStream_t s) {
+    std::vector<double> h(count);
+    if (count) {
+        FKB_CUDA(cudaMemcpyAsync(h.data(), p, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+    }
+    return h;
+}
+static void upload(double* p, const std::vector<double>& h, cudaStream_t s) {
+    if (!h.empty()) FKB_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+}
+
+// Gram C = Aᵀ B for tall-skinny A (n×p), B (n×q) on DMMA with split-K
+static void gram_tn(long long n, int p, int q, const double* A, const double* B, double* C, DBuf<double>& ws,
+                    cudaStream_t s) {
+    GemmArgs g;
+    g.M = p; g.N = q; g.K = int(n);
+    g.A = A; g.lda = n; g.transA = 1;
+    g.B = B; g.ldb = n; g.transB = 0;
+    g.C = C; g.ldc = p;
+    g.splitk = gemm_pick_splitk(p, q, int(n));
+    ws.ensure(gemm_ws_elems(g));
+    gemm(g, ws.p, s);
+}
+// C (n×q) = A (n×p) · W (p×q), W on the device
+static void tall_times_small(long long n, int p, int q, const double* A, const double* W, double* C, cudaStream_t s) {
+    GemmArgs g;
+    g.M = int(n); g.N = q; g.K = p;
+    g.A = A; g.lda = n;
+    g.B = W; g.ldb = p;
+    g.C = C; g.ldc = n;
+    gemm(g, nullptr, s);
+}
+
+// Symmetric eigen of a small device Gram: returns kept columns W = V·diag(w^{-1/2}) for
+// eigenvalues above tol·max (rank-revealing drop), ordered by ascending eigenvalue.
+static std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept) {
+    std::vector<double> G = Gh;
+    for (int j = 0; j < p; ++j)
+        for (int i = 0; i < j; ++i) G[size_t(i) + size_t(j) * p] = G[size_t(j) + size_t(i) * p] =
+                                        0.5 * (G[size_t(i) + size_t(j) * p] + G[size_t(j) + size_t(i) * p]);
+    std::vector<double> w(static_cast<size_t>(p)), V(static_cast<size_t>(p) * p);
+    sym_eig_small(p, G.data(), w.data(), V.data());
+    const double wmax = p ? w[size_t(p - 1)] : 0.0;
+    std::vector<int> keep;
+    if (wmax > 0.0)
+        for (int j = 0; j < p; ++j)
+            if (w[size_t(j)] > tol * wmax) keep.push_back(j);
+    kept = int(keep.size());
+    std::vector<double> W(static_cast<size_t>(p) * std::max(kept, 1));
+    for (int c = 0; c < kept; ++c) {
+        const double sc = 1.0 / std::sqrt(w[size_t(keep[size_t(c)])]);
+        for (int i = 0; i < p; ++i) W[size_t(i) + size_t(c) * p] = V[size_t(i) + size_t(keep[size_t(c)]) * p] * sc;
+    }
+    return W;
+}
+
+void Filter::ghep(long long k, long long p, uint64_t seed) {
+    check_nonneg_args(k, p, n);
+    r = 0;
+    kept_cols = 0;
+    lambda_h.clear();
+    if (k == 0) return;
+    const int l = int(k + p);
+    DBuf<double> A(size_t(n) * l), Y(static_cast<size_t>(n) * l), HO(static_cast<size_t>(m) * l);
+    gaussian_matrix(n, l, seed, 0, A.p, n, s);                    // Ω (lowrank.hpp:157)
+    spmm(H, A.p, n, l, HO.p, m, 1.0, 0.0, s);                      // HΩ
+    spmm(HT, HO.p, m, l, Y.p, n, 1.0 / sigma2, 0.0, s);            // Ȳ = Hᵀ(HΩ)/σ² (:158-159)
+    ws.ensure(4096);
+    if (sumsq(Y.p, (long long)n * l, ws.p, s) == 0.0) return;     // A = 0 (:161)
+    DBuf<double>& Z = A;                                           // Ω no longer needed
+    cov->apply(Y.p, n, l, Z.p, n);                                 // Z = ΓȲ
+    DBuf<double> Gd(size_t(l) * l);
+    gram_tn(n, l, l, Y.p, Z.p, Gd.p, ws, s);                       // G₁ = ȲᵀΓȲ
+    int k1 = 0;
+    std::vector<double> W1 = gram_inv_sqrt(l, download(Gd.p, size_t(l) * l, s), 1e-13, k1);
+    if (k1 == 0)
+        throw std::runtime_error("randomized_ghep: rank collapse — every sketch column was dropped during orthonormalization");
+    DBuf<double> Wd(W1.size());
+    upload(Wd.p, W1, s);
+    DBuf<double> Q1(size_t(n) * k1), Z1(static_cast<size_t>(n) * k1);
+    tall_times_small(n, l, k1, Y.p, Wd.p, Q1.p, s);                // Q̄₁ = Ȳ W₁
+    tall_times_small(n, l, k1, Z.p, Wd.p, Z1.p, s);                // ΓQ̄₁ = Z W₁
+    gram_tn(n, k1, k1, Q1.p, Z1.p, Gd.p, ws, s);                   // G₂ = Q̄₁ᵀ Γ Q̄₁
+    int k2 = 0;
+    std::vector<double> W2 = gram_inv_sqrt(k1, download(Gd.p, size_t(k1) * k1, s), 1e-13, k2);
+    if (k2 == 0)
+        throw std::runtime_error("randomized_ghep: rank collapse — every sketch column was dropped during orthonormalization");
+    kept_cols = k2;
+    upload(Wd.p, W2, s);
+    // Q̄ = Q̄₁W₂ (into Y), Q = ΓQ̄ = Z₁W₂ (into Z)
+    tall_times_small(n, k1, k2, Q1.p, Wd.p, Y.p, s);
+    tall_times_small(n, k1, k2, Z1.p, Wd.p, Z.p, s);
+    Q1.release();
+    Z1.release();
+    // T = Qᵀ(AQ) = (HQ)ᵀ(HQ)/σ², symmetrized (:186-191)
+    spmm(H, Z.p, n, k2, HO.p, m, 1.0, 0.0, s);
+    DBuf<double> Td(size_t(k2) * k2);
+    {
+        GemmArgs g;
+        g.M = k2; g.N = k2; g.K = m;
+        g.A = HO.p; g.lda = m; g.transA = 1;
+        g.B = HO.p; g.ldb = m;
+        g.alpha = 1.0 / sigma2;
+        g.C = Td.p; g.ldc = k2;
+        g.splitk = gemm_pick_splitk(k2, k2, m);
+        ws.ensure(gemm_ws_elems(g));
+        gemm(g, ws.p, s);
+    }
+    std::vector<double> T = download(Td.p, size_t(k2) * k2, s);
+    for (int j = 0; j < k2; ++j)
+        for (int i = 0; i < j; ++i) T[size_t(i) + size_t(j) * k2] = T[size_t(j) + size_t(i) * k2] =
+                                        0.5 * (T[size_t(i) + size_t(j) * k2] + T[size_t(j) + size_t(i) * k2]);
+    std::vector<double> ev(static_cast<size_t>(k2)), Sv(static_cast<size_t>(k2) * k2);
+    sym_eig_small(k2, T.data(), ev.data(), Sv.data());             // (:193)
+    const int kk = int(std::min<long long>(k, k2));                // (:197-205)
+    r = kk;
+    lambda_h.resize(size_t(kk));
+    std::vector<double> Sk(static_cast<size_t>(k2) * kk);
+    for (int i = 0; i < kk; ++i) {
+        const int src = k2 - 1 - i;
+        lambda_h[size_t(i)] = std::max(ev[size_t(src)], 0.0);
+        std::copy(Sv.begin() + size_t(src) * k2, Sv.begin() + size_t(src + 1) * k2, Sk.begin() + size_t(i) * k2);
+    }
+    Wd.ensure(Sk.size());
+    upload(Wd.p, Sk, s);
+    lambda.alloc(size_t(kk));
+    upload(lambda.p, lambda_h, s);
+    U.alloc(size_t(n) * kk);
+    Ubar.alloc(size_t(n) * kk);
+    tall_times_small(n, k2, kk, Z.p, Wd.p, U.p, s);                // U = Q S
+    tall_times_small(n, k2, kk, Y.p, Wd.p, Ubar.p, s);             // Ū = Q̄ S = Γ⁻¹U
+    FKB_CUDA(cudaStreamSynchronize(s));
+}
+
+Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, const double* val, double sig2,
+               long long k, long long p, uint64_t seed)
+    : cov(c), s(c->stream), n(c->size()), m(m_), sigma2(sig2) {
+    if (m < 0) throw std::invalid_argument("fkf_init: negative measurement count");
+    if ((long long)h_cols != n) throw std::invalid_argument("fkf_init: H columns do not match state dimension");
+    for (int i = 0; i < m; ++i)
+        for (int e = rowptr[i]; e < rowptr[i + 1]; ++e)
+            if (col[e] < 0 || col[e] >= n) throw std::invalid_argument("fkf_init: H column index out of range");
+    if (!(sigma2 > 0.0)) throw std::invalid_argument("fkf_init: sigma2 must be positive");  // :54-57
+    upload_csr_pair(m, int(n), rowptr, col, val, H, HT);
+    ghep(k, p, seed);                                                                    // :63-66
+    // G = H·ΓHᵀ, symmetrized (:68-72): ΓHᵀ streamed in column batches, never stored.
+    G.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
+    if (m > 0) {
+        const int bc = int(std::max<long long>(1, std::min<long long>(m, (1LL << 27) / std::max<long long>(n, 1))));
+        DBuf<double> E(size_t(n) * bc);
+        for (int c0 = 0; c0 < m; c0 += bc) {
+            const int nb = std::min(bc, m - c0);
+            FKB_CUDA(cudaMemsetAsync(E.p, 0, sizeof(double) * size_t(n) * nb, s));
+            k_densify_rows<<<dim3(1, nb), 128, 0, s>>>(H.rowptr.p, H.col.p, H.val.p, c0, nb, E.p, n);
+            FKB_LAUNCH_CHECK();
+            count_launch();
+            cov->apply(E.p, n, nb, E.p, n);
+            spmm(H, E.p, n, nb, G.p + (long long)c0 * m, m, 1.0, 0.0, s);
+        }
+        k_symmetrize<<<std::min(ceil_div((long long)m * m, 256), 4096), 256, 0, s>>>(G.p, m, m);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
+    B.alloc(size_t(std::max(m, 1)) * std::max(r, 1));  // HU (:73)
+    spmm(H, U.p, n, r, B.p, m, 1.0, 0.0, s);
+    colsq.alloc(size_t(std::max(r, 1)));
+    if (r > 0) {
+        k_colsq<<<r, 256, 0, s>>>(n, U.p, colsq.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
+    // state + workspaces
+    alpha_dev.alloc(2);
+    d.alloc(size_t(std::max(r, 1)));
+    mean.alloc(size_t(n));
+    S.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
+    z.alloc(size_t(std::max(m, 1)));
+    t.alloc(size_t(n));
+    cvec.alloc(size_t(std::max(r, 1)));
+    ybuf.alloc(size_t(std::max(m, 1)));
+    info.alloc(1);
+    flags.alloc(size_t(2 * ceil_div(std::max(m, 1), 64) + 2));
+    reset();
+}
+
+Filter::~Filter() {
+    if (graph) cudaGraphExecDestroy(graph);
+}
+
+void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
+    FKB_CUDA(cudaMemsetAsync(alpha_dev.p, 0, 2 * sizeof(double), s));
+    FKB_CUDA(cudaMemsetAsync(d.p, 0, d.bytes(), s));
+    FKB_CUDA(cudaMemsetAsync(mean.p, 0, mean.bytes(), s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    alpha = 0.0;
+    step_no = 0;
+    state_rank = 0;
+}
+
+void Filter::enqueue_step(const double* d_y) {
+    FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+    k_step_begin<<<1, 1, 0, s>>>(alpha_dev.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    // S = α·G − B·diag(d)·Bᵀ + σ²I (lower triangle; :100-103)
+    GemmArgs g;
+    g.M = m; g.N = m; g.K = r;
+    g.A = B.p; g.lda = m; g.transA = 0;
+    g.B = B.p; g.ldb = m; g.transB = 1;
+    g.dA = d.p;
+    g.alpha = -1.0;
+    g.beta_ptr = alpha_dev.p + 1;
+    g.beta = 1.0;
+    g.Cin = G.p; g.ldcin = m;
+    g.C = S.p; g.ldc = m;
+    g.diag_add = sigma2;
+    g.lower_only = 1;
+    gemm(g, nullptr, s);
+    potrf_lower(m, S.p, m, info.p, nullptr, 0, s);  // LLT (:104-106)
+    // z = S⁻¹ (y − H·mean) (:108)
+    FKB_CUDA(cudaMemcpyAsync(z.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
+    spmm(H, mean.p, n, 1, z.p, m, -1.0, 1.0, s);
+    potrs_lower(m, S.p, m, z.p, flags.p, s);
+    // t = Γ(Hᵀz) = (ΓHᵀ)z ; c = Bᵀz
+    spmm(HT, z.p, m, 1, t.p, n, 1.0, 0.0, s);
+    cov->apply(t.p, n, 1, t.p, n);
+    if (r > 0) gemv_t(m, r, B.p, m, z.p, 1.0, 0.0, cvec.p, s);
+    const int blocks = std::min(ceil_div(n, 256), 148 * 4);
+    k_mean_update<<<blocks, 256, sizeof(double) * size_t(std::max(r, 1)), s>>>(n, r, U.p, d.p, cvec.p, t.p,
+                                                                            alpha_dev.p, mean.p, info.p);
+    FKB_LAUNCH_CHECK();
+    k_d_update<<<std::max(1, ceil_div(r, 256)), 256, 0, s>>>(r, d.p, lambda.p, alpha_dev.p, info.p);
+    FKB_LAUNCH_CHECK();
+    count_launch(2);
+}
+
+void Filter::check_info() {
+    int h = 0;
+    FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    if (h) throw std::runtime_error("fkf_step: innovation system is singular");
+}
+
+void Filter::launch_step() {
+    if (!graph_ready) {
+        // Capture the whole step once (it reads y from ybuf and α from alpha_dev);
+        // replays remove the per-kernel launch latency of ~100 small kernels.
+        const unsigned long long before = g_launches;
+        cudaGraph_t gr;
+        FKB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_step(ybuf.p);
+        } catch (...) {
+            cudaStreamEndCapture(s, &gr);
+            throw;
+        }
+        FKB_CUDA(cudaStreamEndCapture(s, &gr));
+        FKB_CUDA(cudaGraphInstantiate(&graph, gr, 0));
+        cudaGraphDestroy(gr);
+        launches_per_step = int(g_launches - before);
+        g_launches = before;
+        graph_ready = true;
+    }
+    FKB_CUDA(cudaGraphLaunch(graph, s));
+    count_launch(launches_per_step);
+}
+
+void Filter::step(const double* d_y) {
+    if (d_y != ybuf.p)
+        FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
+    launch_step();
+    check_info();
+    alpha += 1.0;
+    ++step_no;
+    state_rank = r;
+}
+
+void Filter::step_host(const double* h_y) {
+    if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_y, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+    step(ybuf.p);
+}
+
+void Filter::steps_async(const double* d_ys, int nsteps, long long ldy) {
+    // Device-resident observation sequence; one deferred singularity check at the end.
+    for (int k = 0; k < nsteps; ++k) {
+        FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_ys + (long long)k * ldy, sizeof(double) * size_t(m),
+                                 cudaMemcpyDeviceToDevice, s));
+        launch_step();
+    }
+}
+
+void Filter::finish_async(int nsteps) {
+    check_info();
+    alpha += double(nsteps);
+    step_no += nsteps;
+    if (nsteps > 0) state_rank = r;
+}
+
+std::vector<double> Filter::d_host() const { return download(d.p, size_t(r), s); }
+
+void Filter::variance(double* d_out) {
+    const int blocks = std::min(ceil_div(n, 256), 148 * 4);
+    k_uq<<<blocks, 256, sizeof(double) * size_t(std::max(r, 1)), s>>>(n, state_rank ? r : 0, U.p, d.p, alpha_dev.p,
+                                                                     cov->spec.theta, mean.p, 0, nullptr, nullptr,
+                                                                     nullptr, d_out);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
+double Filter::trace_criterion() {  // uq.hpp:27-34
+    double out = alpha * (double(n) * cov->spec.theta);
+    if (state_rank) {
+        const auto dh = d_host();
+        const auto ch = download(colsq.p, size_t(r), s);
+        for (int j = 0; j < r; ++j) out -= dh[size_t(j)] * ch[size_t(j)];
+    }
+    return out;
+}
+
+double Filter::relative_entropy() {  // uq.hpp:39-53
+    if (!(alpha > 0.0)) throw std::invalid_argument("relative_entropy: requires alpha > 0");
+    const int rk = state_rank;
+    double sum = (double(n) - double(rk)) * std::log(alpha);
+    if (rk) {
+        const auto dh = d_host();
+        for (int i = 0; i < rk; ++i) {
+            const double gap = alpha - dh[size_t(i)];
+            if (!(gap > 0.0))
+                throw std::runtime_error("relative_entropy: D_" + std::to_string(i) + " = " + std::to_string(dh[size_t(i)]) +
+                                         " is not below alpha = " + std::to_string(alpha));
+            sum += std::log(gap);
+        }
+    }
+    return 0.5 * sum;
+}
+
+// count realizations x_s = mean + √α(z_s − U Σ₋ Ūᵀ z_s); draw s = sample_pair(seed, s/2),
+// Re for even s, Im for odd.  Draws and Ūᵀz_s are cached per (seed, count) so each later
+// state costs one pass over U (RealizationPropagator, uq.hpp:86-112).
+void Filter::realizations(uint64_t seed, int count, double* d_out, double* d_var) {
+    if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
+    if (count == 0 && !d_var) return;
+    if (count > 0 && (draw_count != count || draw_seed != seed)) {
+        draws.alloc(size_t(n) * count);
+        DBuf<double> spare(static_cast<size_t>(n));
+        for (int sidx = 0; sidx < count; sidx += 2) {
+            double* a = draws.p + (long long)sidx * n;
+            double* b = sidx + 1 < count ? draws.p + (long long)(sidx + 1) * n : spare.p;
+            cov->sample_pair(seed, uint64_t(sidx / 2), a, b);
+        }
+        draw_proj.alloc(size_t(std::max(r, 1)) * count);
+        if (r > 0) {
+            GemmArgs g;
+            g.M = r; g.N = count; g.K = int(n);
+            g.A = Ubar.p; g.lda = n; g.transA = 1;
+            g.B = draws.p; g.ldb = n;
+            g.C = draw_proj.p; g.ldc = r;
+            g.splitk = gemm_pick_splitk(r, count, int(n));
+            ws.ensure(gemm_ws_elems(g));
+            gemm(g, ws.p, s);
+        }
+        FKB_CUDA(cudaStreamSynchronize(s));
+        draw_seed = seed;
+        draw_count = count;
+    }
+    const int blocks = std::min(ceil_div(n, 256), 148 * 4);
+    const int rr = state_rank ? r : 0;
+    const size_t shm = sizeof(double) * size_t(std::max(rr, 1)) * (1 + std::max(count, 1));
+    k_uq<<<blocks, 256, shm, s>>>(n, rr, U.p, d.p, alpha_dev.p, cov->spec.theta, mean.p, count,
+                                  count ? draws.p : nullptr, count ? draw_proj.p : nullptr, d_out, d_var);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace fkb

@@ -1,0 +1,69 @@
+// filter.cuh — the constant-H fast filter on the device (fkf_init / fkf_step / UQ).
+#pragma once
+
+#include <vector>
+
+#include "cov.cuh"
+#include "dense.cuh"
+#include "sparse.cuh"
+
+namespace fkb {
+
+struct Filter {
+    Cov* cov = nullptr;
+    cudaStream_t s = nullptr;
+    long long n = 0;
+    int m = 0;
+    double sigma2 = 0.0;
+    DevCsr H, HT;
+
+    // offline products (FkfContext, fast_filter.hpp:42-49); ΓHᵀ is not stored — the step
+    // applies Γ to Hᵀz instead (same product)
+    int r = 0;          // GEP rank
+    int kept_cols = 0;  // columns surviving Γ-orthonormalization
+    std::vector<double> lambda_h;
+    DBuf<double> lambda, U, Ubar, G, B, colsq;
+
+    // LowRankState (fast_filter.hpp:21-37), device resident; W ≡ U
+    double alpha = 0.0;
+    int step_no = 0;
+    int state_rank = 0;
+    DBuf<double> alpha_dev, d, mean;
+
+    // step workspaces
+    DBuf<double> S, z, t, cvec, ws;
+    DBuf<int> info, flags;
+    cudaGraphExec_t graph = nullptr;
+    bool graph_ready = false;
+    int launches_per_step = 0;
+
+    // cached realization draws (RealizationPropagator, uq.hpp:86-112)
+    uint64_t draw_seed = 0;
+    int draw_count = 0;
+    DBuf<double> draws, draw_proj;  // N×count, r×count (Ūᵀz)
+    DBuf<double> sig_minus;
+
+    DBuf<double> ybuf;
+
+    Filter(Cov* cov, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,
+           long long k, long long p, uint64_t seed);
+    ~Filter();
+    void ghep(long long k, long long p, uint64_t seed);  // lowrank.hpp:141-213
+    void step(const double* d_y);                        // fast_filter.hpp:84-125 (device y)
+    void step_host(const double* h_y);                   // same, y from host memory
+    // k steps over device-resident observations (column k at d_ys + k·ldy), no host sync;
+    // finish_async() performs the deferred singularity check and commits host mirrors.
+    void steps_async(const double* d_ys, int nsteps, long long ldy);
+    void finish_async(int nsteps);
+    void enqueue_step(const double* d_y);                // kernels only, no host sync
+    void launch_step();                                  // graph replay of enqueue_step(ybuf)
+    void check_info();                                   // throws on a singular innovation system
+    void reset();                                        // zero_start (:30-36)
+    void variance(double* d_out);                        // uq.hpp:16-23
+    double trace_criterion();                            // uq.hpp:27-34
+    double relative_entropy();                           // uq.hpp:39-53
+    void realizations(uint64_t seed, int count, double* d_out, double* d_var);
+    std::vector<double> d_host() const;
+};
+
+}  // namespace fkb

@@ -1,0 +1,27 @@
+// sparse.cuh — K2 (CSR SpMM over ray paths) and K3 (Ω generator).
+#pragma once
+
+#include "common.cuh"
+
+namespace fkb {
+
+struct DevCsr {  // SparseRowMatrix (grid.hpp:15) on the device: int32 indices, FP64 values
+    int rows = 0, cols = 0;
+    long long nnz = 0;
+    DBuf<int> rowptr, col;
+    DBuf<double> val;
+};
+
+// Y[:, b] = alpha · A X[:, b] (+ beta · Y) for b < ncols; X, Y column-major device blocks.
+void spmm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
+          double beta, cudaStream_t s);
+// Upload host CSR and build the explicit transposed CSR (rows ascending inside each column).
+void upload_csr_pair(int rows, int cols, const int* rowptr, const int* col, const double* val, DevCsr& A,
+                     DevCsr& AT);
+// Ω: N×l column-major, column j = normals of Rng(seed, j) (rng.hpp:79-86)
+void gaussian_matrix(long long rows, int cols, uint64_t seed, uint64_t base_stream, double* out, long long ld,
+                     cudaStream_t s);
+// sum of squares of a device vector (deterministic two-stage reduction), result on host
+double sumsq(const double* x, long long n, double* ws, cudaStream_t s);
+
+}  // namespace fkb

@@ -1,0 +1,158 @@
+"""GPU parity for the filter: GHEP (K2–K5), fkf_init/fkf_step (K6–K8) and UQ.
+
+Desk-scale cases restate proj/tests/test_lowrank.cpp:117-144, test_filters.cpp:115-201
+and test_uq.cpp:46-101; BASELINE configs compare against the CPU oracle step by step
+with the north-star tolerance (≤ 1e-9 relative, FP64)."""
+import numpy as np
+import pytest
+
+import paper_1405_2276_b200 as P
+from oracle import oracle as O
+from tests.helpers import Problem, csr_dense, dense_ghep, dense_kf, rel_err, workload_inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def _ghep_problem():
+    p = Problem(20, 20, 4, 6, 1, 2e-4)
+    return p
+
+
+def test_ghep_matches_dense_and_oracle():  # test_lowrank.cpp:117-144
+    p = _ghep_problem()
+    cov = P.CovarianceOperator(p.grid, p.spec())
+    ctx = P.fkf_init(cov, p.h, p.sigma2, 24, 20, 19)
+    assert ctx.rank() == 24
+    Hd = csr_dense(p.h)
+    gamma = p.gamma()
+    lam_ref, _ = dense_ghep(Hd.T @ Hd / p.sigma2, gamma)
+    lam = ctx.lam
+    assert np.all(np.abs(lam - lam_ref[:24]) / lam_ref[:24] < 1e-8)
+    assert np.all(np.diff(lam) <= 0) and lam[-1] >= 0
+    U = ctx.U()
+    gram = U.T @ np.linalg.solve(gamma, U)
+    assert np.linalg.norm(gram - np.eye(24)) < 1e-10
+    lo, Uo, _, _ = O.randomized_ghep(p.oracle_cov(), p.oracle_h(), p.sigma2, 24, 20, 19)
+    assert np.max(np.abs(lam - lo)) / lo[0] < TOL
+    # Ū = Γ⁻¹U
+    assert rel_err(gamma @ ctx.Ubar(), U) < 1e-10
+
+
+def test_offline_reconstruction_and_cross_covariance():  # test_filters.cpp:115-128
+    p = Problem(20, 20, 4, 6, 1, 2e-4)
+    cov = P.CovarianceOperator(p.grid, p.spec())
+    ctx = P.fkf_init(cov, p.h, p.sigma2, 24, 20, 5)
+    Hd = csr_dense(p.h)
+    A = Hd.T @ Hd / p.sigma2
+    gamma = p.gamma()
+    gu = np.linalg.solve(gamma, ctx.U())
+    recon = gu @ np.diag(ctx.lam) @ gu.T
+    assert np.linalg.norm(recon - A) <= 1e-8 * np.linalg.norm(A)
+    G = Hd @ gamma @ Hd.T
+    assert rel_err(ctx.h_gamma_ht(), G) < 1e-11
+    assert rel_err(ctx.h_u(), Hd @ ctx.U()) < 1e-12
+
+
+def test_zero_measurement_operator():  # test_filters.cpp:130-145
+    g = P.Grid(6, 6)
+    cov = P.CovarianceOperator(g, P.KernelSpec(family=0, theta=1e-4, length=0.2, power=0.5))
+    h = P.CsrMatrix(4, 36, np.zeros(5, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    ctx = P.fkf_init(cov, h, 2e-4, 4, 10, 7)
+    assert ctx.rank() == 0
+    st = P.fkf_step(ctx, np.zeros(4))
+    assert st["alpha"] == 1.0 and st["rank"] == 0 and np.linalg.norm(st["mean"]) == 0.0
+
+
+def test_first_step_diagonal_closed_form():  # test_filters.cpp:147-160
+    p = Problem(10, 10, 2, 4, 1, 2e-4)
+    ctx = P.fkf_init(P.CovarianceOperator(p.grid, p.spec()), p.h, p.sigma2, 8, 20, 9)
+    assert ctx.rank() == 8
+    st = P.fkf_step(ctx, p.obs[0])
+    lam = ctx.lam
+    assert np.all(np.abs(st["d"] - lam / (1 + lam)) <= 1e-12 * lam / (1 + lam))
+
+
+def test_full_rank_tracks_dense_kf():  # test_filters.cpp:162-191
+    p = Problem(12, 12, 3, 8, 10, 2e-4)
+    ctx = P.fkf_init(P.CovarianceOperator(p.grid, p.spec()), p.h, p.sigma2, p.h.rows, 20, 11)
+    assert ctx.rank() == p.h.rows
+    gamma = p.gamma()
+    ref = dense_kf(gamma, csr_dense(p.h), p.obs, p.sigma2)
+    U = ctx.U()
+    d_prev = np.zeros(p.h.rows)
+    for k, y in enumerate(p.obs):
+        st = P.fkf_step(ctx, y)
+        mean_ref, cov_ref = ref[k]
+        assert rel_err(st["mean"], mean_ref) < 1e-8
+        sigma = st["alpha"] * gamma - U @ np.diag(st["d"]) @ U.T
+        assert rel_err(sigma, cov_ref) < 1e-8
+        assert st["alpha"] == k + 1
+        assert st["d"].min() >= 0 and st["d"].max() < st["alpha"]
+        assert np.all(st["d"] >= d_prev - 1e-14)
+        d_prev = st["d"]
+
+
+def test_rejects_mismatched_state_rank():  # test_filters.cpp:193-201
+    p = Problem(6, 6, 2, 3, 1, 2e-4)
+    ctx = P.fkf_init(P.CovarianceOperator(p.grid, p.spec()), p.h, p.sigma2, 6, 10, 13)
+    with pytest.raises(ValueError):
+        ctx.set_state(1.0, np.full(2, 0.1), np.zeros(36))
+    with pytest.raises(ValueError):
+        ctx.step(np.zeros(p.h.rows + 1))
+
+
+def test_rank_zero_uq():  # test_uq.cpp:46-58
+    g = P.Grid(5, 5)
+    cov = P.CovarianceOperator(g, P.KernelSpec(family=0, theta=1e-4, length=0.2, power=0.5))
+    h = P.build_H(g, P.SourceReceiverLayout.cross_well(g, 2, 2))
+    ctx = P.fkf_init(cov, h, 2e-4, 4, 10, 7)
+    ctx.set_state(2.0, np.zeros(0), np.zeros(25))
+    assert rel_err(ctx.variance(), np.full(25, 2e-4)) < 1e-14
+    assert abs(ctx.trace_criterion() - 2.0 * 25 * 1e-4) <= 1e-14 * 5e-3
+    ctx.set_state(1.0, np.zeros(0), np.zeros(25))
+    assert ctx.relative_entropy() == 0.0
+
+
+def _run_both(name, steps, uq=False, realizations=0):
+    w, h, ys, s2 = workload_inputs(name, steps)
+    kern = dict(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), P.KernelSpec(**kern))
+    ctx = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    ocov = O.CovarianceOperator(w.n, w.n, **kern)
+    oh = O.Csr.from_arrays(h.rows, h.cols, h.rowptr, h.col, h.val)
+    of = O.FastFilter(ocov, oh, s2, k, p, w.ghep_seed)
+    assert ctx.rank() == of.rank
+    lo = of.context()["lam"]
+    assert np.max(np.abs(ctx.lam - lo)) / lo[0] < TOL
+    worst = dict(mean=0.0, d=0.0, var=0.0, real=0.0)
+    for y in ys:
+        st = P.fkf_step(ctx, y)
+        of.step(y)
+        so = of.state()
+        assert st["alpha"] == so["alpha"]
+        worst["mean"] = max(worst["mean"], rel_err(st["mean"], so["mean"]))
+        worst["d"] = max(worst["d"], np.max(np.abs(st["d"] - so["d"])) / so["alpha"])
+        if uq:
+            worst["var"] = max(worst["var"], rel_err(ctx.variance(), of.variance()))
+        if realizations:
+            xg = ctx.realizations(w.sample_seed, realizations)
+            xo = of.realizations(w.sample_seed, realizations)
+            worst["real"] = max(worst["real"], max(rel_err(xg[:, j] - so["mean"], xo[:, j] - so["mean"])
+                                                   for j in range(realizations)))
+    return worst
+
+
+def test_c0_parity_all_steps():
+    worst = _run_both("c0", None, uq=True, realizations=2)
+    assert worst["mean"] < TOL, worst
+    assert worst["d"] < TOL, worst
+    assert worst["var"] < TOL, worst
+    assert worst["real"] < TOL, worst
+
+
+@pytest.mark.slow
+def test_c1_parity_first_steps():
+    worst = _run_both("c1", 4, uq=True)
+    assert worst["mean"] < TOL and worst["d"] < TOL and worst["var"] < TOL, worst
