@@ -115,6 +115,25 @@ int fkb_filter_spmm(fkb_filter* f, int trans, const double* dX, long long ldx, i
                     long long ldy);
 void* fkb_filter_stream(fkb_filter* f);
 int fkb_filter_launches_per_step(fkb_filter* f);
+/* innovation solve: 1 (default) Woodbury in the offline eigenbasis of G = HΓHᵀ with a
+ * k×k capacitance factorization; 0 the reference order (form S, m×m LLT) */
+int fkb_filter_set_solver(fkb_filter* f, int mode);
+int fkb_filter_eig_sweeps(fkb_filter* f);
+/* eigenpairs of G (θ unsorted, P m×m column-major) */
+int fkb_filter_get_eig(fkb_filter* f, double* theta, double* P);
+/* runs `reps` real steps un-graphed with CUDA events at phase boundaries; ms[i] = mean
+ * duration of phase i, names = comma-separated phase names (advances the state) */
+int fkb_filter_phase_times(fkb_filter* f, int reps, double* ms, char* names, int names_len, int* nphases);
+
+/* capacitance factor+solve kernel on a host SPD matrix (test/profiling hook): L lower
+ * factor, x = K⁻¹b; stamps (optional, 128 entries) receive %globaltimer phase stamps */
+int fkb_chol_solve_small(int n, const double* K, const double* b, double* L, double* x,
+                         unsigned long long* stamps);
+
+/* measured FP64 peak of this GPU (mode 0: DFMA pipe, 1: DMMA tensor path), TFLOP/s */
+int fkb_fp64_peak(int mode, double* tflops);
+int fkb_set_device(int device);  /* cudaSetDevice for this library's runtime */
+int fkb_profiler(int on);        /* cudaProfilerStart/Stop (ncu --profile-from-start off) */
 
 /* device memory helpers (so bindings need no CUDA runtime of their own) */
 int fkb_dmalloc(void** p, size_t bytes);

@@ -69,6 +69,14 @@ SIGNATURES = {
     "fkb_filter_spmm": (_i, [_p, _i, _p, _ll, _i, _p, _ll]),
     "fkb_filter_stream": (_p, [_p]),
     "fkb_filter_launches_per_step": (_i, [_p]),
+    "fkb_filter_set_solver": (_i, [_p, _i]),
+    "fkb_filter_eig_sweeps": (_i, [_p]),
+    "fkb_filter_get_eig": (_i, [_p, _p, _p]),
+    "fkb_filter_phase_times": (_i, [_p, _i, _dp, C.c_char_p, _i, _PI]),
+    "fkb_fp64_peak": (_i, [_i, _PD]),
+    "fkb_chol_solve_small": (_i, [_i, _dp, _dp, _dp, _dp, np.ctypeslib.ndpointer(dtype=np.uint64)]),
+    "fkb_set_device": (_i, [_i]),
+    "fkb_profiler": (_i, [_i]),
     "fkb_dmalloc": (_i, [C.POINTER(_p), _sz]),
     "fkb_dfree": (_i, [_p]),
     "fkb_h2d": (_i, [_p, _p, _sz]),

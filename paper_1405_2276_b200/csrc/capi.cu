@@ -352,6 +352,39 @@ int fkb_filter_spmm(fkb_filter* f, int trans, const double* dX, long long ldx, i
     });
 }
 void* fkb_filter_stream(fkb_filter* f) { return f ? (void*)f->f->s : nullptr; }
+int fkb_filter_set_solver(fkb_filter* f, int mode) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->set_solver(mode);
+    });
+}
+int fkb_filter_eig_sweeps(fkb_filter* f) { return f ? f->f->eig_sweeps : 0; }
+int fkb_filter_phase_times(fkb_filter* f, int reps, double* ms, char* names, int names_len, int* nphases) {
+    return guarded([&] {
+        need(f, "filter");
+        auto v = f->f->phase_times(reps);
+        std::string joined;
+        for (size_t i = 0; i < v.size(); ++i) {
+            if (ms) ms[i] = v[i].second;
+            if (i) joined += ",";
+            joined += v[i].first;
+        }
+        if (names && names_len > 0) {
+            std::strncpy(names, joined.c_str(), size_t(names_len) - 1);
+            names[names_len - 1] = 0;
+        }
+        *nphases = int(v.size());
+    });
+}
+int fkb_filter_get_eig(fkb_filter* f, double* theta, double* P) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (theta) FKB_CUDA(cudaMemcpyAsync(theta, F.theta.p, sizeof(double) * F.m, cudaMemcpyDeviceToHost, F.s));
+        if (P) FKB_CUDA(cudaMemcpyAsync(P, F.P.p, sizeof(double) * size_t(F.m) * F.m, cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
 int fkb_filter_launches_per_step(fkb_filter* f) { return f ? f->f->launches_per_step : 0; }
 
 int fkb_dmalloc(void** p, size_t bytes) { return guarded([&] { FKB_CUDA(cudaMalloc(p, bytes)); }); }

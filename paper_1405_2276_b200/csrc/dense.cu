@@ -8,6 +8,7 @@
 #include <algorithm>
 
 #include "dense.cuh"
+#include "gemv.cuh"
 
 namespace fkb {
 
@@ -116,7 +117,10 @@ __global__ void __launch_bounds__(GTHREADS) k_gemm(GemmArgs g, int kchunk, doubl
                 if (partial) {
                     partial[(long long)blockIdx.z * g.M * g.N + i + (long long)j * g.M] = acc[mi][ni][q];
                 } else {
-                    double out = g.alpha * acc[mi][ni][q];
+                    double a = acc[mi][ni][q];
+                    if (g.rs) a *= g.rs[i];
+                    if (g.cs) a *= g.cs[j];
+                    double out = g.alpha * a;
                     if (beta != 0.0) out += beta * g.Cin[i + (long long)j * g.ldcin];
                     if (i == j) out += g.diag_add;
                     g.C[i + (long long)j * g.ldc] = out;
@@ -131,6 +135,8 @@ __global__ void k_splitk_reduce(GemmArgs g, const double* __restrict__ partial) 
         if (g.lower_only && (j / GBN) * GBN > (i / GBM) * GBM + GBM - 1) continue;
         double s = 0.0;
         for (int z = 0; z < g.splitk; ++z) s += partial[(long long)z * total + e];
+        if (g.rs) s *= g.rs[i];
+        if (g.cs) s *= g.cs[j];
         double out = g.alpha * s;
         const double beta = g.beta_ptr ? *g.beta_ptr : g.beta;
         if (beta != 0.0) out += beta * g.Cin[i + (long long)j * g.ldcin];
@@ -141,9 +147,9 @@ __global__ void k_splitk_reduce(GemmArgs g, const double* __restrict__ partial) 
 
 int gemm_pick_splitk(int M, int N, int K) {
     const long long tiles = (long long)ceil_div(M, GBM) * ceil_div(N, GBN);
-    if (tiles >= 296 || K < 512) return 1;
+    if (tiles >= 296 || K < 256) return 1;
     const long long want = (296 + tiles - 1) / tiles;
-    return int(std::max<long long>(1, std::min<long long>(want, K / 256)));
+    return int(std::max<long long>(1, std::min<long long>(want, K / 128)));
 }
 
 size_t gemm_ws_elems(const GemmArgs& g) { return g.splitk > 1 ? size_t(g.splitk) * g.M * g.N : 0; }
@@ -205,10 +211,7 @@ void gemv_n(int n, int k, const double* A, long long lda, const double* x, doubl
         }
         return;
     }
-    const int blocks = std::min(ceil_div(n, 256), 148 * 8);
-    k_gemv_n<<<blocks, 256, size_t(k) * sizeof(double), s>>>(n, k, A, lda, x, alpha, beta, y);
-    FKB_LAUNCH_CHECK();
-    count_launch();
+    launch_gemv_rows(n, k, A, lda, XPlain{x}, EpiAxpby{y, alpha, beta}, s);
 }
 
 __global__ void k_gemv_t(int n, const double* __restrict__ A, long long lda, const double* __restrict__ x,
@@ -230,10 +233,7 @@ __global__ void k_gemv_t(int n, const double* __restrict__ A, long long lda, con
 
 void gemv_t(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
             cudaStream_t s) {
-    if (k <= 0) return;
-    k_gemv_t<<<k, 256, 0, s>>>(n, A, lda, x, alpha, beta, y);
-    FKB_LAUNCH_CHECK();
-    count_launch();
+    launch_gemv_cols(n, k, A, lda, XPlain{x}, EpiAxpby{y, alpha, beta}, s);
 }
 
 // --------------------------------------------------------------------------- Cholesky

@@ -28,6 +28,8 @@ struct GemmArgs {
     double* C = nullptr;
     long long ldc = 0;
     double diag_add = 0.0;
+    const double* rs = nullptr;  // optional epilogue row scale:    acc_ij · rs_i
+    const double* cs = nullptr;  // optional epilogue column scale: acc_ij · cs_j
     int lower_only = 0;
     int splitk = 1;
 };

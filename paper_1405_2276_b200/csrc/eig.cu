@@ -1,0 +1,283 @@
+// eig.cu — offline symmetric eigendecomposition G = P·diag(θ)·Pᵀ on the GPU (two-sided
+// block Jacobi).  Used once per fkf_init to diagonalize the α-dependence of the innovation
+// system S(α, d) = αG + σ²I − B·D·Bᵀ (fast_filter.hpp:100-103), so that every fkf_step
+// needs only a k×k capacitance factorization instead of the reference's m×m LLT
+// (fast_filter.hpp:104).  Jacobi is chosen for its backward stability and high relative
+// accuracy: P is orthogonal and P·diag(θ)·Pᵀ reproduces G to a few ulp·‖G‖.
+//
+// Schedule: the m indices are split into blocks of JB; each round pairs the blocks with a
+// round-robin tournament; every pair (p, q) is diagonalized exactly in shared memory by an
+// inner cyclic Jacobi (k_pair_eig); the pair rotations Q are then applied to the columns of
+// A and V (k_apply_cols) and to the rows of A (k_apply_rows).  Sweeps repeat until every
+// off-diagonal entry satisfies |a_ij| ≤ tol·√(a_ii·a_jj).
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "eig.cuh"
+
+namespace fkb {
+
+constexpr int JB = 32;        // block size
+constexpr int J2 = 2 * JB;    // pair subproblem size
+constexpr int JLD = J2 + 1;   // padded smem leading dimension
+
+__host__ __device__ inline int rr_block(int pos, int round, int nbp) {
+    // tournament position → block index (position 0 fixed, others rotate); nbp even
+    if (pos == 0) return 0;
+    return 1 + ((pos - 1 + round) % (nbp - 1));
+}
+
+struct PairInfo {
+    int p0, np, q0, nq;  // first index and size of each block (np/nq = 0: idle)
+};
+
+__device__ inline PairInfo pair_info(int m, int nb, int nbp, int round, int pair) {
+    int bp = rr_block(pair, round, nbp);
+    int bq = rr_block(nbp - 1 - pair, round, nbp);
+    if (bp > bq) { const int t = bp; bp = bq; bq = t; }
+    PairInfo pi;
+    pi.p0 = bp * JB;
+    pi.np = bp < nb ? min(JB, m - pi.p0) : 0;
+    pi.q0 = bq * JB;
+    pi.nq = bq < nb ? min(JB, m - pi.q0) : 0;
+    return pi;
+}
+__device__ inline int pair_index(const PairInfo& pi, int i) {  // local 0..J2 → global (−1 = pad)
+    if (i < JB) return i < pi.np ? pi.p0 + i : -1;
+    return (i - JB) < pi.nq ? pi.q0 + (i - JB) : -1;
+}
+
+// Diagonalize the 64×64 symmetric pair block exactly (inner cyclic Jacobi, round-robin
+// parallel ordering, 32 disjoint rotations per inner round).  Writes Q (J2×J2, col-major)
+// and the pair's largest relative off-diagonal before rotation into offmax[pair].
+__global__ void __launch_bounds__(256) k_pair_eig(const double* __restrict__ A, long long lda, int m, int nb,
+                                                 int nbp, int round, double* __restrict__ Q,
+                                                 double* __restrict__ offmax) {
+    extern __shared__ double eig_sm[];
+    double* S = eig_sm;
+    double* V = eig_sm + J2 * JLD;
+    __shared__ double cs[J2 / 2][2];
+    __shared__ int pq[J2 / 2][2];
+    __shared__ double red[8];
+    __shared__ int active;
+    const int pair = blockIdx.x;
+    const PairInfo pi = pair_info(m, nb, nbp, round, pair);
+    const int tid = threadIdx.x;
+    double mine = 0.0;
+    for (int e = tid; e < J2 * J2; e += blockDim.x) {
+        const int i = e % J2, j = e / J2;
+        const int gi = pair_index(pi, i), gj = pair_index(pi, j);
+        double v;
+        if (gi >= 0 && gj >= 0) v = A[gi + (long long)gj * lda];
+        else v = (i == j) ? 1.0 : 0.0;
+        S[i + j * JLD] = v;
+        V[i + j * JLD] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < J2 * J2; e += blockDim.x) {
+        const int i = e % J2, j = e / J2;
+        if (i < j) {
+            const double d = sqrt(fabs(S[i + i * JLD] * S[j + j * JLD]));
+            const double a = fabs(S[i + j * JLD]);
+            if (a > 0.0) mine = fmax(mine, d > 0.0 ? a / d : 1.0);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) mine = fmax(mine, __shfl_down_sync(0xffffffffu, mine, o));
+    if ((tid & 31) == 0) red[tid >> 5] = mine;
+    __syncthreads();
+    if (tid == 0) {
+        double mx = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+        offmax[pair] = mx;
+    }
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        if (tid == 0) active = 0;
+        __syncthreads();
+        for (int rnd = 0; rnd < J2 - 1; ++rnd) {
+            if (tid < J2 / 2) {
+                int p = rr_block(tid, rnd, J2), q = rr_block(J2 - 1 - tid, rnd, J2);
+                if (p > q) { const int t = p; p = q; q = t; }
+                const double apq = S[p + q * JLD], app = S[p + p * JLD], aqq = S[q + q * JLD];
+                double c = 1.0, s = 0.0;
+                if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+                    const double th = (aqq - app) / (2.0 * apq);
+                    const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                    c = 1.0 / sqrt(t * t + 1.0);
+                    s = t * c;
+                    active = 1;
+                }
+                cs[tid][0] = c;
+                cs[tid][1] = s;
+                pq[tid][0] = p;
+                pq[tid][1] = q;
+            }
+            __syncthreads();
+            // columns: S ← S·J, V ← V·J
+            for (int e = tid; e < (J2 / 2) * J2; e += blockDim.x) {
+                const int t = e / J2, k = e % J2;
+                const double c = cs[t][0], s = cs[t][1];
+                if (s == 0.0) continue;
+                const int p = pq[t][0], q = pq[t][1];
+                const double skp = S[k + p * JLD], skq = S[k + q * JLD];
+                S[k + p * JLD] = c * skp - s * skq;
+                S[k + q * JLD] = s * skp + c * skq;
+                const double vkp = V[k + p * JLD], vkq = V[k + q * JLD];
+                V[k + p * JLD] = c * vkp - s * vkq;
+                V[k + q * JLD] = s * vkp + c * vkq;
+            }
+            __syncthreads();
+            // rows: S ← Jᵀ·S
+            for (int e = tid; e < (J2 / 2) * J2; e += blockDim.x) {
+                const int t = e / J2, k = e % J2;
+                const double c = cs[t][0], s = cs[t][1];
+                if (s == 0.0) continue;
+                const int p = pq[t][0], q = pq[t][1];
+                const double spk = S[p + k * JLD], sqk = S[q + k * JLD];
+                S[p + k * JLD] = c * spk - s * sqk;
+                S[q + k * JLD] = s * spk + c * sqk;
+            }
+            __syncthreads();
+        }
+        if (!active) break;
+    }
+    double* Qp = Q + (long long)pair * J2 * J2;
+    for (int e = tid; e < J2 * J2; e += blockDim.x) {
+        const int i = e % J2, j = e / J2;
+        Qp[e] = V[i + j * JLD];
+    }
+}
+
+// X[rows, pair cols] ← X[rows, pair cols]·Q for X = A and X = V (grid: row tiles × pairs)
+__global__ void __launch_bounds__(256) k_apply_cols(double* __restrict__ A, double* __restrict__ Vm, long long ld,
+                                                   int m, int nb, int nbp, int round,
+                                                   const double* __restrict__ Q) {
+    extern __shared__ double eig_sm[];
+    double (*T)[J2 + 1] = reinterpret_cast<double (*)[J2 + 1]>(eig_sm);
+    double (*Qs)[J2 + 1] = reinterpret_cast<double (*)[J2 + 1]>(eig_sm + 64 * (J2 + 1));
+    const int pair = blockIdx.y;
+    const PairInfo pi = pair_info(m, nb, nbp, round, pair);
+    if (pi.np + pi.nq == 0) return;
+    const double* Qp = Q + (long long)pair * J2 * J2;
+    for (int e = threadIdx.x; e < J2 * J2; e += blockDim.x) Qs[e % J2][e / J2] = Qp[e];
+    const int r0 = blockIdx.x * 64;
+    for (int which = 0; which < 2; ++which) {
+        double* X = which == 0 ? A : Vm;
+        __syncthreads();
+        for (int e = threadIdx.x; e < 64 * J2; e += blockDim.x) {
+            const int i = e % 64, j = e / 64;
+            const int gj = pair_index(pi, j);
+            T[i][j] = (r0 + i < m && gj >= 0) ? X[(r0 + i) + (long long)gj * ld] : 0.0;
+        }
+        __syncthreads();
+        // each thread: one row i, 16 output columns
+        const int i = threadIdx.x & 63, cg = threadIdx.x >> 6;
+        double acc[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+        for (int kk = 0; kk < J2; ++kk) {
+            const double t = T[i][kk];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = fma(t, Qs[kk][cg * 16 + c], acc[c]);
+        }
+        if (r0 + i < m) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const int gj = pair_index(pi, cg * 16 + c);
+                if (gj >= 0) X[(r0 + i) + (long long)gj * ld] = acc[c];
+            }
+        }
+    }
+}
+
+// A[pair rows, cols] ← Qᵀ·A[pair rows, cols] (grid: column tiles × pairs)
+__global__ void __launch_bounds__(256) k_apply_rows(double* __restrict__ A, long long ld, int m, int nb, int nbp,
+                                                   int round, const double* __restrict__ Q) {
+    extern __shared__ double eig_sm[];
+    double (*T)[64 + 1] = reinterpret_cast<double (*)[64 + 1]>(eig_sm);
+    double (*Qs)[J2 + 1] = reinterpret_cast<double (*)[J2 + 1]>(eig_sm + J2 * 65);
+    const int pair = blockIdx.y;
+    const PairInfo pi = pair_info(m, nb, nbp, round, pair);
+    if (pi.np + pi.nq == 0) return;
+    const double* Qp = Q + (long long)pair * J2 * J2;
+    for (int e = threadIdx.x; e < J2 * J2; e += blockDim.x) Qs[e % J2][e / J2] = Qp[e];
+    const int c0 = blockIdx.x * 64;
+    for (int e = threadIdx.x; e < J2 * 64; e += blockDim.x) {
+        const int i = e % J2, j = e / J2;
+        const int gi = pair_index(pi, i);
+        T[i][j] = (c0 + j < m && gi >= 0) ? A[gi + (long long)(c0 + j) * ld] : 0.0;
+    }
+    __syncthreads();
+    const int j = threadIdx.x & 63, rg = threadIdx.x >> 6;
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int kk = 0; kk < J2; ++kk) {
+        const double t = T[kk][j];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[c] = fma(Qs[kk][rg * 16 + c], t, acc[c]);  // (Qᵀ)_{r,kk} = Q_{kk,r}
+    }
+    if (c0 + j < m) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const int gi = pair_index(pi, rg * 16 + c);
+            if (gi >= 0) A[gi + (long long)(c0 + j) * ld] = acc[c];
+        }
+    }
+}
+
+__global__ void k_eye(double* V, long long ld, int m) {
+    const long long total = (long long)m * m;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        V[(e % m) + (e / m) * ld] = (e % m == e / m) ? 1.0 : 0.0;
+}
+__global__ void k_diag(const double* A, long long ld, int m, double* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) out[i] = A[i + (long long)i * ld];
+}
+
+int sym_eig_device(int m, double* A, long long lda, double* theta, double* V, cudaStream_t s, double tol,
+                   int max_sweeps) {
+    if (m <= 0) return 0;
+    const int nb = ceil_div(m, JB);
+    const int nbp = nb + (nb & 1);  // even number of tournament slots (one idle if odd)
+    const int npairs = nbp / 2;
+    const int rounds = nbp - 1;
+    DBuf<double> Q(size_t(npairs) * J2 * J2), off(size_t(npairs) * std::max(rounds, 1));
+    k_eye<<<std::min(4096, ceil_div((long long)m * m, 256)), 256, 0, s>>>(V, m, m);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    int sweeps = 0;
+    const size_t sm_pair = sizeof(double) * 2 * J2 * JLD, sm_apply = sizeof(double) * 2 * 64 * (J2 + 1);
+    static bool attr = false;
+    if (!attr) {
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_pair_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_pair)));
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_apply_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_apply)));
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_apply_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_apply)));
+        attr = true;
+    }
+    std::vector<double> offh(off.n);
+    for (; sweeps < max_sweeps; ++sweeps) {
+        for (int r = 0; r < rounds; ++r) {
+            k_pair_eig<<<npairs, 256, sm_pair, s>>>(A, lda, m, nb, nbp, r, Q.p, off.p + (long long)r * npairs);
+            FKB_LAUNCH_CHECK();
+            k_apply_cols<<<dim3(ceil_div(m, 64), npairs), 256, sm_apply, s>>>(A, V, lda, m, nb, nbp, r, Q.p);
+            FKB_LAUNCH_CHECK();
+            k_apply_rows<<<dim3(ceil_div(m, 64), npairs), 256, sm_apply, s>>>(A, lda, m, nb, nbp, r, Q.p);
+            FKB_LAUNCH_CHECK();
+            count_launch(3);
+        }
+        FKB_CUDA(cudaMemcpyAsync(offh.data(), off.p, sizeof(double) * offh.size(), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+        double mx = 0.0;
+        for (double v : offh) mx = std::max(mx, v);
+        if (mx <= tol) break;
+    }
+    k_diag<<<ceil_div(m, 256), 256, 0, s>>>(A, lda, m, theta);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    return sweeps;
+}
+
+}  // namespace fkb

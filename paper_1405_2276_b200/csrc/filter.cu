@@ -16,8 +16,11 @@
 #include <cmath>
 #include <string>
 
+#include "eig.cuh"
 #include "filter.cuh"
+#include "gemv.cuh"
 #include "host_linalg.h"
+#include "smallchol.cuh"
 
 namespace fkb {
 
@@ -58,27 +61,40 @@ __global__ void k_colsq(long long n, const double* __restrict__ U, double* __res
 
 __global__ void k_step_begin(double* alpha_dev) { alpha_dev[1] = alpha_dev[0] + 1.0; }  // α ← α + 1 (:97)
 
-// mean ← mean + α·t − U·(d ⊙ c)   (fast_filter.hpp:114-116), skipped if the LLT failed
-__global__ void __launch_bounds__(256) k_mean_update(long long n, int r, const double* __restrict__ U,
-                                                    const double* __restrict__ d, const double* __restrict__ c,
-                                                    const double* __restrict__ t, const double* __restrict__ alpha_dev,
-                                                    double* __restrict__ mean, const int* __restrict__ info) {
-    extern __shared__ double dc[];
-    if (*info) return;
-    for (int j = threadIdx.x; j < r; j += blockDim.x) dc[j] = d[j] * c[j];
-    __syncthreads();
+// Woodbury per-step scalars: wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j
+__global__ void k_prep(int m, int r, const double* __restrict__ theta, const double* __restrict__ d,
+                       const double* __restrict__ alpha_dev, double sigma2, double* __restrict__ wsq,
+                       double* __restrict__ sqd) {
     const double alpha = alpha_dev[1];
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double s0 = 0.0, s1 = 0.0;
-        int j = 0;
-        for (; j + 1 < r; j += 2) {
-            s0 = fma(U[i + (long long)j * n], dc[j], s0);
-            s1 = fma(U[i + (long long)(j + 1) * n], dc[j + 1], s1);
-        }
-        if (j < r) s0 = fma(U[i + (long long)j * n], dc[j], s0);
-        mean[i] = (mean[i] + alpha * t[i]) - (s0 + s1);
-    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) sqd[j] = sqrt(d[j]);
 }
+
+// u_j = sqd_j · Σ_i E_ij · (wsq_i · rt_i)   (F̃ᵀx̃ of the capacitance system)
+struct EpiScaleOut {
+    double* u;
+    const double* sc;
+    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sc[j] * v; }
+};
+// s̃_i = wsq_i · (rt_i + Σ_j E_ij · (sqd_j · x_j))   ([Λ_M − EDEᵀ]⁻¹ r̃ via Woodbury)
+struct EpiWoodbury {
+    double* st;
+    const double* wsq;
+    const double* rt;
+    __device__ __forceinline__ void operator()(long long i, double v) const { st[i] = wsq[i] * (rt[i] + v); }
+};
+// mean_i ← (mean_i + α·t_i) − Σ_j U_ij (d_j c_j)   (fast_filter.hpp:114-116), skipped on LLT failure
+struct EpiMean {
+    double* mean;
+    const double* t;
+    const double* alpha_dev;
+    const int* info;
+    __device__ __forceinline__ void operator()(long long i, double v) const {
+        if (*info) return;
+        mean[i] = (mean[i] + alpha_dev[1] * t[i]) - v;
+    }
+};
 
 // d'_i = (d_i + αλ_i(α − d_i)) / (1 + λ_i(α − d_i))  (fast_filter.hpp:118-123); commits α
 __global__ void k_d_update(int r, double* __restrict__ d, const double* __restrict__ lam, double* alpha_dev,
@@ -292,15 +308,15 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     G.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
     if (m > 0) {
         const int bc = int(std::max<long long>(1, std::min<long long>(m, (1LL << 27) / std::max<long long>(n, 1))));
-        DBuf<double> E(size_t(n) * bc);
+        DBuf<double> Ec(size_t(n) * bc);
         for (int c0 = 0; c0 < m; c0 += bc) {
             const int nb = std::min(bc, m - c0);
-            FKB_CUDA(cudaMemsetAsync(E.p, 0, sizeof(double) * size_t(n) * nb, s));
-            k_densify_rows<<<dim3(1, nb), 128, 0, s>>>(H.rowptr.p, H.col.p, H.val.p, c0, nb, E.p, n);
+            FKB_CUDA(cudaMemsetAsync(Ec.p, 0, sizeof(double) * size_t(n) * nb, s));
+            k_densify_rows<<<dim3(1, nb), 128, 0, s>>>(H.rowptr.p, H.col.p, H.val.p, c0, nb, Ec.p, n);
             FKB_LAUNCH_CHECK();
             count_launch();
-            cov->apply(E.p, n, nb, E.p, n);
-            spmm(H, E.p, n, nb, G.p + (long long)c0 * m, m, 1.0, 0.0, s);
+            cov->apply(Ec.p, n, nb, Ec.p, n);
+            spmm(H, Ec.p, n, nb, G.p + (long long)c0 * m, m, 1.0, 0.0, s);
         }
         k_symmetrize<<<std::min(ceil_div((long long)m * m, 256), 4096), 256, 0, s>>>(G.p, m, m);
         FKB_LAUNCH_CHECK();
@@ -314,11 +330,41 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
         FKB_LAUNCH_CHECK();
         count_launch();
     }
+    // Offline diagonalization of the α-dependence: G = P·diag(θ)·Pᵀ (block Jacobi), E = PᵀB.
+    P.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
+    theta.alloc(size_t(std::max(m, 1)));
+    E.alloc(size_t(std::max(m, 1)) * std::max(r, 1));
+    if (m > 0) {
+        S.alloc(size_t(m) * m);
+        FKB_CUDA(cudaMemcpyAsync(S.p, G.p, sizeof(double) * size_t(m) * m, cudaMemcpyDeviceToDevice, s));
+        eig_sweeps = sym_eig_device(m, S.p, m, theta.p, P.p, s);
+        if (r > 0) {
+            GemmArgs g;
+            g.M = m; g.N = r; g.K = m;
+            g.A = P.p; g.lda = m; g.transA = 1;
+            g.B = B.p; g.ldb = m;
+            g.C = E.p; g.ldc = m;
+            gemm(g, nullptr, s);
+        }
+        S.release();
+    }
     // state + workspaces
     alpha_dev.alloc(2);
     d.alloc(size_t(std::max(r, 1)));
     mean.alloc(size_t(n));
-    S.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
+    wsq.alloc(size_t(std::max(m, 1)));
+    sqd.alloc(size_t(std::max(r, 1)));
+    rt.alloc(size_t(std::max(m, 1)));
+    st.alloc(size_t(std::max(m, 1)));
+    ucap.alloc(size_t(std::max(r, 1)));
+    Kcap.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
+    rdg.alloc(std::max<size_t>(chol_solve_scratch(r), 1));
+    {
+        GemmArgs g;  // split-K workspace of the capacitance Gram
+        g.M = r; g.N = r; g.K = m;
+        g.splitk = gemm_pick_splitk(r, r, m);
+        ws_step.alloc(std::max<size_t>(gemm_ws_elems(g), 1));  // fixed address: graph-captured
+    }
     z.alloc(size_t(std::max(m, 1)));
     t.alloc(size_t(n));
     cvec.alloc(size_t(std::max(r, 1)));
@@ -342,12 +388,113 @@ void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
     state_rank = 0;
 }
 
+void Filter::mark(const char* name) {
+    if (!phase_events) return;
+    cudaEvent_t e;
+    FKB_CUDA(cudaEventCreate(&e));
+    FKB_CUDA(cudaEventRecord(e, s));
+    phase_events->push_back(e);
+    phase_names.emplace_back(name);
+}
+
+std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
+    std::vector<std::pair<std::string, double>> acc;
+    for (int rep = 0; rep < reps; ++rep) {
+        std::vector<cudaEvent_t> ev;
+        phase_events = &ev;
+        phase_names.clear();
+        mark("begin");
+        try {
+            enqueue_step(ybuf.p);
+        } catch (...) {
+            phase_events = nullptr;
+            throw;
+        }
+        phase_events = nullptr;
+        FKB_CUDA(cudaStreamSynchronize(s));
+        if (acc.empty())
+            for (size_t i = 1; i < ev.size(); ++i) acc.emplace_back(phase_names[i], 0.0);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            FKB_CUDA(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+            acc[i - 1].second += ms / reps;
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        check_info();
+        alpha += 1.0;
+        ++step_no;
+        state_rank = r;
+    }
+    return acc;
+}
+
+void Filter::set_solver(int mode) {
+    if (mode != 0 && mode != 1) throw std::invalid_argument("fkf: solver must be 0 (dense LLT) or 1 (Woodbury)");
+    if (mode == solver) return;
+    solver = mode;
+    if (mode == 0 && S.n < size_t(m) * m) S.alloc(size_t(std::max(m, 1)) * std::max(m, 1));  // before any capture
+    if (graph) cudaGraphExecDestroy(graph);
+    graph = nullptr;
+    graph_ready = false;
+}
+
 void Filter::enqueue_step(const double* d_y) {
     FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
     k_step_begin<<<1, 1, 0, s>>>(alpha_dev.p);
     FKB_LAUNCH_CHECK();
     count_launch();
-    // S = α·G − B·diag(d)·Bᵀ + σ²I (lower triangle; :100-103)
+    // z = y − H·mean (:108)
+    FKB_CUDA(cudaMemcpyAsync(z.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
+    spmm(H, mean.p, n, 1, z.p, m, -1.0, 1.0, s);
+    mark("residual");
+    if (solver == 0) enqueue_solve_dense();
+    else enqueue_solve_woodbury();
+    // t = Γ(Hᵀz) = (ΓHᵀ)z ; c = Bᵀz
+    spmm(HT, z.p, m, 1, t.p, n, 1.0, 0.0, s);
+    cov->apply(t.p, n, 1, t.p, n);
+    if (r > 0) gemv_t(m, r, B.p, m, z.p, 1.0, 0.0, cvec.p, s);
+    mark("gamma_ht_z");
+    launch_gemv_rows(n, r, U.p, n, XProd{d.p, cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+    mark("mean_update");
+    k_d_update<<<std::max(1, ceil_div(r, 256)), 256, 0, s>>>(r, d.p, lambda.p, alpha_dev.p, info.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    mark("d_update");
+}
+
+// z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
+void Filter::enqueue_solve_woodbury() {
+    const int pb = std::max(1, std::min(ceil_div(std::max(m, r), 256), 148));
+    k_prep<<<pb, 256, 0, s>>>(m, r, theta.p, d.p, alpha_dev.p, sigma2, wsq.p, sqd.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    gemv_t(m, m, P.p, m, z.p, 1.0, 0.0, rt.p, s);  // r̃ = Pᵀ(y − H·mean)
+    mark("rotate_in");
+    if (r > 0) {
+        launch_gemv_cols(m, r, E.p, m, XProd{wsq.p, rt.p}, EpiScaleOut{ucap.p, sqd.p}, s);
+        GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½ (lower tiles)
+        g.M = r; g.N = r; g.K = m;
+        g.A = E.p; g.lda = m; g.transA = 1;
+        g.B = E.p; g.ldb = m;
+        g.dA = wsq.p;
+        g.rs = sqd.p; g.cs = sqd.p;
+        g.alpha = -1.0;
+        g.C = Kcap.p; g.ldc = r;
+        g.diag_add = 1.0;
+        g.lower_only = 1;
+        g.splitk = gemm_pick_splitk(r, r, m);
+        gemm(g, ws_step.p, s);
+        mark("capacitance");
+        chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s);  // x = K⁻¹u
+        mark("cap_factor_solve");
+    }
+    launch_gemv_rows(m, r, E.p, m, XProd{sqd.p, ucap.p}, EpiWoodbury{st.p, wsq.p, rt.p}, s);
+    gemv_n(m, m, P.p, m, st.p, 1.0, 0.0, z.p, s);  // z = P·s̃
+    mark("rotate_out");
+}
+
+// z ← S⁻¹z forming S = α·G − B·diag(d)·Bᵀ + σ²I and its LLT, as fast_filter.hpp:100-108.
+void Filter::enqueue_solve_dense() {
     GemmArgs g;
     g.M = m; g.N = m; g.K = r;
     g.A = B.p; g.lda = m; g.transA = 0;
@@ -361,22 +508,11 @@ void Filter::enqueue_step(const double* d_y) {
     g.diag_add = sigma2;
     g.lower_only = 1;
     gemm(g, nullptr, s);
+    mark("innovation_build");
     potrf_lower(m, S.p, m, info.p, nullptr, 0, s);  // LLT (:104-106)
-    // z = S⁻¹ (y − H·mean) (:108)
-    FKB_CUDA(cudaMemcpyAsync(z.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
-    spmm(H, mean.p, n, 1, z.p, m, -1.0, 1.0, s);
-    potrs_lower(m, S.p, m, z.p, flags.p, s);
-    // t = Γ(Hᵀz) = (ΓHᵀ)z ; c = Bᵀz
-    spmm(HT, z.p, m, 1, t.p, n, 1.0, 0.0, s);
-    cov->apply(t.p, n, 1, t.p, n);
-    if (r > 0) gemv_t(m, r, B.p, m, z.p, 1.0, 0.0, cvec.p, s);
-    const int blocks = std::min(ceil_div(n, 256), 148 * 4);
-    k_mean_update<<<blocks, 256, sizeof(double) * size_t(std::max(r, 1)), s>>>(n, r, U.p, d.p, cvec.p, t.p,
-                                                                            alpha_dev.p, mean.p, info.p);
-    FKB_LAUNCH_CHECK();
-    k_d_update<<<std::max(1, ceil_div(r, 256)), 256, 0, s>>>(r, d.p, lambda.p, alpha_dev.p, info.p);
-    FKB_LAUNCH_CHECK();
-    count_launch(2);
+    mark("llt");
+    potrs_lower(m, S.p, m, z.p, flags.p, s);         // z = S⁻¹(y − H·mean) (:108)
+    mark("llt_solve");
 }
 
 void Filter::check_info() {

@@ -1,6 +1,8 @@
 // filter.cuh — the constant-H fast filter on the device (fkf_init / fkf_step / UQ).
 #pragma once
 
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "cov.cuh"
@@ -30,8 +32,16 @@ struct Filter {
     int state_rank = 0;
     DBuf<double> alpha_dev, d, mean;
 
+    // Woodbury form of the innovation solve (solver = 1, default): G = P·diag(θ)·Pᵀ and
+    // E = PᵀB precomputed once, so S(α,d)⁻¹ = P·[Λ_M − E·D·Eᵀ]⁻¹·Pᵀ with Λ_M = αθ + σ²
+    // needs only the k×k capacitance K = I − D^½EᵀΛ_M⁻¹ED^½ per step.
+    // solver = 0 reproduces the reference order: form S and LLT it (m×m) every step.
+    int solver = 1;
+    int eig_sweeps = 0;
+    DBuf<double> P, theta, E, wsq, sqd, rt, ucap, Kcap, st, rdg;
+
     // step workspaces
-    DBuf<double> S, z, t, cvec, ws;
+    DBuf<double> S, z, t, cvec, ws, ws_step;
     DBuf<int> info, flags;
     cudaGraphExec_t graph = nullptr;
     bool graph_ready = false;
@@ -56,6 +66,14 @@ struct Filter {
     void steps_async(const double* d_ys, int nsteps, long long ldy);
     void finish_async(int nsteps);
     void enqueue_step(const double* d_y);                // kernels only, no host sync
+    void enqueue_solve_dense();                          // z ← S⁻¹z, reference order (solver 0)
+    void enqueue_solve_woodbury();                       // z ← S⁻¹z via G's eigenbasis (solver 1)
+    void set_solver(int mode);
+    // Un-graphed steps with CUDA events at phase boundaries: average ms per phase.
+    std::vector<std::pair<std::string, double>> phase_times(int reps);
+    std::vector<cudaEvent_t>* phase_events = nullptr;
+    std::vector<std::string> phase_names;
+    void mark(const char* name);
     void launch_step();                                  // graph replay of enqueue_step(ybuf)
     void check_info();                                   // throws on a singular innovation system
     void reset();                                        // zero_start (:30-36)

@@ -352,6 +352,28 @@ class FkfContext:
     def launches_per_step(self):
         return int(lib().fkb_filter_launches_per_step(self._f))
 
+    def set_solver(self, mode: int):
+        """1 (default): Woodbury solve in G's eigenbasis; 0: reference-order m×m LLT."""
+        check(lib().fkb_filter_set_solver(self._f, int(mode)))
+
+    def eig_sweeps(self) -> int:
+        return int(lib().fkb_filter_eig_sweeps(self._f))
+
+    def g_eig(self):
+        th = np.empty(max(self.m, 1))
+        Pm = np.empty(max(self.m * self.m, 1))
+        check(lib().fkb_filter_get_eig(self._f, ptr(th), ptr(Pm)))
+        return th[: self.m], Pm[: self.m * self.m].reshape(self.m, self.m).T
+
+    def phase_times(self, reps: int = 3):
+        """Runs `reps` real steps (advancing the state) with CUDA events per phase."""
+        ms = np.zeros(32)
+        names = C.create_string_buffer(1024)
+        cnt = C.c_int()
+        check(lib().fkb_filter_phase_times(self._f, int(reps), ms, names, 1024, C.byref(cnt)))
+        keys = names.value.decode().split(",") if cnt.value else []
+        return dict(zip(keys, ms[: cnt.value].tolist()))
+
 
 def fkf_init(cov, h, sigma2, k_rank, p_oversample, seed) -> FkfContext:
     return FkfContext(cov, h, sigma2, k_rank, p_oversample, seed)

@@ -114,12 +114,38 @@ def test_rank_zero_uq():  # test_uq.cpp:46-58
     assert ctx.relative_entropy() == 0.0
 
 
-def _run_both(name, steps, uq=False, realizations=0):
+def test_offline_eigendecomposition_of_g():
+    """G = HΓHᵀ = P·diag(θ)·Pᵀ with P orthogonal (block Jacobi, eig.cu)."""
+    p = Problem(20, 20, 4, 6, 1, 2e-4)
+    ctx = P.fkf_init(P.CovarianceOperator(p.grid, p.spec()), p.h, p.sigma2, 24, 20, 5)
+    th, Pm = ctx.g_eig()
+    G = ctx.h_gamma_ht()
+    assert np.linalg.norm(Pm.T @ Pm - np.eye(p.h.rows)) < 1e-13
+    assert np.linalg.norm(Pm @ np.diag(th) @ Pm.T - G) < 1e-14 * np.linalg.norm(G)
+    assert np.allclose(np.sort(th), np.linalg.eigvalsh(G), rtol=1e-12, atol=1e-15 * np.abs(th).max())
+
+
+@pytest.mark.parametrize("solver", [0, 1])
+def test_solvers_agree_on_desk_problem(solver):
+    p = Problem(12, 12, 3, 8, 6, 2e-4)
+    ctx = P.fkf_init(P.CovarianceOperator(p.grid, p.spec()), p.h, p.sigma2, 16, 20, 3)
+    ctx.set_solver(solver)
+    of = O.FastFilter(p.oracle_cov(), p.oracle_h(), p.sigma2, 16, 20, 3)
+    for y in p.obs:
+        st = P.fkf_step(ctx, y)
+        of.step(y)
+        so = of.state()
+        assert rel_err(st["mean"], so["mean"]) < TOL
+        assert np.max(np.abs(st["d"] - so["d"])) / so["alpha"] < TOL
+
+
+def _run_both(name, steps, uq=False, realizations=0, solver=1):
     w, h, ys, s2 = workload_inputs(name, steps)
     kern = dict(family=1, theta=w.theta, length=w.length, nu=w.nu)
     k, p = w.ghep_sizes()
     cov = P.CovarianceOperator(P.Grid(w.n, w.n), P.KernelSpec(**kern))
     ctx = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    ctx.set_solver(solver)
     ocov = O.CovarianceOperator(w.n, w.n, **kern)
     oh = O.Csr.from_arrays(h.rows, h.cols, h.rowptr, h.col, h.val)
     of = O.FastFilter(ocov, oh, s2, k, p, w.ghep_seed)
@@ -144,8 +170,9 @@ def _run_both(name, steps, uq=False, realizations=0):
     return worst
 
 
-def test_c0_parity_all_steps():
-    worst = _run_both("c0", None, uq=True, realizations=2)
+@pytest.mark.parametrize("solver", [0, 1])
+def test_c0_parity_all_steps(solver):
+    worst = _run_both("c0", None, uq=True, realizations=2, solver=solver)
     assert worst["mean"] < TOL, worst
     assert worst["d"] < TOL, worst
     assert worst["var"] < TOL, worst
