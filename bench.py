@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py — fast Kalman filter hot path (arXiv 1405.2276, reference `fastkf`) on B200.
+
+One timed "step" is one fkf_step (fast_filter.hpp:84-125) of the constant-H filter on the
+BASELINE.json configuration c2 (N = 256², m = 2048, rank cap 300): innovation solve,
+mean update through Γ(Hᵀz) and the SMW update of α and D, for one observation vector
+already resident in HBM.  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+--impl reference times the reference algorithm on the host cores: the CPU restatement in
+oracle/ (the reference C++ needs Eigen3+FFTW3, absent here and on the box).
+Multi-GPU (torchrun): the per-step filter does not shard, so each rank runs
+an independent replica ("replicas only"), timed on the device, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BASELINE_METRIC = "filter steps/s at N=256²; Γ·X FP64 TFLOP/s and SpMM HBM GB/s vs B200 peak"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps timed for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.path = tempfile.mktemp(prefix="fkb_clocks_", suffix=".csv")
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines() if l.strip()]
+        except Exception:
+            return out
+        sm = []
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                out["sm_max_mhz"] = float(r[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if sm:
+            out["sm_mhz"] = statistics.median(sm)
+        out["reasons"] = sorted(reasons)
+        out["samples"] = len(sm)
+        return out
+
+
+# ----------------------------------------------------------------------------- work accounting
+def phase_work(w, r, fft_flops):
+    """Algorithmic work per launch of each step phase."""
+    N, m = w.N, w.m
+    nnz = w.m * (2.5 * w.n)  # overwritten by the caller with the true nnz
+    return {
+        "residual": ("hbm", None),
+        "rotate_in": ("hbm", 8.0 * m * m + 16.0 * m),
+        "capacitance": ("tensor", 2.0 * m * r * r),
+        "cap_factor_solve": ("tensor", r ** 3 / 3.0 + 2.0 * r * r),
+        "rotate_out": ("hbm", 8.0 * m * m + 8.0 * m * r + 32.0 * m),
+        "gamma_ht_z": ("tensor", fft_flops),
+        "mean_update": ("hbm", 8.0 * N * r + 32.0 * N),
+        "d_update": ("hbm", 32.0 * r),
+        "_nnz": nnz,
+    }
+
+
+def gamma_x_flops(w, mx, my):
+    """Pruned-R2C '5 n log2 n' count per column."""
+    nx = w.n
+    return (5 * nx * my * math.log2(my) + 10 * (my // 2 + 1) * mx * math.log2(mx) + 2 * mx * (my // 2 + 1))
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    from paper_1405_2276_b200 import workloads as W
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    w = W.CONFIGS[args.config]
+    blocks = W.layout_points(w)
+    hs = [O.build_H(w.n, w.n, s, r) for s, r in blocks]
+    arrs = [h.arrays() for h in hs]
+    rp = arrs[0][0]
+    for a in arrs[1:]:
+        rp = np.concatenate([rp, a[0][1:] + rp[-1]])
+    col = np.concatenate([a[1] for a in arrs])
+    val = np.concatenate([a[2] for a in arrs])
+    (rp, col, val), ys, s2 = W.make_inputs(w, (rp, col, val))
+    cov = O.CovarianceOperator(w.n, w.n, family=1, theta=w.theta, length=w.length, nu=w.nu)
+    H = O.Csr.from_arrays(w.m, w.N, rp, col, val)
+    k, p = w.ghep_sizes()
+    t0 = time.perf_counter()
+    f = O.FastFilter(cov, H, s2, k, p, w.ghep_seed)
+    offline = time.perf_counter() - t0
+    for i in range(args.warmup):
+        f.step(ys[i % len(ys)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        f.step(ys[(args.warmup + i) % len(ys)])
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    sample = (f"{args.steps} oracle fkf_step on {args.config} after {args.warmup} warm-up steps "
+              f"(oracle fkf_init {offline:.1f}s untimed), {threads} OpenMP threads")
+    return {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": k,
+                   "parallelism": "host cores"},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "offline_s": offline,
+    }
+
+
+def cpu_baseline(args, w, h, ys, s2):
+    """Single-thread oracle (the reference is single-threaded) on the same inputs."""
+    from oracle import oracle as O
+    O.set_threads(os.cpu_count() or 1)  # setup parallel (untimed)
+    cov = O.CovarianceOperator(w.n, w.n, family=1, theta=w.theta, length=w.length, nu=w.nu)
+    H = O.Csr.from_arrays(h.rows, h.cols, h.rowptr, h.col, h.val)
+    k, p = w.ghep_sizes()
+    t0 = time.perf_counter()
+    f = O.FastFilter(cov, H, s2, k, p, w.ghep_seed)
+    init_s = time.perf_counter() - t0
+    O.set_threads(1)
+    f.step(ys[0])
+    n = max(1, args.cpu_steps)
+    t0 = time.perf_counter()
+    for i in range(n):
+        f.step(ys[(1 + i) % len(ys)])
+    dt = time.perf_counter() - t0
+    O.set_threads(os.cpu_count() or 1)
+    return {"value": n / dt, "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": f"{n} oracle fkf_step on {args.config} (1 thread) after 1 warm step; oracle fkf_init "
+                      f"{init_s:.1f}s with {os.cpu_count()} threads, untimed"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1405_2276_b200 as P
+    from paper_1405_2276_b200 import workloads as W
+    from paper_1405_2276_b200._native import DeviceArray, check, lib
+
+    torch.cuda.set_device(local_rank)
+    check(lib().fkb_set_device(local_rank))
+    L = lib()
+    w, h, ys, s2 = W.problem(args.config)
+    k, p = w.ghep_sizes()
+    S = len(ys)
+
+    # ---- offline stage (CovarianceOperator + fkf_init), untimed for the step metric
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), W.kernel_spec(w))
+    ctx = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    check(L.fkb_dsync())
+    offline_s = time.perf_counter() - t0
+    r = ctx.rank()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    dys = DeviceArray.from_host(np.stack(ys).ravel())
+    yptr = lambda i: C.c_void_p(dys.ptr.value + 8 * w.m * (i % S))  # noqa: E731
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local_rank}")  # 256 MiB > L2
+
+    # ---- warm-up
+    for i in range(args.warmup):
+        ctx.steps_async(yptr(i), 1, w.m)
+    ctx.sync(args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, CUDA events on the library stream, L2 flushed between steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = int(L.fkb_launch_count())
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            evs[i][0].record(stream)
+            ctx.steps_async(yptr(args.warmup + i), 1, w.m)
+            evs[i][1].record(stream)
+            with torch.cuda.stream(stream):
+                flush.zero_()
+        torch.cuda.synchronize()
+        ctx.sync(args.steps)
+    launches = int(L.fkb_launch_count()) - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    value = world * args.steps / (total_ms / 1e3)
+
+    # ---- per-phase device timing (real steps, un-graphed, events at phase boundaries)
+    phases = ctx.phase_times(5)
+
+    # ---- end-to-end through the public API with host buffers
+    ctx.reset()
+    pin_y = torch.empty((S, w.m), dtype=torch.float64).pin_memory()
+    pin_y.numpy()[:] = np.stack(ys)
+    pin_mean = torch.empty(w.N, dtype=torch.float64).pin_memory()
+    pin_d = torch.empty(max(r, 1), dtype=torch.float64).pin_memory()
+    a_ = C.c_double()
+    st_ = C.c_int()
+    rk_ = C.c_int()
+    for i in range(args.warmup):
+        check(L.fkb_fkf_step(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        check(L.fkb_fkf_step(ctx._f, C.c_void_p(pin_y[(args.warmup + i) % S].data_ptr()), w.m))
+        check(L.fkb_filter_state(ctx._f, C.byref(a_), C.byref(st_), C.byref(rk_), C.c_void_p(pin_d.data_ptr()),
+                                 C.c_void_p(pin_mean.data_ptr())))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": 8 * w.m,
+           "d2h_bytes_per_step": 8 * (w.N + r) + 8 + 4 + 4}
+
+    # ---- offline kernels: Γ·X on the m + l offline columns, H·X SpMM with l columns
+    ncols = w.m + k + p
+    X = torch.randn(ncols, w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
+    Y = torch.empty_like(X)
+    cov.apply_device(C.c_void_p(X.data_ptr()), w.N, ncols, C.c_void_p(Y.data_ptr()), w.N)
+    torch.cuda.synchronize()
+    ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ga.record(torch.cuda.ExternalStream(cov.stream))
+    reps = 3
+    for _ in range(reps):
+        cov.apply_device(C.c_void_p(X.data_ptr()), w.N, ncols, C.c_void_p(Y.data_ptr()), w.N)
+    gb.record(torch.cuda.ExternalStream(cov.stream))
+    torch.cuda.synchronize()
+    gx_ms = ga.elapsed_time(gb) / reps
+    fcol = gamma_x_flops(w, cov.mx, cov.my)
+    fp64_dmma = C.c_double()
+    fp64_dfma = C.c_double()
+    check(L.fkb_fp64_peak(1, C.byref(fp64_dmma)))
+    check(L.fkb_fp64_peak(0, C.byref(fp64_dfma)))
+    fp64_peak = max(fp64_dmma.value, fp64_dfma.value)
+    gx_tf = fcol * ncols / (gx_ms * 1e-3) / 1e12
+    l = k + p
+    Z = torch.empty(l, w.m, dtype=torch.float64, device=f"cuda:{local_rank}")
+    ctx.spmm_device(0, C.c_void_p(X.data_ptr()), w.N, l, C.c_void_p(Z.data_ptr()), w.m)
+    torch.cuda.synchronize()
+    ga.record(stream)
+    for _ in range(reps):
+        ctx.spmm_device(0, C.c_void_p(X.data_ptr()), w.N, l, C.c_void_p(Z.data_ptr()), w.m)
+    gb.record(stream)
+    torch.cuda.synchronize()
+    sp_ms = ga.elapsed_time(gb) / reps
+    sp_bytes = 12 * h.nnz + 4 * (h.rows + 1) + 8 * (w.N + w.m) * l
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    # ---- roofline of the dominant step phase
+    work = phase_work(w, r, fcol)
+    work["residual"] = ("hbm", 12.0 * h.nnz + 4.0 * (h.rows + 1) + 8.0 * (w.N + 2 * w.m))
+    dom = max((kk for kk in phases if kk in work), key=lambda kk: phases[kk])
+    bound, amount = work[dom]
+    dom_ms = phases[dom]
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    if bound == "hbm":
+        ach = amount / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                "kernel": dom, "algorithmic_per_launch": amount, "launch_ms": dom_ms,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
+    else:
+        ach = amount / (dom_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                "traffic": traffic, "kernel": dom, "algorithmic_per_launch": amount, "launch_ms": dom_ms,
+                "peak_source": "FP64 DMMA/DFMA peak measured in-run by fkb_fp64_peak (MEASURED_PEAKS.json has no FP64)"}
+
+    out = {
+        "metric": BASELINE_METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": r,
+                   "torus": f"{cov.mx}x{cov.my}", "nnz_H": int(h.nnz), "solver": "woodbury-eig",
+                   "l2": "flushed between timed steps (256 MiB write on the filter stream)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roof,
+        "phases_ms": phases,
+        "gamma_x": {"tflops": gx_tf, "frac": gx_tf / fp64_peak, "columns": ncols, "ms": gx_ms,
+                    "flops_per_column": fcol, "peak_tflops": fp64_peak},
+        "spmm": {"gbs": sp_bytes / (sp_ms * 1e-3) / 1e9, "frac": sp_bytes / (sp_ms * 1e-3) / 1e9 / hbm,
+                 "columns": l, "us": sp_ms * 1e3, "bytes": sp_bytes},
+        "fp64_peak_tflops": {"dmma": fp64_dmma.value, "dfma": fp64_dfma.value},
+        "offline_s": offline_s,
+        "eig_sweeps": ctx.eig_sweeps(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, w, h, ys, s2)
+    return out
+
+
+def main():
+    args = parse()
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

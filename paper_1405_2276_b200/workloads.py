@@ -235,3 +235,20 @@ def make_inputs(w: Workload, H, steps: int | None = None):
         val = val / sd[rows]
         ys = [y / sd for y in ys]
     return (rowptr.astype(np.int32), col.astype(np.int32), val.astype(np.float64)), ys, w.sigma2
+
+
+def problem(name: str, steps: int | None = None):
+    """(workload, H (CsrMatrix, whitened for c3), observations, σ²) built with the product's
+    host-side build_H (tomography.hpp:130-146)."""
+    from . import fastkf as P
+    w = CONFIGS[name]
+    g = P.Grid(w.n, w.n)
+    hs = [P.build_H(g, P.SourceReceiverLayout(s, r)) for s, r in layout_points(w)]
+    h = P.CsrMatrix.vstack(hs) if len(hs) > 1 else hs[0]
+    (rp, col, val), ys, s2 = make_inputs(w, (h.rowptr, h.col, h.val), steps)
+    return w, P.CsrMatrix(h.rows, h.cols, rp, col, val), ys, s2
+
+
+def kernel_spec(w: Workload):
+    from . import fastkf as P
+    return P.KernelSpec(family=P.MATERN, theta=w.theta, length=w.length, nu=w.nu)

@@ -133,10 +133,4 @@ def csr_dense(h):
 
 def workload_inputs(name, steps=None):
     """BASELINE config inputs: (workload, H CsrMatrix (whitened for c3), ys, sigma2)."""
-    import paper_1405_2276_b200 as P
-    w = W.CONFIGS[name]
-    g = P.Grid(w.n, w.n)
-    hs = [P.build_H(g, P.SourceReceiverLayout(s, r)) for s, r in W.layout_points(w)]
-    h = P.CsrMatrix.vstack(hs) if len(hs) > 1 else hs[0]
-    (rp, col, val), ys, s2 = W.make_inputs(w, (h.rowptr, h.col, h.val), steps)
-    return w, P.CsrMatrix(h.rows, h.cols, rp, col, val), ys, s2
+    return W.problem(name, steps)
