@@ -110,6 +110,23 @@ class ClockSampler:
         return out
 
 
+# ----------------------------------------------------------------------------- replicas
+def max_over_ranks(local_ms: float, device) -> float:
+    """Device-timed milliseconds → max over all ranks (NCCL on GPUs, gloo in CPU tests)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(local_ms)
+    t = torch.tensor([float(local_ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(local_ms: float, steps: int, world: int, device) -> float:
+    """Whole-job steps/s of `world` independent replicas: world·steps / max-over-ranks time."""
+    return world * steps / (max_over_ranks(local_ms, device) / 1e3)
+
+
 # ----------------------------------------------------------------------------- work accounting
 def phase_work(w, r, fft_flops):
     """Algorithmic work per launch of each step phase."""
@@ -254,13 +271,10 @@ def run_ours(args, rank, world, local_rank):
         ctx.sync(args.steps)
     launches = int(L.fkb_launch_count()) - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
+    total_ms = max_over_ranks(float(sum(step_ms)), f"cuda:{local_rank}")
+    value = replica_throughput(total_ms, args.steps, world, f"cuda:{local_rank}")
     if world > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
-    value = world * args.steps / (total_ms / 1e3)
 
     # ---- per-phase device timing (real steps, un-graphed, events at phase boundaries)
     phases = ctx.phase_times(5)
@@ -285,11 +299,7 @@ def run_ours(args, rank, world, local_rank):
                                  C.c_void_p(pin_mean.data_ptr())))
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), f"cuda:{local_rank}")
     e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": 8 * w.m,
            "d2h_bytes_per_step": 8 * (w.N + r) + 8 + 4 + 4}
 
