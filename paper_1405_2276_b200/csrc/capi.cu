@@ -359,6 +359,21 @@ int fkb_filter_set_solver(fkb_filter* f, int mode) {
     });
 }
 int fkb_filter_eig_sweeps(fkb_filter* f) { return f ? f->f->eig_sweeps : 0; }
+int fkb_filter_cap_stats(fkb_filter* f, int* iterations, int* fallback) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        double it = 0.0;
+        int fb = 0;
+        if (F.r > 0 && F.solver == 1) {
+            FKB_CUDA(cudaMemcpyAsync(&it, F.pcgwork.p + F.r, sizeof(double), cudaMemcpyDeviceToHost, F.s));
+            FKB_CUDA(cudaMemcpyAsync(&fb, F.pcgflag.p, sizeof(int), cudaMemcpyDeviceToHost, F.s));
+            FKB_CUDA(cudaStreamSynchronize(F.s));
+        }
+        if (iterations) *iterations = int(it);
+        if (fallback) *fallback = fb;
+    });
+}
 int fkb_filter_phase_times(fkb_filter* f, int reps, double* ms, char* names, int names_len, int* nphases) {
     return guarded([&] {
         need(f, "filter");

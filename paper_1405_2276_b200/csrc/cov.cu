@@ -389,18 +389,23 @@ std::vector<double> Cov::spectrum_host() const {
 void Cov::apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy) {
     if (ncols <= 0) return;
     ++applies;
-    const int pairs = pairs_for(my), kt = kt_for(mx);
+    // Few columns (the per-step Γ(Hᵀz)): one transform per CTA and narrow CTAs so the three
+    // passes still spread over the SMs; wide blocks of columns keep the batched shapes.
+    const bool narrow = ncols < 8;
+    const int pairs = narrow ? 1 : pairs_for(my), kt = narrow ? 1 : kt_for(mx);
+    const int tA = narrow ? std::max(64, std::min(kThreads, my / 4)) : kThreads;
+    const int tB = narrow ? std::max(64, std::min(kThreads, mx / 4)) : kThreads;
     const long long ldw = (long long)nky * nx;
     const double scale = 1.0 / double(M());
     for (int c0 = 0; c0 < ncols; c0 += batch_cap) {
         const int bc = std::min(batch_cap, ncols - c0);
-        k_rows_fwd<<<dim3(ceil_div(nx, 2 * pairs), bc), kThreads, smem_bytes(pairs, my), stream>>>(
+        k_rows_fwd<<<dim3(ceil_div(nx, 2 * pairs), bc), tA, smem_bytes(pairs, my), stream>>>(
             dX + (long long)c0 * ldx, ldx, nx, ny, nx, fy, work.p, ldw, pairs);
         FKB_LAUNCH_CHECK();
-        k_cols<<<dim3(ceil_div(nky, kt), bc), kThreads, smem_bytes(kt, mx), stream>>>(work.p, ldw, nx, fx, nky,
-                                                                                     spec_half.p, kt, 0);
+        k_cols<<<dim3(ceil_div(nky, kt), bc), tB, smem_bytes(kt, mx), stream>>>(work.p, ldw, nx, fx, nky,
+                                                                               spec_half.p, kt, 0);
         FKB_LAUNCH_CHECK();
-        k_rows_inv<<<dim3(ceil_div(nx, 2 * pairs), bc), kThreads, smem_bytes(pairs, my), stream>>>(
+        k_rows_inv<<<dim3(ceil_div(nx, 2 * pairs), bc), tA, smem_bytes(pairs, my), stream>>>(
             work.p, ldw, nx, ny, fy, dY + (long long)c0 * ldy, ldy, pairs, scale);
         FKB_LAUNCH_CHECK();
         count_launch(3);

@@ -21,6 +21,7 @@
 #include "gemv.cuh"
 #include "host_linalg.h"
 #include "smallchol.cuh"
+#include "cappcg.cuh"
 
 namespace fkb {
 
@@ -359,6 +360,9 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     ucap.alloc(size_t(std::max(r, 1)));
     Kcap.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
     rdg.alloc(std::max<size_t>(chol_solve_scratch(r), 1));
+    gpart.alloc(size_t(592) * 32 + size_t(std::max(m, 1)) + 64);  // split-GEMV partials
+    pcgwork.alloc(size_t(std::max(r, 1)) + 1);
+    pcgflag.alloc(1);
     {
         GemmArgs g;  // split-K workspace of the capacitance Gram
         g.M = r; g.N = r; g.K = m;
@@ -481,15 +485,18 @@ void Filter::enqueue_solve_woodbury() {
         g.alpha = -1.0;
         g.C = Kcap.p; g.ldc = r;
         g.diag_add = 1.0;
-        g.lower_only = 1;
+        g.lower_only = 0;  // full K: the PCG reads columns
         g.splitk = gemm_pick_splitk(r, r, m);
         gemm(g, ws_step.p, s);
         mark("capacitance");
-        chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s);  // x = K⁻¹u
-        mark("cap_factor_solve");
+        // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
+        FKB_CUDA(cudaMemsetAsync(pcgflag.p, 0, sizeof(int), s));
+        cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s);
+        chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
+        mark("cap_solve");
     }
-    launch_gemv_rows(m, r, E.p, m, XProd{sqd.p, ucap.p}, EpiWoodbury{st.p, wsq.p, rt.p}, s);
-    gemv_n(m, m, P.p, m, st.p, 1.0, 0.0, z.p, s);  // z = P·s̃
+    launch_gemv_rows(m, r, E.p, m, XProd{sqd.p, ucap.p}, EpiWoodbury{st.p, wsq.p, rt.p}, s, gpart.p);
+    launch_gemv_rows(m, m, P.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s, gpart.p);  // z = P·s̃
     mark("rotate_out");
 }
 

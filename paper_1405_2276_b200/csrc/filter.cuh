@@ -38,7 +38,8 @@ struct Filter {
     // solver = 0 reproduces the reference order: form S and LLT it (m×m) every step.
     int solver = 1;
     int eig_sweeps = 0;
-    DBuf<double> P, theta, E, wsq, sqd, rt, ucap, Kcap, st, rdg;
+    DBuf<double> P, theta, E, wsq, sqd, rt, ucap, Kcap, st, rdg, gpart, pcgwork;
+    DBuf<int> pcgflag;  // 1 when the capacitance PCG fell back to the cluster Cholesky
 
     // step workspaces
     DBuf<double> S, z, t, cvec, ws, ws_step;

@@ -1,11 +1,12 @@
 // gemv.cuh — HBM-bound FP64 matrix–vector kernels with fused prologue/epilogue functors.
 //
-// k_gemv_rows: y = A·x for column-major A (m×k).  A CTA owns 32 rows; its 8 warps split the
-//   columns (stride 8) so each warp load is one coalesced 256-B row segment, four
-//   independent accumulators per lane keep loads in flight, and a fixed-order shared-memory
-//   reduction keeps results deterministic.  Grid = ⌈m/32⌉ CTAs (m = 2048 → 64 CTAs,
-//   N = 65536 → 2048 CTAs).
-// k_gemv_cols: y = Aᵀ·x, one warp per column, lanes stride the rows, 4 accumulators.
+// k_gemv_rows: y = A·x for column-major A (m×k).  A CTA owns 32 rows and a chunk of
+//   columns; its 8 warps split the chunk (stride 8) so each warp load is one coalesced
+//   256-B row segment, and 8 independent accumulators per lane keep 8 loads in flight.
+//   When ⌈m/32⌉ CTAs cannot fill the GPU (m×m rotations with m = 2048 → 64 CTAs) the
+//   columns are split over S CTAs and a second kernel reduces the partials in a fixed
+//   order (deterministic), then applies the epilogue.
+// k_gemv_cols: y = Aᵀ·x, one warp per column, lanes stride the rows, 8 loads in flight.
 #pragma once
 
 #include "common.cuh"
@@ -28,32 +29,46 @@ struct EpiAxpby {  // y_i = α·v + β·y_i
         y[i] = beta == 0.0 ? alpha * v : alpha * v + beta * y[i];
     }
 };
+struct EpiStore {  // partial sums
+    double* p;
+    __device__ __forceinline__ void operator()(long long i, double v) const { p[i] = v; }
+};
 
 template <class XL, class Epi>
 __global__ void __launch_bounds__(256) k_gemv_rows(long long m, int k, const double* __restrict__ A, long long lda,
-                                                  XL xl, Epi epi) {
+                                                  XL xl, Epi epi, int kchunk, long long pstride) {
     __shared__ double red[8][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long row = blockIdx.x * 32LL + lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int c0 = blockIdx.y * kchunk, c1 = min(k, c0 + kchunk);
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = 0.0;
     if (row < m) {
         const double* Ar = A + row;
-        int c = w;
-        for (; c + 24 < k; c += 32) {
-            a0 = fma(Ar[(long long)c * lda], xl(c), a0);
-            a1 = fma(Ar[(long long)(c + 8) * lda], xl(c + 8), a1);
-            a2 = fma(Ar[(long long)(c + 16) * lda], xl(c + 16), a2);
-            a3 = fma(Ar[(long long)(c + 24) * lda], xl(c + 24), a3);
+        int c = c0 + w;
+        for (; c + 56 < c1; c += 64) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] = fma(Ar[(long long)(c + 8 * q) * lda], xl(c + 8 * q), a[q]);
         }
-        for (; c < k; c += 8) a0 = fma(Ar[(long long)c * lda], xl(c), a0);
+        for (; c < c1; c += 8) a[0] = fma(Ar[(long long)c * lda], xl(c), a[0]);
     }
-    red[w][lane] = (a0 + a1) + (a2 + a3);
+    red[w][lane] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     __syncthreads();
     if (w == 0 && row < m) {
         double v = red[0][lane];
 #pragma unroll
         for (int q = 1; q < 8; ++q) v += red[q][lane];
-        epi(row, v);
+        epi(row + blockIdx.y * pstride, v);
+    }
+}
+
+template <class Epi>
+__global__ void k_gemv_rows_reduce(long long m, int S, const double* __restrict__ part, Epi epi) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int s = 0; s < S; ++s) v += part[i + s * m];
+        epi(i, v);
     }
 }
 
@@ -64,26 +79,46 @@ __global__ void __launch_bounds__(256) k_gemv_cols(long long n, int k, const dou
     const long long col = blockIdx.x * 8LL + (threadIdx.x >> 5);
     if (col >= k) return;
     const double* a = A + col * lda;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = 0.0;
     long long i = lane;
-    for (; i + 96 < n; i += 128) {
-        s0 = fma(a[i], xl(i), s0);
-        s1 = fma(a[i + 32], xl(i + 32), s1);
-        s2 = fma(a[i + 64], xl(i + 64), s2);
-        s3 = fma(a[i + 96], xl(i + 96), s3);
+    for (; i + 224 < n; i += 256) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] = fma(a[i + 32 * q], xl(i + 32 * q), s[q]);
     }
-    for (; i < n; i += 32) s0 = fma(a[i], xl(i), s0);
-    double s = (s0 + s1) + (s2 + s3);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (lane == 0) epi(col, s);
+    for (; i < n; i += 32) s[0] = fma(a[i], xl(i), s[0]);
+    double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (lane == 0) epi(col, t);
+}
+
+// Column splits so that the launch covers ≥ ~4 CTAs per SM; part needs S·m doubles.
+inline int gemv_rows_splits(long long m, int k) {
+    const long long tiles = (m + 31) / 32;
+    if (tiles >= 592 || k < 256) return 1;
+    return int(std::max<long long>(1, std::min<long long>((592 + tiles - 1) / tiles, k / 128)));
 }
 
 template <class XL, class Epi>
-inline void launch_gemv_rows(long long m, int k, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s) {
+inline void launch_gemv_rows(long long m, int k, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s,
+                             double* part = nullptr) {
     if (m <= 0) return;
-    k_gemv_rows<XL, Epi><<<(unsigned)((m + 31) / 32), 256, 0, s>>>(m, k, A, lda, xl, epi);
+    const unsigned tiles = (unsigned)((m + 31) / 32);
+    const int S = part ? gemv_rows_splits(m, k) : 1;
+    if (S == 1) {
+        k_gemv_rows<XL, Epi><<<tiles, 256, 0, s>>>(m, k, A, lda, xl, epi, std::max(k, 1), 0);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
+    const int kchunk = ((k + S - 1) / S + 7) / 8 * 8;
+    const int Sx = (k + kchunk - 1) / kchunk;
+    k_gemv_rows<XL, EpiStore><<<dim3(tiles, Sx), 256, 0, s>>>(m, k, A, lda, xl, EpiStore{part}, kchunk, m);
     FKB_LAUNCH_CHECK();
-    count_launch();
+    k_gemv_rows_reduce<Epi><<<(unsigned)std::min<long long>((m + 255) / 256, 1184), 256, 0, s>>>(m, Sx, part, epi);
+    FKB_LAUNCH_CHECK();
+    count_launch(2);
 }
 template <class XL, class Epi>
 inline void launch_gemv_cols(long long n, int k, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s) {

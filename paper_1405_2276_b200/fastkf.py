@@ -359,6 +359,12 @@ class FkfContext:
     def eig_sweeps(self) -> int:
         return int(lib().fkb_filter_eig_sweeps(self._f))
 
+    def cap_stats(self):
+        """(PCG iterations, Cholesky fallback used) of the last step's capacitance solve."""
+        it, fb = C.c_int(), C.c_int()
+        check(lib().fkb_filter_cap_stats(self._f, C.byref(it), C.byref(fb)))
+        return it.value, bool(fb.value)
+
     def g_eig(self):
         th = np.empty(max(self.m, 1))
         Pm = np.empty(max(self.m * self.m, 1))

@@ -27,7 +27,8 @@ for i in range(nsteps):
     ctx.steps_async(dys.ptr, 1, w.m)
 ctx.sync(nsteps)
 t3 = time.perf_counter()
-print(f"steps: {(t3-t)/nsteps*1e3:.3f} ms/step ({nsteps} steps, launches/step {ctx.launches_per_step()})", flush=True)
+print(f"steps: {(t3-t)/nsteps*1e3:.3f} ms/step ({nsteps} steps, launches/step {ctx.launches_per_step()}) "
+      f"cap PCG (iters, fallback) {ctx.cap_stats()}", flush=True)
 # Γ·X on m+l columns
 N = w.N; c = w.m + k + p
 X = DeviceArray.from_host(np.random.default_rng(0).standard_normal(N * c))

@@ -24,3 +24,4 @@ for j in range(T):
 print("total", prev - t0, "ns")
 cyc = int(st[159]) - int(st[158])
 print("SM clock during kernel: %.0f MHz" % (cyc / (prev - t0) * 1e3))
+print("initial diag factor (A0):", int(st[151]) - int(st[150]), "ns")
