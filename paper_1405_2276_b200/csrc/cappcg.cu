@@ -38,11 +38,12 @@ struct PcgShared {
 
 __device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, PcgShared& sh, int slot) {
     // every CTA has written sh.part[slot]; sum them in rank order (deterministic)
+    double v[PC_CL];
+#pragma unroll
+    for (int c = 0; c < PC_CL; ++c) v[c] = cl.map_shared_rank(&sh, c)->part[slot];  // all loads in flight
     double s = 0.0;
-    for (int c = 0; c < PC_CL; ++c) {
-        PcgShared* rs = cl.map_shared_rank(&sh, c);
-        s += rs->part[slot];
-    }
+#pragma unroll
+    for (int c = 0; c < PC_CL; ++c) s += v[c];
     return s;
 }
 
@@ -59,13 +60,31 @@ __device__ __forceinline__ void block_partial(PcgShared& sh, double v, int slot)
 
 __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, long long ld, int n,
                                                  double* __restrict__ u, double* __restrict__ work,
-                                                 int* __restrict__ fallback, int maxit, double tol) {
+                                                 int* __restrict__ fallback, int maxit, double tol, int kstage) {
     __shared__ PcgShared sh;
+    extern __shared__ double Ks[];  // this CTA's columns of K (rb × n) when kstage
     cg::cluster_group cl = cg::this_cluster();
     const int crank = int(cl.block_rank());
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rb = (n + PC_CL - 1) / PC_CL;
     const int r0 = crank * rb, r1 = min(n, r0 + rb);
+    if (kstage) {
+        const int cnt = (r1 - r0) * n;
+        for (int e0 = 0; e0 < cnt; e0 += 4 * PC_T) {
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = e0 + tid + q * PC_T;
+                v[q] = e < cnt ? K[(long long)(r0 + e / n) * ld + e % n] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = e0 + tid + q * PC_T;
+                if (e < cnt) Ks[e] = v[q];
+            }
+        }
+        __syncthreads();
+    }
     // per-row state lives in registers of the owning thread (rows r0 + tid, r0 + tid + 256, …)
     // rb ≤ 64 for n ≤ 1024 → one row per thread among the first rb threads
     const int row = r0 + tid;
@@ -95,16 +114,24 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     //   rewritten only after S3; each partial slot is rewritten only after every CTA has
     //   read it (slot 2 after S2 of the next iteration, slots 0/3 after S3).
     while (!done && it < maxit) {
-        for (int c = 0; c < PC_CL; ++c) {
-            if (c == crank) continue;
-            PcgShared* rs = cl.map_shared_rank(&sh, c);
-            const int c0 = c * rb, c1 = min(n, c0 + rb);
-            for (int i = c0 + tid; i < c1; i += PC_T) sh.p[i] = rs->p[i];
+        {  // gather remote p blocks: every thread issues its remote loads at once (one latency)
+            double v[PC_MAXN / PC_T];
+#pragma unroll
+            for (int q = 0; q < PC_MAXN / PC_T; ++q) {
+                const int i = tid + q * PC_T;
+                const int owner = i / rb;
+                v[q] = (i < n && owner != crank) ? cl.map_shared_rank(&sh, owner)->p[i] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < PC_MAXN / PC_T; ++q) {
+                const int i = tid + q * PC_T;
+                if (i < n && i / rb != crank) sh.p[i] = v[q];
+            }
         }
         __syncthreads();
-        // q_i = (K p)_i = Σ_j K_ji p_j (K symmetric: read column i, contiguous)
+        // q_i = (K p)_i = Σ_j K_ji p_j (K symmetric: column i, staged in shared memory)
         for (int i = r0 + warp; i < r1; i += PC_T / 32) {
-            const double* Kc = K + (long long)i * ld;
+            const double* Kc = kstage ? Ks + (long long)(i - r0) * n : K + (long long)i * ld;
             double s0 = 0.0, s1 = 0.0;
             int j = lane;
             for (; j + 32 < n; j += 64) {
@@ -156,14 +183,19 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
              double tol) {
     if (n <= 0) return;
     if (n > PC_MAXN) throw std::invalid_argument("cap_pcg: n exceeds 1024");
+    const int rb = (n + PC_CL - 1) / PC_CL;
+    const size_t stage = sizeof(double) * size_t(rb) * n;
+    const int kstage = stage <= 190 * 1024 ? 1 : 0;  // K columns resident in shared memory
     if (!g_pcg_attr) {
         FKB_CUDA(cudaFuncSetAttribute((const void*)k_cap_pcg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_cap_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      190 * 1024));
         g_pcg_attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(PC_CL, 1, 1);
     cfg.blockDim = dim3(PC_T, 1, 1);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = kstage ? stage : 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -172,7 +204,7 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg, K, ld, n, u, work, fallback, maxit, tol));
+    FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg, K, ld, n, u, work, fallback, maxit, tol, kstage));
     count_launch();
 }
 

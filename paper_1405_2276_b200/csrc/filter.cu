@@ -456,7 +456,7 @@ void Filter::enqueue_step(const double* d_y) {
     // t = Γ(Hᵀz) = (ΓHᵀ)z ; c = Bᵀz
     spmm(HT, z.p, m, 1, t.p, n, 1.0, 0.0, s);
     cov->apply(t.p, n, 1, t.p, n);
-    if (r > 0) gemv_t(m, r, B.p, m, z.p, 1.0, 0.0, cvec.p, s);
+    if (r > 0) launch_gemv_cols(m, r, B.p, m, XPlain{z.p}, EpiAxpby{cvec.p, 1.0, 0.0}, s, gpart.p);
     mark("gamma_ht_z");
     launch_gemv_rows(n, r, U.p, n, XProd{d.p, cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
     mark("mean_update");
@@ -472,10 +472,10 @@ void Filter::enqueue_solve_woodbury() {
     k_prep<<<pb, 256, 0, s>>>(m, r, theta.p, d.p, alpha_dev.p, sigma2, wsq.p, sqd.p);
     FKB_LAUNCH_CHECK();
     count_launch();
-    gemv_t(m, m, P.p, m, z.p, 1.0, 0.0, rt.p, s);  // r̃ = Pᵀ(y − H·mean)
+    launch_gemv_cols(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, gpart.p);  // r̃ = Pᵀ(y − H·mean)
     mark("rotate_in");
     if (r > 0) {
-        launch_gemv_cols(m, r, E.p, m, XProd{wsq.p, rt.p}, EpiScaleOut{ucap.p, sqd.p}, s);
+        launch_gemv_cols(m, r, E.p, m, XProd{wsq.p, rt.p}, EpiScaleOut{ucap.p, sqd.p}, s, gpart.p);
         GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½ (lower tiles)
         g.M = r; g.N = r; g.K = m;
         g.A = E.p; g.lda = m; g.transA = 1;

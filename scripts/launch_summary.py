@@ -9,7 +9,7 @@ tot = 0.0
 for r in rows[hdr_i + 1:]:
     if len(r) <= vi: continue
     v = float(r[vi].replace(",", "")); u = r[ui]
-    us = v / 1000.0 if u == "nsecond" else (v if u == "usecond" else v * 1000.0)
+    us = v / 1000.0 if u in ("ns", "nsecond") else (v if u in ("us", "usecond") else v * 1000.0)
     name = r[ki].split("(")[0]
     c, t = agg.get(name, (0, 0.0)); agg[name] = (c + 1, t + us); tot += us
 print(f"total {tot:.1f} us over {sum(c for c,_ in agg.values())} launches")
