@@ -147,7 +147,7 @@ __global__ void k_splitk_reduce(GemmArgs g, const double* __restrict__ partial) 
 
 int gemm_pick_splitk(int M, int N, int K) {
     const long long tiles = (long long)ceil_div(M, GBM) * ceil_div(N, GBN);
-    if (tiles >= 296 || K < 256) return 1;
+    if (tiles <= 0 || tiles >= 296 || K < 256) return 1;
     const long long want = (296 + tiles - 1) / tiles;
     return int(std::max<long long>(1, std::min<long long>(want, K / 128)));
 }
@@ -178,6 +178,141 @@ void gemm(const GemmArgs& g_in, double* ws, cudaStream_t s) {
         FKB_LAUNCH_CHECK();
         count_launch();
     }
+}
+
+// --------------------------------------------------------------------------- Gram C = Aᵀ·diag(w)·B
+// A (K×M) and B (K×N) column-major with k contiguous (Gram/capacitance shapes).  64×64 tiles,
+// BK = 32, 256 threads (2×4 warps, warp tile 32×16 = 4×2 DMMA 8×8), 16-byte cp.async into
+// k-contiguous shared rows (ld 36 doubles: conflict-free fragment loads), double buffered.
+// Split-K partials go to `partial` (reduced by k_splitk_reduce with the same epilogue).
+constexpr int QB = 64, QK = 32, QLD = 36, QT = 256;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid, const void* safe) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(valid ? src : safe), "r"(sz));
+}
+
+__global__ void __launch_bounds__(QT) k_gram(GemmArgs g, int kchunk, double* __restrict__ partial) {
+    extern __shared__ __align__(16) double qsm[];
+    double* As = qsm;                       // [2][QB][QLD]
+    double* Bs = qsm + 2 * QB * QLD;        // [2][QB][QLD]
+    const int i0 = blockIdx.x * QB, j0 = blockIdx.y * QB;
+    if (g.lower_only && j0 > i0 + QB - 1) return;
+    const int kbeg = blockIdx.z * kchunk, kend = min(g.K, kbeg + kchunk);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    auto load = [&](int st, int k0) {
+#pragma unroll
+        for (int q = 0; q < (QB * QK / 2) / QT; ++q) {  // 4 chunks of 2 doubles per operand
+            const int e = tid + q * QT;
+            const int row = e / (QK / 2), kc = (e % (QK / 2)) * 2;
+            const int gk = k0 + kc;
+            const int ga = i0 + row, gb = j0 + row;
+            const bool kv = gk + 1 < kend;  // K chunk edges are even (kchunk % QK == 0, K even checked)
+            cp_async16(As + (st * QB + row) * QLD + kc, g.A + gk + (long long)ga * g.lda, kv && ga < g.M, g.A);
+            cp_async16(Bs + (st * QB + row) * QLD + kc, g.B + gk + (long long)gb * g.ldb, kv && gb < g.N, g.B);
+        }
+        cp_async_commit();
+    };
+    const int nk = (kend - kbeg + QK - 1) / QK;
+    if (nk > 0) load(0, kbeg);
+    for (int it = 0; it < nk; ++it) {
+        const int st = it & 1;
+        if (it + 1 < nk) {
+            load(st ^ 1, kbeg + (it + 1) * QK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* Ab = As + st * QB * QLD;
+        const double* Bb = Bs + st * QB * QLD;
+#pragma unroll
+        for (int kk = 0; kk < QK; kk += 4) {
+            const int gk = kbeg + it * QK + kk + tq;
+            const double wk = (g.dA && gk < kend) ? __ldg(g.dA + gk) : 1.0;
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(wm + mi * 8 + gq) * QLD + kk + tq];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bb[(wn + ni * 8 + gq) * QLD + kk + tq] * wk;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+    const double beta = g.beta_ptr ? *g.beta_ptr : g.beta;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int i = i0 + wm + mi * 8 + gq;
+                const int j = j0 + wn + ni * 8 + tq * 2 + q;
+                if (i >= g.M || j >= g.N) continue;
+                if (partial) {
+                    partial[(long long)blockIdx.z * g.M * g.N + i + (long long)j * g.M] = acc[mi][ni][q];
+                } else {
+                    double v = acc[mi][ni][q];
+                    if (g.rs) v *= g.rs[i];
+                    if (g.cs) v *= g.cs[j];
+                    double out = g.alpha * v;
+                    if (beta != 0.0) out += beta * g.Cin[i + (long long)j * g.ldcin];
+                    if (i == j) out += g.diag_add;
+                    g.C[i + (long long)j * g.ldc] = out;
+                }
+            }
+}
+
+// C = epilogue(Aᵀ·diag(dA)·B) for k-contiguous A (K×M) and B (K×N); same GemmArgs semantics
+// as gemm() with transA = 1, transB = 0.  Requires K, lda, ldb even (16-byte chunks).
+void gram(const GemmArgs& g_in, double* ws, cudaStream_t s) {
+    GemmArgs g = g_in;
+    if (g.M <= 0 || g.N <= 0) return;
+    if (g.K <= 0 || (g.K & 1) || (g.lda & 1) || (g.ldb & 1) || g.transA != 1 || g.transB != 0) {
+        gemm(g, ws, s);  // shapes the 16-byte path cannot take: the general DMMA kernel
+        return;
+    }
+    if (!g.Cin) { g.Cin = g.C; g.ldcin = g.ldc; }
+    const long long tiles = (long long)ceil_div(g.M, QB) * ceil_div(g.N, QB);
+    int splitk = 1;
+    if (ws && tiles < 296) splitk = int(std::max<long long>(1, std::min<long long>((296 + tiles - 1) / tiles, g.K / 128)));
+    int kchunk = ((ceil_div(g.K, splitk) + QK - 1) / QK) * QK;
+    splitk = ceil_div(g.K, kchunk);
+    g.splitk = splitk;
+    const size_t smem = sizeof(double) * 4 * QB * QLD;
+    static bool attr = false;
+    if (!attr) {
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    k_gram<<<dim3(ceil_div(g.M, QB), ceil_div(g.N, QB), splitk), QT, smem, s>>>(g, kchunk, splitk > 1 ? ws : nullptr);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    if (splitk > 1) {
+        const long long total = (long long)g.M * g.N;
+        k_splitk_reduce<<<std::min<long long>(4096, (total + 255) / 256), 256, 0, s>>>(g, ws);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
+}
+
+size_t gram_ws_elems(int M, int N, int K) {
+    const long long tiles = (long long)ceil_div(M, QB) * ceil_div(N, QB);
+    if (tiles <= 0 || tiles >= 296) return 0;
+    const long long s = std::max<long long>(1, std::min<long long>((296 + tiles - 1) / tiles, K / 128));
+    return size_t(s + 1) * M * N;
 }
 
 // --------------------------------------------------------------------------- GEMV

@@ -34,6 +34,10 @@ struct GemmArgs {
     int splitk = 1;
 };
 size_t gemm_ws_elems(const GemmArgs& g);
+// Gram-shaped product (transA = 1, transB = 0, k contiguous in both operands): 16-byte
+// cp.async DMMA kernel; falls back to gemm() for odd K/ld.
+void gram(const GemmArgs& g, double* ws, cudaStream_t s);
+size_t gram_ws_elems(int M, int N, int K);
 void gemm(const GemmArgs& g, double* ws, cudaStream_t s);
 int gemm_pick_splitk(int M, int N, int K);
 

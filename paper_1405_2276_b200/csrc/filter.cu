@@ -62,6 +62,24 @@ __global__ void k_colsq(long long n, const double* __restrict__ U, double* __res
 
 __global__ void k_step_begin(double* alpha_dev) { alpha_dev[1] = alpha_dev[0] + 1.0; }  // α ← α + 1 (:97)
 
+// out (cols×rows... row-major copy): out[i·r + j] = in[i + j·n]  (32×32 tiles through smem)
+__global__ void k_transpose(long long n, int r, const double* __restrict__ in, double* __restrict__ out) {
+    __shared__ double t[32][33];
+    const long long i0 = blockIdx.x * 32LL;
+    const int j0 = blockIdx.y * 32;
+    for (int q = threadIdx.y; q < 32; q += blockDim.y) {
+        const long long i = i0 + threadIdx.x;
+        const int j = j0 + q;
+        t[q][threadIdx.x] = (i < n && j < r) ? in[i + (long long)j * n] : 0.0;
+    }
+    __syncthreads();
+    for (int q = threadIdx.y; q < 32; q += blockDim.y) {
+        const long long i = i0 + q;
+        const int j = j0 + threadIdx.x;
+        if (i < n && j < r) out[i * r + j] = t[threadIdx.x][q];
+    }
+}
+
 // Woodbury per-step scalars: wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j
 __global__ void k_prep(int m, int r, const double* __restrict__ theta, const double* __restrict__ d,
                        const double* __restrict__ alpha_dev, double sigma2, double* __restrict__ wsq,
@@ -180,8 +198,8 @@ static void gram_tn(long long n, int p, int q, const double* A, const double* B,
     g.B = B; g.ldb = n; g.transB = 0;
     g.C = C; g.ldc = p;
     g.splitk = gemm_pick_splitk(p, q, int(n));
-    ws.ensure(gemm_ws_elems(g));
-    gemm(g, ws.p, s);
+    ws.ensure(std::max(gemm_ws_elems(g), gram_ws_elems(p, q, int(n))));
+    gram(g, ws.p, s);
 }
 // C (n×q) = A (n×p) · W (p×q), W on the device
 static void tall_times_small(long long n, int p, int q, const double* A, const double* W, double* C, cudaStream_t s) {
@@ -326,10 +344,13 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     B.alloc(size_t(std::max(m, 1)) * std::max(r, 1));  // HU (:73)
     spmm(H, U.p, n, r, B.p, m, 1.0, 0.0, s);
     colsq.alloc(size_t(std::max(r, 1)));
+    Urow.alloc(size_t(n) * std::max(r, 1));
     if (r > 0) {
         k_colsq<<<r, 256, 0, s>>>(n, U.p, colsq.p);
         FKB_LAUNCH_CHECK();
-        count_launch();
+        k_transpose<<<dim3(ceil_div(n, 32), ceil_div(r, 32)), dim3(32, 8), 0, s>>>(n, r, U.p, Urow.p);
+        FKB_LAUNCH_CHECK();
+        count_launch(2);
     }
     // Offline diagonalization of the α-dependence: G = P·diag(θ)·Pᵀ (block Jacobi), E = PᵀB.
     P.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
@@ -367,7 +388,7 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
         GemmArgs g;  // split-K workspace of the capacitance Gram
         g.M = r; g.N = r; g.K = m;
         g.splitk = gemm_pick_splitk(r, r, m);
-        ws_step.alloc(std::max<size_t>(gemm_ws_elems(g), 1));  // fixed address: graph-captured
+        ws_step.alloc(std::max<size_t>(std::max(gemm_ws_elems(g), gram_ws_elems(r, r, m)), 1));  // graph-captured
     }
     z.alloc(size_t(std::max(m, 1)));
     t.alloc(size_t(n));
@@ -458,7 +479,7 @@ void Filter::enqueue_step(const double* d_y) {
     cov->apply(t.p, n, 1, t.p, n);
     if (r > 0) launch_gemv_cols(m, r, B.p, m, XPlain{z.p}, EpiAxpby{cvec.p, 1.0, 0.0}, s, gpart.p);
     mark("gamma_ht_z");
-    launch_gemv_rows(n, r, U.p, n, XProd{d.p, cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+    launch_gemv_rowmajor(n, r, Urow.p, r, XProd{d.p, cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
     mark("mean_update");
     k_d_update<<<std::max(1, ceil_div(r, 256)), 256, 0, s>>>(r, d.p, lambda.p, alpha_dev.p, info.p);
     FKB_LAUNCH_CHECK();
@@ -486,8 +507,7 @@ void Filter::enqueue_solve_woodbury() {
         g.C = Kcap.p; g.ldc = r;
         g.diag_add = 1.0;
         g.lower_only = 0;  // full K: the PCG reads columns
-        g.splitk = gemm_pick_splitk(r, r, m);
-        gemm(g, ws_step.p, s);
+        gram(g, ws_step.p, s);
         mark("capacitance");
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
         FKB_CUDA(cudaMemsetAsync(pcgflag.p, 0, sizeof(int), s));

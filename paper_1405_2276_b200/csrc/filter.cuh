@@ -25,6 +25,7 @@ struct Filter {
     int kept_cols = 0;  // columns surviving Γ-orthonormalization
     std::vector<double> lambda_h;
     DBuf<double> lambda, U, Ubar, G, B, colsq;
+    DBuf<double> Urow;  // U row-major (N×r): the per-step U-pass streams it linearly
 
     // LowRankState (fast_filter.hpp:21-37), device resident; W ≡ U
     double alpha = 0.0;

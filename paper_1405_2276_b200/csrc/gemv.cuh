@@ -97,6 +97,60 @@ __global__ void __launch_bounds__(256) k_gemv_cols(long long n, int k, const dou
     if (lane == 0) epi(col, t);
 }
 
+// y_i = epi(i, Σ_j A_ij·x_j) for ROW-MAJOR A (m×k, ld ≥ k): each warp owns 4 rows and reads
+// each row as contiguous 256-B chunks, so the matrix streams linearly from HBM (the
+// step's U-pass; U is stored once more row-major for this).
+template <class XL, class Epi>
+__global__ void __launch_bounds__(256) k_gemv_rowmajor(long long m, int k, const double* __restrict__ A,
+                                                      long long ld, XL xl, Epi epi) {
+    extern __shared__ double xs[];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) xs[c] = xl(c);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long r0 = w * 4;
+    if (r0 >= m) return;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nq = (int)min(4LL, m - r0);
+    int c = lane;
+    for (; c + 96 < k; c += 128) {  // 16 independent loads in flight per lane
+        double v[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[q][u] = q < nq ? __ldcs(A + (r0 + q) * ld + c + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double xv = xs[c + 32 * u];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s[q] = fma(v[q][u], xv, s[q]);
+        }
+    }
+    for (; c < k; c += 32) {
+        const double xv = xs[c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q < nq) s[q] = fma(__ldcs(A + (r0 + q) * ld + c), xv, s[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+    if (lane < 4 && r0 + lane < m) {
+        const double v = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
+        epi(r0 + lane, v);
+    }
+}
+
+template <class XL, class Epi>
+inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long ld, XL xl, Epi epi, cudaStream_t s) {
+    if (m <= 0) return;
+    const long long warps = (m + 3) / 4;
+    k_gemv_rowmajor<XL, Epi><<<(unsigned)((warps + 7) / 8), 256, sizeof(double) * size_t(std::max(k, 1)), s>>>(
+        m, k, A, ld, xl, epi);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
 // Column splits so that the launch covers ≥ ~4 CTAs per SM; part needs S·m doubles.
 inline int gemv_rows_splits(long long m, int k) {
     const long long tiles = (m + 31) / 32;
