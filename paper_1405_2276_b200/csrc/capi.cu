@@ -1,4 +1,8 @@
 // capi.cu — extern "C" boundary (include/fastkf_b200.h) over the device runtime.
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -10,7 +14,25 @@
 
 namespace fkb {
 unsigned long long g_launches = 0;
+int g_sync_check = std::getenv("FKB_SYNC_CHECK") ? std::atoi(std::getenv("FKB_SYNC_CHECK")) : 0;
+
+__attribute__((noinline)) void sync_check(const char*) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        Dl_info info{};
+        void* ra = __builtin_return_address(0);
+        dladdr(ra, &info);
+        const long off = long((char*)ra - (char*)info.dli_fbase);
+        throw CudaError(std::string("CUDA error ") + cudaGetErrorString(e) + " after launch #" +
+                        std::to_string(g_launches) + " caller offset 0x" + [&] {
+                            char b[32];
+                            std::snprintf(b, sizeof b, "%lx", off);
+                            return std::string(b);
+                        }());
+    }
 }
+}  // namespace fkb
 
 struct fkb_cov {
     cudaStream_t stream = nullptr;

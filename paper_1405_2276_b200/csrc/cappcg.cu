@@ -47,6 +47,43 @@ __device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, PcgShared& 
     return s;
 }
 
+// three block partials with one __syncthreads → sh.part[0..2]
+__device__ __forceinline__ void block_partial3(PcgShared& sh, double a, double b, double c) {
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sh.red[threadIdx.x >> 5][0] = a;
+        sh.red[threadIdx.x >> 5][1] = b;
+        sh.red[threadIdx.x >> 5][2] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int w = 0; w < PC_T / 32; ++w) s += sh.red[w][threadIdx.x];
+        sh.part[threadIdx.x] = s;
+    }
+}
+
+__device__ __forceinline__ void cluster_sum3(cg::cluster_group& cl, PcgShared& sh, double* out) {
+    double v[PC_CL][3];
+#pragma unroll
+    for (int c = 0; c < PC_CL; ++c) {
+        PcgShared* rs = cl.map_shared_rank(&sh, c);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[c][q] = rs->part[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < PC_CL; ++c) s += v[c][q];
+        out[q] = s;
+    }
+}
+
 __device__ __forceinline__ void block_partial(PcgShared& sh, double v, int slot) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5][slot] = v;
@@ -89,86 +126,85 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     // rb ≤ 64 for n ≤ 1024 → one row per thread among the first rb threads
     const int row = r0 + tid;
     const bool own = tid < rb && row < r1;
-    double dinv = 0.0, b = 0.0, x = 0.0, r = 0.0, z = 0.0, p = 0.0;
+    double dinv = 0.0, b = 0.0, x = 0.0, r = 0.0;
     if (own) {
         dinv = 1.0 / K[row + (long long)row * ld];
         b = u[row];
-        x = 0.0;
         r = b;
-        z = dinv * r;
-        p = z;
     }
-    // rz = rᵀz, bb = bᵀb
-    block_partial(sh, own ? r * z : 0.0, 0);
-    block_partial(sh, own ? b * b : 0.0, 1);
-    if (own) sh.p[row] = p;  // publish own block of p in local smem (gathered below)
-    cl.sync();
-    double rz = cluster_sum(cl, sh, 0);
-    const double bb = cluster_sum(cl, sh, 1);
-    const double stop = tol * tol * bb;
+    // w = K·z for the owned rows: gather the full z through DSMEM (every remote load in
+    // flight at once), then one warp per row over this CTA's staged columns of K.
+    // Chronopoulos–Gear PCG (one fused reduction per iteration): with z = M⁻¹r, w = Kz,
+    // γ = rᵀz, δ = zᵀw: β = γ/γ_prev, α = γ/(δ − βγ/α_prev), p = z + βp, s = w + βs,
+    // x += αp, r −= αs.  Two cluster barriers per iteration: z published (inside matvec) and
+    // the partials of (γ, δ, rᵀr) published.  Every CTA sees identical sums (rank-ordered),
+    // so all leave the loop together.
+    double p = 0.0, sv = 0.0, gamma_prev = 1.0, alpha_prev = 1.0;
     int it = 0;
-    bool done = bb == 0.0;
-    // Three cluster barriers per iteration:
-    //   gather p (DSMEM) → q = K·p, pᵀq partial → [S2] → x, r, z, rᵀz / rᵀr partials → [S3]
-    //   → β, p update, publish own p → [S4].  Remote p blocks are read only before S2 and
-    //   rewritten only after S3; each partial slot is rewritten only after every CTA has
-    //   read it (slot 2 after S2 of the next iteration, slots 0/3 after S3).
-    while (!done && it < maxit) {
-        {  // gather remote p blocks: every thread issues its remote loads at once (one latency)
-            double v[PC_MAXN / PC_T];
+    bool done = false;
+    double stop = 0.0;
+    while (true) {
+        const double z = dinv * r;
+        double w = 0.0;
+        {  // w = K·z for the owned rows (z gathered through DSMEM)
+            if (own) sh.p[row] = z;
+            cl.sync();  // all z blocks published
+            {
+                double v[PC_MAXN / PC_T];
 #pragma unroll
-            for (int q = 0; q < PC_MAXN / PC_T; ++q) {
-                const int i = tid + q * PC_T;
-                const int owner = i / rb;
-                v[q] = (i < n && owner != crank) ? cl.map_shared_rank(&sh, owner)->p[i] : 0.0;
-            }
+                for (int q = 0; q < PC_MAXN / PC_T; ++q) {
+                    const int i = tid + q * PC_T;
+                    const int owner = min(i / rb, PC_CL - 1);  // never form an out-of-cluster address
+                    v[q] = 0.0;
+                    if (i < n && owner != crank) v[q] = cl.map_shared_rank(&sh, owner)->p[i];
+                }
 #pragma unroll
-            for (int q = 0; q < PC_MAXN / PC_T; ++q) {
-                const int i = tid + q * PC_T;
-                if (i < n && i / rb != crank) sh.p[i] = v[q];
+                for (int q = 0; q < PC_MAXN / PC_T; ++q) {
+                    const int i = tid + q * PC_T;
+                    if (i < n && i / rb != crank) sh.p[i] = v[q];
+                }
             }
-        }
-        __syncthreads();
-        // q_i = (K p)_i = Σ_j K_ji p_j (K symmetric: column i, staged in shared memory)
-        for (int i = r0 + warp; i < r1; i += PC_T / 32) {
-            const double* Kc = kstage ? Ks + (long long)(i - r0) * n : K + (long long)i * ld;
-            double s0 = 0.0, s1 = 0.0;
-            int j = lane;
-            for (; j + 32 < n; j += 64) {
-                s0 = fma(Kc[j], sh.p[j], s0);
-                s1 = fma(Kc[j + 32], sh.p[j + 32], s1);
+            __syncthreads();
+            for (int i = r0 + warp; i < r1; i += PC_T / 32) {
+                const double* Kc = kstage ? Ks + (long long)(i - r0) * n : K + (long long)i * ld;
+                double s0 = 0.0, s1 = 0.0;
+                int j = lane;
+                for (; j + 32 < n; j += 64) {
+                    s0 = fma(Kc[j], sh.p[j], s0);
+                    s1 = fma(Kc[j + 32], sh.p[j + 32], s1);
+                }
+                if (j < n) s0 = fma(Kc[j], sh.p[j], s0);
+                double s = s0 + s1;
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+                if (lane == 0) sh.q[i - r0] = s;
             }
-            if (j < n) s0 = fma(Kc[j], sh.p[j], s0);
-            double s = s0 + s1;
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-            if (lane == 0) sh.q[i - r0] = s;
+            __syncthreads();
+            w = own ? sh.q[tid] : 0.0;
         }
-        __syncthreads();
-        const double qown = own ? sh.q[tid] : 0.0;
-        block_partial(sh, own ? p * qown : 0.0, 2);
-        cl.sync();  // S2
-        const double pq = cluster_sum(cl, sh, 2);
-        const double a = rz / pq;
-        if (own) {
-            x = fma(a, p, x);
-            r = fma(-a, qown, r);
-            z = dinv * r;
+        block_partial3(sh, own ? r * z : 0.0, own ? z * w : 0.0, own ? r * r : 0.0);
+        cl.sync();
+        double g3[3];
+        cluster_sum3(cl, sh, g3);
+        const double gamma = g3[0], delta = g3[1], rr = g3[2];
+        if (it == 0) stop = tol * tol * rr;  // r₀ = b
+        if (rr <= stop || rr == 0.0) {
+            done = true;
+            break;
         }
-        block_partial(sh, own ? r * z : 0.0, 0);
-        block_partial(sh, own ? r * r : 0.0, 3);
-        cl.sync();  // S3
-        const double rz_new = cluster_sum(cl, sh, 0);
-        const double rr = cluster_sum(cl, sh, 3);
-        ++it;
-        done = rr <= stop;
-        const double beta = rz_new / rz;
-        rz = rz_new;
+        if (it >= maxit) break;
+        const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
+        const double alpha = it == 0 ? gamma / delta : gamma / (delta - beta * gamma / alpha_prev);
         if (own) {
             p = fma(beta, p, z);
-            sh.p[row] = p;
+            sv = fma(beta, sv, w);
+            x = fma(alpha, p, x);
+            r = fma(-alpha, sv, r);
         }
-        cl.sync();  // S4: new p blocks published
+        gamma_prev = gamma;
+        alpha_prev = alpha;
+        ++it;
     }
+    cl.sync();  // no CTA may exit while a peer still reads its partials through DSMEM
     if (done) {
         if (own) u[row] = x;
     } else if (crank == 0 && tid == 0) {

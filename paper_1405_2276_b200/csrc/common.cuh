@@ -62,6 +62,11 @@ struct DBuf {
 // Launch counter: every kernel launch of this library goes through count_launch()
 // so bench.py can report gpu_launches honestly.
 extern unsigned long long g_launches;
-inline void count_launch(int k = 1) { g_launches += (unsigned long long)k; }
+extern int g_sync_check;  // FKB_SYNC_CHECK=1: synchronize + check after every launch (debug)
+void sync_check(const char* where);
+inline void count_launch(int k = 1) {
+    g_launches += (unsigned long long)k;
+    if (g_sync_check) sync_check("count_launch");
+}
 
 }  // namespace fkb

@@ -80,11 +80,17 @@ __global__ void k_transpose(long long n, int r, const double* __restrict__ in, d
     }
 }
 
-// Woodbury per-step scalars: wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j
+// Step prologue of the Woodbury solver: α ← α + 1 (fast_filter.hpp:97), clears the failure
+// flags, and the per-step scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j.
 __global__ void k_prep(int m, int r, const double* __restrict__ theta, const double* __restrict__ d,
-                       const double* __restrict__ alpha_dev, double sigma2, double* __restrict__ wsq,
-                       double* __restrict__ sqd) {
-    const double alpha = alpha_dev[1];
+                       double* alpha_dev, double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
+                       int* __restrict__ info, int* __restrict__ pcgflag) {
+    const double alpha = alpha_dev[0] + 1.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        alpha_dev[1] = alpha;
+        *info = 0;
+        *pcgflag = 0;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
         wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) sqd[j] = sqrt(d[j]);
@@ -464,13 +470,17 @@ void Filter::set_solver(int mode) {
 }
 
 void Filter::enqueue_step(const double* d_y) {
-    FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
-    k_step_begin<<<1, 1, 0, s>>>(alpha_dev.p);
+    if (solver == 1) {
+        const int pb = std::max(1, std::min(ceil_div(std::max(m, r), 256), 148));
+        k_prep<<<pb, 256, 0, s>>>(m, r, theta.p, d.p, alpha_dev.p, sigma2, wsq.p, sqd.p, info.p, pcgflag.p);
+    } else {
+        FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+        k_step_begin<<<1, 1, 0, s>>>(alpha_dev.p);
+    }
     FKB_LAUNCH_CHECK();
     count_launch();
-    // z = y − H·mean (:108)
-    FKB_CUDA(cudaMemcpyAsync(z.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
-    spmm(H, mean.p, n, 1, z.p, m, -1.0, 1.0, s);
+    // z = y − H·mean (:108), one fused SpMV
+    spmm(H, mean.p, n, 1, z.p, m, -1.0, 1.0, s, d_y);
     mark("residual");
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
@@ -489,10 +499,6 @@ void Filter::enqueue_step(const double* d_y) {
 
 // z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
 void Filter::enqueue_solve_woodbury() {
-    const int pb = std::max(1, std::min(ceil_div(std::max(m, r), 256), 148));
-    k_prep<<<pb, 256, 0, s>>>(m, r, theta.p, d.p, alpha_dev.p, sigma2, wsq.p, sqd.p);
-    FKB_LAUNCH_CHECK();
-    count_launch();
     launch_gemv_cols(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, gpart.p);  // r̃ = Pᵀ(y − H·mean)
     mark("rotate_in");
     if (r > 0) {
@@ -510,7 +516,6 @@ void Filter::enqueue_solve_woodbury() {
         gram(g, ws_step.p, s);
         mark("capacitance");
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
-        FKB_CUDA(cudaMemsetAsync(pcgflag.p, 0, sizeof(int), s));
         cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s);
         chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
         mark("cap_solve");

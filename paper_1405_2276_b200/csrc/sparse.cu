@@ -19,7 +19,7 @@ namespace fkb {
 __global__ void __launch_bounds__(256) k_spmm_warp(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
                                                   const double* __restrict__ v, const double* __restrict__ X,
                                                   long long ldx, int ncols, double* __restrict__ Y, long long ldy,
-                                                  double alpha, double beta) {
+                                                  double alpha, double beta, const double* __restrict__ Yin) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int b0 = blockIdx.y * 4;
@@ -45,14 +45,14 @@ __global__ void __launch_bounds__(256) k_spmm_warp(int rows, const int* __restri
     if (lane < nb) {
         const double r = lane == 0 ? t0 : lane == 1 ? t1 : lane == 2 ? t2 : t3;
         double* y = Y + warp + (long long)(b0 + lane) * ldy;
-        *y = beta == 0.0 ? alpha * r : alpha * r + beta * *y;
+        *y = beta == 0.0 ? alpha * r : alpha * r + beta * Yin[warp + (long long)(b0 + lane) * ldy];
     }
 }
 
 __global__ void __launch_bounds__(256) k_spmm_thread(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
                                                     const double* __restrict__ v, const double* __restrict__ X,
                                                     long long ldx, double* __restrict__ Y, long long ldy,
-                                                    double alpha, double beta) {
+                                                    double alpha, double beta, const double* __restrict__ Yin) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
     if (r >= rows) return;
@@ -60,11 +60,12 @@ __global__ void __launch_bounds__(256) k_spmm_thread(int rows, const int* __rest
     double s = 0.0;
     for (int e = rp[r]; e < rp[r + 1]; ++e) s = fma(v[e], __ldg(x + ci[e]), s);
     double* y = Y + r + (long long)b * ldy;
-    *y = beta == 0.0 ? alpha * s : alpha * s + beta * *y;
+    *y = beta == 0.0 ? alpha * s : alpha * s + beta * Yin[r + (long long)b * ldy];
 }
 
 void spmm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
-          double beta, cudaStream_t s) {
+          double beta, cudaStream_t s, const double* Yin) {
+    if (!Yin) Yin = Y;
     if (A.rows <= 0 || ncols <= 0) return;
     const double avg = A.rows ? double(A.nnz) / A.rows : 0.0;
     if (avg > 24.0) {
@@ -72,7 +73,7 @@ void spmm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y,
             const int nc = std::min(ncols - c0, 4 * 65535);
             dim3 grid(ceil_div((long long)A.rows * 32, 256), ceil_div(nc, 4));
             k_spmm_warp<<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X + (long long)c0 * ldx, ldx, nc,
-                                             Y + (long long)c0 * ldy, ldy, alpha, beta);
+                                             Y + (long long)c0 * ldy, ldy, alpha, beta, Yin + (long long)c0 * ldy);
             FKB_LAUNCH_CHECK();
             count_launch();
         }
@@ -81,7 +82,7 @@ void spmm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y,
             const int nc = std::min(ncols - c0, 65535);
             dim3 grid(ceil_div(A.rows, 256), nc);
             k_spmm_thread<<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X + (long long)c0 * ldx, ldx,
-                                               Y + (long long)c0 * ldy, ldy, alpha, beta);
+                                               Y + (long long)c0 * ldy, ldy, alpha, beta, Yin + (long long)c0 * ldy);
             FKB_LAUNCH_CHECK();
             count_launch();
         }

@@ -12,9 +12,10 @@ struct DevCsr {  // SparseRowMatrix (grid.hpp:15) on the device: int32 indices, 
     DBuf<double> val;
 };
 
-// Y[:, b] = alpha · A X[:, b] (+ beta · Y) for b < ncols; X, Y column-major device blocks.
+// Y[:, b] = alpha · A X[:, b] + beta · Yin[:, b] for b < ncols (Yin defaults to Y);
+// X, Y, Yin column-major device blocks (Yin shares Y's leading dimension).
 void spmm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
-          double beta, cudaStream_t s);
+          double beta, cudaStream_t s, const double* Yin = nullptr);
 // Upload host CSR and build the explicit transposed CSR (rows ascending inside each column).
 void upload_csr_pair(int rows, int cols, const int* rowptr, const int* col, const double* val, DevCsr& A,
                      DevCsr& AT);
