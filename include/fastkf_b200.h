@@ -131,6 +131,10 @@ int fkb_filter_phase_times(fkb_filter* f, int reps, double* ms, char* names, int
  * factor, x = K⁻¹b; stamps (optional, 128 entries) receive %globaltimer phase stamps */
 int fkb_chol_solve_small(int n, const double* K, const double* b, double* L, double* x,
                          unsigned long long* stamps);
+/* capacitance Jacobi-PCG kernel on a host SPD matrix (test/profiling hook): x = K⁻¹b,
+ * *iters = iterations; returns 2 if the iteration cap was hit; stamps: 64 entries */
+int fkb_cap_pcg_test(int n, const double* K, const double* b, double* x, int* iters,
+                     unsigned long long* stamps);
 
 /* measured FP64 peak of this GPU (mode 0: DFMA pipe, 1: DMMA tensor path), TFLOP/s */
 int fkb_fp64_peak(int mode, double* tflops);

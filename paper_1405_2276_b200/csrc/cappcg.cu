@@ -25,198 +25,224 @@ namespace cg = cooperative_groups;
 
 namespace fkb {
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 constexpr int PC_CL = 16;   // CTAs per cluster (non-portable size, opt-in attribute)
-constexpr int PC_T = 256;   // threads per CTA
+constexpr int PC_T = 512;   // threads per CTA
 constexpr int PC_MAXN = 1024;
 
 struct PcgShared {
-    double p[PC_MAXN];      // full search direction (gathered)
+    double v[2][PC_MAXN];      // vector being multiplied by K, double-buffered by iteration parity
+    double part[2][PC_CL][4];  // (γ, δ, rᵀr) partials, slot c written by CTA c
     double q[PC_MAXN / PC_CL];
-    double part[4];         // this CTA's partial sums
     double red[PC_T / 32][4];
 };
 
-__device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, PcgShared& sh, int slot) {
-    // every CTA has written sh.part[slot]; sum them in rank order (deterministic)
-    double v[PC_CL];
-#pragma unroll
-    for (int c = 0; c < PC_CL; ++c) v[c] = cl.map_shared_rank(&sh, c)->part[slot];  // all loads in flight
-    double s = 0.0;
-#pragma unroll
-    for (int c = 0; c < PC_CL; ++c) s += v[c];
-    return s;
+__device__ __forceinline__ void st_cluster(double* local_addr, int rank, double v) {
+    // remote shared-memory store into CTA `rank` of this cluster (fire and forget; made
+    // visible by the next barrier.cluster arrive.release / wait.acquire pair)
+    unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local_addr)), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
 
-// three block partials with one __syncthreads → sh.part[0..2]
-__device__ __forceinline__ void block_partial3(PcgShared& sh, double a, double b, double c) {
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_down_sync(0xffffffffu, a, o);
-        b += __shfl_down_sync(0xffffffffu, b, o);
-        c += __shfl_down_sync(0xffffffffu, c, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        sh.red[threadIdx.x >> 5][0] = a;
-        sh.red[threadIdx.x >> 5][1] = b;
-        sh.red[threadIdx.x >> 5][2] = c;
+__device__ __forceinline__ void cp_async8(double* smem, const double* g) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a), "l"(g) : "memory");
+}
+
+// sh.q[i − r0] = (K·v)_i for this CTA's rows, v = sh.v[buf]: 16 lanes per row (two rows
+// per warp, PC_T/16 rows per pass) over the staged K block, 4-level shuffle reduction
+__device__ __forceinline__ void block_matvec(PcgShared& sh, const double* Ks, const double* K, long long ld, int n,
+                                             int r0, int r1, int buf, int kstage) {
+    const int sub = threadIdx.x & 15, slot = threadIdx.x >> 4;
+    const double* v = sh.v[buf];
+    for (int i0 = r0; i0 < r1; i0 += PC_T / 16) {  // uniform trip count across the CTA
+        const int i = i0 + slot;
+        double s0 = 0.0, s1 = 0.0;
+        if (i < r1) {
+            const double* Kc = kstage ? Ks + (long long)(i - r0) * n : K + (long long)i * ld;
+            int j = sub;
+            for (; j + 16 < n; j += 32) {
+                s0 = fma(Kc[j], v[j], s0);
+                s1 = fma(Kc[j + 16], v[j + 16], s1);
+            }
+            if (j < n) s0 = fma(Kc[j], v[j], s0);
+        }
+        double s = s0 + s1;
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (sub == 0 && i < r1) sh.q[i - r0] = s;
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
-        double s = 0.0;
-        for (int w = 0; w < PC_T / 32; ++w) s += sh.red[w][threadIdx.x];
-        sh.part[threadIdx.x] = s;
-    }
-}
-
-__device__ __forceinline__ void cluster_sum3(cg::cluster_group& cl, PcgShared& sh, double* out) {
-    double v[PC_CL][3];
-#pragma unroll
-    for (int c = 0; c < PC_CL; ++c) {
-        PcgShared* rs = cl.map_shared_rank(&sh, c);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) v[c][q] = rs->part[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        double s = 0.0;
-#pragma unroll
-        for (int c = 0; c < PC_CL; ++c) s += v[c][q];
-        out[q] = s;
-    }
-}
-
-__device__ __forceinline__ void block_partial(PcgShared& sh, double v, int slot) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5][slot] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < PC_T / 32; ++w) s += sh.red[w][slot];
-        sh.part[slot] = s;
-    }
 }
 
 __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, long long ld, int n,
                                                  double* __restrict__ u, double* __restrict__ work,
-                                                 int* __restrict__ fallback, int maxit, double tol, int kstage) {
+                                                 int* __restrict__ fallback, int maxit, double tol, int kstage,
+                                                 unsigned long long* __restrict__ ts) {
     __shared__ PcgShared sh;
     extern __shared__ double Ks[];  // this CTA's columns of K (rb × n) when kstage
+    const bool stamp = ts && blockIdx.x == 0 && threadIdx.x == 0;
+    if (stamp) ts[0] = gtimer();
     cg::cluster_group cl = cg::this_cluster();
     const int crank = int(cl.block_rank());
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rb = (n + PC_CL - 1) / PC_CL;
-    const int r0 = crank * rb, r1 = min(n, r0 + rb);
-    if (kstage) {
-        const int cnt = (r1 - r0) * n;
-        for (int e0 = 0; e0 < cnt; e0 += 4 * PC_T) {
-            double v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = e0 + tid + q * PC_T;
-                v[q] = e < cnt ? K[(long long)(r0 + e / n) * ld + e % n] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = e0 + tid + q * PC_T;
-                if (e < cnt) Ks[e] = v[q];
-            }
+    const int rb = (n + PC_CL - 1) / PC_CL;  // ≤ 64: owned rows live in warps 0–1
+    const int r0 = min(n, crank * rb), r1 = min(n, r0 + rb);
+    // Stage this CTA's K block (columns r0..r1, contiguous when ld == n): one TMA bulk copy
+    // tracked by an mbarrier when 16-byte aligned, else 8-byte cp.async; it lands while the
+    // initial residual is exchanged.
+    __shared__ alignas(8) unsigned long long kbar;
+    const int cnt = kstage ? (r1 - r0) * n : 0;
+    const unsigned bytes = unsigned(cnt) * 8u;
+    const bool bulk = kstage && ld == n && ((long long)r0 * n) % 2 == 0 && bytes % 16 == 0 && bytes > 0;
+    const unsigned kbar_a = static_cast<unsigned>(__cvta_generic_to_shared(&kbar));
+    if (bulk) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(kbar_a) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(kbar_a), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    static_cast<unsigned>(__cvta_generic_to_shared(Ks))),
+                "l"(K + (long long)r0 * n), "r"(bytes), "r"(kbar_a)
+                : "memory");
         }
-        __syncthreads();
+    } else if (kstage) {
+        for (int e = tid; e < cnt; e += PC_T) cp_async8(Ks + e, K + (long long)(r0 + e / n) * ld + e % n);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    // per-row state lives in registers of the owning thread (rows r0 + tid, r0 + tid + 256, …)
-    // rb ≤ 64 for n ≤ 1024 → one row per thread among the first rb threads
+    // Pipelined Jacobi-PCG (Ghysels–Vanroose): the matvec n = K·m and the reductions
+    // γ = rᵀu, δ = wᵀu of the same iteration are independent, so one cluster exchange per
+    // iteration carries both: owners push m into every CTA and every CTA pushes its
+    // partials into every CTA (DSMEM stores), one cluster barrier, then each CTA sums the 16
+    // slots in rank order (identical values everywhere → all CTAs branch alike) and
+    // multiplies its own K rows locally.  Buffers alternate by parity, so a CTA that runs
+    // ahead never overwrites data a peer is still reading.
     const int row = r0 + tid;
-    const bool own = tid < rb && row < r1;
-    double dinv = 0.0, b = 0.0, x = 0.0, r = 0.0;
+    const bool own = row < r1;
+    double dinv = 0.0, x = 0.0, r = 0.0, uu = 0.0, w = 0.0;
+    double zv = 0.0, qv = 0.0, sv = 0.0, pv = 0.0;
     if (own) {
         dinv = 1.0 / K[row + (long long)row * ld];
-        b = u[row];
-        r = b;
+        r = u[row];
+        uu = dinv * r;
+#pragma unroll
+        for (int c = 0; c < PC_CL; ++c) st_cluster(&sh.v[1][row], c, uu);
     }
-    // w = K·z for the owned rows: gather the full z through DSMEM (every remote load in
-    // flight at once), then one warp per row over this CTA's staged columns of K.
-    // Chronopoulos–Gear PCG (one fused reduction per iteration): with z = M⁻¹r, w = Kz,
-    // γ = rᵀz, δ = zᵀw: β = γ/γ_prev, α = γ/(δ − βγ/α_prev), p = z + βp, s = w + βs,
-    // x += αp, r −= αs.  Two cluster barriers per iteration: z published (inside matvec) and
-    // the partials of (γ, δ, rᵀr) published.  Every CTA sees identical sums (rank-ordered),
-    // so all leave the loop together.
-    double p = 0.0, sv = 0.0, gamma_prev = 1.0, alpha_prev = 1.0;
+    if (bulk) {
+        unsigned ok = 0;
+        while (!ok)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(kbar_a)
+                : "memory");
+    } else if (kstage) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    cl.sync();  // u₀ exchanged; also orders every thread's staged K before the first matvec
+    block_matvec(sh, Ks, K, ld, n, r0, r1, 1, kstage);  // w₀ = K u₀
+    if (own) w = sh.q[tid];
+    if (stamp) ts[1] = gtimer();
+    double gamma_prev = 1.0, alpha_prev = 1.0, stop = 0.0;
     int it = 0;
     bool done = false;
-    double stop = 0.0;
     while (true) {
-        const double z = dinv * r;
-        double w = 0.0;
-        {  // w = K·z for the owned rows (z gathered through DSMEM)
-            if (own) sh.p[row] = z;
-            cl.sync();  // all z blocks published
-            {
-                double v[PC_MAXN / PC_T];
-#pragma unroll
-                for (int q = 0; q < PC_MAXN / PC_T; ++q) {
-                    const int i = tid + q * PC_T;
-                    const int owner = min(i / rb, PC_CL - 1);  // never form an out-of-cluster address
-                    v[q] = 0.0;
-                    if (i < n && owner != crank) v[q] = cl.map_shared_rank(&sh, owner)->p[i];
-                }
-#pragma unroll
-                for (int q = 0; q < PC_MAXN / PC_T; ++q) {
-                    const int i = tid + q * PC_T;
-                    if (i < n && i / rb != crank) sh.p[i] = v[q];
+        const int buf = it & 1;
+        const double mv = dinv * w;
+        if (stamp && it == 3) ts[39] = gtimer();
+        {
+            double a = own ? r * uu : 0.0, bq = own ? w * uu : 0.0, c = own ? r * r : 0.0;
+            if (warp < 2) {
+                for (int o = 16; o > 0; o >>= 1) {
+                    a += __shfl_xor_sync(0xffffffffu, a, o);
+                    bq += __shfl_xor_sync(0xffffffffu, bq, o);
+                    c += __shfl_xor_sync(0xffffffffu, c, o);
                 }
             }
-            __syncthreads();
-            for (int i = r0 + warp; i < r1; i += PC_T / 32) {
-                const double* Kc = kstage ? Ks + (long long)(i - r0) * n : K + (long long)i * ld;
-                double s0 = 0.0, s1 = 0.0;
-                int j = lane;
-                for (; j + 32 < n; j += 64) {
-                    s0 = fma(Kc[j], sh.p[j], s0);
-                    s1 = fma(Kc[j + 32], sh.p[j + 32], s1);
+            if (own)
+#pragma unroll
+                for (int cc = 0; cc < PC_CL; ++cc) st_cluster(&sh.v[buf][row], cc, mv);
+            if (rb <= 32) {  // one owning warp: its lanes 0..15 push the three sums to every CTA
+                const double a0 = __shfl_sync(0xffffffffu, a, 0), b0 = __shfl_sync(0xffffffffu, bq, 0),
+                             c0 = __shfl_sync(0xffffffffu, c, 0);
+                if (warp == 0) {
+                    if (lane < PC_CL) {
+                        st_cluster(&sh.part[buf][crank][0], lane, a0);
+                        st_cluster(&sh.part[buf][crank][1], lane, b0);
+                        st_cluster(&sh.part[buf][crank][2], lane, c0);
+                    }
                 }
-                if (j < n) s0 = fma(Kc[j], sh.p[j], s0);
-                double s = s0 + s1;
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-                if (lane == 0) sh.q[i - r0] = s;
+            } else {
+                if (warp < 2 && lane == 0) {
+                    sh.red[warp][0] = a;
+                    sh.red[warp][1] = bq;
+                    sh.red[warp][2] = c;
+                }
+                __syncthreads();
+                if (tid < 3 * PC_CL) {
+                    const int qq = tid % 3, dest = tid / 3;
+                    st_cluster(&sh.part[buf][crank][qq], dest, sh.red[0][qq] + sh.red[1][qq]);
+                }
             }
-            __syncthreads();
-            w = own ? sh.q[tid] : 0.0;
         }
-        block_partial3(sh, own ? r * z : 0.0, own ? z * w : 0.0, own ? r * r : 0.0);
-        cl.sync();
-        double g3[3];
-        cluster_sum3(cl, sh, g3);
-        const double gamma = g3[0], delta = g3[1], rr = g3[2];
-        if (it == 0) stop = tol * tol * rr;  // r₀ = b
+        if (stamp && it == 3) ts[40] = gtimer();
+        cl.sync();  // m and all partials delivered
+        if (stamp && it == 3) ts[41] = gtimer();
+        double gamma = 0.0, delta = 0.0, rr = 0.0;
+#pragma unroll
+        for (int c = 0; c < PC_CL; ++c) {
+            gamma += sh.part[buf][c][0];
+            delta += sh.part[buf][c][1];
+            rr += sh.part[buf][c][2];
+        }
+        if (it == 0) stop = tol * tol * rr;  // r₀ = u
         if (rr <= stop || rr == 0.0) {
             done = true;
             break;
         }
         if (it >= maxit) break;
+        if (stamp && it == 3) ts[42] = gtimer();
+        block_matvec(sh, Ks, K, ld, n, r0, r1, buf, kstage);  // n = K m
+        if (stamp && it == 3) ts[43] = gtimer();
         const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
         const double alpha = it == 0 ? gamma / delta : gamma / (delta - beta * gamma / alpha_prev);
         if (own) {
-            p = fma(beta, p, z);
+            const double nv = sh.q[tid];
+            zv = fma(beta, zv, nv);
+            qv = fma(beta, qv, mv);
             sv = fma(beta, sv, w);
-            x = fma(alpha, p, x);
+            pv = fma(beta, pv, uu);
+            x = fma(alpha, pv, x);
             r = fma(-alpha, sv, r);
+            uu = fma(-alpha, qv, uu);
+            w = fma(-alpha, zv, w);
         }
         gamma_prev = gamma;
         alpha_prev = alpha;
         ++it;
+        if (stamp && it < 60) ts[1 + it] = gtimer();
     }
-    cl.sync();  // no CTA may exit while a peer still reads its partials through DSMEM
+    // every DSMEM store of the last iteration completed before its barrier and nothing is
+    // read remotely, so CTAs may exit independently
     if (done) {
         if (own) u[row] = x;
     } else if (crank == 0 && tid == 0) {
         *fallback = 1;
     }
     if (crank == 0 && tid == 0) work[n] = double(it);  // iteration count (diagnostics)
+    if (stamp) ts[63] = gtimer();
 }
 
 static bool g_pcg_attr = false;
 
 void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int* fallback, cudaStream_t s, int maxit,
-             double tol) {
+             double tol, unsigned long long* ts) {
     if (n <= 0) return;
     if (n > PC_MAXN) throw std::invalid_argument("cap_pcg: n exceeds 1024");
     const int rb = (n + PC_CL - 1) / PC_CL;
@@ -240,8 +266,35 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg, K, ld, n, u, work, fallback, maxit, tol, kstage));
+    FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
     count_launch();
 }
 
 }  // namespace fkb
+
+// test hook: solve K x = b (host K column-major, n ≤ 1024); iteration count and %globaltimer
+// stamps (ns; [0] start, [1] K staged, [1+it] per iteration, [63] end) returned.
+extern "C" int fkb_cap_pcg_test(int n, const double* K, const double* b, double* x, int* iters,
+                                unsigned long long* stamps) {
+    try {
+        fkb::DBuf<double> dK(static_cast<size_t>(n) * n), du(static_cast<size_t>(n)), w(static_cast<size_t>(n) + 1);
+        fkb::DBuf<int> fb(1);
+        fkb::DBuf<unsigned long long> ts(64);
+        FKB_CUDA(cudaMemcpy(dK.p, K, sizeof(double) * size_t(n) * n, cudaMemcpyHostToDevice));
+        FKB_CUDA(cudaMemcpy(du.p, b, sizeof(double) * size_t(n), cudaMemcpyHostToDevice));
+        FKB_CUDA(cudaMemset(fb.p, 0, sizeof(int)));
+        FKB_CUDA(cudaMemset(ts.p, 0, ts.bytes()));
+        fkb::cap_pcg(n, dK.p, n, du.p, w.p, fb.p, nullptr, 200, 1e-14, stamps ? ts.p : nullptr);
+        FKB_CUDA(cudaDeviceSynchronize());
+        int h = 0;
+        double itd = 0.0;
+        FKB_CUDA(cudaMemcpy(&h, fb.p, sizeof(int), cudaMemcpyDeviceToHost));
+        FKB_CUDA(cudaMemcpy(&itd, w.p + n, sizeof(double), cudaMemcpyDeviceToHost));
+        if (iters) *iters = int(itd);
+        if (x) FKB_CUDA(cudaMemcpy(x, du.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost));
+        if (stamps) FKB_CUDA(cudaMemcpy(stamps, ts.p, ts.bytes(), cudaMemcpyDeviceToHost));
+        return h ? 2 : 0;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}

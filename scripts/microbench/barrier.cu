@@ -88,6 +88,34 @@ __global__ void __cluster_dims__(16, 1, 1) k_cluster(int iters, double* out) {
 
 __global__ void k_empty() {}
 
+__device__ __forceinline__ void st_cluster(double* local_addr, int rank, double v) {
+    unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local_addr)), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+
+// per iteration: `senders` threads each push `per` doubles to every CTA, then cluster sync
+__global__ void __cluster_dims__(16, 1, 1) k_cluster_push(int iters, int senders, int mode, double* out) {
+    __shared__ double buf[2][1024];
+    cg::cluster_group cl = cg::this_cluster();
+    double acc = 0.0;
+    for (int i = 0; i < iters; ++i) {
+        const int b = i & 1;
+        if (mode == 0) {
+            if (threadIdx.x < senders)
+                for (int c = 0; c < 16; ++c) st_cluster(&buf[b][threadIdx.x], c, acc + c);
+        } else if (mode == 1) {  // spread: thread t → rank t % 16
+            if (threadIdx.x < senders * 16) st_cluster(&buf[b][threadIdx.x / 16], threadIdx.x % 16, acc);
+        } else if (mode == 2) {  // remote loads after the barrier instead
+            cl.sync();
+            if (threadIdx.x < senders * 16) acc += cl.map_shared_rank(&buf[b][0], threadIdx.x % 16)[threadIdx.x / 16];
+        }
+        cl.sync();
+        acc += buf[b][threadIdx.x & 63];
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = acc;
+}
+
 int main() {
     double* out;
     unsigned* bar;
@@ -145,6 +173,19 @@ int main() {
         cudaEventElapsedTime(&ms, a, b);
         printf("cluster(16) sync: %.3f us/barrier (%s)\n", ms * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
     }
+    for (int mode = 0; mode < 3; ++mode)
+        for (int senders : {1, 4, 19, 32}) {
+            cudaFuncSetAttribute((const void*)k_cluster_push, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            k_cluster_push<<<16, 256>>>(iters, senders, mode, out);
+            cudaEventRecord(a);
+            k_cluster_push<<<16, 256>>>(iters, senders, mode, out);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            printf("cluster push mode %d senders %2d: %.3f us/iter (%s)\n", mode, senders, ms * 1e3 / iters,
+                   cudaGetErrorString(cudaGetLastError()));
+        }
     {
         // back-to-back empty kernels in a graph: per-launch overhead
         cudaStream_t s;
