@@ -121,6 +121,8 @@ int fkb_filter_set_solver(fkb_filter* f, int mode);
 int fkb_filter_eig_sweeps(fkb_filter* f);
 /* last step's capacitance solve: PCG iterations and whether the exact Cholesky fallback ran */
 int fkb_filter_cap_stats(fkb_filter* f, int* iterations, int* fallback);
+/* profiling aid: 64 %globaltimer stamps of the last PCG launch (needs FKB_PCG_STAMPS=1) */
+int fkb_filter_pcg_stamps(fkb_filter* f, unsigned long long* out);
 /* eigenpairs of G (θ unsorted, P m×m column-major) */
 int fkb_filter_get_eig(fkb_filter* f, double* theta, double* P);
 /* runs `reps` real steps un-graphed with CUDA events at phase boundaries; ms[i] = mean

@@ -381,6 +381,16 @@ int fkb_filter_set_solver(fkb_filter* f, int mode) {
     });
 }
 int fkb_filter_eig_sweeps(fkb_filter* f) { return f ? f->f->eig_sweeps : 0; }
+int fkb_filter_pcg_stamps(fkb_filter* f, unsigned long long* out) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (!F.pcg_ts.p) throw std::invalid_argument("PCG stamps need FKB_PCG_STAMPS=1 at fkf_init");
+        FKB_CUDA(cudaMemcpyAsync(out, F.pcg_ts.p, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+
 int fkb_filter_cap_stats(fkb_filter* f, int* iterations, int* fallback) {
     return guarded([&] {
         need(f, "filter");

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         for (int e = tid; e < cnt; e += PC_T) cp_async8(Ks + e, K + (long long)(r0 + e / n) * ld + e % n);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    __syncthreads();  // mbarrier initialized before anyone waits on it
     // Pipelined Jacobi-PCG (Ghysels–Vanroose): the matvec n = K·m and the reductions
     // γ = rᵀu, δ = wᵀu of the same iteration are independent, so one cluster exchange per
     // iteration carries both: owners push m into every CTA and every CTA pushes its

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "eig.cuh"
@@ -96,19 +97,64 @@ __global__ void k_prep(int m, int r, const double* __restrict__ theta, const dou
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) sqd[j] = sqrt(d[j]);
 }
 
-// u_j = sqd_j · Σ_i E_ij · (wsq_i · rt_i)   (F̃ᵀx̃ of the capacitance system)
-struct EpiScaleOut {
-    double* u;
-    const double* sc;
-    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sc[j] * v; }
-};
-// s̃_i = wsq_i · (rt_i + Σ_j E_ij · (sqd_j · x_j))   ([Λ_M − EDEᵀ]⁻¹ r̃ via Woodbury)
-struct EpiWoodbury {
-    double* st;
-    const double* wsq;
-    const double* rt;
-    __device__ __forceinline__ void operator()(long long i, double v) const { st[i] = wsq[i] * (rt[i] + v); }
-};
+// u_j = sqd_j · Σ_i E_ij · wsq_i · r̃_i  (right-hand side of the capacitance system); CTA j
+__global__ void __launch_bounds__(256) k_cap_rhs(int m, const double* __restrict__ E, const double* __restrict__ wsq,
+                                                const double* __restrict__ rt, const double* __restrict__ sqd,
+                                                double* __restrict__ u) {
+    const int j = blockIdx.x;
+    const double* Ec = E + (long long)j * m;
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = 0.0;
+    for (int i0 = 0; i0 < m; i0 += 8 * 256) {
+        double e[8], w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int i = i0 + threadIdx.x + q * 256;
+            e[q] = i < m ? Ec[i] : 0.0;
+            w[q] = i < m ? wsq[i] * rt[i] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = fma(e[q], w[q], a[q]);
+    }
+    double v = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += red[w];
+        u[j] = sqd[j] * t;
+    }
+}
+
+// s̃_i = wsq_i · (r̃_i + Σ_j E_ij · (sqd_j · x_j))   ([Λ_M − EDEᵀ]⁻¹ r̃ via Woodbury); warp per
+// row of the row-major E copy, every load of the row in flight
+__global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double* __restrict__ Erow,
+                                                    const double* __restrict__ sqd, const double* __restrict__ x,
+                                                    const double* __restrict__ wsq, const double* __restrict__ rt,
+                                                    double* __restrict__ st) {
+    const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (i >= m) return;
+    const double* er = Erow + (long long)i * r;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < r; j0 += 32 * 16) {
+        double e[16], y[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int j = j0 + lane + 32 * q;
+            e[q] = j < r ? er[j] : 0.0;
+            y[q] = j < r ? sqd[j] * x[j] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc = fma(e[q], y[q], acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) st[i] = wsq[i] * (rt[i] + acc);
+}
+
 // mean_i ← (mean_i + α·t_i) − Σ_j U_ij (d_j c_j)   (fast_filter.hpp:114-116), skipped on LLT failure
 struct EpiMean {
     double* mean;
@@ -373,6 +419,10 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
             g.B = B.p; g.ldb = m;
             g.C = E.p; g.ldc = m;
             gemm(g, nullptr, s);
+            Erow.alloc(size_t(m) * r);  // row-major copy for the per-step s̃ rows
+            k_transpose<<<dim3(ceil_div(m, 32), ceil_div(r, 32)), dim3(32, 8), 0, s>>>(m, r, E.p, Erow.p);
+            FKB_LAUNCH_CHECK();
+            count_launch();
         }
         S.release();
     }
@@ -390,6 +440,7 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     gpart.alloc(size_t(592) * 32 + size_t(std::max(m, 1)) + 64);  // split-GEMV partials
     pcgwork.alloc(size_t(std::max(r, 1)) + 1);
     pcgflag.alloc(1);
+    if (std::getenv("FKB_PCG_STAMPS")) pcg_ts.alloc(64);
     {
         GemmArgs g;  // split-K workspace of the capacitance Gram
         g.M = r; g.N = r; g.K = m;
@@ -502,7 +553,10 @@ void Filter::enqueue_solve_woodbury() {
     launch_gemv_cols(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, gpart.p);  // r̃ = Pᵀ(y − H·mean)
     mark("rotate_in");
     if (r > 0) {
-        launch_gemv_cols(m, r, E.p, m, XProd{wsq.p, rt.p}, EpiScaleOut{ucap.p, sqd.p}, s, gpart.p);
+        // u = D^½·Eᵀ·Λ_M⁻¹·r̃: one CTA per column of E
+        k_cap_rhs<<<r, 256, 0, s>>>(m, E.p, wsq.p, rt.p, sqd.p, ucap.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
         GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½ (lower tiles)
         g.M = r; g.N = r; g.K = m;
         g.A = E.p; g.lda = m; g.transA = 1;
@@ -516,11 +570,14 @@ void Filter::enqueue_solve_woodbury() {
         gram(g, ws_step.p, s);
         mark("capacitance");
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
-        cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s);
+        cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s, 200, 1e-14, pcg_ts.p);
         chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
         mark("cap_solve");
     }
-    launch_gemv_rows(m, r, E.p, m, XProd{sqd.p, ucap.p}, EpiWoodbury{st.p, wsq.p, rt.p}, s, gpart.p);
+    // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
+    k_woodbury_st<<<std::max(1, ceil_div(m, 8)), 256, 0, s>>>(m, r, Erow.p, sqd.p, ucap.p, wsq.p, rt.p, st.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
     launch_gemv_rows(m, m, P.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s, gpart.p);  // z = P·s̃
     mark("rotate_out");
 }
