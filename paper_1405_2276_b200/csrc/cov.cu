@@ -13,9 +13,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numbers>
 #include <sstream>
+#include <type_traits>
 
 #include "cov.cuh"
 #include "fft_device.cuh"
@@ -183,6 +185,131 @@ __global__ void __launch_bounds__(kThreads) k_rows_inv(const double2* __restrict
     }
 }
 
+// ---- single-vector path (the per-step Γ(Hᵀz)).  One transform per CTA with a radix-≤8
+// schedule and n/8 threads, so each thread's serial chain is a few radix-8 butterflies (the
+// batched radix-16 kernels keep one butterfly per thread busy for ~4× longer); twiddles are
+// staged in shared memory alongside the data.
+
+// Every global load of a kernel is issued before the first shared-memory store (≤ 8 elements
+// per thread since blockDim ≥ n/8), so the load phase costs one memory latency, not eight.
+constexpr int kEpt = 8;
+
+// Pass A: CTA = real rows 2b, 2b+1 (two-for-one) → W[ky][ix].
+template <int NT>
+__global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x, int nx, int ny, FftLen fy,
+                                                   double2* __restrict__ W) {
+    extern __shared__ double2 sm[];
+    const int my = fy.n, nky = my / 2 + 1, T = blockDim.x;
+    double2* tw = sm;
+    double2* a = sm + my;
+    double2* b = a + my;
+    const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
+    double2 tv[kEpt];
+    double v0[kEpt], v1[kEpt];
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int iy = threadIdx.x + q * T;
+        tv[q] = iy < my ? fy.tw[iy] : make_double2(0.0, 0.0);
+        v0[q] = iy < ny ? x[(long long)r0 * ny + iy] : 0.0;
+        v1[q] = (iy < ny && r1 < nx) ? x[(long long)r1 * ny + iy] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int iy = threadIdx.x + q * T;
+        if (iy < my) {
+            tw[iy] = tv[q];
+            a[iy] = make_double2(v0[q], v1[q]);
+        }
+    }
+    __syncthreads();
+    const double2* z = NT ? fft_block_c<-1, (NT ? NT : 1)>(a, b, tw) : fft_block<-1>(a, b, fy, tw);
+    for (int ky = threadIdx.x; ky < nky; ky += T) {
+        const double2 p = z[ky];
+        const double2 q = cconj(z[ky == 0 ? 0 : my - ky]);
+        W[(long long)ky * nx + r0] = make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));      // (Z + conj Z−)/2
+        if (r1 < nx) W[(long long)ky * nx + r1] = make_double2(0.5 * (p.y - q.y), -0.5 * (p.x - q.x));  // /(2i)
+    }
+}
+
+// Pass B: CTA = column ky: zero-pad, FFT, × spectrum, iFFT, keep ix < nx.
+template <int NT>
+__global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx, FftLen fx,
+                                               const double* __restrict__ spec_half) {
+    extern __shared__ double2 sm[];
+    const int mx = fx.n, T = blockDim.x;
+    double2* tw = sm;
+    double2* a = sm + mx;
+    double2* b = a + mx;
+    double2* w = W + (long long)blockIdx.x * nx;
+    const double* sp = spec_half + (long long)blockIdx.x * mx;
+    double2 tv[kEpt], dv[kEpt];
+    double spv[kEpt];
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int ix = threadIdx.x + q * T;
+        tv[q] = ix < mx ? fx.tw[ix] : make_double2(0.0, 0.0);
+        dv[q] = ix < nx ? w[ix] : make_double2(0.0, 0.0);
+        spv[q] = ix < mx ? __ldg(sp + ix) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int ix = threadIdx.x + q * T;
+        if (ix < mx) {
+            tw[ix] = tv[q];
+            a[ix] = dv[q];
+        }
+    }
+    __syncthreads();
+    double2* f = NT ? fft_block_c<-1, (NT ? NT : 1)>(a, b, tw) : fft_block<-1>(a, b, fx, tw);
+    double2* g = (f == a) ? b : a;
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int kx = threadIdx.x + q * T;
+        if (kx < mx) f[kx] = cscale(f[kx], spv[q]);
+    }
+    __syncthreads();
+    f = NT ? fft_block_c<+1, (NT ? NT : 1)>(f, g, tw) : fft_block<+1>(f, g, fx, tw);
+    for (int ix = threadIdx.x; ix < nx; ix += T) w[ix] = f[ix];
+}
+
+// Pass C: CTA = rows 2b, 2b+1 rebuilt from the Hermitian half, ×scale, crop.
+template <int NT>
+__global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ W, int nx, int ny, FftLen fy,
+                                                   double* __restrict__ y, double scale) {
+    extern __shared__ double2 sm[];
+    const int my = fy.n, T = blockDim.x;
+    double2* tw = sm;
+    double2* a = sm + my;
+    double2* b = a + my;
+    const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
+    double2 tv[kEpt], x1[kEpt], x2[kEpt];
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int ky = threadIdx.x + q * T;
+        const int kk = ky > my / 2 ? my - ky : ky;
+        tv[q] = ky < my ? fy.tw[ky] : make_double2(0.0, 0.0);
+        x1[q] = ky < my ? W[(long long)kk * nx + r0] : make_double2(0.0, 0.0);
+        x2[q] = (ky < my && r1 < nx) ? W[(long long)kk * nx + r1] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+        const int ky = threadIdx.x + q * T;
+        if (ky < my) {
+            tw[ky] = tv[q];
+            double2 u1 = x1[q], u2 = x2[q];
+            if (ky > my / 2) { u1 = cconj(u1); u2 = cconj(u2); }
+            a[ky] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
+        }
+    }
+    __syncthreads();
+    const double2* z = NT ? fft_block_c<+1, (NT ? NT : 1)>(a, b, tw) : fft_block<+1>(a, b, fy, tw);
+    for (int iy = threadIdx.x; iy < ny; iy += T) {
+        const double2 v = z[iy];
+        y[(long long)r0 * ny + iy] = v.x * scale;
+        if (r1 < nx) y[(long long)r1 * ny + iy] = v.y * scale;
+    }
+}
+
 // Sampler pass 1: draw amp·(n_re + i n_im) on the torus for a tile of ky columns,
 // inverse FFT along x, keep ix < nx → T[ky][ix] (full ky range).
 __global__ void __launch_bounds__(kThreads) k_sampler_cols(const double* __restrict__ amp, int my, int nx,
@@ -241,7 +368,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_rows(const double2* __rest
 }
 
 // --------------------------------------------------------------------------- host orchestration
-static void plan_radices(FftLen& L, int n) {
+static void plan_radices(FftLen& L, int n, bool max8 = false) {
     L.n = n;
     L.npass = 0;
     int v = n;
@@ -249,6 +376,8 @@ static void plan_radices(FftLen& L, int n) {
         if (L.npass >= kMaxPasses) throw std::runtime_error("fft: too many passes");
         L.radix[L.npass++] = r;
     };
+    if (max8)
+        while (v % 8 == 0) { push(8); v /= 8; }
     while (v % 16 == 0) { push(16); v /= 16; }
     if (v % 8 == 0) { push(8); v /= 8; }
     if (v % 4 == 0) { push(4); v /= 4; }
@@ -313,6 +442,10 @@ bool Cov::try_spectrum(double& worst) {  // covariance.hpp:264-298
     nky = my / 2 + 1;
     setup_len(fx, twx, mx);
     setup_len(fy, twy, my);
+    fx8 = fx;  // same twiddle tables, radix ≤ 8 schedules for the single-vector kernels
+    fy8 = fy;
+    plan_radices(fx8, mx, true);
+    plan_radices(fy8, my, true);
     // Symbol on the torus at wrapped distances (:269-277), evaluated on the host with the
     // reference formula (std::cyl_bessel_k); only the unique quarter is evaluated.
     const double dx = lx / nx, dy = ly / ny;
@@ -386,9 +519,64 @@ std::vector<double> Cov::spectrum_host() const {
     return amp;
 }
 
+// threads per transform of the single-vector kernels: n/8 (one radix-8 butterfly each per
+// pass), a multiple of 32 in [32, 256]
+static int threads_1(int n) { return std::max(32, ((n / kEpt + 31) / 32) * 32); }
+
+template <int NT>
+static void set_smem_1() {
+    set_smem((const void*)k_rows_fwd_1<NT>, 0);
+    set_smem((const void*)k_cols_1<NT>, 0);
+    set_smem((const void*)k_rows_inv_1<NT>, 0);
+}
+
+// launch one of the three single-vector passes with a compile-time length when n is a
+// supported power of two (radix-8 schedule folded to constants), else the runtime plan
+template <class F>
+static void with_len(int n, F&& f) {
+    switch (n) {
+        case 64: f(std::integral_constant<int, 64>{}); break;
+        case 128: f(std::integral_constant<int, 128>{}); break;
+        case 256: f(std::integral_constant<int, 256>{}); break;
+        case 512: f(std::integral_constant<int, 512>{}); break;
+        case 1024: f(std::integral_constant<int, 1024>{}); break;
+        case 2048: f(std::integral_constant<int, 2048>{}); break;
+        default: f(std::integral_constant<int, 0>{}); break;
+    }
+}
+
+void Cov::apply1(const double* dx, double* dy) {
+    static bool attr = false;
+    if (!attr) {
+        for (int n : {64, 128, 256, 512, 1024, 2048, 0}) with_len(n, [](auto c) { set_smem_1<decltype(c)::value>(); });
+        attr = true;
+    }
+    const size_t sy = 3 * size_t(my) * sizeof(double2), sx = 3 * size_t(mx) * sizeof(double2);
+    if (sy > 227 * 1024 || sx > 227 * 1024 || threads_1(mx) > 256 || threads_1(my) > 256)
+        throw std::invalid_argument("fft: transform too large for the single-vector kernels");
+    with_len(my, [&](auto c) {
+        k_rows_fwd_1<decltype(c)::value><<<ceil_div(nx, 2), threads_1(my), sy, stream>>>(dx, nx, ny, fy8, work.p);
+    });
+    FKB_LAUNCH_CHECK();
+    with_len(mx, [&](auto c) {
+        k_cols_1<decltype(c)::value><<<nky, threads_1(mx), sx, stream>>>(work.p, nx, fx8, spec_half.p);
+    });
+    FKB_LAUNCH_CHECK();
+    with_len(my, [&](auto c) {
+        k_rows_inv_1<decltype(c)::value><<<ceil_div(nx, 2), threads_1(my), sy, stream>>>(work.p, nx, ny, fy8, dy,
+                                                                                        1.0 / double(M()));
+    });
+    FKB_LAUNCH_CHECK();
+    count_launch(3);
+}
+
 void Cov::apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy) {
     if (ncols <= 0) return;
     ++applies;
+    if (ncols == 1) {
+        apply1(dX, dY);
+        return;
+    }
     // Few columns (the per-step Γ(Hᵀz)): one transform per CTA and narrow CTAs so the three
     // passes still spread over the SMs; wide blocks of columns keep the batched shapes.
     const bool narrow = ncols < 8;

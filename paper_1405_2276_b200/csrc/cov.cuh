@@ -22,6 +22,7 @@ struct Cov {
     int mx = 0, my = 0, nky = 0;  // nky = my/2 + 1 (Hermitian half along y)
     cudaStream_t stream = nullptr;
     FftLen fx, fy;
+    FftLen fx8, fy8;  // radix ≤ 8 schedules (single-vector kernels), same twiddle tables
     DBuf<double2> twx, twy;
     DBuf<double> spec_half;  // [ky][kx], clipped ≥ 0 (covariance.hpp:295)
     DBuf<double> amp_full;   // √spectrum on the full torus, row-major mx×my (sampler :339)
@@ -35,6 +36,7 @@ struct Cov {
 
     // Y = Γ X, X/Y column-major device blocks (covariance.hpp:101-115); Y may alias X.
     void apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy);
+    void apply1(const double* dx, double* dy);  // single vector (warp-per-transform kernels)
     // Two N(0,Γ) draws (covariance.hpp:332-353) into device vectors.
     void sample_pair(uint64_t seed, uint64_t stream_id, double* da, double* db);
     // Host copy of the full clipped spectrum (covariance.hpp:207-211), row-major mx×my.

@@ -170,4 +170,102 @@ __device__ double2* fft_smem(double2* a, double2* b, const FftLen& L, int batch)
     return in;
 }
 
+// Generic-thread-range Stockham pass (same arithmetic as stockham_pass): threads t0, t0+nt, …
+// of the caller cover the butterflies of ONE transform; twiddles from `tw` (shared memory).
+template <int R, int SIGN>
+__device__ __forceinline__ void stockham_pass_r(const double2* __restrict__ in, double2* __restrict__ out, int n,
+                                                const double2* __restrict__ tw, int Ns, int t0, int nt) {
+    const int nb = n / R;
+    const int tws = n / (Ns * R);
+    for (int j = t0; j < nb; j += nt) {
+        const int k = j % Ns;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
+        if (Ns > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 w = tw[r * k * tws];
+                if (SIGN > 0) w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+        }
+        dft<R, SIGN>(v);
+        const int d = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[d + r * Ns] = v[r];
+    }
+}
+
+// One transform of length L.n per CTA (all blockDim.x threads), twiddle table in shared
+// memory.  Returns the result buffer.  Caller must __syncthreads() after filling a and tw.
+template <int SIGN>
+__device__ double2* fft_block(double2* a, double2* b, const FftLen& L, const double2* tw) {
+    double2* in = a;
+    double2* out = b;
+    int Ns = 1;
+    for (int p = 0; p < L.npass; ++p) {
+        const int R = L.radix[p];
+        switch (R) {
+            case 16: stockham_pass_r<16, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+            case 8: stockham_pass_r<8, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+            case 4: stockham_pass_r<4, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+            case 2: stockham_pass_r<2, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+            case 3: stockham_pass_r<3, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+            case 5: stockham_pass_r<5, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+            default: stockham_pass_r<7, SIGN>(in, out, L.n, tw, Ns, threadIdx.x, blockDim.x); break;
+        }
+        __syncthreads();
+        double2* t = in;
+        in = out;
+        out = t;
+        Ns *= R;
+    }
+    return in;
+}
+
+// ---- compile-time schedules for power-of-two lengths (single-vector kernels): radix-8
+// passes then one radix-2/4 pass; Ns, strides and index math fold to constants.
+template <int R, int SIGN, int N, int NS>
+__device__ __forceinline__ void stockham_pass_c(const double2* __restrict__ in, double2* __restrict__ out,
+                                                const double2* __restrict__ tw) {
+    constexpr int nb = N / R, tws = N / (NS * R);
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+        const int k = j % NS;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
+        if constexpr (NS > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 w = tw[r * k * tws];
+                if (SIGN > 0) w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+        }
+        dft<R, SIGN>(v);
+        const int d = (j / NS) * NS * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[d + r * NS] = v[r];
+    }
+}
+
+template <int N>
+constexpr int static_radix(int ns) {  // radix of the pass that starts at stride ns
+    return (N / ns) % 8 == 0 ? 8 : N / ns;
+}
+
+// Returns the result buffer (a or b); caller __syncthreads() after filling a and tw.
+template <int SIGN, int N, int NS = 1>
+__device__ __forceinline__ double2* fft_block_c(double2* a, double2* b, const double2* tw) {
+    if constexpr (NS >= N) {
+        return a;
+    } else {
+        constexpr int R = static_radix<N>(NS);
+        stockham_pass_c<R, SIGN, N, NS>(a, b, tw);
+        __syncthreads();
+        return fft_block_c<SIGN, N, NS * R>(b, a, tw);
+    }
+}
+
 }  // namespace fkb

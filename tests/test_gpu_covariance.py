@@ -77,6 +77,19 @@ def test_baseline_tori_and_apply(name):
     assert rel_err(gpu.apply(X), orc.apply(X)) < 1e-12
 
 
+@pytest.mark.parametrize("nx,ny,lx,ly", GRIDS + [(256, 256, 1.0, 1.0), (128, 96, 1.5, 1.0)])
+def test_single_vector_path_matches_batched(nx, ny, lx, ly):
+    """The per-step Γ·x path (warp-per-transform kernels) against the batched kernels and the
+    oracle on the same vectors."""
+    gpu, orc = _pair(nx, ny, lx, ly, EXPERIMENT)
+    X = O.gaussian_matrix(nx * ny, 8, 13, 0)
+    Yb = gpu.apply(X)
+    for j in (0, 5):
+        y1 = gpu.apply(np.ascontiguousarray(X[:, j]))
+        assert rel_err(y1, Yb[:, j]) < 1e-14
+        assert rel_err(y1, orc.apply(np.ascontiguousarray(X[:, j]))) < 1e-12
+
+
 def test_embedding_failure_names_the_kernel():  # test_kernel_covariance.cpp:304-320
     with pytest.raises(RuntimeError, match="powered-exponential.*theta"):
         P.CovarianceOperator(P.Grid(16, 16), P.KernelSpec(family=0, theta=1.0, length=2.0, power=2.0))
