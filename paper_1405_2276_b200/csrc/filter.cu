@@ -61,8 +61,6 @@ __global__ void k_colsq(long long n, const double* __restrict__ U, double* __res
     }
 }
 
-__global__ void k_step_begin(double* alpha_dev) { alpha_dev[1] = alpha_dev[0] + 1.0; }  // α ← α + 1 (:97)
-
 // out (cols×rows... row-major copy): out[i·r + j] = in[i + j·n]  (32×32 tiles through smem)
 __global__ void k_transpose(long long n, int r, const double* __restrict__ in, double* __restrict__ out) {
     __shared__ double t[32][33];
@@ -81,54 +79,74 @@ __global__ void k_transpose(long long n, int r, const double* __restrict__ in, d
     }
 }
 
-// Step prologue of the Woodbury solver: α ← α + 1 (fast_filter.hpp:97), clears the failure
-// flags, and the per-step scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j.
-__global__ void k_prep(int m, int r, const double* __restrict__ theta, const double* __restrict__ d,
-                       double* alpha_dev, double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
-                       int* __restrict__ info, int* __restrict__ pcgflag) {
+// Step prologue fused with the residual (fast_filter.hpp:97, :108): α ← α + 1, failure flags
+// cleared, Woodbury scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j (when wsq ≠ null),
+// and z_i = y_i − H_i·mean with one warp per ray: every lane prefetches 16 (col, val) pairs,
+// then gathers the 16 mean values — two memory latencies per 512 nonzeros.
+__global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* __restrict__ rp,
+                                                      const int* __restrict__ ci, const double* __restrict__ hv,
+                                                      const double* __restrict__ mean, const double* __restrict__ y,
+                                                      double* __restrict__ z, double* alpha_dev,
+                                                      const double* __restrict__ theta, const double* __restrict__ d,
+                                                      double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
+                                                      int* __restrict__ info, int* __restrict__ pcgflag) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const double alpha = alpha_dev[0] + 1.0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (gid == 0) {
         alpha_dev[1] = alpha;
         *info = 0;
-        *pcgflag = 0;
+        if (pcgflag) *pcgflag = 0;
     }
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-        wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) sqd[j] = sqrt(d[j]);
-}
-
-// u_j = sqd_j · Σ_i E_ij · wsq_i · r̃_i  (right-hand side of the capacitance system); CTA j
-__global__ void __launch_bounds__(256) k_cap_rhs(int m, const double* __restrict__ E, const double* __restrict__ wsq,
-                                                const double* __restrict__ rt, const double* __restrict__ sqd,
-                                                double* __restrict__ u) {
-    const int j = blockIdx.x;
-    const double* Ec = E + (long long)j * m;
-    double a[8];
+    if (wsq) {
+        for (int i = gid; i < m; i += nthreads) wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
+        for (int j = gid; j < r; j += nthreads) sqd[j] = sqrt(d[j]);
+    }
+    const int row = gid >> 5, lane = threadIdx.x & 31;
+    if (row >= m) return;
+    const int e0 = rp[row], e1 = rp[row + 1];
+    double s = 0.0;
+    for (int eb = e0; eb < e1; eb += 32 * 16) {
+        int c[16];
+        double w[16], xv[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = 0.0;
-    for (int i0 = 0; i0 < m; i0 += 8 * 256) {
-        double e[8], w[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int i = i0 + threadIdx.x + q * 256;
-            e[q] = i < m ? Ec[i] : 0.0;
-            w[q] = i < m ? wsq[i] * rt[i] : 0.0;
+        for (int q = 0; q < 16; ++q) {
+            const int e = eb + lane + 32 * q;
+            c[q] = e < e1 ? ci[e] : 0;
+            w[q] = e < e1 ? hv[e] : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = fma(e[q], w[q], a[q]);
-    }
-    double v = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __shared__ double red[8];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
+        for (int q = 0; q < 16; ++q) xv[q] = __ldg(mean + c[q]);
 #pragma unroll
-        for (int w = 0; w < 8; ++w) t += red[w];
-        u[j] = sqd[j] * t;
+        for (int q = 0; q < 16; ++q) s = fma(w[q], xv[q], s);
     }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) z[row] = y[row] - s;
 }
+
+// u_j = sqd_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃))
+struct EpiScaleOut {
+    double* u;
+    const double* sc;
+    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sc[j] * v; }
+};
+// (Bᵀz)_j → dc_j = d_j·(Bᵀz)_j for the mean update, then d_j ← (d_j + αλ_j(α − d_j)) /
+// (1 + λ_j(α − d_j)) (fast_filter.hpp:114-123); column 0 commits α.  Skipped when the step
+// failed (*info).
+struct EpiCtzD {
+    double* dc;
+    double* d;
+    const double* lam;
+    double* alpha_dev;
+    const int* info;
+    __device__ __forceinline__ void operator()(long long j, double v) const {
+        if (*info) return;
+        const double alpha = alpha_dev[1];
+        const double dj = d[j], l = lam[j], c = alpha - dj;
+        dc[j] = dj * v;
+        d[j] = (dj + alpha * l * c) / (1.0 + l * c);
+        if (j == 0) alpha_dev[0] = alpha;
+    }
+};
 
 // s̃_i = wsq_i · (r̃_i + Σ_j E_ij · (sqd_j · x_j))   ([Λ_M − EDEᵀ]⁻¹ r̃ via Woodbury); warp per
 // row of the row-major E copy, every load of the row in flight
@@ -412,6 +430,10 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
         S.alloc(size_t(m) * m);
         FKB_CUDA(cudaMemcpyAsync(S.p, G.p, sizeof(double) * size_t(m) * m, cudaMemcpyDeviceToDevice, s));
         eig_sweeps = sym_eig_device(m, S.p, m, theta.p, P.p, s);
+        Pt.alloc(size_t(m) * m);  // Pᵀ (row-major P) for the per-step z = P·s̃ column dots
+        k_transpose<<<dim3(ceil_div(m, 32), ceil_div(m, 32)), dim3(32, 8), 0, s>>>(m, m, P.p, Pt.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
         if (r > 0) {
             GemmArgs g;
             g.M = m; g.N = r; g.K = m;
@@ -521,43 +543,47 @@ void Filter::set_solver(int mode) {
 }
 
 void Filter::enqueue_step(const double* d_y) {
-    if (solver == 1) {
-        const int pb = std::max(1, std::min(ceil_div(std::max(m, r), 256), 148));
-        k_prep<<<pb, 256, 0, s>>>(m, r, theta.p, d.p, alpha_dev.p, sigma2, wsq.p, sqd.p, info.p, pcgflag.p);
-    } else {
-        FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
-        k_step_begin<<<1, 1, 0, s>>>(alpha_dev.p);
+    // α ← α + 1, flags, Woodbury scalars, z = y − H·mean (:97, :108): one kernel
+    {
+        const bool wb = solver == 1;
+        const int blocks = std::max(1, ceil_div((long long)std::max(m, 1) * 32, 256));
+        k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
+                                               theta.p, d.p, sigma2, wb ? wsq.p : nullptr, wb ? sqd.p : nullptr,
+                                               info.p, wb ? pcgflag.p : nullptr);
+        FKB_LAUNCH_CHECK();
+        count_launch();
     }
-    FKB_LAUNCH_CHECK();
-    count_launch();
-    // z = y − H·mean (:108), one fused SpMV
-    spmm(H, mean.p, n, 1, z.p, m, -1.0, 1.0, s, d_y);
     mark("residual");
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
-    // t = Γ(Hᵀz) = (ΓHᵀ)z ; c = Bᵀz
-    spmm(HT, z.p, m, 1, t.p, n, 1.0, 0.0, s);
+    // t = Γ(Hᵀz) = (ΓHᵀ)z
+    spmv_short(HT, z.p, t.p, 1.0, s);
+    mark("ht_z");
     cov->apply(t.p, n, 1, t.p, n);
-    if (r > 0) launch_gemv_cols(m, r, B.p, m, XPlain{z.p}, EpiAxpby{cvec.p, 1.0, 0.0}, s, gpart.p);
-    mark("gamma_ht_z");
-    launch_gemv_rowmajor(n, r, Urow.p, r, XProd{d.p, cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+    mark("gamma_apply");
+    // dc = d ⊙ Bᵀz, then d and α updated in the same pass; mean += α·t − U·dc (:114-123)
+    if (r > 0) {
+        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, s);
+        mark("ctz_d_update");
+        launch_gemv_rowmajor(n, r, Urow.p, r, XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+    } else {
+        launch_gemv_rowmajor(n, 0, Urow.p, 1, XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+        k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
     mark("mean_update");
-    k_d_update<<<std::max(1, ceil_div(r, 256)), 256, 0, s>>>(r, d.p, lambda.p, alpha_dev.p, info.p);
-    FKB_LAUNCH_CHECK();
-    count_launch();
-    mark("d_update");
 }
 
 // z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
 void Filter::enqueue_solve_woodbury() {
-    launch_gemv_cols(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, gpart.p);  // r̃ = Pᵀ(y − H·mean)
+    launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
     mark("rotate_in");
     if (r > 0) {
-        // u = D^½·Eᵀ·Λ_M⁻¹·r̃: one CTA per column of E
-        k_cap_rhs<<<r, 256, 0, s>>>(m, E.p, wsq.p, rt.p, sqd.p, ucap.p);
-        FKB_LAUNCH_CHECK();
-        count_launch();
-        GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½ (lower tiles)
+        // u = D^½·Eᵀ·Λ_M⁻¹·r̃
+        launch_coldot(m, r, E.p, m, XProd{wsq.p, rt.p}, EpiScaleOut{ucap.p, sqd.p}, s);
+        mark("cap_rhs");
+        GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
         g.M = r; g.N = r; g.K = m;
         g.A = E.p; g.lda = m; g.transA = 1;
         g.B = E.p; g.ldb = m;
@@ -578,7 +604,8 @@ void Filter::enqueue_solve_woodbury() {
     k_woodbury_st<<<std::max(1, ceil_div(m, 8)), 256, 0, s>>>(m, r, Erow.p, sqd.p, ucap.p, wsq.p, rt.p, st.p);
     FKB_LAUNCH_CHECK();
     count_launch();
-    launch_gemv_rows(m, m, P.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s, gpart.p);  // z = P·s̃
+    mark("woodbury_st");
+    launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s);  // z = P·s̃ (rows of P)
     mark("rotate_out");
 }
 

@@ -39,7 +39,7 @@ struct Filter {
     // solver = 0 reproduces the reference order: form S and LLT it (m×m) every step.
     int solver = 1;
     int eig_sweeps = 0;
-    DBuf<double> P, theta, E, Erow, wsq, sqd, rt, ucap, Kcap, st, rdg, gpart, pcgwork;
+    DBuf<double> P, Pt, theta, E, Erow, wsq, sqd, rt, ucap, Kcap, st, rdg, gpart, pcgwork;
     DBuf<unsigned long long> pcg_ts;  // %globaltimer stamps of the PCG kernel (FKB_PCG_STAMPS=1)
     DBuf<int> pcgflag;  // 1 when the capacitance PCG fell back to the cluster Cholesky
 

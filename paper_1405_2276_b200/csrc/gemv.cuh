@@ -239,4 +239,63 @@ inline void launch_gemv_cols(long long n, int k, const double* A, long long lda,
     count_launch(2);
 }
 
+// ---- single-launch column dots: out_j = epi(j, Σ_i A_ij·x_i) for column-major A (m×n).
+// A CTA owns CPC consecutive columns; each thread keeps its x values in registers (reused
+// over the CPC columns) and issues every load of a 2048-row chunk × CPC columns before the
+// first FMA, so a chunk costs one memory latency.  Fixed-order reductions (deterministic),
+// no split partials and no second kernel.
+template <class XL, class Epi, int CPC>
+__global__ void __launch_bounds__(256) k_coldot(int m, int n, const double* __restrict__ A, long long lda, XL xl,
+                                               Epi epi) {
+    constexpr int EPT = 8;
+    const int j0 = blockIdx.x * CPC;
+    double acc[CPC];
+#pragma unroll
+    for (int c = 0; c < CPC; ++c) acc[c] = 0.0;
+    for (int i0 = 0; i0 < m; i0 += 256 * EPT) {
+        double xv[EPT], e[CPC][EPT];
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int i = i0 + threadIdx.x + 256 * q;
+            xv[q] = i < m ? xl(i) : 0.0;
+#pragma unroll
+            for (int c = 0; c < CPC; ++c) e[c][q] = (i < m && j0 + c < n) ? A[i + (long long)(j0 + c) * lda] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < CPC; ++c)
+#pragma unroll
+            for (int q = 0; q < EPT; ++q) acc[c] = fma(e[c][q], xv[q], acc[c]);
+    }
+    __shared__ double red[8][CPC];
+#pragma unroll
+    for (int c = 0; c < CPC; ++c) {
+        double v = acc[c];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < CPC && j0 + threadIdx.x < n) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+        epi(j0 + threadIdx.x, v);
+    }
+}
+
+template <class XL, class Epi>
+inline void launch_coldot(int m, int n, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s) {
+    if (n <= 0) return;
+    if (n >= 8 * 296) {
+        k_coldot<XL, Epi, 8><<<(unsigned)((n + 7) / 8), 256, 0, s>>>(m, n, A, lda, xl, epi);
+    } else if (n >= 4 * 296) {
+        k_coldot<XL, Epi, 4><<<(unsigned)((n + 3) / 4), 256, 0, s>>>(m, n, A, lda, xl, epi);
+    } else if (n >= 2 * 296) {
+        k_coldot<XL, Epi, 2><<<(unsigned)((n + 1) / 2), 256, 0, s>>>(m, n, A, lda, xl, epi);
+    } else {
+        k_coldot<XL, Epi, 1><<<(unsigned)n, 256, 0, s>>>(m, n, A, lda, xl, epi);
+    }
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
 }  // namespace fkb
