@@ -128,20 +128,22 @@ def replica_throughput(local_ms: float, steps: int, world: int, device) -> float
 
 
 # ----------------------------------------------------------------------------- work accounting
-def phase_work(w, r, fft_flops):
-    """Algorithmic work per launch of each step phase."""
+def phase_work(w, r, fft_flops, nnz):
+    """Algorithmic work per launch of each step phase: unique bytes a
+    kernel must move for HBM-bound phases, minimal flops for arithmetic phases."""
     N, m = w.N, w.m
-    nnz = w.m * (2.5 * w.n)  # overwritten by the caller with the true nnz
     return {
-        "residual": ("hbm", None),
+        "residual": ("hbm", 12.0 * nnz + 4.0 * (m + 1) + 8.0 * N + 16.0 * m),
+        "capacitance": ("tensor", 1.0 * m * r * (r + 1)),  # symmetric Eᵀ·diag·E (lower half)
         "rotate_in": ("hbm", 8.0 * m * m + 16.0 * m),
-        "capacitance": ("tensor", 2.0 * m * r * r),
-        "cap_factor_solve": ("tensor", r ** 3 / 3.0 + 2.0 * r * r),
-        "rotate_out": ("hbm", 8.0 * m * m + 8.0 * m * r + 32.0 * m),
-        "gamma_ht_z": ("tensor", fft_flops),
-        "mean_update": ("hbm", 8.0 * N * r + 32.0 * N),
-        "d_update": ("hbm", 32.0 * r),
-        "_nnz": nnz,
+        "cap_rhs": ("hbm", 8.0 * m * r + 24.0 * m + 16.0 * r),
+        "cap_solve": ("hbm", 8.0 * r * r + 16.0 * r),
+        "woodbury_st": ("hbm", 8.0 * m * r + 32.0 * m + 16.0 * r),
+        "rotate_out": ("hbm", 8.0 * m * m + 16.0 * m),
+        "ctz_d_update": ("hbm", 8.0 * m * r + 8.0 * m + 48.0 * r),
+        "ht_z": ("hbm", 12.0 * nnz + 4.0 * (N + 1) + 8.0 * (N + m)),
+        "gamma_apply": ("tensor", fft_flops),
+        "mean_update": ("hbm", 8.0 * N * r + 24.0 * N + 8.0 * r),
     }
 
 
@@ -344,8 +346,7 @@ def run_ours(args, rank, world, local_rank):
     hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
     # ---- roofline of the dominant step phase
-    work = phase_work(w, r, fcol)
-    work["residual"] = ("hbm", 12.0 * h.nnz + 4.0 * (h.rows + 1) + 8.0 * (w.N + 2 * w.m))
+    work = phase_work(w, r, fcol, float(h.nnz))
     dom = max((kk for kk in phases if kk in work), key=lambda kk: phases[kk])
     bound, amount = work[dom]
     dom_ms = phases[dom]

@@ -5,7 +5,10 @@
 // Replaces the reference's Eigen products and LLT (fast_filter.hpp:100-108,
 // lowrank.hpp:186-205).
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cmath>
 
 #include "dense.cuh"
 #include "gemv.cuh"
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(QT) k_gram(GemmArgs g, int kchunk, double* __r
     extern __shared__ __align__(16) double qsm[];
     double* As = qsm;                       // [2][QB][QLD]
     double* Bs = qsm + 2 * QB * QLD;        // [2][QB][QLD]
+    double* Ws = qsm + 4 * QB * QLD;        // [2][QK] diagonal weights dA
     const int i0 = blockIdx.x * QB, j0 = blockIdx.y * QB;
     if (g.lower_only && j0 > i0 + QB - 1) return;
     const int kbeg = blockIdx.z * kchunk, kend = min(g.K, kbeg + kchunk);
@@ -220,6 +224,10 @@ __global__ void __launch_bounds__(QT) k_gram(GemmArgs g, int kchunk, double* __r
             cp_async16(As + (st * QB + row) * QLD + kc, g.A + gk + (long long)ga * g.lda, kv && ga < g.M, g.A);
             cp_async16(Bs + (st * QB + row) * QLD + kc, g.B + gk + (long long)gb * g.ldb, kv && gb < g.N, g.B);
         }
+        if (g.dA && tid < QK / 2) {  // the chunk's diagonal weights ride along with the tiles
+            const int gk = k0 + 2 * tid;
+            cp_async16(Ws + st * QK + 2 * tid, g.dA + gk, gk + 1 < kend, g.dA);
+        }
         cp_async_commit();
     };
     const int nk = (kend - kbeg + QK - 1) / QK;
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(QT) k_gram(GemmArgs g, int kchunk, double* __r
 #pragma unroll
         for (int kk = 0; kk < QK; kk += 4) {
             const int gk = kbeg + it * QK + kk + tq;
-            const double wk = (g.dA && gk < kend) ? __ldg(g.dA + gk) : 1.0;
+            const double wk = g.dA ? (gk < kend ? Ws[st * QK + kk + tq] : 0.0) : 1.0;
             double a[4], b[2];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(wm + mi * 8 + gq) * QLD + kk + tq];
@@ -291,7 +299,7 @@ void gram(const GemmArgs& g_in, double* ws, cudaStream_t s) {
     int kchunk = ((ceil_div(g.K, splitk) + QK - 1) / QK) * QK;
     splitk = ceil_div(g.K, kchunk);
     g.splitk = splitk;
-    const size_t smem = sizeof(double) * 4 * QB * QLD;
+    const size_t smem = sizeof(double) * (4 * QB * QLD + 2 * QK);
     static bool attr = false;
     if (!attr) {
         FKB_CUDA(cudaFuncSetAttribute((const void*)k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -306,6 +314,144 @@ void gram(const GemmArgs& g_in, double* ws, cudaStream_t s) {
         FKB_LAUNCH_CHECK();
         count_launch();
     }
+}
+
+// ---- symmetric Gram with cluster split-K: C = epi(Aᵀ·diag(dA)·A) for the per-step
+// capacitance K = I − D^½EᵀΛ_M⁻¹ED^½.  Only lower 64×64 tiles are computed (half the
+// DMMA work of the full product); the S CTAs of a cluster split K, park their partial tile
+// in shared memory and reduce it through DSMEM in rank order (deterministic, no workspace,
+// no second kernel); each CTA finalizes 64/S rows of the tile and writes them and their
+// mirror, so K is exactly symmetric.
+__global__ void __launch_bounds__(QT) k_gram_sym(GemmArgs g, int kchunk) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) double qsm[];
+    double* As = qsm;
+    double* Bs = qsm + 2 * QB * QLD;
+    double* Ws = qsm + 4 * QB * QLD;
+    cg::cluster_group cl = cg::this_cluster();
+    const int S = int(cl.num_blocks()), z = int(cl.block_rank());
+    int ti = int((std::sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= int(blockIdx.x)) ++ti;
+    while (ti * (ti + 1) / 2 > int(blockIdx.x)) --ti;
+    const int tj = int(blockIdx.x) - ti * (ti + 1) / 2;
+    const int i0 = ti * QB, j0 = tj * QB;
+    const int kbeg = z * kchunk, kend = min(g.K, kbeg + kchunk);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    auto load = [&](int st, int k0) {
+#pragma unroll
+        for (int q = 0; q < (QB * QK / 2) / QT; ++q) {
+            const int e = tid + q * QT;
+            const int row = e / (QK / 2), kc = (e % (QK / 2)) * 2;
+            const int gk = k0 + kc;
+            const int ga = i0 + row, gb = j0 + row;
+            const bool kv = gk + 1 < kend;
+            cp_async16(As + (st * QB + row) * QLD + kc, g.A + gk + (long long)ga * g.lda, kv && ga < g.M, g.A);
+            cp_async16(Bs + (st * QB + row) * QLD + kc, g.B + gk + (long long)gb * g.ldb, kv && gb < g.N, g.B);
+        }
+        if (g.dA && tid < QK / 2) {  // the chunk's diagonal weights ride along with the tiles
+            const int gk = k0 + 2 * tid;
+            cp_async16(Ws + st * QK + 2 * tid, g.dA + gk, gk + 1 < kend, g.dA);
+        }
+        cp_async_commit();
+    };
+    const int nk = kend > kbeg ? (kend - kbeg + QK - 1) / QK : 0;
+    if (nk > 0) load(0, kbeg);
+    for (int it = 0; it < nk; ++it) {
+        const int st = it & 1;
+        if (it + 1 < nk) {
+            load(st ^ 1, kbeg + (it + 1) * QK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* Ab = As + st * QB * QLD;
+        const double* Bb = Bs + st * QB * QLD;
+#pragma unroll
+        for (int kk = 0; kk < QK; kk += 4) {
+            const int gk = kbeg + it * QK + kk + tq;
+            const double wk = g.dA ? (gk < kend ? Ws[st * QK + kk + tq] : 0.0) : 1.0;
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(wm + mi * 8 + gq) * QLD + kk + tq];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bb[(wn + ni * 8 + gq) * QLD + kk + tq] * wk;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+    // partial tile → this CTA's shared memory (row-major, ld 65), then cluster-wide reduction
+    constexpr int PLD = QB + 1;
+    double* part = qsm;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                part[(wm + mi * 8 + gq) * PLD + wn + ni * 8 + tq * 2 + q] = acc[mi][ni][q];
+    cl.sync();
+    const int rows_per = QB / S;
+    for (int e = tid; e < rows_per * QB; e += QT) {
+        const int il = z * rows_per + e / QB, jl = e % QB;
+        double v = 0.0;
+        for (int c = 0; c < S; ++c) v += cl.map_shared_rank(part, c)[il * PLD + jl];
+        const int i = i0 + il, j = j0 + jl;
+        if (i >= g.M || j >= g.N || (ti == tj && i < j)) continue;
+        if (g.rs) v *= g.rs[i];
+        if (g.cs) v *= g.cs[j];
+        double out = g.alpha * v;
+        if (i == j) out += g.diag_add;
+        g.C[i + (long long)j * g.ldc] = out;
+        if (i != j) g.C[j + (long long)i * g.ldc] = out;
+    }
+    cl.sync();  // peers may still be reading this CTA's partial tile
+}
+
+void gram_sym(const GemmArgs& g_in, cudaStream_t s) {
+    GemmArgs g = g_in;
+    if (g.M <= 0) return;
+    if (g.M != g.N || g.A != g.B || g.lda != g.ldb || g.K <= 0 || (g.K & 1) || (g.lda & 1) || g.transA != 1 ||
+        g.transB != 0 || g.rs != g.cs || g.beta != 0.0 || g.beta_ptr) {
+        g.lower_only = 0;
+        gram(g, nullptr, s);  // general path (not expected on the step)
+        return;
+    }
+    const int nt = ceil_div(g.M, QB), tiles = nt * (nt + 1) / 2;
+    int S = 16;
+    while (S > 1 && (tiles * S > 2 * 148 || g.K / S < 2 * QK)) S >>= 1;
+    const int kchunk = ((ceil_div(g.K, S) + QK - 1) / QK) * QK;
+    const size_t smem = sizeof(double) * (4 * QB * QLD + 2 * QK);
+    static bool attr = false;
+    if (!attr) {
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_gram_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_gram_sym, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tiles, 1, S);
+    cfg.blockDim = dim3(QT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_[1];
+    attr_[0].id = cudaLaunchAttributeClusterDimension;
+    attr_[0].val.clusterDim.x = 1;
+    attr_[0].val.clusterDim.y = 1;
+    attr_[0].val.clusterDim.z = S;
+    cfg.attrs = attr_;
+    cfg.numAttrs = 1;
+    FKB_CUDA(cudaLaunchKernelEx(&cfg, k_gram_sym, g, kchunk));
+    count_launch();
 }
 
 size_t gram_ws_elems(int M, int N, int K) {

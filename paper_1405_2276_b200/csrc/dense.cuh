@@ -38,6 +38,9 @@ size_t gemm_ws_elems(const GemmArgs& g);
 // cp.async DMMA kernel; falls back to gemm() for odd K/ld.
 void gram(const GemmArgs& g, double* ws, cudaStream_t s);
 size_t gram_ws_elems(int M, int N, int K);
+// Symmetric Gram C = epi(Aᵀ·diag(dA)·A) (rs = cs, beta = 0): lower tiles, cluster split-K
+// reduced through DSMEM, both triangles written; one launch, no workspace.
+void gram_sym(const GemmArgs& g, cudaStream_t s);
 void gemm(const GemmArgs& g, double* ws, cudaStream_t s);
 int gemm_pick_splitk(int M, int N, int K);
 

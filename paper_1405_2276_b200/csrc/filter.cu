@@ -123,11 +123,34 @@ __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* 
     if (lane == 0) z[row] = y[row] - s;
 }
 
-// u_j = sqd_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃))
-struct EpiScaleOut {
+// Woodbury scalars of this step on the side branch (α of this step = α_prev + 1):
+// wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j.  Reads only state committed by the previous step.
+__global__ void k_woodbury_scalars(int m, int r, const double* __restrict__ alpha_dev,
+                                   const double* __restrict__ theta, const double* __restrict__ d, double sigma2,
+                                   double* __restrict__ wsq, double* __restrict__ sqd) {
+    const double alpha = alpha_dev[0] + 1.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) sqd[j] = sqrt(d[j]);
+}
+
+// x_i = r̃_i / (α θ_i + σ²) (Λ_M⁻¹ r̃ with this step's α, computed in place of wsq so the
+// capacitance RHS does not wait for the side branch)
+struct XWr {
+    const double* rt;
+    const double* theta;
+    const double* alpha_dev;
+    double sigma2;
+    __device__ __forceinline__ double operator()(long long i) const {
+        return __ldg(rt + i) / (alpha_dev[1] * __ldg(theta + i) + sigma2);
+    }
+};
+
+// u_j = √d_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃))
+struct EpiSqrtD {
     double* u;
-    const double* sc;
-    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sc[j] * v; }
+    const double* d;
+    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sqrt(d[j]) * v; }
 };
 // (Bᵀz)_j → dc_j = d_j·(Bᵀz)_j for the mean update, then d_j ← (d_j + αλ_j(α − d_j)) /
 // (1 + λ_j(α − d_j)) (fast_filter.hpp:114-123); column 0 commits α.  Skipped when the step
@@ -385,6 +408,9 @@ void Filter::ghep(long long k, long long p, uint64_t seed) {
 Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, const double* val, double sig2,
                long long k, long long p, uint64_t seed)
     : cov(c), s(c->stream), n(c->size()), m(m_), sigma2(sig2) {
+    FKB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     if (m < 0) throw std::invalid_argument("fkf_init: negative measurement count");
     if ((long long)h_cols != n) throw std::invalid_argument("fkf_init: H columns do not match state dimension");
     for (int i = 0; i < m; ++i)
@@ -480,6 +506,9 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
 
 Filter::~Filter() {
     if (graph) cudaGraphExecDestroy(graph);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s2) cudaStreamDestroy(s2);
 }
 
 void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
@@ -542,29 +571,65 @@ void Filter::set_solver(int mode) {
     graph_ready = false;
 }
 
+void Filter::fork() {
+    if (side() == s) return;
+    FKB_CUDA(cudaEventRecord(ev_fork, s));
+    FKB_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
+}
+void Filter::join() {
+    if (side() == s) return;
+    FKB_CUDA(cudaEventRecord(ev_join, s2));
+    FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+}
+
 void Filter::enqueue_step(const double* d_y) {
-    // α ← α + 1, flags, Woodbury scalars, z = y − H·mean (:97, :108): one kernel
+    const bool wb = solver == 1 && r > 0;
+    if (wb) {
+        // side branch: Woodbury scalars and the capacitance K depend only on α and d (state of
+        // the previous step), so they overlap the residual, r̃ = Pᵀz and the RHS on the main branch
+        fork();
+        cudaStream_t b = side();
+        k_woodbury_scalars<<<std::max(1, std::min(ceil_div(std::max(m, r), 256), 148)), 256, 0, b>>>(
+            m, r, alpha_dev.p, theta.p, d.p, sigma2, wsq.p, sqd.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
+        g.M = r; g.N = r; g.K = m;
+        g.A = E.p; g.lda = m; g.transA = 1;
+        g.B = E.p; g.ldb = m;
+        g.dA = wsq.p;
+        g.rs = sqd.p; g.cs = sqd.p;
+        g.alpha = -1.0;
+        g.C = Kcap.p; g.ldc = r;
+        g.diag_add = 1.0;
+        gram_sym(g, b);  // full symmetric K (the PCG reads columns)
+        mark("capacitance");
+    }
+    // α ← α + 1, flags, z = y − H·mean (:97, :108): one kernel
     {
-        const bool wb = solver == 1;
         const int blocks = std::max(1, ceil_div((long long)std::max(m, 1) * 32, 256));
         k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
-                                               theta.p, d.p, sigma2, wb ? wsq.p : nullptr, wb ? sqd.p : nullptr,
-                                               info.p, wb ? pcgflag.p : nullptr);
+                                               theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq.p : nullptr,
+                                               sqd.p, info.p, solver == 1 ? pcgflag.p : nullptr);
         FKB_LAUNCH_CHECK();
         count_launch();
     }
     mark("residual");
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
-    // t = Γ(Hᵀz) = (ΓHᵀ)z
+    // dc = d ⊙ Bᵀz with d and α updated in the same pass (side branch) ∥ t = Γ(Hᵀz) (main);
+    // then mean += α·t − U·dc (:114-123)
+    if (r > 0) {
+        fork();
+        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
+        mark("ctz_d_update");
+    }
     spmv_short(HT, z.p, t.p, 1.0, s);
     mark("ht_z");
     cov->apply(t.p, n, 1, t.p, n);
     mark("gamma_apply");
-    // dc = d ⊙ Bᵀz, then d and α updated in the same pass; mean += α·t − U·dc (:114-123)
     if (r > 0) {
-        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, s);
-        mark("ctz_d_update");
+        join();
         launch_gemv_rowmajor(n, r, Urow.p, r, XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
     } else {
         launch_gemv_rowmajor(n, 0, Urow.p, 1, XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
@@ -581,20 +646,9 @@ void Filter::enqueue_solve_woodbury() {
     mark("rotate_in");
     if (r > 0) {
         // u = D^½·Eᵀ·Λ_M⁻¹·r̃
-        launch_coldot(m, r, E.p, m, XProd{wsq.p, rt.p}, EpiScaleOut{ucap.p, sqd.p}, s);
+        launch_coldot(m, r, E.p, m, XWr{rt.p, theta.p, alpha_dev.p, sigma2}, EpiSqrtD{ucap.p, d.p}, s);
         mark("cap_rhs");
-        GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
-        g.M = r; g.N = r; g.K = m;
-        g.A = E.p; g.lda = m; g.transA = 1;
-        g.B = E.p; g.ldb = m;
-        g.dA = wsq.p;
-        g.rs = sqd.p; g.cs = sqd.p;
-        g.alpha = -1.0;
-        g.C = Kcap.p; g.ldc = r;
-        g.diag_add = 1.0;
-        g.lower_only = 0;  // full K: the PCG reads columns
-        gram(g, ws_step.p, s);
-        mark("capacitance");
+        join();  // K and the scalars from the side branch
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
         cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s, 200, 1e-14, pcg_ts.p);
         chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);

@@ -48,6 +48,14 @@ struct Filter {
     DBuf<int> info, flags;
     cudaGraphExec_t graph = nullptr;
     bool graph_ready = false;
+    // side stream for the independent branches of a step (captured into the same graph):
+    // fork() makes it wait for the main stream, join() makes the main stream wait for it.
+    // Phase timing runs the branches serially on the main stream.
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side() const { return phase_events ? s : s2; }
+    void fork();
+    void join();
     int launches_per_step = 0;
 
     // cached realization draws (RealizationPropagator, uq.hpp:86-112)
