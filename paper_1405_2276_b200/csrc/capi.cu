@@ -304,6 +304,7 @@ int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const 
         F.alpha = alpha;
         F.step_no = step;
         F.state_rank = rank;
+        F.k_valid = false;  // the precomputed capacitance belongs to the old (α, d)
     });
 }
 int fkb_filter_reset(fkb_filter* f) {

@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
 // Pass C: CTA = rows 2b, 2b+1 rebuilt from the Hermitian half, ×scale, crop.
 template <int NT>
 __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ W, int nx, int ny, FftLen fy,
-                                                   double* __restrict__ y, double scale) {
+                                                   double* __restrict__ y, double scale,
+                                                   const double* __restrict__ acc_coef, const int* __restrict__ gate) {
     extern __shared__ double2 sm[];
     const int my = fy.n, T = blockDim.x;
     double2* tw = sm;
@@ -303,6 +304,20 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
     }
     __syncthreads();
     const double2* z = NT ? fft_block_c<+1, (NT ? NT : 1)>(a, b, tw) : fft_block<+1>(a, b, fy, tw);
+    if (acc_coef) {  // y += c·Γx (the mean update's α·Γ(Hᵀz) term), skipped when *gate
+        if (gate && *gate) return;
+        const double c = *acc_coef;
+        for (int iy = threadIdx.x; iy < ny; iy += T) {
+            const double2 v = z[iy];
+            double* y0 = y + (long long)r0 * ny + iy;
+            *y0 = *y0 + c * (v.x * scale);
+            if (r1 < nx) {
+                double* y1 = y + (long long)r1 * ny + iy;
+                *y1 = *y1 + c * (v.y * scale);
+            }
+        }
+        return;
+    }
     for (int iy = threadIdx.x; iy < ny; iy += T) {
         const double2 v = z[iy];
         y[(long long)r0 * ny + iy] = v.x * scale;
@@ -546,6 +561,11 @@ static void with_len(int n, F&& f) {
 }
 
 void Cov::apply1(const double* dx, double* dy) {
+    apply1_fwd(dx);
+    apply1_inv(dy, nullptr, nullptr);
+}
+
+void Cov::apply1_fwd(const double* dx) {
     static bool attr = false;
     if (!attr) {
         for (int n : {64, 128, 256, 512, 1024, 2048, 0}) with_len(n, [](auto c) { set_smem_1<decltype(c)::value>(); });
@@ -562,12 +582,17 @@ void Cov::apply1(const double* dx, double* dy) {
         k_cols_1<decltype(c)::value><<<nky, threads_1(mx), sx, stream>>>(work.p, nx, fx8, spec_half.p);
     });
     FKB_LAUNCH_CHECK();
+    count_launch(2);
+}
+
+void Cov::apply1_inv(double* dy, const double* acc_coef, const int* gate) {
+    const size_t sy = 3 * size_t(my) * sizeof(double2);
     with_len(my, [&](auto c) {
-        k_rows_inv_1<decltype(c)::value><<<ceil_div(nx, 2), threads_1(my), sy, stream>>>(work.p, nx, ny, fy8, dy,
-                                                                                        1.0 / double(M()));
+        k_rows_inv_1<decltype(c)::value><<<ceil_div(nx, 2), threads_1(my), sy, stream>>>(
+            work.p, nx, ny, fy8, dy, 1.0 / double(M()), acc_coef, gate);
     });
     FKB_LAUNCH_CHECK();
-    count_launch(3);
+    count_launch();
 }
 
 void Cov::apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy) {

@@ -36,7 +36,12 @@ struct Cov {
 
     // Y = Γ X, X/Y column-major device blocks (covariance.hpp:101-115); Y may alias X.
     void apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy);
-    void apply1(const double* dx, double* dy);  // single vector (warp-per-transform kernels)
+    void apply1(const double* dx, double* dy);  // single vector (CTA-per-transform kernels)
+    // the single-vector apply split at its last pass: forward rows + column pass into the work
+    // buffer, then the inverse rows pass storing Γx into dy, or (acc_coef ≠ null) adding
+    // (*acc_coef)·Γx to dy unless *gate
+    void apply1_fwd(const double* dx);
+    void apply1_inv(double* dy, const double* acc_coef, const int* gate);
     // Two N(0,Γ) draws (covariance.hpp:332-353) into device vectors.
     void sample_pair(uint64_t seed, uint64_t stream_id, double* da, double* db);
     // Host copy of the full clipped spectrum (covariance.hpp:207-211), row-major mx×my.

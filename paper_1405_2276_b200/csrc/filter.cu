@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double*
     if (lane == 0) st[i] = wsq[i] * (rt[i] + acc);
 }
 
-// mean_i ← (mean_i + α·t_i) − Σ_j U_ij (d_j c_j)   (fast_filter.hpp:114-116), skipped on LLT failure
+// mean_i ← (mean_i + α·t_i) − Σ_j U_ij·dc_j  (fast_filter.hpp:114-116), skipped on a failed step
 struct EpiMean {
     double* mean;
     const double* t;
@@ -411,6 +411,9 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     FKB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
     FKB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     FKB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_ctz, cudaEventDisableTiming));
+    FKB_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
     if (m < 0) throw std::invalid_argument("fkf_init: negative measurement count");
     if ((long long)h_cols != n) throw std::invalid_argument("fkf_init: H columns do not match state dimension");
     for (int i = 0; i < m; ++i)
@@ -508,6 +511,9 @@ Filter::~Filter() {
     if (graph) cudaGraphExecDestroy(graph);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_join2) cudaEventDestroy(ev_join2);
+    if (ev_ctz) cudaEventDestroy(ev_ctz);
+    if (s3) cudaStreamDestroy(s3);
     if (s2) cudaStreamDestroy(s2);
 }
 
@@ -519,6 +525,7 @@ void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
     alpha = 0.0;
     step_no = 0;
     state_rank = 0;
+    k_valid = false;
 }
 
 void Filter::mark(const char* name) {
@@ -536,6 +543,7 @@ std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
         std::vector<cudaEvent_t> ev;
         phase_events = &ev;
         phase_names.clear();
+        prime_capacitance();
         mark("begin");
         try {
             enqueue_step(ybuf.p);
@@ -565,6 +573,7 @@ void Filter::set_solver(int mode) {
     if (mode != 0 && mode != 1) throw std::invalid_argument("fkf: solver must be 0 (dense LLT) or 1 (Woodbury)");
     if (mode == solver) return;
     solver = mode;
+    k_valid = false;
     if (mode == 0 && S.n < size_t(m) * m) S.alloc(size_t(std::max(m, 1)) * std::max(m, 1));  // before any capture
     if (graph) cudaGraphExecDestroy(graph);
     graph = nullptr;
@@ -576,35 +585,38 @@ void Filter::fork() {
     FKB_CUDA(cudaEventRecord(ev_fork, s));
     FKB_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
 }
-void Filter::join() {
+void Filter::join(cudaEvent_t ev) {
     if (side() == s) return;
-    FKB_CUDA(cudaEventRecord(ev_join, s2));
-    FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    FKB_CUDA(cudaEventRecord(ev, s2));
+    FKB_CUDA(cudaStreamWaitEvent(s, ev, 0));
+}
+
+// Woodbury scalars and K for the step that follows the committed state (α_dev[0] + 1, d).
+void Filter::enqueue_capacitance(cudaStream_t b) {
+    if (solver != 1 || r <= 0) return;
+    k_woodbury_scalars<<<std::max(1, std::min(ceil_div(std::max(m, r), 256), 148)), 256, 0, b>>>(
+        m, r, alpha_dev.p, theta.p, d.p, sigma2, wsq.p, sqd.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
+    g.M = r; g.N = r; g.K = m;
+    g.A = E.p; g.lda = m; g.transA = 1;
+    g.B = E.p; g.ldb = m;
+    g.dA = wsq.p;
+    g.rs = sqd.p; g.cs = sqd.p;
+    g.alpha = -1.0;
+    g.C = Kcap.p; g.ldc = r;
+    g.diag_add = 1.0;
+    gram_sym(g, b);  // full symmetric K (the PCG reads columns)
+}
+
+void Filter::prime_capacitance() {
+    if (k_valid || solver != 1 || r <= 0) return;
+    enqueue_capacitance(s);
+    k_valid = true;
 }
 
 void Filter::enqueue_step(const double* d_y) {
-    const bool wb = solver == 1 && r > 0;
-    if (wb) {
-        // side branch: Woodbury scalars and the capacitance K depend only on α and d (state of
-        // the previous step), so they overlap the residual, r̃ = Pᵀz and the RHS on the main branch
-        fork();
-        cudaStream_t b = side();
-        k_woodbury_scalars<<<std::max(1, std::min(ceil_div(std::max(m, r), 256), 148)), 256, 0, b>>>(
-            m, r, alpha_dev.p, theta.p, d.p, sigma2, wsq.p, sqd.p);
-        FKB_LAUNCH_CHECK();
-        count_launch();
-        GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
-        g.M = r; g.N = r; g.K = m;
-        g.A = E.p; g.lda = m; g.transA = 1;
-        g.B = E.p; g.ldb = m;
-        g.dA = wsq.p;
-        g.rs = sqd.p; g.cs = sqd.p;
-        g.alpha = -1.0;
-        g.C = Kcap.p; g.ldc = r;
-        g.diag_add = 1.0;
-        gram_sym(g, b);  // full symmetric K (the PCG reads columns)
-        mark("capacitance");
-    }
     // α ← α + 1, flags, z = y − H·mean (:97, :108): one kernel
     {
         const int blocks = std::max(1, ceil_div((long long)std::max(m, 1) * 32, 256));
@@ -617,26 +629,30 @@ void Filter::enqueue_step(const double* d_y) {
     mark("residual");
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
-    // dc = d ⊙ Bᵀz with d and α updated in the same pass (side branch) ∥ t = Γ(Hᵀz) (main);
-    // then mean += α·t − U·dc (:114-123)
+    // side branch: dc = d ⊙ Bᵀz with d and α updated in the same pass, then the next step's
+    // Woodbury scalars and K; main branch: t = Γ(Hᵀz); then mean += α·t − U·dc (:114-123).
+    // (The U pass stays on the main branch: run concurrently it starves the FFT passes of SMs.)
+    const bool par = side() != s;
     if (r > 0) {
         fork();
         launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
+        if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
         mark("ctz_d_update");
-    }
-    spmv_short(HT, z.p, t.p, 1.0, s);
-    mark("ht_z");
-    cov->apply(t.p, n, 1, t.p, n);
-    mark("gamma_apply");
-    if (r > 0) {
-        join();
-        launch_gemv_rowmajor(n, r, Urow.p, r, XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+        enqueue_capacitance(side());
+        if (par) FKB_CUDA(cudaEventRecord(ev_join2, s2));
+        mark("capacitance");
     } else {
-        launch_gemv_rowmajor(n, 0, Urow.p, 1, XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
-        k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α
+        k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α (reads α_dev[1] only)
         FKB_LAUNCH_CHECK();
         count_launch();
     }
+    spmv_short(HT, z.p, t.p, 1.0, s);
+    mark("ht_z");
+    cov->apply1(t.p, t.p);
+    mark("gamma_apply");
+    if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
+    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+    if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0)); // next K ready
     mark("mean_update");
 }
 
@@ -648,7 +664,6 @@ void Filter::enqueue_solve_woodbury() {
         // u = D^½·Eᵀ·Λ_M⁻¹·r̃
         launch_coldot(m, r, E.p, m, XWr{rt.p, theta.p, alpha_dev.p, sigma2}, EpiSqrtD{ucap.p, d.p}, s);
         mark("cap_rhs");
-        join();  // K and the scalars from the side branch
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
         cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s, 200, 1e-14, pcg_ts.p);
         chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
@@ -712,6 +727,7 @@ void Filter::launch_step() {
         g_launches = before;
         graph_ready = true;
     }
+    prime_capacitance();
     FKB_CUDA(cudaGraphLaunch(graph, s));
     count_launch(launches_per_step);
 }

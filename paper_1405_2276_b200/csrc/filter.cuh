@@ -52,10 +52,18 @@ struct Filter {
     // fork() makes it wait for the main stream, join() makes the main stream wait for it.
     // Phase timing runs the branches serially on the main stream.
     cudaStream_t s2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t s3 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_ctz = nullptr;
     cudaStream_t side() const { return phase_events ? s : s2; }
     void fork();
-    void join();
+    void join(cudaEvent_t ev);
+    // The capacitance K = I − D^½EᵀΛ_M⁻¹ED^½ depends only on α and d, so each step computes
+    // the NEXT step's K on the side branch as soon as d and α are updated (overlapping the
+    // Γ(Hᵀz) and U passes); k_valid says Kcap/wsq/sqd hold it.  Invalidated by reset,
+    // set_state and set_solver; prime_capacitance() recomputes it eagerly when needed.
+    bool k_valid = false;
+    void enqueue_capacitance(cudaStream_t b);
+    void prime_capacitance();
     int launches_per_step = 0;
 
     // cached realization draws (RealizationPropagator, uq.hpp:86-112)

@@ -107,9 +107,9 @@ __global__ void __launch_bounds__(256) k_gemv_rowmajor(long long m, int k, const
     for (int c = threadIdx.x; c < k; c += blockDim.x) xs[c] = xl(c);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;  // grid-stride over 4-row groups
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w * 4 < m; w += nw) {
     const long long r0 = w * 4;
-    if (r0 >= m) return;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     const int nq = (int)min(4LL, m - r0);
     int c = lane;
@@ -139,14 +139,18 @@ __global__ void __launch_bounds__(256) k_gemv_rowmajor(long long m, int k, const
         const double v = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
         epi(r0 + lane, v);
     }
+    }
 }
 
 template <class XL, class Epi>
-inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long ld, XL xl, Epi epi, cudaStream_t s) {
+inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long ld, XL xl, Epi epi, cudaStream_t s,
+                                 long long max_ctas = 0) {
     if (m <= 0) return;
     const long long warps = (m + 3) / 4;
-    k_gemv_rowmajor<XL, Epi><<<(unsigned)((warps + 7) / 8), 256, sizeof(double) * size_t(std::max(k, 1)), s>>>(
-        m, k, A, ld, xl, epi);
+    long long ctas = (warps + 7) / 8;
+    if (max_ctas > 0) ctas = std::min(ctas, max_ctas);
+    k_gemv_rowmajor<XL, Epi><<<(unsigned)ctas, 256, sizeof(double) * size_t(std::max(k, 1)), s>>>(m, k, A, ld, xl,
+                                                                                                 epi);
     FKB_LAUNCH_CHECK();
     count_launch();
 }
