@@ -248,7 +248,11 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.ExternalStream(ctx.stream)
     dys = DeviceArray.from_host(np.stack(ys).ravel())
     yptr = lambda i: C.c_void_p(dys.ptr.value + 8 * w.m * (i % S))  # noqa: E731
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local_rank}")  # 256 MiB > L2
+    # L2 flush between timed steps: write 256 MiB (> 126 MB L2), then read another 256 MiB so
+    # the flush's own dirty lines are written back before the next step rather than inside it
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local_rank}")
+    sweep = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local_rank}")
+    sweep_out = torch.empty(1, dtype=torch.float32, device=f"cuda:{local_rank}")
 
     # ---- warm-up
     for i in range(args.warmup):
@@ -269,6 +273,7 @@ def run_ours(args, rank, world, local_rank):
             evs[i][1].record(stream)
             with torch.cuda.stream(stream):
                 flush.zero_()
+                torch.sum(sweep, dim=0, keepdim=True, out=sweep_out)
         torch.cuda.synchronize()
         ctx.sync(args.steps)
     launches = int(L.fkb_launch_count()) - launches0
@@ -373,7 +378,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": r,
                    "torus": f"{cov.mx}x{cov.my}", "nnz_H": int(h.nnz), "solver": "woodbury-eig",
-                   "l2": "flushed between timed steps (256 MiB write on the filter stream)",
+                   "l2": "flushed between timed steps (256 MiB write + 256 MiB read sweep on the filter stream)",
                    "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -50,6 +50,17 @@ __device__ __forceinline__ void st_cluster(double* local_addr, int rank, double 
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
 
+// remote store into CTA `rank` that also signals `bytes` on that CTA's mbarrier (the mbarrier
+// is at the same shared offset in every CTA): no cluster barrier needed on the receive side
+__device__ __forceinline__ void st_async_cluster(double* local_addr, unsigned long long* local_bar, int rank, double v) {
+    unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local_addr)), ra;
+    unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(local_bar)), rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(b), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(v), "r"(rb)
+                 : "memory");
+}
+
 __device__ __forceinline__ void cp_async8(double* smem, const double* g) {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a), "l"(g) : "memory");
@@ -97,10 +108,18 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     // tracked by an mbarrier when 16-byte aligned, else 8-byte cp.async; it lands while the
     // initial residual is exchanged.
     __shared__ alignas(8) unsigned long long kbar;
+    __shared__ alignas(8) unsigned long long xbar[2];  // per-parity exchange barriers
     const int cnt = kstage ? (r1 - r0) * n : 0;
     const unsigned bytes = unsigned(cnt) * 8u;
     const bool bulk = kstage && ld == n && ((long long)r0 * n) % 2 == 0 && bytes % 16 == 0 && bytes > 0;
     const unsigned kbar_a = static_cast<unsigned>(__cvta_generic_to_shared(&kbar));
+    if (tid == 0) {
+        for (int q = 0; q < 2; ++q) {
+            const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[q]));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xa) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (bulk) {
         if (tid == 0) {
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(kbar_a) : "memory");
@@ -153,10 +172,17 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     double gamma_prev = 1.0, alpha_prev = 1.0, stop = 0.0;
     int it = 0;
     bool done = false;
+    // exchange bytes every CTA receives per iteration: all n entries of m + 16×3 partials
+    const unsigned xbytes = unsigned(n) * 8u + unsigned(PC_CL) * 24u;
     while (true) {
         const int buf = it & 1;
+        const unsigned parity = unsigned((it >> 1) & 1);
         const double mv = dinv * w;
         if (stamp && it == 3) ts[39] = gtimer();
+        if (tid == 0) {
+            const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[buf]));
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xa), "r"(xbytes) : "memory");
+        }
         {
             double a = own ? r * uu : 0.0, bq = own ? w * uu : 0.0, c = own ? r * r : 0.0;
             if (warp < 2) {
@@ -168,16 +194,14 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
             }
             if (own)
 #pragma unroll
-                for (int cc = 0; cc < PC_CL; ++cc) st_cluster(&sh.v[buf][row], cc, mv);
+                for (int cc = 0; cc < PC_CL; ++cc) st_async_cluster(&sh.v[buf][row], &xbar[buf], cc, mv);
             if (rb <= 32) {  // one owning warp: its lanes 0..15 push the three sums to every CTA
-                const double a0 = __shfl_sync(0xffffffffu, a, 0), b0 = __shfl_sync(0xffffffffu, bq, 0),
-                             c0 = __shfl_sync(0xffffffffu, c, 0);
-                if (warp == 0) {
-                    if (lane < PC_CL) {
-                        st_cluster(&sh.part[buf][crank][0], lane, a0);
-                        st_cluster(&sh.part[buf][crank][1], lane, b0);
-                        st_cluster(&sh.part[buf][crank][2], lane, c0);
-                    }
+                if (warp == 0 && lane < PC_CL) {
+                    const double a0 = __shfl_sync(0x0000ffffu, a, 0), b0 = __shfl_sync(0x0000ffffu, bq, 0),
+                                 c0 = __shfl_sync(0x0000ffffu, c, 0);
+                    st_async_cluster(&sh.part[buf][crank][0], &xbar[buf], lane, a0);
+                    st_async_cluster(&sh.part[buf][crank][1], &xbar[buf], lane, b0);
+                    st_async_cluster(&sh.part[buf][crank][2], &xbar[buf], lane, c0);
                 }
             } else {
                 if (warp < 2 && lane == 0) {
@@ -188,12 +212,21 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
                 __syncthreads();
                 if (tid < 3 * PC_CL) {
                     const int qq = tid % 3, dest = tid / 3;
-                    st_cluster(&sh.part[buf][crank][qq], dest, sh.red[0][qq] + sh.red[1][qq]);
+                    st_async_cluster(&sh.part[buf][crank][qq], &xbar[buf], dest, sh.red[0][qq] + sh.red[1][qq]);
                 }
             }
         }
         if (stamp && it == 3) ts[40] = gtimer();
-        cl.sync();  // m and all partials delivered
+        {  // m and all partials delivered (this CTA's barrier of this parity)
+            const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[buf]));
+            unsigned ok = 0;
+            while (!ok)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(ok)
+                    : "r"(xa), "r"(parity)
+                    : "memory");
+        }
         if (stamp && it == 3) ts[41] = gtimer();
         double gamma = 0.0, delta = 0.0, rr = 0.0;
 #pragma unroll
@@ -229,8 +262,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         ++it;
         if (stamp && it < 60) ts[1 + it] = gtimer();
     }
-    // every DSMEM store of the last iteration completed before its barrier and nothing is
-    // read remotely, so CTAs may exit independently
+    cl.sync();  // no CTA exits while a peer's asynchronous stores may still target it
     if (done) {
         if (own) u[row] = x;
     } else if (crank == 0 && tid == 0) {
