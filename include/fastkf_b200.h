@@ -128,6 +128,10 @@ int fkb_filter_get_eig(fkb_filter* f, double* theta, double* P);
 /* runs `reps` real steps un-graphed with CUDA events at phase boundaries; ms[i] = mean
  * duration of phase i, names = comma-separated phase names (advances the state) */
 int fkb_filter_phase_times(fkb_filter* f, int reps, double* ms, char* names, int names_len, int* nphases);
+/* in-graph kernel timing: on != 0 re-captures the step graph with timing events at every
+ * phase boundary; graph_phase_times then returns the per-phase device ms of the LAST replay */
+int fkb_filter_graph_timing(fkb_filter* f, int on);
+int fkb_filter_graph_phase_times(fkb_filter* f, double* ms, char* names, int names_len, int* nphases);
 
 /* capacitance factor+solve kernel on a host SPD matrix (test/profiling hook): L lower
  * factor, x = K⁻¹b; stamps (optional, 128 entries) receive %globaltimer phase stamps */

@@ -424,6 +424,29 @@ int fkb_filter_phase_times(fkb_filter* f, int reps, double* ms, char* names, int
         *nphases = int(v.size());
     });
 }
+int fkb_filter_graph_timing(fkb_filter* f, int on) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->set_graph_timing(on != 0);
+    });
+}
+int fkb_filter_graph_phase_times(fkb_filter* f, double* ms, char* names, int names_len, int* nphases) {
+    return guarded([&] {
+        need(f, "filter");
+        auto v = f->f->graph_phase_times();
+        std::string joined;
+        for (size_t i = 0; i < v.size(); ++i) {
+            if (ms) ms[i] = v[i].second;
+            if (i) joined += ",";
+            joined += v[i].first;
+        }
+        if (names && names_len > 0) {
+            std::strncpy(names, joined.c_str(), size_t(names_len) - 1);
+            names[names_len - 1] = 0;
+        }
+        *nphases = int(v.size());
+    });
+}
 int fkb_filter_get_eig(fkb_filter* f, double* theta, double* P) {
     return guarded([&] {
         need(f, "filter");

@@ -123,15 +123,26 @@ __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* 
     if (lane == 0) z[row] = y[row] - s;
 }
 
-// Woodbury scalars of this step on the side branch (α of this step = α_prev + 1):
-// wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹), sqd_j = √d_j.  Reads only state committed by the previous step.
-__global__ void k_woodbury_scalars(int m, int r, const double* __restrict__ alpha_dev,
-                                   const double* __restrict__ theta, const double* __restrict__ d, double sigma2,
-                                   double* __restrict__ wsq, double* __restrict__ sqd) {
-    const double alpha = alpha_dev[0] + 1.0;
+// Woodbury scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j for a step that has not
+// run yet.  mode 0: α = α_dev[0] + 1 with the committed d; mode 1 (side branch of step t): the
+// step after t, α = α_dev[1] + 1 and d_j advanced by the same SMW update the step commits
+// (fast_filter.hpp:118-123; d does not depend on the observation).
+__global__ void k_woodbury_scalars(int m, int r, int mode, const double* __restrict__ alpha_dev,
+                                   const double* __restrict__ theta, const double* __restrict__ d,
+                                   const double* __restrict__ lam, double sigma2, double* __restrict__ wsq,
+                                   double* __restrict__ sqd) {
+    const double a_step = mode == 0 ? alpha_dev[0] + 1.0 : alpha_dev[1];
+    const double alpha = mode == 0 ? a_step : a_step + 1.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
         wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) sqd[j] = sqrt(d[j]);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) {
+        double dj = d[j];
+        if (mode == 1) {
+            const double c = a_step - dj, l = lam[j];
+            dj = (dj + a_step * l * c) / (1.0 + l * c);
+        }
+        sqd[j] = sqrt(dj);
+    }
 }
 
 // x_i = r̃_i / (α θ_i + σ²) (Λ_M⁻¹ r̃ with this step's α, computed in place of wsq so the
@@ -481,12 +492,15 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     alpha_dev.alloc(2);
     d.alloc(size_t(std::max(r, 1)));
     mean.alloc(size_t(n));
-    wsq.alloc(size_t(std::max(m, 1)));
-    sqd.alloc(size_t(std::max(r, 1)));
+    for (int q = 0; q < 2; ++q) {
+        wsqb[q].alloc(size_t(std::max(m, 1)));
+        sqdb[q].alloc(size_t(std::max(r, 1)));
+        Kb[q].alloc(size_t(std::max(r, 1)) * std::max(r, 1));
+    }
+    select_parity(0);
     rt.alloc(size_t(std::max(m, 1)));
     st.alloc(size_t(std::max(m, 1)));
     ucap.alloc(size_t(std::max(r, 1)));
-    Kcap.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
     rdg.alloc(std::max<size_t>(chol_solve_scratch(r), 1));
     gpart.alloc(size_t(592) * 32 + size_t(std::max(m, 1)) + 64);  // split-GEMV partials
     pcgwork.alloc(size_t(std::max(r, 1)) + 1);
@@ -508,7 +522,7 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
 }
 
 Filter::~Filter() {
-    if (graph) cudaGraphExecDestroy(graph);
+    drop_graphs();
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join2) cudaEventDestroy(ev_join2);
@@ -528,13 +542,64 @@ void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
     k_valid = false;
 }
 
-void Filter::mark(const char* name) {
-    if (!phase_events) return;
+void Filter::mark_on(cudaStream_t st, const char* name) {
+    if (phase_events) {  // un-graphed serial phase timing: everything runs on s
+        cudaEvent_t e;
+        FKB_CUDA(cudaEventCreate(&e));
+        FKB_CUDA(cudaEventRecord(e, s));
+        phase_events->push_back(e);
+        phase_names.emplace_back(name);
+        return;
+    }
+    if (!(capturing && gtime)) return;
     cudaEvent_t e;
     FKB_CUDA(cudaEventCreate(&e));
-    FKB_CUDA(cudaEventRecord(e, s));
-    phase_events->push_back(e);
-    phase_names.emplace_back(name);
+    FKB_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    const int q = par_next;  // the graph being captured
+    int prev = -1;
+    bool seen = false;
+    for (auto& pl : gt_last)
+        if (pl.first == st) {
+            prev = pl.second;
+            pl.second = int(gt_ev[q].size());
+            seen = true;
+        }
+    if (!seen) gt_last.emplace_back(st, int(gt_ev[q].size()));
+    gt_ev[q].push_back(e);
+    gt_name[q].emplace_back(name);
+    gt_prev[q].push_back(prev);
+}
+
+void Filter::drop_graphs() {
+    for (int q = 0; q < 2; ++q) {
+        if (graph[q]) cudaGraphExecDestroy(graph[q]);
+        graph[q] = nullptr;
+        graph_ready[q] = false;
+        for (auto e : gt_ev[q]) cudaEventDestroy(e);
+        gt_ev[q].clear();
+        gt_name[q].clear();
+        gt_prev[q].clear();
+    }
+}
+
+void Filter::set_graph_timing(bool on) {
+    if (on == gtime) return;
+    gtime = on;
+    drop_graphs();
+}
+
+std::vector<std::pair<std::string, double>> Filter::graph_phase_times() {
+    std::vector<std::pair<std::string, double>> out;
+    const int q = gt_last_par;
+    if (!gtime || !graph_ready[q]) return out;
+    FKB_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < gt_ev[q].size(); ++i) {
+        if (gt_prev[q][i] < 0) continue;
+        float ms = 0.f;
+        FKB_CUDA(cudaEventElapsedTime(&ms, gt_ev[q][size_t(gt_prev[q][i])], gt_ev[q][i]));
+        out.emplace_back(gt_name[q][i], double(ms));
+    }
+    return out;
 }
 
 std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
@@ -544,6 +609,7 @@ std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
         phase_events = &ev;
         phase_names.clear();
         prime_capacitance();
+        select_parity(par_next);
         mark("begin");
         try {
             enqueue_step(ybuf.p);
@@ -561,6 +627,7 @@ std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
             acc[i - 1].second += ms / reps;
         }
         for (auto e : ev) cudaEventDestroy(e);
+        par_next ^= 1;
         check_info();
         alpha += 1.0;
         ++step_no;
@@ -575,15 +642,14 @@ void Filter::set_solver(int mode) {
     solver = mode;
     k_valid = false;
     if (mode == 0 && S.n < size_t(m) * m) S.alloc(size_t(std::max(m, 1)) * std::max(m, 1));  // before any capture
-    if (graph) cudaGraphExecDestroy(graph);
-    graph = nullptr;
-    graph_ready = false;
+    drop_graphs();
 }
 
 void Filter::fork() {
     if (side() == s) return;
     FKB_CUDA(cudaEventRecord(ev_fork, s));
     FKB_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
+    mark_on(s2, "fork");
 }
 void Filter::join(cudaEvent_t ev) {
     if (side() == s) return;
@@ -591,28 +657,27 @@ void Filter::join(cudaEvent_t ev) {
     FKB_CUDA(cudaStreamWaitEvent(s, ev, 0));
 }
 
-// Woodbury scalars and K for the step that follows the committed state (α_dev[0] + 1, d).
-void Filter::enqueue_capacitance(cudaStream_t b) {
+void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double* sqd_o, double* K_o) {
     if (solver != 1 || r <= 0) return;
     k_woodbury_scalars<<<std::max(1, std::min(ceil_div(std::max(m, r), 256), 148)), 256, 0, b>>>(
-        m, r, alpha_dev.p, theta.p, d.p, sigma2, wsq.p, sqd.p);
+        m, r, mode, alpha_dev.p, theta.p, d.p, lambda.p, sigma2, wsq_o, sqd_o);
     FKB_LAUNCH_CHECK();
     count_launch();
     GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
     g.M = r; g.N = r; g.K = m;
     g.A = E.p; g.lda = m; g.transA = 1;
     g.B = E.p; g.ldb = m;
-    g.dA = wsq.p;
-    g.rs = sqd.p; g.cs = sqd.p;
+    g.dA = wsq_o;
+    g.rs = sqd_o; g.cs = sqd_o;
     g.alpha = -1.0;
-    g.C = Kcap.p; g.ldc = r;
+    g.C = K_o; g.ldc = r;
     g.diag_add = 1.0;
     gram_sym(g, b);  // full symmetric K (the PCG reads columns)
 }
 
-void Filter::prime_capacitance() {
+void Filter::prime_capacitance() {  // K, wsq, sqd of the next step (parity par_next), eagerly
     if (k_valid || solver != 1 || r <= 0) return;
-    enqueue_capacitance(s);
+    enqueue_capacitance(s, 0, wsqb[par_next].p, sqdb[par_next].p, Kb[par_next].p);
     k_valid = true;
 }
 
@@ -621,26 +686,23 @@ void Filter::enqueue_step(const double* d_y) {
     {
         const int blocks = std::max(1, ceil_div((long long)std::max(m, 1) * 32, 256));
         k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
-                                               theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq.p : nullptr,
-                                               sqd.p, info.p, solver == 1 ? pcgflag.p : nullptr);
+                                               theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq_c : nullptr,
+                                               sqd_c, info.p, solver == 1 ? pcgflag.p : nullptr);
         FKB_LAUNCH_CHECK();
         count_launch();
     }
     mark("residual");
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
-    // side branch: dc = d ⊙ Bᵀz with d and α updated in the same pass, then the next step's
-    // Woodbury scalars and K; main branch: t = Γ(Hᵀz); then mean += α·t − U·dc (:114-123).
-    // (The U pass stays on the main branch: run concurrently it starves the FFT passes of SMs.)
+    // side branch: dc = d ⊙ Bᵀz with d and α updated in the same pass; main branch:
+    // t = Γ(Hᵀz); then mean += α·t − U·dc (:114-123).  (The U pass stays on the main branch:
+    // run concurrently it starves the FFT passes of SMs.)
     const bool par = side() != s;
     if (r > 0) {
         fork();
         launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
+        mark_on(side(), "ctz_d_update");
         if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
-        mark("ctz_d_update");
-        enqueue_capacitance(side());
-        if (par) FKB_CUDA(cudaEventRecord(ev_join2, s2));
-        mark("capacitance");
     } else {
         k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α (reads α_dev[1] only)
         FKB_LAUNCH_CHECK();
@@ -652,7 +714,7 @@ void Filter::enqueue_step(const double* d_y) {
     mark("gamma_apply");
     if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
     launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
-    if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0)); // next K ready
+    if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
 
@@ -664,13 +726,23 @@ void Filter::enqueue_solve_woodbury() {
         // u = D^½·Eᵀ·Λ_M⁻¹·r̃
         launch_coldot(m, r, E.p, m, XWr{rt.p, theta.p, alpha_dev.p, sigma2}, EpiSqrtD{ucap.p, d.p}, s);
         mark("cap_rhs");
+        // side branch (runs beside the 16-SM PCG cluster): the NEXT step's Woodbury scalars
+        // and K into the other parity's buffers
+        if (side() != s) {
+            FKB_CUDA(cudaEventRecord(ev_ctz, s));
+            FKB_CUDA(cudaStreamWaitEvent(s3, ev_ctz, 0));
+            mark_on(s3, "fork_k");
+        }
+        enqueue_capacitance(side() != s ? s3 : s, 1, wsq_n, sqd_n, K_n);
+        mark_on(side() != s ? s3 : s, "capacitance");
+        if (side() != s) FKB_CUDA(cudaEventRecord(ev_join2, s3));
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
-        cap_pcg(r, Kcap.p, r, ucap.p, pcgwork.p, pcgflag.p, s, 200, 1e-14, pcg_ts.p);
-        chol_solve_small(r, Kcap.p, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
+        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, 200, 1e-14, pcg_ts.p);
+        chol_solve_small(r, K_c, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
         mark("cap_solve");
     }
     // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
-    k_woodbury_st<<<std::max(1, ceil_div(m, 8)), 256, 0, s>>>(m, r, Erow.p, sqd.p, ucap.p, wsq.p, rt.p, st.p);
+    k_woodbury_st<<<std::max(1, ceil_div(m, 8)), 256, 0, s>>>(m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p);
     FKB_LAUNCH_CHECK();
     count_launch();
     mark("woodbury_st");
@@ -704,32 +776,48 @@ void Filter::check_info() {
     int h = 0;
     FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FKB_CUDA(cudaStreamSynchronize(s));
-    if (h) throw std::runtime_error("fkf_step: innovation system is singular");
+    if (h) {
+        k_valid = false;  // the side branch assumed the step would commit its d update
+        throw std::runtime_error("fkf_step: innovation system is singular");
+    }
 }
 
 void Filter::launch_step() {
-    if (!graph_ready) {
-        // Capture the whole step once (it reads y from ybuf and α from alpha_dev);
-        // replays remove the per-kernel launch latency of ~100 small kernels.
+    prime_capacitance();
+    const int q = par_next;
+    if (!graph_ready[q]) {
+        // Capture the step once per parity (it reads y from ybuf and α from alpha_dev);
+        // replays remove the per-kernel launch latency.
         const unsigned long long before = g_launches;
+        for (auto e : gt_ev[q]) cudaEventDestroy(e);
+        gt_ev[q].clear();
+        gt_name[q].clear();
+        gt_prev[q].clear();
+        gt_last.clear();
+        select_parity(q);
         cudaGraph_t gr;
         FKB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
         try {
+            mark("begin");
             enqueue_step(ybuf.p);
         } catch (...) {
+            capturing = false;
             cudaStreamEndCapture(s, &gr);
             throw;
         }
+        capturing = false;
         FKB_CUDA(cudaStreamEndCapture(s, &gr));
-        FKB_CUDA(cudaGraphInstantiate(&graph, gr, 0));
+        FKB_CUDA(cudaGraphInstantiate(&graph[q], gr, 0));
         cudaGraphDestroy(gr);
         launches_per_step = int(g_launches - before);
         g_launches = before;
-        graph_ready = true;
+        graph_ready[q] = true;
     }
-    prime_capacitance();
-    FKB_CUDA(cudaGraphLaunch(graph, s));
+    FKB_CUDA(cudaGraphLaunch(graph[q], s));
     count_launch(launches_per_step);
+    gt_last_par = q;
+    par_next ^= 1;
 }
 
 void Filter::step(const double* d_y) {

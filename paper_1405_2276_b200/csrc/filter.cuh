@@ -39,15 +39,27 @@ struct Filter {
     // solver = 0 reproduces the reference order: form S and LLT it (m×m) every step.
     int solver = 1;
     int eig_sweeps = 0;
-    DBuf<double> P, Pt, theta, E, Erow, wsq, sqd, rt, ucap, Kcap, st, rdg, gpart, pcgwork;
+    DBuf<double> P, Pt, theta, E, Erow, rt, ucap, st, rdg, gpart, pcgwork;
+    // Per-step Woodbury scalars Λ_M⁻¹ (wsq), D^½ (sqd) and capacitance K, double-buffered by
+    // step parity: step t reads buffer t&1 while its side branch forms step t+1's into the
+    // other (they depend only on α and d, not on the observation).
+    DBuf<double> wsqb[2], sqdb[2], Kb[2];
+    double *wsq_c = nullptr, *sqd_c = nullptr, *K_c = nullptr;  // this step's (capture-time)
+    double *wsq_n = nullptr, *sqd_n = nullptr, *K_n = nullptr;  // next step's
+    int par_next = 0;  // parity of the next step to run
+    void select_parity(int p) {
+        wsq_c = wsqb[p].p; sqd_c = sqdb[p].p; K_c = Kb[p].p;
+        wsq_n = wsqb[p ^ 1].p; sqd_n = sqdb[p ^ 1].p; K_n = Kb[p ^ 1].p;
+    }
     DBuf<unsigned long long> pcg_ts;  // %globaltimer stamps of the PCG kernel (FKB_PCG_STAMPS=1)
     DBuf<int> pcgflag;  // 1 when the capacitance PCG fell back to the cluster Cholesky
 
     // step workspaces
     DBuf<double> S, z, t, cvec, ws, ws_step;
     DBuf<int> info, flags;
-    cudaGraphExec_t graph = nullptr;
-    bool graph_ready = false;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one per step parity
+    bool graph_ready[2] = {false, false};
+    void drop_graphs();
     // side stream for the independent branches of a step (captured into the same graph):
     // fork() makes it wait for the main stream, join() makes the main stream wait for it.
     // Phase timing runs the branches serially on the main stream.
@@ -62,7 +74,9 @@ struct Filter {
     // Γ(Hᵀz) and U passes); k_valid says Kcap/wsq/sqd hold it.  Invalidated by reset,
     // set_state and set_solver; prime_capacitance() recomputes it eagerly when needed.
     bool k_valid = false;
-    void enqueue_capacitance(cudaStream_t b);
+    // mode 0: K for α_dev[0]+1 and the committed d (priming); mode 1: K for the step after the
+    // one being enqueued (α_dev[1]+1 and d updated from α_dev[1]), written to the next buffers
+    void enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double* sqd_o, double* K_o);
     void prime_capacitance();
     int launches_per_step = 0;
 
@@ -92,7 +106,19 @@ struct Filter {
     std::vector<std::pair<std::string, double>> phase_times(int reps);
     std::vector<cudaEvent_t>* phase_events = nullptr;
     std::vector<std::string> phase_names;
-    void mark(const char* name);
+    void mark(const char* name) { mark_on(s, name); }
+    void mark_on(cudaStream_t st, const char* name);
+    // In-graph kernel timing: with gtime set, the captured step graph records external timing
+    // events at every phase boundary (on the phase's own stream), so per-kernel device times
+    // come from real graph replays (bench.py's roofline) rather than from un-graphed steps.
+    bool gtime = false, capturing = false;
+    int gt_last_par = 0;  // parity of the last replayed graph
+    std::vector<cudaEvent_t> gt_ev[2];
+    std::vector<std::string> gt_name[2];
+    std::vector<int> gt_prev[2];
+    std::vector<std::pair<cudaStream_t, int>> gt_last;
+    void set_graph_timing(bool on);
+    std::vector<std::pair<std::string, double>> graph_phase_times();
     void launch_step();                                  // graph replay of enqueue_step(ybuf)
     void check_info();                                   // throws on a singular innovation system
     void reset();                                        // zero_start (:30-36)

@@ -381,6 +381,20 @@ class FkfContext:
         return dict(zip(keys, ms[: cnt.value].tolist()))
 
 
+    def graph_timing(self, on: bool = True):
+        """Re-captures the step graph with timing events at every phase boundary."""
+        check(lib().fkb_filter_graph_timing(self._f, 1 if on else 0))
+
+    def graph_phase_times(self):
+        """Per-phase device ms of the last graph replay (needs graph_timing(True))."""
+        ms = np.zeros(64)
+        names = C.create_string_buffer(2048)
+        cnt = C.c_int()
+        check(lib().fkb_filter_graph_phase_times(self._f, ms, names, 2048, C.byref(cnt)))
+        keys = names.value.decode().split(",") if cnt.value else []
+        return dict(zip(keys, ms[: cnt.value].tolist()))
+
+
 def fkf_init(cov, h, sigma2, k_rank, p_oversample, seed) -> FkfContext:
     return FkfContext(cov, h, sigma2, k_rank, p_oversample, seed)
 
