@@ -70,6 +70,47 @@ __global__ void __launch_bounds__(256) k_upass_v2(long long m, int k, const doub
     }
 }
 
+// column dots with 16-byte loads: CTA owns CPC columns, thread t covers row pairs
+template <int CPC, int EP>
+__global__ void __launch_bounds__(256) k_coldot2(int m, int n, const double* __restrict__ A, long long lda,
+                                                const double* __restrict__ x, double* __restrict__ y) {
+    const int j0 = blockIdx.x * CPC;
+    double acc[CPC];
+#pragma unroll
+    for (int c = 0; c < CPC; ++c) acc[c] = 0.0;
+    const int m2 = m / 2;
+    for (int i0 = 0; i0 < m2; i0 += 256 * EP) {
+        double2 xv[EP], e[CPC][EP];
+#pragma unroll
+        for (int q = 0; q < EP; ++q) {
+            const int i = i0 + threadIdx.x + 256 * q;
+            xv[q] = i < m2 ? reinterpret_cast<const double2*>(x)[i] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < CPC; ++c)
+                e[c][q] = (i < m2 && j0 + c < n) ? __ldcs(reinterpret_cast<const double2*>(A + (long long)(j0 + c) * lda) + i)
+                                                 : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int c = 0; c < CPC; ++c)
+#pragma unroll
+            for (int q = 0; q < EP; ++q) acc[c] = fma(e[c][q].x, xv[q].x, fma(e[c][q].y, xv[q].y, acc[c]));
+    }
+    __shared__ double red[8][CPC];
+#pragma unroll
+    for (int c = 0; c < CPC; ++c) {
+        double v = acc[c];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < CPC && j0 + threadIdx.x < n) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+        y[j0 + threadIdx.x] = v;
+    }
+}
+
 template <class F>
 float time_ms(F&& f, int reps, cudaStream_t s) {
     cudaEvent_t a, b;
@@ -111,7 +152,7 @@ int main() {
         launch_gemv_rowmajor((256LL << 20) / 8 / 256, 256, flush, 256, XPlain{x}, EpiSt{y}, s);
     };
     float tf = time_ms(fl, reps, s);
-    for (long long tb : {16 << 10, 24 << 10, 40 << 10, 64 << 10}) {
+    for (long long tb : {64 << 10}) {
         float t = time_ms([&] { fl(); launch_stream_dot(n, r, r, U, XPlain{x}, EpiSt{y}, s, tb); }, reps, s) - tf;
         printf("U pass stream_dot tile %3lld KB: %.2f us  %.0f GB/s\n", tb >> 10, t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
     }
@@ -119,7 +160,7 @@ int main() {
         float t = time_ms([&] { fl(); launch_gemv_rowmajor(n, r, U, r, XPlain{x}, EpiSt{y}, s); }, reps, s) - tf;
         printf("U pass gemv_rowmajor:          %.2f us  %.0f GB/s\n", t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
     }
-    for (int ctas : {0, 1184, 2368}) {
+    for (int ctas : {0}) {
         auto run = [&](auto rpw) {
             constexpr int RPW = decltype(rpw)::value;
             long long need = (n / RPW + 7) / 8;
@@ -131,7 +172,7 @@ int main() {
         run(std::integral_constant<int, 4>{});
         run(std::integral_constant<int, 8>{});
     }
-    for (long long tb : {16 << 10, 32 << 10, 64 << 10}) {
+    for (long long tb : {64 << 10}) {
         float t = time_ms([&] { fl(); launch_stream_dot(m, m, m, P, XPlain{x}, EpiSt{y}, s, tb); }, reps, s) - tf;
         printf("P pass stream_dot tile %3lld KB: %.2f us  %.0f GB/s\n", tb >> 10, t * 1e3, 8.0 * m * m / (t * 1e-3) / 1e9);
     }
@@ -144,8 +185,17 @@ int main() {
         printf("P pass coldot CPC2:            %.2f us  %.0f GB/s\n", t * 1e3, 8.0 * m * m / (t * 1e-3) / 1e9);
         t = time_ms([&] { fl(); k_coldot<XPlain, EpiSt, 8><<<m / 8, 256, 0, s>>>(m, m, P, m, XPlain{x}, EpiSt{y}); }, reps, s) - tf;
         printf("P pass coldot CPC8:            %.2f us  %.0f GB/s\n", t * 1e3, 8.0 * m * m / (t * 1e-3) / 1e9);
-        t = time_ms([&] { fl(); launch_gemv_rowmajor(m, m, P, m, XPlain{x}, EpiSt{y}, s); }, reps, s) - tf;
-        printf("P pass gemv_rowmajor:          %.2f us  %.0f GB/s\n", t * 1e3, 8.0 * m * m / (t * 1e-3) / 1e9);
+        auto run2 = [&](auto cpc, auto ep) {
+            constexpr int CPC = decltype(cpc)::value, EP = decltype(ep)::value;
+            float t2 = time_ms([&] { fl(); k_coldot2<CPC, EP><<<m / CPC, 256, 0, s>>>(m, m, P, m, x, y); }, reps, s) - tf;
+            printf("P pass coldot2 CPC %d EP %d:    %.2f us  %.0f GB/s\n", CPC, EP, t2 * 1e3, 8.0 * m * m / (t2 * 1e-3) / 1e9);
+        };
+        run2(std::integral_constant<int, 1>{}, std::integral_constant<int, 4>{});
+        run2(std::integral_constant<int, 2>{}, std::integral_constant<int, 4>{});
+        run2(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
+        run2(std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{});
+        run2(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{});
+        run2(std::integral_constant<int, 4>{}, std::integral_constant<int, 2>{});
     }
     printf("flush %.2f us; %s\n", tf * 1e3, cudaGetErrorString(cudaGetLastError()));
     return 0;
