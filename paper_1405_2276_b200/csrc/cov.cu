@@ -194,38 +194,57 @@ __global__ void __launch_bounds__(kThreads) k_rows_inv(const double2* __restrict
 // per thread since blockDim ≥ n/8), so the load phase costs one memory latency, not eight.
 constexpr int kEpt = 8;
 
+// Shared layout of the single-transform kernels: twiddles | a | b.  NT > 0 (compile-time
+// power-of-two length): per-pass twiddle table and padded buffers (fft_block_p); NT = 0:
+// base table tw[0..n) and plain buffers (runtime schedule, fft_block).
+template <int NT>
+struct Lay1 {
+    static constexpr bool ST = NT > 0;
+    __device__ __forceinline__ static int tlen(int n) { return ST ? static_tw_len(NT) : n; }
+    __device__ __forceinline__ static int blen(int n) { return ST ? NT + NT / 8 + 1 : n; }
+    __device__ __forceinline__ static int ix(int e) { return ST ? fpad(e) : e; }
+    __device__ __forceinline__ static double2 twv(const FftLen& L, int i) { return ST ? L.twp[i] : L.tw[i]; }
+    template <int SIGN>
+    __device__ __forceinline__ static double2* fft(double2* a, double2* b, const FftLen& L, const double2* tw) {
+        if constexpr (ST) return fft_block_p<SIGN, NT>(a, b, tw);
+        else return fft_block<SIGN>(a, b, L, tw);
+    }
+};
+
 // Pass A: CTA = real rows 2b, 2b+1 (two-for-one) → W[ky][ix].
 template <int NT>
 __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x, int nx, int ny, FftLen fy,
-                                                   double2* __restrict__ W) {
+                                                   double2* __restrict__ W, long long ldx, long long ldw) {
+    using L = Lay1<NT>;
     extern __shared__ double2 sm[];
+    x += blockIdx.y * ldx;  // column blockIdx.y of a batch
+    W += blockIdx.y * ldw;
     const int my = fy.n, nky = my / 2 + 1, T = blockDim.x;
+    const int tl = L::tlen(my);
     double2* tw = sm;
-    double2* a = sm + my;
-    double2* b = a + my;
+    double2* a = sm + tl;
+    double2* b = a + L::blen(my);
     const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
     double2 tv[kEpt];
     double v0[kEpt], v1[kEpt];
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int iy = threadIdx.x + q * T;
-        tv[q] = iy < my ? fy.tw[iy] : make_double2(0.0, 0.0);
+        tv[q] = iy < tl ? L::twv(fy, iy) : make_double2(0.0, 0.0);
         v0[q] = iy < ny ? x[(long long)r0 * ny + iy] : 0.0;
         v1[q] = (iy < ny && r1 < nx) ? x[(long long)r1 * ny + iy] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int iy = threadIdx.x + q * T;
-        if (iy < my) {
-            tw[iy] = tv[q];
-            a[iy] = make_double2(v0[q], v1[q]);
-        }
+        if (iy < tl) tw[iy] = tv[q];
+        if (iy < my) a[L::ix(iy)] = make_double2(v0[q], v1[q]);
     }
     __syncthreads();
-    const double2* z = NT ? fft_block_c<-1, (NT ? NT : 1)>(a, b, tw) : fft_block<-1>(a, b, fy, tw);
+    const double2* z = L::template fft<-1>(a, b, fy, tw);
     for (int ky = threadIdx.x; ky < nky; ky += T) {
-        const double2 p = z[ky];
-        const double2 q = cconj(z[ky == 0 ? 0 : my - ky]);
+        const double2 p = z[L::ix(ky)];
+        const double2 q = cconj(z[L::ix(ky == 0 ? 0 : my - ky)]);
         W[(long long)ky * nx + r0] = make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));      // (Z + conj Z−)/2
         if (r1 < nx) W[(long long)ky * nx + r1] = make_double2(0.5 * (p.y - q.y), -0.5 * (p.x - q.x));  // /(2i)
     }
@@ -234,12 +253,15 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
 // Pass B: CTA = column ky: zero-pad, FFT, × spectrum, iFFT, keep ix < nx.
 template <int NT>
 __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx, FftLen fx,
-                                               const double* __restrict__ spec_half) {
+                                               const double* __restrict__ spec_half, long long ldw) {
+    using L = Lay1<NT>;
     extern __shared__ double2 sm[];
+    W += blockIdx.y * ldw;
     const int mx = fx.n, T = blockDim.x;
+    const int tl = L::tlen(mx);
     double2* tw = sm;
-    double2* a = sm + mx;
-    double2* b = a + mx;
+    double2* a = sm + tl;
+    double2* b = a + L::blen(mx);
     double2* w = W + (long long)blockIdx.x * nx;
     const double* sp = spec_half + (long long)blockIdx.x * mx;
     double2 tv[kEpt], dv[kEpt];
@@ -247,68 +269,71 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int ix = threadIdx.x + q * T;
-        tv[q] = ix < mx ? fx.tw[ix] : make_double2(0.0, 0.0);
+        tv[q] = ix < tl ? L::twv(fx, ix) : make_double2(0.0, 0.0);
         dv[q] = ix < nx ? w[ix] : make_double2(0.0, 0.0);
         spv[q] = ix < mx ? __ldg(sp + ix) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int ix = threadIdx.x + q * T;
-        if (ix < mx) {
-            tw[ix] = tv[q];
-            a[ix] = dv[q];
-        }
+        if (ix < tl) tw[ix] = tv[q];
+        if (ix < mx) a[L::ix(ix)] = dv[q];
     }
     __syncthreads();
-    double2* f = NT ? fft_block_c<-1, (NT ? NT : 1)>(a, b, tw) : fft_block<-1>(a, b, fx, tw);
+    double2* f = L::template fft<-1>(a, b, fx, tw);
     double2* g = (f == a) ? b : a;
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int kx = threadIdx.x + q * T;
-        if (kx < mx) f[kx] = cscale(f[kx], spv[q]);
+        if (kx < mx) f[L::ix(kx)] = cscale(f[L::ix(kx)], spv[q]);
     }
     __syncthreads();
-    f = NT ? fft_block_c<+1, (NT ? NT : 1)>(f, g, tw) : fft_block<+1>(f, g, fx, tw);
-    for (int ix = threadIdx.x; ix < nx; ix += T) w[ix] = f[ix];
+    f = L::template fft<+1>(f, g, fx, tw);
+    for (int ix = threadIdx.x; ix < nx; ix += T) w[ix] = f[L::ix(ix)];
 }
 
 // Pass C: CTA = rows 2b, 2b+1 rebuilt from the Hermitian half, ×scale, crop.
 template <int NT>
 __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ W, int nx, int ny, FftLen fy,
                                                    double* __restrict__ y, double scale,
-                                                   const double* __restrict__ acc_coef, const int* __restrict__ gate) {
+                                                   const double* __restrict__ acc_coef, const int* __restrict__ gate,
+                                                   long long ldw, long long ldy) {
+    using L = Lay1<NT>;
     extern __shared__ double2 sm[];
+    W += blockIdx.y * ldw;
+    y += blockIdx.y * ldy;
     const int my = fy.n, T = blockDim.x;
+    const int tl = L::tlen(my);
     double2* tw = sm;
-    double2* a = sm + my;
-    double2* b = a + my;
+    double2* a = sm + tl;
+    double2* b = a + L::blen(my);
     const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
     double2 tv[kEpt], x1[kEpt], x2[kEpt];
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int ky = threadIdx.x + q * T;
         const int kk = ky > my / 2 ? my - ky : ky;
-        tv[q] = ky < my ? fy.tw[ky] : make_double2(0.0, 0.0);
+        tv[q] = ky < tl ? L::twv(fy, ky) : make_double2(0.0, 0.0);
         x1[q] = ky < my ? W[(long long)kk * nx + r0] : make_double2(0.0, 0.0);
         x2[q] = (ky < my && r1 < nx) ? W[(long long)kk * nx + r1] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
         const int ky = threadIdx.x + q * T;
+        if (ky < tl) tw[ky] = tv[q];
         if (ky < my) {
-            tw[ky] = tv[q];
             double2 u1 = x1[q], u2 = x2[q];
             if (ky > my / 2) { u1 = cconj(u1); u2 = cconj(u2); }
-            a[ky] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
+            a[L::ix(ky)] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
         }
     }
     __syncthreads();
-    const double2* z = NT ? fft_block_c<+1, (NT ? NT : 1)>(a, b, tw) : fft_block<+1>(a, b, fy, tw);
+    const double2* z = L::template fft<+1>(a, b, fy, tw);
     if (acc_coef) {  // y += c·Γx (the mean update's α·Γ(Hᵀz) term), skipped when *gate
         if (gate && *gate) return;
         const double c = *acc_coef;
         for (int iy = threadIdx.x; iy < ny; iy += T) {
-            const double2 v = z[iy];
+            const double2 v = z[L::ix(iy)];
             double* y0 = y + (long long)r0 * ny + iy;
             *y0 = *y0 + c * (v.x * scale);
             if (r1 < nx) {
@@ -319,7 +344,7 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
         return;
     }
     for (int iy = threadIdx.x; iy < ny; iy += T) {
-        const double2 v = z[iy];
+        const double2 v = z[L::ix(iy)];
         y[(long long)r0 * ny + iy] = v.x * scale;
         if (r1 < nx) y[(long long)r1 * ny + iy] = v.y * scale;
     }
@@ -383,6 +408,9 @@ __global__ void __launch_bounds__(kThreads) k_sampler_rows(const double2* __rest
 }
 
 // --------------------------------------------------------------------------- host orchestration
+// lengths with a compile-time single-transform schedule (see with_len)
+static bool static_len(int n) { return n == 64 || n == 128 || n == 256 || n == 512 || n == 1024 || n == 2048; }
+
 static void plan_radices(FftLen& L, int n, bool max8 = false) {
     L.n = n;
     L.npass = 0;
@@ -400,6 +428,29 @@ static void plan_radices(FftLen& L, int n, bool max8 = false) {
     for (int f : {3, 5, 7})
         while (v % f == 0) { push(f); v /= f; }
     if (v != 1) throw std::invalid_argument("fft: length " + std::to_string(n) + " is not {2,3,5,7}-smooth");
+}
+
+// per-pass twiddle table of the compile-time schedule (FftLen::twp), same angles as the
+// base table: exp(−2πi·r·k·(n/(NS·R))/n)
+void Cov::setup_static_tw(FftLen& L, DBuf<double2>& tw, int n) {
+    L.twp = nullptr;
+    if (!static_len(n)) return;
+    std::vector<double2> h;
+    for (int ns = 1; ns < n;) {
+        const int R = (n / ns) % 8 == 0 ? 8 : n / ns;
+        if (ns > 1)
+            for (int r = 1; r < R; ++r)
+                for (int k = 0; k < ns; ++k) {
+                    const long long e = (long long)r * k * (n / (ns * R));
+                    const long double ang = -2.0L * std::numbers::pi_v<long double> * (long double)e / n;
+                    h.push_back(make_double2(double(cosl(ang)), double(sinl(ang))));
+                }
+        ns *= R;
+    }
+    if (int(h.size()) != static_tw_len(n)) throw std::logic_error("fft: static twiddle table size");
+    tw.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) FKB_CUDA(cudaMemcpy(tw.p, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
+    L.twp = tw.p;
 }
 
 void Cov::setup_len(FftLen& L, DBuf<double2>& tw, int n) {
@@ -461,6 +512,8 @@ bool Cov::try_spectrum(double& worst) {  // covariance.hpp:264-298
     fy8 = fy;
     plan_radices(fx8, mx, true);
     plan_radices(fy8, my, true);
+    setup_static_tw(fx8, twpx, mx);
+    setup_static_tw(fy8, twpy, my);
     // Symbol on the torus at wrapped distances (:269-277), evaluated on the host with the
     // reference formula (std::cyl_bessel_k); only the unique quarter is evaluated.
     const double dx = lx / nx, dy = ly / ny;
@@ -537,6 +590,11 @@ std::vector<double> Cov::spectrum_host() const {
 // threads per transform of the single-vector kernels: n/8 (one radix-8 butterfly each per
 // pass), a multiple of 32 in [32, 256]
 static int threads_1(int n) { return std::max(32, ((n / kEpt + 31) / 32) * 32); }
+// shared bytes of a single-transform kernel of length n (see Lay1)
+static size_t smem_1(int n) {
+    if (static_len(n)) return (size_t(static_tw_len(n)) + 2 * size_t(n + n / 8 + 1)) * sizeof(double2);
+    return 3 * size_t(n) * sizeof(double2);
+}
 
 template <int NT>
 static void set_smem_1() {
@@ -565,31 +623,35 @@ void Cov::apply1(const double* dx, double* dy) {
     apply1_inv(dy, nullptr, nullptr);
 }
 
-void Cov::apply1_fwd(const double* dx) {
+void Cov::apply1_fwd(const double* dx, int ncols, long long ldx) {
     static bool attr = false;
     if (!attr) {
         for (int n : {64, 128, 256, 512, 1024, 2048, 0}) with_len(n, [](auto c) { set_smem_1<decltype(c)::value>(); });
         attr = true;
     }
-    const size_t sy = 3 * size_t(my) * sizeof(double2), sx = 3 * size_t(mx) * sizeof(double2);
+    const size_t sy = smem_1(my), sx = smem_1(mx);
     if (sy > 227 * 1024 || sx > 227 * 1024 || threads_1(mx) > 256 || threads_1(my) > 256)
         throw std::invalid_argument("fft: transform too large for the single-vector kernels");
+    const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
-        k_rows_fwd_1<decltype(c)::value><<<ceil_div(nx, 2), threads_1(my), sy, stream>>>(dx, nx, ny, fy8, work.p);
+        k_rows_fwd_1<decltype(c)::value><<<dim3(ceil_div(nx, 2), ncols), threads_1(my), sy, stream>>>(
+            dx, nx, ny, fy8, work.p, ldx, ldw);
     });
     FKB_LAUNCH_CHECK();
     with_len(mx, [&](auto c) {
-        k_cols_1<decltype(c)::value><<<nky, threads_1(mx), sx, stream>>>(work.p, nx, fx8, spec_half.p);
+        k_cols_1<decltype(c)::value><<<dim3(nky, ncols), threads_1(mx), sx, stream>>>(work.p, nx, fx8, spec_half.p,
+                                                                                     ldw);
     });
     FKB_LAUNCH_CHECK();
     count_launch(2);
 }
 
-void Cov::apply1_inv(double* dy, const double* acc_coef, const int* gate) {
-    const size_t sy = 3 * size_t(my) * sizeof(double2);
+void Cov::apply1_inv(double* dy, const double* acc_coef, const int* gate, int ncols, long long ldy) {
+    const size_t sy = smem_1(my);
+    const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
-        k_rows_inv_1<decltype(c)::value><<<ceil_div(nx, 2), threads_1(my), sy, stream>>>(
-            work.p, nx, ny, fy8, dy, 1.0 / double(M()), acc_coef, gate);
+        k_rows_inv_1<decltype(c)::value><<<dim3(ceil_div(nx, 2), ncols), threads_1(my), sy, stream>>>(
+            work.p, nx, ny, fy8, dy, 1.0 / double(M()), acc_coef, gate, ldw, ldy);
     });
     FKB_LAUNCH_CHECK();
     count_launch();
@@ -602,8 +664,17 @@ void Cov::apply(const double* dX, long long ldx, int ncols, double* dY, long lon
         apply1(dX, dY);
         return;
     }
-    // Few columns (the per-step Γ(Hᵀz)): one transform per CTA and narrow CTAs so the three
-    // passes still spread over the SMs; wide blocks of columns keep the batched shapes.
+    // Blocks of columns: the CTA-per-transform kernels with blockIdx.y = column, in batches
+    // whose intermediate stays L2-resident (the generic batched kernels below remain for
+    // lengths the single-transform kernels cannot hold).
+    if (smem_1(mx) <= 227 * 1024 && smem_1(my) <= 227 * 1024 && threads_1(mx) <= 256 && threads_1(my) <= 256) {
+        for (int c0 = 0; c0 < ncols; c0 += batch_cap) {
+            const int bc = std::min(batch_cap, ncols - c0);
+            apply1_fwd(dX + (long long)c0 * ldx, bc, ldx);
+            apply1_inv(dY + (long long)c0 * ldy, nullptr, nullptr, bc, ldy);
+        }
+        return;
+    }
     const bool narrow = ncols < 8;
     const int pairs = narrow ? 1 : pairs_for(my), kt = narrow ? 1 : kt_for(mx);
     const int tA = narrow ? std::max(64, std::min(kThreads, my / 4)) : kThreads;

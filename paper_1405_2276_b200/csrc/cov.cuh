@@ -24,6 +24,7 @@ struct Cov {
     FftLen fx, fy;
     FftLen fx8, fy8;  // radix ≤ 8 schedules (single-vector kernels), same twiddle tables
     DBuf<double2> twx, twy;
+    DBuf<double2> twpx, twpy;  // per-pass twiddles of the compile-time schedules (FftLen::twp)
     DBuf<double> spec_half;  // [ky][kx], clipped ≥ 0 (covariance.hpp:295)
     DBuf<double> amp_full;   // √spectrum on the full torus, row-major mx×my (sampler :339)
     DBuf<double2> work;      // intermediate [col][ky][ix]
@@ -40,8 +41,8 @@ struct Cov {
     // the single-vector apply split at its last pass: forward rows + column pass into the work
     // buffer, then the inverse rows pass storing Γx into dy, or (acc_coef ≠ null) adding
     // (*acc_coef)·Γx to dy unless *gate
-    void apply1_fwd(const double* dx);
-    void apply1_inv(double* dy, const double* acc_coef, const int* gate);
+    void apply1_fwd(const double* dx, int ncols = 1, long long ldx = 0);
+    void apply1_inv(double* dy, const double* acc_coef, const int* gate, int ncols = 1, long long ldy = 0);
     // Two N(0,Γ) draws (covariance.hpp:332-353) into device vectors.
     void sample_pair(uint64_t seed, uint64_t stream_id, double* da, double* db);
     // Host copy of the full clipped spectrum (covariance.hpp:207-211), row-major mx×my.
@@ -50,6 +51,7 @@ struct Cov {
   private:
     bool try_spectrum(double& worst);
     void setup_len(FftLen& L, DBuf<double2>& tw, int n);
+    void setup_static_tw(FftLen& L, DBuf<double2>& tw, int n);
     void ensure_work(int ncols);
 };
 

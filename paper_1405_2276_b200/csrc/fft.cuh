@@ -19,7 +19,21 @@ struct FftLen {
     int npass = 0;
     int radix[kMaxPasses] = {0};
     const double2* tw = nullptr;
+    // compile-time-schedule twiddles (radix-8 passes, then one radix-2/4): for each pass that
+    // starts at stride NS > 1, entries [(r−1)·NS + k] = exp(−2πi·r·k/(NS·R)), r = 1..R−1
+    const double2* twp = nullptr;
 };
+
+// host/device: length of that table for a power-of-two n (0 for n ≤ 8)
+constexpr int static_tw_len(int n) {
+    int tot = 0, ns = 1;
+    while (ns < n) {
+        const int R = (n / ns) % 8 == 0 ? 8 : n / ns;
+        if (ns > 1) tot += (R - 1) * ns;
+        ns *= R;
+    }
+    return tot;
+}
 
 // constants for the generic odd radices 3, 5, 7: cos/sin(2π j/R), filled at init
 struct OddRadixTables {

@@ -268,4 +268,46 @@ __device__ __forceinline__ double2* fft_block_c(double2* a, double2* b, const do
     }
 }
 
+// ---- compile-time schedules on a PADDED shared layout (slot(e) = e + e/8): every radix-8
+// pass's strided stores (stride 8·16 B at NS = 1) and loads become ≤ 4-way bank-conflict-free
+// (the 16-byte minimum), and each pass reads its own r-major twiddle sub-table (consecutive
+// k → consecutive banks).  Padded buffers hold n + n/8 + 1 entries.
+__device__ __forceinline__ int fpad(int e) { return e + (e >> 3); }
+
+template <int R, int SIGN, int N, int NS>
+__device__ __forceinline__ void stockham_pass_p(const double2* __restrict__ in, double2* __restrict__ out,
+                                                const double2* __restrict__ tp) {
+    constexpr int nb = N / R;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+        const int k = j % NS;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = in[fpad(j + r * nb)];
+        if constexpr (NS > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 w = tp[(r - 1) * NS + k];
+                if (SIGN > 0) w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+        }
+        dft<R, SIGN>(v);
+        const int d = (j / NS) * NS * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[fpad(d + r * NS)] = v[r];
+    }
+}
+
+template <int SIGN, int N, int NS = 1, int OFF = 0>
+__device__ __forceinline__ double2* fft_block_p(double2* a, double2* b, const double2* tp) {
+    if constexpr (NS >= N) {
+        return a;
+    } else {
+        constexpr int R = static_radix<N>(NS);
+        stockham_pass_p<R, SIGN, N, NS>(a, b, tp + OFF);
+        __syncthreads();
+        return fft_block_p<SIGN, N, NS * R, OFF + (NS > 1 ? (R - 1) * NS : 0)>(b, a, tp);
+    }
+}
+
 }  // namespace fkb
