@@ -225,6 +225,31 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
     double2* a = sm + tl;
     double2* b = a + L::blen(my);
     const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
+    if constexpr (reg_fft_len<NT>()) {  // register-resident transform (T = NT/8, 8 elements each)
+        const int j = threadIdx.x;
+        double2 v[8], tv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int iy = j + q * T;
+            tv[q] = iy < tl ? fy.twp[iy] : make_double2(0.0, 0.0);
+            v[q] = make_double2(iy < ny ? x[(long long)r0 * ny + iy] : 0.0,
+                                (iy < ny && r1 < nx) ? x[(long long)r1 * ny + iy] : 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (j + q * T < tl) tw[j + q * T] = tv[q];
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[fpad(j + q * T)] = v[q];
+        __syncthreads();
+        for (int ky = j; ky < nky; ky += T) {
+            const double2 p = a[fpad(ky)];
+            const double2 q = cconj(a[fpad(ky == 0 ? 0 : my - ky)]);
+            W[(long long)ky * nx + r0] = make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));
+            if (r1 < nx) W[(long long)ky * nx + r1] = make_double2(0.5 * (p.y - q.y), -0.5 * (p.x - q.x));
+        }
+        return;
+    }
     double2 tv[kEpt];
     double v0[kEpt], v1[kEpt];
 #pragma unroll
@@ -264,6 +289,29 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
     double2* b = a + L::blen(mx);
     double2* w = W + (long long)blockIdx.x * nx;
     const double* sp = spec_half + (long long)blockIdx.x * mx;
+    if constexpr (reg_fft_len<NT>()) {  // forward → × spectrum → inverse, all in registers
+        const int j = threadIdx.x;
+        double2 v[8], tv[8];
+        double spv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int ix = j + q * T;
+            tv[q] = ix < tl ? fx.twp[ix] : make_double2(0.0, 0.0);
+            v[q] = ix < nx ? w[ix] : make_double2(0.0, 0.0);
+            spv[q] = __ldg(sp + ix);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (j + q * T < tl) tw[j + q * T] = tv[q];
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = cscale(v[q], spv[q]);
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (j + q * T < nx) w[j + q * T] = v[q];
+        return;
+    }
     double2 tv[kEpt], dv[kEpt];
     double spv[kEpt];
 #pragma unroll
@@ -308,6 +356,41 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
     double2* a = sm + tl;
     double2* b = a + L::blen(my);
     const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
+    if constexpr (reg_fft_len<NT>()) {
+        const int j = threadIdx.x;
+        double2 v[8], tv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int ky = j + q * T;
+            const bool hi = ky > my / 2;
+            const int kk = hi ? my - ky : ky;
+            tv[q] = ky < tl ? fy.twp[ky] : make_double2(0.0, 0.0);
+            double2 u1 = W[(long long)kk * nx + r0], u2 = r1 < nx ? W[(long long)kk * nx + r1] : make_double2(0.0, 0.0);
+            if (hi) { u1 = cconj(u1); u2 = cconj(u2); }
+            v[q] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (j + q * T < tl) tw[j + q * T] = tv[q];
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+        if (acc_coef && gate && *gate) return;
+        const double c = acc_coef ? *acc_coef : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int iy = j + q * T;
+            if (iy >= ny) continue;
+            double* y0 = y + (long long)r0 * ny + iy;
+            double* y1 = y + (long long)r1 * ny + iy;
+            if (acc_coef) {
+                *y0 = *y0 + c * (v[q].x * scale);
+                if (r1 < nx) *y1 = *y1 + c * (v[q].y * scale);
+            } else {
+                *y0 = v[q].x * scale;
+                if (r1 < nx) *y1 = v[q].y * scale;
+            }
+        }
+        return;
+    }
     double2 tv[kEpt], x1[kEpt], x2[kEpt];
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {

@@ -310,4 +310,43 @@ __device__ __forceinline__ double2* fft_block_p(double2* a, double2* b, const do
     }
 }
 
+// ---- register-resident radix-8 FFT for N = 8^a with N/8 threads: thread j holds
+// v[r] = x[j + r·N/8] on entry and X[j + r·N/8] on exit (the Stockham input and output
+// orderings coincide for this mapping), so the first pass needs no shared-memory load and the
+// last pass no store — a forward and an inverse transform chain through registers.  Passes
+// exchange through two padded ping-pong buffers (one barrier each); twiddles as fft_block_p.
+template <int N>
+constexpr bool reg_fft_len() { return N == 512 || N == 4096; }  // N/8 threads: ≥ 64
+
+template <int SIGN, int N>
+__device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2* bufB, const double2* __restrict__ tp) {
+    static_assert(reg_fft_len<N>(), "fft_reg: N must be a power of 8");
+    constexpr int nb = N / 8;
+    const int j = threadIdx.x;
+    dft<8, SIGN>(v);  // pass NS = 1: no twiddles
+    int off = 0;
+    double2* buf = bufA;
+#pragma unroll
+    for (int ns = 1; ns < nb; ns *= 8) {
+        {
+            const int k = j % ns, d = (j / ns) * ns * 8 + k;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) buf[fpad(d + r * ns)] = v[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = buf[fpad(j + r * nb)];
+        const int ns2 = ns * 8, k2 = j % ns2;
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+            double2 w = tp[off + (r - 1) * ns2 + k2];
+            if (SIGN > 0) w.y = -w.y;
+            v[r] = cmul(v[r], w);
+        }
+        off += 7 * ns2;
+        dft<8, SIGN>(v);
+        buf = (buf == bufA) ? bufB : bufA;
+    }
+}
+
 }  // namespace fkb
