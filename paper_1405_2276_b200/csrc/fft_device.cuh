@@ -337,11 +337,19 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2*
 #pragma unroll
         for (int r = 0; r < 8; ++r) v[r] = buf[fpad(j + r * nb)];
         const int ns2 = ns * 8, k2 = j % ns2;
-#pragma unroll
-        for (int r = 1; r < 8; ++r) {
-            double2 w = tp[off + (r - 1) * ns2 + k2];
-            if (SIGN > 0) w.y = -w.y;
-            v[r] = cmul(v[r], w);
+        {  // w^r from one shared-memory load: w² = w·w, w³ = w²·w, … (≤ 4 ulp; halves the
+           // pass's shared-memory wavefronts, the kernel's limiter)
+            double2 w1 = tp[off + k2];
+            if (SIGN > 0) w1.y = -w1.y;
+            const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
+            const double2 w5 = cmul(w4, w1), w6 = cmul(w3, w3), w7 = cmul(w6, w1);
+            v[1] = cmul(v[1], w1);
+            v[2] = cmul(v[2], w2);
+            v[3] = cmul(v[3], w3);
+            v[4] = cmul(v[4], w4);
+            v[5] = cmul(v[5], w5);
+            v[6] = cmul(v[6], w6);
+            v[7] = cmul(v[7], w7);
         }
         off += 7 * ns2;
         dft<8, SIGN>(v);
