@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_inv(const double2* __restrict
 // Every global load of a kernel is issued before the first shared-memory store (≤ 8 elements
 // per thread since blockDim ≥ n/8), so the load phase costs one memory latency, not eight.
 constexpr int kEpt = 8;
+constexpr int kRowPairs = 4;   // batched: 8 consecutive rows per CTA (128-byte W segments)
+constexpr int kRowPairs1 = 2;  // single vector: fewer, still-coalesced CTAs (measured best)  // transforms per CTA in the batched register-resident rows passes
 
 // Shared layout of the single-transform kernels: twiddles | a | b.  NT > 0 (compile-time
 // power-of-two length): per-pass twiddle table and padded buffers (fft_block_p); NT = 0:
@@ -225,28 +227,50 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
     double2* a = sm + tl;
     double2* b = a + L::blen(my);
     const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
-    if constexpr (reg_fft_len<NT>()) {  // register-resident transform (T = NT/8, 8 elements each)
-        const int j = threadIdx.x;
-        double2 v[8], tv[8];
+    if constexpr (reg_fft_len<NT>()) {
+        // register-resident transforms, kRowPairs per CTA (rows ix0 … ix0 + 2·kRowPairs − 1):
+        // thread (pair p, index j) loads 32 consecutive y of two rows per warp, and the W tile
+        // is written 2·kRowPairs consecutive ix (128 B) per ky
+        constexpr int TPT = (reg_fft_len<NT>() ? NT : 512) / 8;  // threads per transform
+        const int RP = blockDim.x / TPT;                          // transforms (row pairs) per CTA
+        const int t = threadIdx.x, p = t / TPT, j = t % TPT;
+        const int ix0 = blockIdx.x * 2 * RP;
+        const int q0 = ix0 + 2 * p, q1 = q0 + 1;
+        const int bl = L::blen(my);
+        double2* ap = sm + tl + p * bl;
+        double2 v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int iy = j + q * T;
-            tv[q] = iy < tl ? fy.twp[iy] : make_double2(0.0, 0.0);
-            v[q] = make_double2(iy < ny ? x[(long long)r0 * ny + iy] : 0.0,
-                                (iy < ny && r1 < nx) ? x[(long long)r1 * ny + iy] : 0.0);
+            const int iy = j + q * TPT;
+            v[q] = make_double2((iy < ny && q0 < nx) ? x[(long long)q0 * ny + iy] : 0.0,
+                                (iy < ny && q1 < nx) ? x[(long long)q1 * ny + iy] : 0.0);
         }
+        {  // twiddles: every load in flight before the first store (≤ 8 per thread)
+            double2 tv[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (j + q * T < tl) tw[j + q * T] = tv[q];
-        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+            for (int q = 0; q < 8; ++q) {
+                const int e = t + q * int(blockDim.x);
+                tv[q] = e < tl ? fy.twp[e] : make_double2(0.0, 0.0);
+            }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[fpad(j + q * T)] = v[q];
+            for (int q = 0; q < 8; ++q)
+                if (t + q * int(blockDim.x) < tl) tw[t + q * int(blockDim.x)] = tv[q];
+        }
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, tw, j);  // ping-pong if alone
+        __syncthreads();  // last exchange loads done before the result overwrites the buffer
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ap[fpad(j + q * TPT)] = v[q];
         __syncthreads();
-        for (int ky = j; ky < nky; ky += T) {
-            const double2 p = a[fpad(ky)];
-            const double2 q = cconj(a[fpad(ky == 0 ? 0 : my - ky)]);
-            W[(long long)ky * nx + r0] = make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));
-            if (r1 < nx) W[(long long)ky * nx + r1] = make_double2(0.5 * (p.y - q.y), -0.5 * (p.x - q.x));
+        const int rows = 2 * RP;
+        for (int e = t; e < rows * nky; e += blockDim.x) {
+            const int ky = e / rows, rl = e - ky * rows;
+            const int ix = ix0 + rl;
+            if (ix >= nx) continue;
+            const double2* zt = sm + tl + (rl >> 1) * bl;
+            const double2 pp = zt[fpad(ky)];
+            const double2 qq = cconj(zt[fpad(ky == 0 ? 0 : my - ky)]);
+            W[(long long)ky * nx + ix] = (rl & 1) == 0 ? make_double2(0.5 * (pp.x + qq.x), 0.5 * (pp.y + qq.y))
+                                                       : make_double2(0.5 * (pp.y - qq.y), -0.5 * (pp.x - qq.x));
         }
         return;
     }
@@ -303,10 +327,10 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             if (j + q * T < tl) tw[j + q * T] = tv[q];
-        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw, j);
 #pragma unroll
         for (int q = 0; q < 8; ++q) v[q] = cscale(v[q], spv[q]);
-        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw, j);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             if (j + q * T < nx) w[j + q * T] = v[q];
@@ -357,36 +381,51 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
     double2* b = a + L::blen(my);
     const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
     if constexpr (reg_fft_len<NT>()) {
-        const int j = threadIdx.x;
-        double2 v[8], tv[8];
+        // kRowPairs transforms per CTA; thread (p = t % kRowPairs, j = t / kRowPairs) so the
+        // 2·kRowPairs consecutive W entries of a ky (128 B) are read by consecutive lanes
+        constexpr int TPT = (reg_fft_len<NT>() ? NT : 512) / 8;
+        const int RP = blockDim.x / TPT;
+        const int t = threadIdx.x, p = t % RP, j = t / RP;
+        const int ix0 = blockIdx.x * 2 * RP;
+        const int q0 = ix0 + 2 * p, q1 = q0 + 1;
+        const int bl = L::blen(my);
+        double2* ap = sm + tl + p * bl;
+        double2 v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int ky = j + q * T;
+            const int ky = j + q * TPT;
             const bool hi = ky > my / 2;
             const int kk = hi ? my - ky : ky;
-            tv[q] = ky < tl ? fy.twp[ky] : make_double2(0.0, 0.0);
-            double2 u1 = W[(long long)kk * nx + r0], u2 = r1 < nx ? W[(long long)kk * nx + r1] : make_double2(0.0, 0.0);
+            double2 u1 = q0 < nx ? W[(long long)kk * nx + q0] : make_double2(0.0, 0.0);
+            double2 u2 = q1 < nx ? W[(long long)kk * nx + q1] : make_double2(0.0, 0.0);
             if (hi) { u1 = cconj(u1); u2 = cconj(u2); }
             v[q] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
         }
+        {  // twiddles: every load in flight before the first store (≤ 8 per thread)
+            double2 tv[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (j + q * T < tl) tw[j + q * T] = tv[q];
-        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw);
+            for (int q = 0; q < 8; ++q) {
+                const int e = t + q * int(blockDim.x);
+                tv[q] = e < tl ? fy.twp[e] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (t + q * int(blockDim.x) < tl) tw[t + q * int(blockDim.x)] = tv[q];
+        }
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, tw, j);
         if (acc_coef && gate && *gate) return;
         const double c = acc_coef ? *acc_coef : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int iy = j + q * T;
+            const int iy = j + q * TPT;
             if (iy >= ny) continue;
-            double* y0 = y + (long long)r0 * ny + iy;
-            double* y1 = y + (long long)r1 * ny + iy;
-            if (acc_coef) {
-                *y0 = *y0 + c * (v[q].x * scale);
-                if (r1 < nx) *y1 = *y1 + c * (v[q].y * scale);
-            } else {
-                *y0 = v[q].x * scale;
-                if (r1 < nx) *y1 = v[q].y * scale;
+            if (q0 < nx) {
+                double* y0 = y + (long long)q0 * ny + iy;
+                *y0 = acc_coef ? *y0 + c * (v[q].x * scale) : v[q].x * scale;
+            }
+            if (q1 < nx) {
+                double* y1 = y + (long long)q1 * ny + iy;
+                *y1 = acc_coef ? *y1 + c * (v[q].y * scale) : v[q].y * scale;
             }
         }
         return;
@@ -678,6 +717,11 @@ static size_t smem_1(int n) {
     if (static_len(n)) return (size_t(static_tw_len(n)) + 2 * size_t(n + n / 8 + 1)) * sizeof(double2);
     return 3 * size_t(n) * sizeof(double2);
 }
+// rows passes: register-resident lengths hold kRowPairs single buffers
+static size_t smem_rows(int n, int rp) {
+    if (n == 512) return (size_t(static_tw_len(n)) + size_t(std::max(rp, 2)) * (n + n / 8 + 1)) * sizeof(double2);
+    return smem_1(n);
+}
 
 template <int NT>
 static void set_smem_1() {
@@ -717,7 +761,9 @@ void Cov::apply1_fwd(const double* dx, int ncols, long long ldx) {
         throw std::invalid_argument("fft: transform too large for the single-vector kernels");
     const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
-        k_rows_fwd_1<decltype(c)::value><<<dim3(ceil_div(nx, 2), ncols), threads_1(my), sy, stream>>>(
+        constexpr int NT = decltype(c)::value;
+        const int rp = reg_fft_len<NT>() ? (ncols >= 8 ? kRowPairs : kRowPairs1) : 1;  // coalescing vs CTA count
+        k_rows_fwd_1<NT><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
             dx, nx, ny, fy8, work.p, ldx, ldw);
     });
     FKB_LAUNCH_CHECK();
@@ -733,7 +779,9 @@ void Cov::apply1_inv(double* dy, const double* acc_coef, const int* gate, int nc
     const size_t sy = smem_1(my);
     const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
-        k_rows_inv_1<decltype(c)::value><<<dim3(ceil_div(nx, 2), ncols), threads_1(my), sy, stream>>>(
+        constexpr int NT = decltype(c)::value;
+        const int rp = reg_fft_len<NT>() ? (ncols >= 8 ? kRowPairs : kRowPairs1) : 1;
+        k_rows_inv_1<NT><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
             work.p, nx, ny, fy8, dy, 1.0 / double(M()), acc_coef, gate, ldw, ldy);
     });
     FKB_LAUNCH_CHECK();

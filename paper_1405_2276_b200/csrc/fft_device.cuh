@@ -318,16 +318,20 @@ __device__ __forceinline__ double2* fft_block_p(double2* a, double2* b, const do
 template <int N>
 constexpr bool reg_fft_len() { return N == 512 || N == 4096; }  // N/8 threads: ≥ 64
 
+// j = index within the transform (0..N/8−1); several transforms may share a CTA (every
+// thread of the CTA must call with the same N).  bufB == nullptr: one buffer per transform
+// and a second barrier per exchange.
 template <int SIGN, int N>
-__device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2* bufB, const double2* __restrict__ tp) {
+__device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2* bufB, const double2* __restrict__ tp,
+                                        int j) {
     static_assert(reg_fft_len<N>(), "fft_reg: N must be a power of 8");
     constexpr int nb = N / 8;
-    const int j = threadIdx.x;
     dft<8, SIGN>(v);  // pass NS = 1: no twiddles
     int off = 0;
     double2* buf = bufA;
 #pragma unroll
     for (int ns = 1; ns < nb; ns *= 8) {
+        if (!bufB && ns > 1) __syncthreads();  // single buffer: previous loads done
         {
             const int k = j % ns, d = (j / ns) * ns * 8 + k;
 #pragma unroll
@@ -353,7 +357,7 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2*
         }
         off += 7 * ns2;
         dft<8, SIGN>(v);
-        buf = (buf == bufA) ? bufB : bufA;
+        if (bufB) buf = (buf == bufA) ? bufB : bufA;
     }
 }
 
