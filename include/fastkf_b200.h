@@ -113,6 +113,8 @@ int fkb_realizations_device(fkb_filter* f, uint64_t seed, int count, double* d_o
 /* Y = H X (trans = 0) or Hᵀ X (trans = 1) with the filter's uploaded operator */
 int fkb_filter_spmm(fkb_filter* f, int trans, const double* dX, long long ldx, int ncols, double* dY,
                     long long ldy);
+/* same products on ROW-major blocks (X: cols × ncols, Y: rows × ncols, row stride ncols) */
+int fkb_filter_spmm_rm(fkb_filter* f, int trans, const double* dX, int ncols, double* dY);
 void* fkb_filter_stream(fkb_filter* f);
 int fkb_filter_launches_per_step(fkb_filter* f);
 /* innovation solve: 1 (default) Woodbury in the offline eigenbasis of G = HΓHᵀ with a

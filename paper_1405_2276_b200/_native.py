@@ -68,6 +68,7 @@ SIGNATURES = {
     "fkb_realizations_device": (_i, [_p, _u64, _i, _p, _p]),
     "fkb_filter_spmm": (_i, [_p, _i, _p, _ll, _i, _p, _ll]),
     "fkb_filter_stream": (_p, [_p]),
+    "fkb_filter_spmm_rm": (_i, [_p, _i, _p, _i, _p]),
     "fkb_filter_launches_per_step": (_i, [_p]),
     "fkb_filter_set_solver": (_i, [_p, _i]),
     "fkb_filter_eig_sweeps": (_i, [_p]),

@@ -38,6 +38,7 @@ struct fkb_cov {
     cudaStream_t stream = nullptr;
     std::unique_ptr<fkb::Cov> cov;
     ~fkb_cov() {
+        if (stream) cudaStreamSynchronize(stream);
         cov.reset();
         if (stream) cudaStreamDestroy(stream);
     }
@@ -374,6 +375,14 @@ int fkb_filter_spmm(fkb_filter* f, int trans, const double* dX, long long ldx, i
         fkb::spmm(trans ? F.HT : F.H, dX, ldx, ncols, dY, ldy, 1.0, 0.0, F.s);
     });
 }
+int fkb_filter_spmm_rm(fkb_filter* f, int trans, const double* dX, int ncols, double* dY) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (ncols < 0) throw std::invalid_argument("spmm: negative column count");
+        fkb::spmm_rm(trans ? F.HT : F.H, dX, ncols, ncols, dY, ncols, 1.0, F.s);
+    });
+}
 void* fkb_filter_stream(fkb_filter* f) { return f ? (void*)f->f->s : nullptr; }
 int fkb_filter_set_solver(fkb_filter* f, int mode) {
     return guarded([&] {
@@ -460,11 +469,23 @@ int fkb_filter_launches_per_step(fkb_filter* f) { return f ? f->f->launches_per_
 
 int fkb_dmalloc(void** p, size_t bytes) { return guarded([&] { FKB_CUDA(cudaMalloc(p, bytes)); }); }
 int fkb_dfree(void* p) { return guarded([&] { FKB_CUDA(cudaFree(p)); }); }
+// The library's streams are non-blocking (they do not order against the legacy default
+// stream), so these plumbing copies synchronize the device first: a copy never races a kernel
+// still writing or reading the buffer on a context stream.
 int fkb_h2d(void* dst, const void* src, size_t bytes) {
-    return guarded([&] { FKB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+    return guarded([&] {
+        FKB_CUDA(cudaDeviceSynchronize());
+        FKB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+        // a pageable-source cudaMemcpy may return before its DMA lands; kernels on the
+        // library's non-blocking streams are not ordered after it, so wait here
+        FKB_CUDA(cudaDeviceSynchronize());
+    });
 }
 int fkb_d2h(void* dst, const void* src, size_t bytes) {
-    return guarded([&] { FKB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+    return guarded([&] {
+        FKB_CUDA(cudaDeviceSynchronize());
+        FKB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    });
 }
 int fkb_dsync(void) { return guarded([&] { FKB_CUDA(cudaDeviceSynchronize()); }); }
 

@@ -347,8 +347,19 @@ void Filter::ghep(long long k, long long p, uint64_t seed) {
     const int l = int(k + p);
     DBuf<double> A(size_t(n) * l), Y(static_cast<size_t>(n) * l), HO(static_cast<size_t>(m) * l);
     gaussian_matrix(n, l, seed, 0, A.p, n, s);                    // Ω (lowrank.hpp:157)
-    spmm(H, A.p, n, l, HO.p, m, 1.0, 0.0, s);                      // HΩ
-    spmm(HT, HO.p, m, l, Y.p, n, 1.0 / sigma2, 0.0, s);            // Ȳ = Hᵀ(HΩ)/σ² (:158-159)
+    {
+        // Ȳ = Hᵀ(HΩ)/σ² (:158-159) on row-major blocks: every nonzero then streams one
+        // contiguous 8·l-byte row of its operand (the column-major kernel gathers 8-byte
+        // pieces); Ω is transposed in, Ȳ transposed back for the column-major stages.
+        k_transpose<<<dim3(ceil_div(n, 32), ceil_div(l, 32)), dim3(32, 8), 0, s>>>(n, l, A.p, Y.p);  // Ω row-major
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        spmm_rm(H, Y.p, l, l, HO.p, l, 1.0, s);                     // HΩ (row-major m×l)
+        spmm_rm(HT, HO.p, l, l, A.p, l, 1.0 / sigma2, s);           // Ȳ (row-major N×l)
+        k_transpose<<<dim3(ceil_div(l, 32), ceil_div(n, 32)), dim3(32, 8), 0, s>>>(l, int(n), A.p, Y.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
     ws.ensure(4096);
     if (sumsq(Y.p, (long long)n * l, ws.p, s) == 0.0) return;     // A = 0 (:161)
     DBuf<double>& Z = A;                                           // Ω no longer needed
@@ -522,6 +533,11 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
 }
 
 Filter::~Filter() {
+    // outstanding steps (asynchronous replays on s, s2, s3) must finish before buffers go back
+    // to the allocator, or a later allocation could be overwritten
+    if (s) cudaStreamSynchronize(s);
+    if (s2) cudaStreamSynchronize(s2);
+    if (s3) cudaStreamSynchronize(s3);
     drop_graphs();
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);

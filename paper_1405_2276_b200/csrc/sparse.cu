@@ -9,6 +9,7 @@
 //                   (Hᵀ), consecutive threads write consecutive rows (coalesced).
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "rng_device.cuh"
@@ -96,6 +97,77 @@ __global__ void __launch_bounds__(256) k_spmv_sub8(int rows, const int* __restri
 void spmv_short(const DevCsr& A, const double* x, double* y, double alpha, cudaStream_t s) {
     if (A.rows <= 0) return;
     k_spmv_sub8<<<ceil_div((long long)A.rows * 8, 256), 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, x, y, alpha);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
+// SpMM on ROW-major blocks (X: cols(A) × ncols with row stride ldx, Y: rows(A) × ncols with
+// row stride ldy): one warp per row of A, lanes over 32·Q consecutive columns.  The row's
+// (col, val) pairs are fetched 32 at a time with one coalesced load and broadcast by shuffles;
+// 4 nonzeros × Q columns of X (each nonzero a contiguous 8·ncols-byte row) are in flight per
+// lane.  X rows are shared by the ~10 rays through a cell, so they are served from L2.
+template <int Q, int U>
+__global__ void __launch_bounds__(256) k_spmm_rm(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                const double* __restrict__ v, const double* __restrict__ X,
+                                                long long ldx, int ncols, double* __restrict__ Y, long long ldy,
+                                                double alpha) {
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int col0 = blockIdx.y * 32 * Q;
+    double acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+    const int e0 = rp[row], e1 = rp[row + 1];
+    for (int eb = e0; eb < e1; eb += 32) {
+        const int cnt = min(32, e1 - eb);
+        const int myc = lane < cnt ? ci[eb + lane] : 0;
+        const double myv = lane < cnt ? v[eb + lane] : 0.0;
+        for (int u0 = 0; u0 < cnt; u0 += U) {
+            int c[U];
+            double w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                c[u] = __shfl_sync(0xffffffffu, myc, (u0 + u) & 31);
+                w[u] = __shfl_sync(0xffffffffu, myv, (u0 + u) & 31);
+                if (u0 + u >= cnt) w[u] = 0.0;
+            }
+            double x[U][Q];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const int col = col0 + lane + 32 * q;
+                    x[u][q] = col < ncols ? __ldg(X + (long long)c[u] * ldx + col) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < Q; ++q) acc[q] = fma(w[u], x[u][q], acc[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int col = col0 + lane + 32 * q;
+        if (col < ncols) Y[(long long)row * ldy + col] = alpha * acc[q];
+    }
+}
+
+void spmm_rm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
+             cudaStream_t s) {
+    if (A.rows <= 0 || ncols <= 0) return;
+    // Every nonzero streams a full X row from L2 (X is shared by the ~10 rays through a cell),
+    // so the kernel runs at the L2 bandwidth cap; the shape only decides how much of it is in
+    // flight.  Measured at c2 (l = 320): long rows (rays, ~320 nonzeros) 128 columns per warp
+    // with 16 nonzeros per batch; short rows (cells, ~10) 256 columns with 4.
+    const bool longrows = double(A.nnz) / A.rows > 64.0;
+    const int Q = ncols <= 32 ? 1 : longrows ? 4 : 8;
+    const dim3 grid(ceil_div((long long)A.rows * 32, 256), ceil_div(ncols, 32 * Q));
+    if (Q == 1)
+        k_spmm_rm<1, 8><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
+    else if (Q == 4)
+        k_spmm_rm<4, 16><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
+    else
+        k_spmm_rm<8, 4><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
     FKB_LAUNCH_CHECK();
     count_launch();
 }

@@ -16,6 +16,9 @@ struct DevCsr {  // SparseRowMatrix (grid.hpp:15) on the device: int32 indices, 
 // X, Y, Yin column-major device blocks (Yin shares Y's leading dimension).
 void spmm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
           double beta, cudaStream_t s, const double* Yin = nullptr);
+// Y = alpha · A X on row-major blocks (row strides ldx, ldy; ncols columns), warp per row of A
+void spmm_rm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
+             cudaStream_t s);
 // y = alpha · A x for one vector, rows of ≲ 32 nonzeros (8 lanes per row)
 void spmv_short(const DevCsr& A, const double* x, double* y, double alpha, cudaStream_t s);
 // Upload host CSR and build the explicit transposed CSR (rows ascending inside each column).

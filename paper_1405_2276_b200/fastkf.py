@@ -345,6 +345,10 @@ class FkfContext:
     def spmm_device(self, trans, dX, ldx, ncols, dY, ldy):
         check(lib().fkb_filter_spmm(self._f, trans, dX, ldx, ncols, dY, ldy))
 
+    def spmm_rm_device(self, trans, dX, ncols, dY):
+        """Y = H X (trans 0) / Hᵀ X (trans 1) on row-major device blocks."""
+        check(lib().fkb_filter_spmm_rm(self._f, trans, dX, ncols, dY))
+
     @property
     def stream(self):
         return lib().fkb_filter_stream(self._f)

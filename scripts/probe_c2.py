@@ -50,6 +50,16 @@ for _ in range(reps): ctx.spmm_device(0, X.ptr, N, l, Z.ptr, w.m)
 check(lib().fkb_dsync()); dt = (time.perf_counter() - t) / reps
 B = 12 * h.nnz + 4 * (h.rows + 1) + 8 * (N + w.m) * l
 print(f"SpMM H·X (l={l}): {dt*1e6:.1f} us -> {B/dt/1e9:.0f} GB/s", flush=True)
+ctx.spmm_rm_device(0, X.ptr, l, Z.ptr); check(lib().fkb_dsync())
+t = time.perf_counter()
+for _ in range(reps): ctx.spmm_rm_device(0, X.ptr, l, Z.ptr)
+check(lib().fkb_dsync()); dt = (time.perf_counter() - t) / reps
+print(f"SpMM H·X row-major (l={l}): {dt*1e6:.1f} us -> {B/dt/1e9:.0f} GB/s", flush=True)
+ctx.spmm_rm_device(1, Z.ptr, l, X.ptr); check(lib().fkb_dsync())
+t = time.perf_counter()
+for _ in range(reps): ctx.spmm_rm_device(1, Z.ptr, l, X.ptr)
+check(lib().fkb_dsync()); dt = (time.perf_counter() - t) / reps
+print(f"SpMM Hᵀ·Y row-major (l={l}): {dt*1e6:.1f} us -> {B/dt/1e9:.0f} GB/s", flush=True)
 ctx.spmm_device(1, Z.ptr, w.m, l, X.ptr, N); check(lib().fkb_dsync())
 t = time.perf_counter()
 for _ in range(reps): ctx.spmm_device(1, Z.ptr, w.m, l, X.ptr, N)
