@@ -145,23 +145,12 @@ __global__ void k_woodbury_scalars(int m, int r, int mode, const double* __restr
     }
 }
 
-// x_i = r̃_i / (α θ_i + σ²) (Λ_M⁻¹ r̃ with this step's α, computed in place of wsq so the
-// capacitance RHS does not wait for the side branch)
-struct XWr {
-    const double* rt;
-    const double* theta;
-    const double* alpha_dev;
-    double sigma2;
-    __device__ __forceinline__ double operator()(long long i) const {
-        return __ldg(rt + i) / (alpha_dev[1] * __ldg(theta + i) + sigma2);
-    }
-};
-
-// u_j = √d_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃))
-struct EpiSqrtD {
+// u_j = sqd_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃); Λ_M⁻¹ and D^½
+// of this step were formed by the previous step's side branch)
+struct EpiScaleOut {
     double* u;
-    const double* d;
-    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sqrt(d[j]) * v; }
+    const double* sc;
+    __device__ __forceinline__ void operator()(long long j, double v) const { u[j] = sc[j] * v; }
 };
 // (Bᵀz)_j → dc_j = d_j·(Bᵀz)_j for the mean update, then d_j ← (d_j + αλ_j(α − d_j)) /
 // (1 + λ_j(α − d_j)) (fast_filter.hpp:114-123); column 0 commits α.  Skipped when the step
@@ -713,6 +702,7 @@ void Filter::enqueue_step(const double* d_y) {
     // side branch: dc = d ⊙ Bᵀz with d and α updated in the same pass; main branch:
     // t = Γ(Hᵀz); then mean += α·t − U·dc (:114-123).  (The U pass stays on the main branch:
     // run concurrently it starves the FFT passes of SMs.)
+    // (measured: dc beside Hᵀz costs the step less than dc beside the FFT passes)
     const bool par = side() != s;
     if (r > 0) {
         fork();
@@ -740,7 +730,7 @@ void Filter::enqueue_solve_woodbury() {
     mark("rotate_in");
     if (r > 0) {
         // u = D^½·Eᵀ·Λ_M⁻¹·r̃
-        launch_coldot(m, r, E.p, m, XWr{rt.p, theta.p, alpha_dev.p, sigma2}, EpiSqrtD{ucap.p, d.p}, s);
+        launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
         mark("cap_rhs");
         // side branch (runs beside the 16-SM PCG cluster): the NEXT step's Woodbury scalars
         // and K into the other parity's buffers

@@ -9,6 +9,9 @@
 // k_gemv_cols: y = Aᵀ·x, one warp per column, lanes stride the rows, 8 loads in flight.
 #pragma once
 
+#include <cstdint>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fkb {
