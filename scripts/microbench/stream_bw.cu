@@ -111,6 +111,23 @@ __global__ void __launch_bounds__(256) k_coldot2(int m, int n, const double* __r
     }
 }
 
+// plain streaming read: every thread sums 16-byte loads (grid-stride), UNROLL in flight
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_read(const double2* __restrict__ a, long long n2, double* out) {
+    double acc = 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; i + (UNROLL - 1) * stride < n2; i += UNROLL * stride) {
+        double2 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(a + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) acc += v[u].x + v[u].y;
+    }
+    for (; i < n2; i += stride) acc += a[i].x + a[i].y;
+    if (acc == 12345.678) out[0] = acc;
+}
+
 template <class F>
 float time_ms(F&& f, int reps, cudaStream_t s) {
     cudaEvent_t a, b;
@@ -152,6 +169,12 @@ int main() {
         launch_gemv_rowmajor((256LL << 20) / 8 / 256, 256, flush, 256, XPlain{x}, EpiSt{y}, s);
     };
     float tf = time_ms(fl, reps, s);
+    for (int blocks : {148 * 4, 148 * 8, 148 * 16, 148 * 32}) {
+        float t = time_ms([&] { fl(); k_read<4><<<blocks, 256, 0, s>>>(reinterpret_cast<const double2*>(U), n * r / 2, y); }, reps, s) - tf;
+        printf("plain read U (157 MB) blocks %5d unroll 4: %.2f us  %.0f GB/s\n", blocks, t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
+        t = time_ms([&] { fl(); k_read<8><<<blocks, 256, 0, s>>>(reinterpret_cast<const double2*>(U), n * r / 2, y); }, reps, s) - tf;
+        printf("plain read U (157 MB) blocks %5d unroll 8: %.2f us  %.0f GB/s\n", blocks, t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
+    }
     for (long long tb : {64 << 10}) {
         float t = time_ms([&] { fl(); launch_stream_dot(n, r, r, U, XPlain{x}, EpiSt{y}, s, tb); }, reps, s) - tf;
         printf("U pass stream_dot tile %3lld KB: %.2f us  %.0f GB/s\n", tb >> 10, t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
