@@ -254,9 +254,21 @@ def run_ours(args, rank, world, local_rank):
     sweep = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local_rank}")
     sweep_out = torch.empty(1, dtype=torch.float32, device=f"cuda:{local_rank}")
 
+    # c3-style workloads: diag Σ and the conditional realizations are part of every step
+    uq_count = int(w.realizations_per_step or 0)
+    uq = bool(w.variance_each_step or uq_count)
+    if uq:
+        UQX = torch.empty(max(uq_count, 1), w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
+        UQV = torch.empty(w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
+
+    def step_dev(i):
+        ctx.steps_async(yptr(i), 1, w.m)
+        if uq:
+            ctx.realizations_device(w.sample_seed, uq_count, C.c_void_p(UQX.data_ptr()), C.c_void_p(UQV.data_ptr()))
+
     # ---- warm-up
     for i in range(args.warmup):
-        ctx.steps_async(yptr(i), 1, w.m)
+        step_dev(i)
     ctx.sync(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
@@ -269,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         for i in range(args.steps):
             evs[i][0].record(stream)
-            ctx.steps_async(yptr(args.warmup + i), 1, w.m)
+            step_dev(args.warmup + i)
             evs[i][1].record(stream)
             with torch.cuda.stream(stream):
                 flush.zero_()
@@ -287,11 +299,11 @@ def run_ours(args, rank, world, local_rank):
     # conditions (L2 flushed between steps) with timing events captured at every phase boundary
     ctx.graph_timing(True)
     for i in range(args.warmup):
-        ctx.steps_async(yptr(i), 1, w.m)
+        step_dev(i)
     ctx.sync(args.warmup)
     acc = {}
     for i in range(args.steps):
-        ctx.steps_async(yptr(args.warmup + i), 1, w.m)
+        step_dev(args.warmup + i)
         with torch.cuda.stream(stream):
             flush.zero_()
             torch.sum(sweep, dim=0, keepdim=True, out=sweep_out)
@@ -313,20 +325,31 @@ def run_ours(args, rank, world, local_rank):
     a_ = C.c_double()
     st_ = C.c_int()
     rk_ = C.c_int()
-    for i in range(args.warmup):
+    if uq:
+        pin_x = torch.empty(max(uq_count, 1) * w.N, dtype=torch.float64).pin_memory()
+        pin_v = torch.empty(w.N, dtype=torch.float64).pin_memory()
+
+    def step_e2e(i):
         check(L.fkb_fkf_step(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m))
+        check(L.fkb_filter_state(ctx._f, C.byref(a_), C.byref(st_), C.byref(rk_), C.c_void_p(pin_d.data_ptr()),
+                                 C.c_void_p(pin_mean.data_ptr())))
+        if uq:
+            check(L.fkb_realizations_with_variance(ctx._f, w.sample_seed, uq_count, C.c_void_p(pin_x.data_ptr()),
+                                                   C.c_void_p(pin_v.data_ptr())))
+
+    for i in range(args.warmup):
+        step_e2e(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
-        check(L.fkb_fkf_step(ctx._f, C.c_void_p(pin_y[(args.warmup + i) % S].data_ptr()), w.m))
-        check(L.fkb_filter_state(ctx._f, C.byref(a_), C.byref(st_), C.byref(rk_), C.c_void_p(pin_d.data_ptr()),
-                                 C.c_void_p(pin_mean.data_ptr())))
+        step_e2e(args.warmup + i)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), f"cuda:{local_rank}")
+    d2h = 8 * (w.N + r) + 8 + 4 + 4 + ((8 * w.N * (1 + uq_count)) if uq else 0)
     e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": 8 * w.m,
-           "d2h_bytes_per_step": 8 * (w.N + r) + 8 + 4 + 4}
+           "d2h_bytes_per_step": d2h}
 
     # ---- offline kernels: Γ·X on the m + l offline columns, H·X SpMM with l columns
     ncols = w.m + k + p
@@ -402,6 +425,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": r,
                    "torus": f"{cov.mx}x{cov.my}", "nnz_H": int(h.nnz), "solver": "woodbury-eig",
+                   "uq_per_step": (f"diag Σ + {uq_count} realizations" if uq else "none"),
                    "l2": "flushed between timed steps (256 MiB write + 256 MiB read sweep on the filter stream)",
                    "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
         "clocks": clk.summary(),

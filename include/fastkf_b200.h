@@ -108,6 +108,9 @@ int fkb_relative_entropy(fkb_filter* f, double* out);      /* uq.hpp:39-53 */
  * out: N×count column-major; var (optional) receives diag Σ from the same pass. */
 int fkb_realizations(fkb_filter* f, uint64_t seed, int count, double* out);
 int fkb_realizations_device(fkb_filter* f, uint64_t seed, int count, double* d_out, double* d_var);
+/* host buffers, one pass over U for both: out (N×count, may be null when count = 0) and var
+ * (diag Σ, may be null) */
+int fkb_realizations_with_variance(fkb_filter* f, uint64_t seed, int count, double* out, double* var);
 
 /* ---- kernels exposed for parity tests / benchmarks (device pointers) ------------- */
 /* Y = H X (trans = 0) or Hᵀ X (trans = 1) with the filter's uploaded operator */

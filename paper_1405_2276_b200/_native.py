@@ -66,6 +66,7 @@ SIGNATURES = {
     "fkb_relative_entropy": (_i, [_p, _PD]),
     "fkb_realizations": (_i, [_p, _u64, _i, _dp]),
     "fkb_realizations_device": (_i, [_p, _u64, _i, _p, _p]),
+    "fkb_realizations_with_variance": (_i, [_p, _u64, _i, _p, _p]),
     "fkb_filter_spmm": (_i, [_p, _i, _p, _ll, _i, _p, _ll]),
     "fkb_filter_stream": (_p, [_p]),
     "fkb_filter_spmm_rm": (_i, [_p, _i, _p, _i, _p]),

@@ -331,9 +331,9 @@ int fkb_variance(fkb_filter* f, double* out) {
     return guarded([&] {
         need(f, "filter");
         auto& F = *f->f;
-        fkb::DBuf<double> d(static_cast<size_t>(F.n));
-        F.variance(d.p);
-        FKB_CUDA(cudaMemcpyAsync(out, d.p, d.bytes(), cudaMemcpyDeviceToHost, F.s));
+        F.host_out.ensure(static_cast<size_t>(F.n));  // persistent staging (no per-call allocation)
+        F.variance(F.host_out.p);
+        FKB_CUDA(cudaMemcpyAsync(out, F.host_out.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
         FKB_CUDA(cudaStreamSynchronize(F.s));
     });
 }
@@ -361,9 +361,23 @@ int fkb_realizations(fkb_filter* f, uint64_t seed, int count, double* out) {
         auto& F = *f->f;
         if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
         if (count == 0) return;
-        fkb::DBuf<double> d(size_t(F.n) * count);
-        F.realizations(seed, count, d.p, nullptr);
-        FKB_CUDA(cudaMemcpyAsync(out, d.p, d.bytes(), cudaMemcpyDeviceToHost, F.s));
+        F.host_out.ensure(size_t(F.n) * count);
+        F.realizations(seed, count, F.host_out.p, nullptr);
+        FKB_CUDA(cudaMemcpyAsync(out, F.host_out.p, sizeof(double) * size_t(F.n) * count, cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+int fkb_realizations_with_variance(fkb_filter* f, uint64_t seed, int count, double* out, double* var) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
+        F.host_out.ensure(size_t(F.n) * (count + 1));
+        double* xo = F.host_out.p + F.n;
+        F.realizations(seed, count, xo, F.host_out.p);  // one pass over U for both
+        if (var) FKB_CUDA(cudaMemcpyAsync(var, F.host_out.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
+        if (count && out)
+            FKB_CUDA(cudaMemcpyAsync(out, xo, sizeof(double) * size_t(F.n) * count, cudaMemcpyDeviceToHost, F.s));
         FKB_CUDA(cudaStreamSynchronize(F.s));
     });
 }

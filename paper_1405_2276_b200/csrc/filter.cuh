@@ -87,6 +87,7 @@ struct Filter {
     DBuf<double> sig_minus;
 
     DBuf<double> ybuf;
+    DBuf<double> host_out;  // staging for the host-buffer UQ calls
 
     Filter(Cov* cov, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,
            long long k, long long p, uint64_t seed);

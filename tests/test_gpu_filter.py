@@ -204,3 +204,20 @@ def test_c4_parity_first_steps():
     """The largest config (N = 512², m = 4096, k = 500, torus 1024²): oracle init ≈ 80 s."""
     worst = _run_both("c4", 2, uq=True)
     assert worst["mean"] < TOL and worst["d"] < TOL and worst["var"] < TOL, worst
+
+
+def test_combined_uq_call_matches_separate_calls():
+    """fkb_realizations_with_variance (one U pass) ≡ fkb_variance + fkb_realizations."""
+    import ctypes as C
+    from paper_1405_2276_b200._native import lib
+    w, h, ys, s2 = workload_inputs("c0", 3)
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu))
+    k, p = w.ghep_sizes()
+    ctx = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    for y in ys:
+        P.fkf_step(ctx, y)
+    x = np.empty(w.N * 4)
+    v = np.empty(w.N)
+    assert lib().fkb_realizations_with_variance(ctx._f, 7, 4, C.c_void_p(x.ctypes.data), C.c_void_p(v.ctypes.data)) == 0
+    assert np.array_equal(v, ctx.variance())
+    assert np.array_equal(x.reshape(4, w.N).T, ctx.realizations(7, 4))
