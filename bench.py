@@ -330,9 +330,9 @@ def run_ours(args, rank, world, local_rank):
         pin_v = torch.empty(w.N, dtype=torch.float64).pin_memory()
 
     def step_e2e(i):
-        check(L.fkb_fkf_step(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m))
-        check(L.fkb_filter_state(ctx._f, C.byref(a_), C.byref(st_), C.byref(rk_), C.c_void_p(pin_d.data_ptr()),
-                                 C.c_void_p(pin_mean.data_ptr())))
+        # fkf_step returns the new state (fast_filter.hpp:84-125): y in, α/d/mean out, one round trip
+        check(L.fkb_fkf_step_state(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m, C.byref(a_),
+                                   C.c_void_p(pin_d.data_ptr()), C.c_void_p(pin_mean.data_ptr())))
         if uq:
             check(L.fkb_realizations_with_variance(ctx._f, w.sample_seed, uq_count, C.c_void_p(pin_x.data_ptr()),
                                                    C.c_void_p(pin_v.data_ptr())))

@@ -87,6 +87,9 @@ int fkb_filter_lambda(fkb_filter* f, double* out); /* GepResult::lambda, descend
 int fkb_filter_get(fkb_filter* f, int which, double* out);
 /* fkf_step, fast_filter.hpp:84-125, advancing the device-resident state */
 int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen);
+/* one step from host y AND the new state (α, d (r), mean (N)) in one round trip — the reference's
+ * fkf_step returns the new LowRankState by value (fast_filter.hpp:84-125); d/mean may be null */
+int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* alpha, double* d, double* mean);
 int fkb_fkf_step_device(fkb_filter* f, const double* d_y);
 /* nsteps device-resident observations (column k at d_ys + k*ldy) without host syncs;
  * fkb_fkf_sync performs the deferred singularity check and commits the state. */

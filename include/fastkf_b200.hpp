@@ -275,12 +275,13 @@ inline LowRankState fkf_step(const LowRankState& state, FkfContext& ctx, const V
         throw std::invalid_argument(
             "fkf_step: state rank does not match the eigendecomposition (constant-H regime requires W = U)");
     detail::sync_state(state, ctx);
-    detail::check(fkb_fkf_step(ctx.handle(), y.data(), y.size()));
     LowRankState next;
-    int rank = 0;
     next.d = Vector(ctx.rank());
     next.mean = Vector(state.mean.size());
-    detail::check(fkb_filter_state(ctx.handle(), &next.alpha, &next.step, &rank, next.d.data(), next.mean.data()));
+    // step + new state in one round trip (value semantics of fast_filter.hpp:84-125)
+    detail::check(fkb_fkf_step_state(ctx.handle(), y.data(), y.size(), &next.alpha, next.d.data(), next.mean.data()));
+    int rank = 0;
+    detail::check(fkb_filter_state(ctx.handle(), nullptr, &next.step, &rank, nullptr, nullptr));
     next.d.v.resize(size_t(rank));
     next.token = ctx.handle();
     next.generation = ++ctx.generation;

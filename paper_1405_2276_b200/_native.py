@@ -53,6 +53,7 @@ SIGNATURES = {
     "fkb_filter_lambda": (_i, [_p, _dp]),
     "fkb_filter_get": (_i, [_p, _i, _dp]),
     "fkb_fkf_step": (_i, [_p, _p, _ll]),
+    "fkb_fkf_step_state": (_i, [_p, _p, _ll, _p, _p, _p]),
     "fkb_fkf_step_device": (_i, [_p, _p]),
     "fkb_fkf_steps_async": (_i, [_p, _p, _i, _ll]),
     "fkb_fkf_sync": (_i, [_p, _i]),

@@ -259,6 +259,17 @@ int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen) {
         F.step_host(y);
     });
 }
+int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* alpha, double* d, double* mean) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (ylen != F.m)
+            throw std::invalid_argument("fkf_step: observation length " + std::to_string(ylen) + " does not match " +
+                                        std::to_string(F.m) + " measurements");
+        F.step_host_state(y, d, mean);
+        if (alpha) *alpha = F.alpha;
+    });
+}
 int fkb_fkf_step_device(fkb_filter* f, const double* d_y) {
     return guarded([&] {
         need(f, "filter");

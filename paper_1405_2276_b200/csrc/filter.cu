@@ -528,6 +528,7 @@ Filter::~Filter() {
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
     drop_graphs();
+    if (h_info) cudaFreeHost(h_info);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join2) cudaEventDestroy(ev_join2);
@@ -732,8 +733,8 @@ void Filter::enqueue_solve_woodbury() {
         // u = D^½·Eᵀ·Λ_M⁻¹·r̃
         launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
         mark("cap_rhs");
-        // side branch (runs beside the 16-SM PCG cluster): the NEXT step's Woodbury scalars
-        // and K into the other parity's buffers
+        // side branch (runs beside the 16-SM PCG cluster; measured better than after it): the
+        // NEXT step's Woodbury scalars and K into the other parity's buffers
         if (side() != s) {
             FKB_CUDA(cudaEventRecord(ev_ctz, s));
             FKB_CUDA(cudaStreamWaitEvent(s3, ev_ctz, 0));
@@ -831,6 +832,26 @@ void Filter::step(const double* d_y) {
         FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
     launch_step();
     check_info();
+    alpha += 1.0;
+    ++step_no;
+    state_rank = r;
+}
+
+// One step from a host observation with the new state downloaded in the same round trip
+// (the reference's fkf_step returns the new LowRankState by value): H2D y, graph replay, D2H of
+// the failure flag, d and mean, ONE stream synchronization.
+void Filter::step_host_state(const double* h_y, double* h_d, double* h_mean) {
+    if (!h_info) FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_info), sizeof(int), cudaHostAllocDefault));
+    if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_y, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+    launch_step();
+    FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
+    if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    if (*h_info) {
+        k_valid = false;
+        throw std::runtime_error("fkf_step: innovation system is singular");
+    }
     alpha += 1.0;
     ++step_no;
     state_rank = r;

@@ -95,6 +95,8 @@ struct Filter {
     void ghep(long long k, long long p, uint64_t seed);  // lowrank.hpp:141-213
     void step(const double* d_y);                        // fast_filter.hpp:84-125 (device y)
     void step_host(const double* h_y);                   // same, y from host memory
+    void step_host_state(const double* h_y, double* h_d, double* h_mean);  // + new state, one sync
+    int* h_info = nullptr;                               // pinned failure-flag staging
     // k steps over device-resident observations (column k at d_ys + k·ldy), no host sync;
     // finish_async() performs the deferred singularity check and commits host mirrors.
     void steps_async(const double* d_ys, int nsteps, long long ldy);

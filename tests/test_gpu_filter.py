@@ -221,3 +221,24 @@ def test_combined_uq_call_matches_separate_calls():
     assert lib().fkb_realizations_with_variance(ctx._f, 7, 4, C.c_void_p(x.ctypes.data), C.c_void_p(v.ctypes.data)) == 0
     assert np.array_equal(v, ctx.variance())
     assert np.array_equal(x.reshape(4, w.N).T, ctx.realizations(7, 4))
+
+
+def test_step_state_round_trip_matches_step_then_state():
+    """fkb_fkf_step_state (step + new state, one sync) ≡ fkb_fkf_step followed by fkb_filter_state."""
+    import ctypes as C
+    from paper_1405_2276_b200._native import lib
+    w, h, ys, s2 = workload_inputs("c0", 4)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    a = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    b = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    for y in ys:
+        sa = P.fkf_step(a, y)
+        y = np.ascontiguousarray(y)
+        alpha, d, mean = C.c_double(), np.empty(b.rank()), np.empty(w.N)
+        assert lib().fkb_fkf_step_state(b._f, C.c_void_p(y.ctypes.data), len(y), C.byref(alpha),
+                                        C.c_void_p(d.ctypes.data), C.c_void_p(mean.ctypes.data)) == 0
+        assert alpha.value == sa["alpha"]
+        assert np.array_equal(d, sa["d"]) and np.array_equal(mean, sa["mean"])
+    bad = np.zeros(3)
+    assert lib().fkb_fkf_step_state(b._f, C.c_void_p(bad.ctypes.data), 3, None, None, None) == 1  # invalid_argument
