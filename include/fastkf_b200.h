@@ -129,6 +129,8 @@ int fkb_filter_set_solver(fkb_filter* f, int mode);
 int fkb_filter_eig_sweeps(fkb_filter* f);
 /* last step's capacitance solve: PCG iterations and whether the exact Cholesky fallback ran */
 int fkb_filter_cap_stats(fkb_filter* f, int* iterations, int* fallback);
+/* PCG iteration cap (default 200); 0 forces the exact cluster-Cholesky path (tests) */
+int fkb_filter_set_pcg_maxit(fkb_filter* f, int maxit);
 /* profiling aid: 64 %globaltimer stamps of the last PCG launch (needs FKB_PCG_STAMPS=1) */
 int fkb_filter_pcg_stamps(fkb_filter* f, unsigned long long* out);
 /* eigenpairs of G (θ unsorted, P m×m column-major) */

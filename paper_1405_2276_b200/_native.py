@@ -75,6 +75,7 @@ SIGNATURES = {
     "fkb_filter_set_solver": (_i, [_p, _i]),
     "fkb_filter_eig_sweeps": (_i, [_p]),
     "fkb_filter_cap_stats": (_i, [_p, _PI, _PI]),
+    "fkb_filter_set_pcg_maxit": (_i, [_p, _i]),
     "fkb_filter_pcg_stamps": (_i, [_p, np.ctypeslib.ndpointer(dtype=np.uint64)]),
     "fkb_filter_get_eig": (_i, [_p, _p, _p]),
     "fkb_filter_phase_times": (_i, [_p, _i, _dp, C.c_char_p, _i, _PI]),

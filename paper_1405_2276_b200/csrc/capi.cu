@@ -416,6 +416,15 @@ int fkb_filter_set_solver(fkb_filter* f, int mode) {
     });
 }
 int fkb_filter_eig_sweeps(fkb_filter* f) { return f ? f->f->eig_sweeps : 0; }
+int fkb_filter_set_pcg_maxit(fkb_filter* f, int maxit) {
+    return guarded([&] {
+        need(f, "filter");
+        if (maxit < 0) throw std::invalid_argument("pcg: maxit must be nonnegative");
+        auto& F = *f->f;
+        F.pcg_maxit = maxit;
+        F.drop_graphs();  // the cap is baked into the captured step
+    });
+}
 int fkb_filter_pcg_stamps(fkb_filter* f, unsigned long long* out) {
     return guarded([&] {
         need(f, "filter");

@@ -147,8 +147,11 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     const bool own = row < r1;
     double dinv = 0.0, x = 0.0, r = 0.0, uu = 0.0, w = 0.0;
     double zv = 0.0, qv = 0.0, sv = 0.0, pv = 0.0;
+    double nonpos = 0.0;  // K_ii ≤ 0: K (hence S) is not positive definite
     if (own) {
-        dinv = 1.0 / K[row + (long long)row * ld];
+        const double kii = K[row + (long long)row * ld];
+        nonpos = kii > 0.0 ? 0.0 : 1.0;
+        dinv = 1.0 / kii;
         r = u[row];
         uu = dinv * r;
 #pragma unroll
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     int it = 0;
     bool done = false;
     // exchange bytes every CTA receives per iteration: all n entries of m + 16×3 partials
-    const unsigned xbytes = unsigned(n) * 8u + unsigned(PC_CL) * 24u;
+    const unsigned xbytes = unsigned(n) * 8u + unsigned(PC_CL) * 32u;
     while (true) {
         const int buf = it & 1;
         const unsigned parity = unsigned((it >> 1) & 1);
@@ -185,11 +188,13 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         }
         {
             double a = own ? r * uu : 0.0, bq = own ? w * uu : 0.0, c = own ? r * r : 0.0;
+            double e = it == 0 ? nonpos : 0.0;
             if (warp < 2) {
                 for (int o = 16; o > 0; o >>= 1) {
                     a += __shfl_xor_sync(0xffffffffu, a, o);
                     bq += __shfl_xor_sync(0xffffffffu, bq, o);
                     c += __shfl_xor_sync(0xffffffffu, c, o);
+                    e += __shfl_xor_sync(0xffffffffu, e, o);
                 }
             }
             if (own)
@@ -198,20 +203,22 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
             if (rb <= 32) {  // one owning warp: its lanes 0..15 push the three sums to every CTA
                 if (warp == 0 && lane < PC_CL) {
                     const double a0 = __shfl_sync(0x0000ffffu, a, 0), b0 = __shfl_sync(0x0000ffffu, bq, 0),
-                                 c0 = __shfl_sync(0x0000ffffu, c, 0);
+                                 c0 = __shfl_sync(0x0000ffffu, c, 0), e0 = __shfl_sync(0x0000ffffu, e, 0);
                     st_async_cluster(&sh.part[buf][crank][0], &xbar[buf], lane, a0);
                     st_async_cluster(&sh.part[buf][crank][1], &xbar[buf], lane, b0);
                     st_async_cluster(&sh.part[buf][crank][2], &xbar[buf], lane, c0);
+                    st_async_cluster(&sh.part[buf][crank][3], &xbar[buf], lane, e0);
                 }
             } else {
                 if (warp < 2 && lane == 0) {
                     sh.red[warp][0] = a;
                     sh.red[warp][1] = bq;
                     sh.red[warp][2] = c;
+                    sh.red[warp][3] = e;
                 }
                 __syncthreads();
-                if (tid < 3 * PC_CL) {
-                    const int qq = tid % 3, dest = tid / 3;
+                if (tid < 4 * PC_CL) {
+                    const int qq = tid % 4, dest = tid / 4;
                     st_async_cluster(&sh.part[buf][crank][qq], &xbar[buf], dest, sh.red[0][qq] + sh.red[1][qq]);
                 }
             }
@@ -228,13 +235,17 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
                     : "memory");
         }
         if (stamp && it == 3) ts[41] = gtimer();
-        double gamma = 0.0, delta = 0.0, rr = 0.0;
+        double gamma = 0.0, delta = 0.0, rr = 0.0, bad = 0.0;
 #pragma unroll
         for (int c = 0; c < PC_CL; ++c) {
             gamma += sh.part[buf][c][0];
             delta += sh.part[buf][c][1];
             rr += sh.part[buf][c][2];
+            bad += sh.part[buf][c][3];
         }
+        // a non-positive pivot means K (hence S) is not SPD: leave it to the Cholesky, which
+        // reports "singular" exactly like the reference LLT (fast_filter.hpp:104-106)
+        if (bad > 0.0) break;
         if (it == 0) stop = tol * tol * rr;  // r₀ = u
         if (rr <= stop || rr == 0.0) {
             done = true;
@@ -245,7 +256,9 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         block_matvec(sh, Ks, K, ld, n, r0, r1, buf, kstage);  // n = K m
         if (stamp && it == 3) ts[43] = gtimer();
         const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
-        const double alpha = it == 0 ? gamma / delta : gamma / (delta - beta * gamma / alpha_prev);
+        const double eta = it == 0 ? delta : delta - beta * gamma / alpha_prev;  // = pᵀKp
+        if (!(eta > 0.0)) break;  // non-positive curvature: K is not SPD (or breakdown) → Cholesky
+        const double alpha = gamma / eta;
         if (own) {
             const double nv = sh.q[tid];
             zv = fma(beta, zv, nv);

@@ -744,7 +744,7 @@ void Filter::enqueue_solve_woodbury() {
         mark_on(side() != s ? s3 : s, "capacitance");
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join2, s3));
         // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
-        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, 200, 1e-14, pcg_ts.p);
+        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-14, pcg_ts.p);
         chol_solve_small(r, K_c, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
         mark("cap_solve");
     }

@@ -52,7 +52,8 @@ struct Filter {
         wsq_n = wsqb[p ^ 1].p; sqd_n = sqdb[p ^ 1].p; K_n = Kb[p ^ 1].p;
     }
     DBuf<unsigned long long> pcg_ts;  // %globaltimer stamps of the PCG kernel (FKB_PCG_STAMPS=1)
-    DBuf<int> pcgflag;  // 1 when the capacitance PCG fell back to the cluster Cholesky
+    DBuf<int> pcgflag;
+    int pcg_maxit = 200;  // iteration cap before the exact Cholesky takes over (tests force 0)  // 1 when the capacitance PCG fell back to the cluster Cholesky
 
     // step workspaces
     DBuf<double> S, z, t, cvec, ws, ws_step;

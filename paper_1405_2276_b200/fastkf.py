@@ -363,6 +363,10 @@ class FkfContext:
     def eig_sweeps(self) -> int:
         return int(lib().fkb_filter_eig_sweeps(self._f))
 
+    def set_pcg_maxit(self, maxit: int):
+        """Iteration cap of the capacitance PCG; 0 forces the exact Cholesky fallback."""
+        check(lib().fkb_filter_set_pcg_maxit(self._f, int(maxit)))
+
     def cap_stats(self):
         """(PCG iterations, Cholesky fallback used) of the last step's capacitance solve."""
         it, fb = C.c_int(), C.c_int()

@@ -242,3 +242,47 @@ def test_step_state_round_trip_matches_step_then_state():
         assert np.array_equal(d, sa["d"]) and np.array_equal(mean, sa["mean"])
     bad = np.zeros(3)
     assert lib().fkb_fkf_step_state(b._f, C.c_void_p(bad.ctypes.data), 3, None, None, None) == 1  # invalid_argument
+
+
+def _c0_ctx():
+    w, h, ys, s2 = workload_inputs("c0", 4)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    return w, ys, P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+
+
+def test_cholesky_fallback_matches_pcg():
+    """With the PCG capped at 0 iterations every step takes the exact cluster-Cholesky path
+    (the fallback the device flag routes to); the states agree with the PCG path."""
+    w, ys, a = _c0_ctx()
+    _, _, b = _c0_ctx()
+    b.set_pcg_maxit(0)
+    for i, y in enumerate(ys):
+        sa, sb = P.fkf_step(a, y), P.fkf_step(b, y)
+        if i > 0:  # step 1 has d = 0, so u = 0 and the PCG exits before its cap
+            assert b.cap_stats()[1] is True and a.cap_stats()[1] is False
+        assert sa["alpha"] == sb["alpha"]
+        assert rel_err(sb["mean"], sa["mean"]) < 1e-12
+        assert np.max(np.abs(sb["d"] - sa["d"])) / sa["alpha"] < 1e-12
+
+
+@pytest.mark.parametrize("solver", [0, 1])
+def test_singular_innovation_raises_and_keeps_state(solver):
+    """fast_filter.hpp:104-106: a non-positive-definite S raises "singular"; the device state
+    is left untouched (the step's mutating epilogues are gated on the failure flag)."""
+    w, ys, ctx = _c0_ctx()
+    ctx.set_solver(solver)
+    P.fkf_step(ctx, ys[0])
+    before = ctx.state()
+    # d far above α makes S = αG − B·diag(d)·Bᵀ + σ²I indefinite
+    ctx.set_state(before["alpha"], np.full(ctx.rank(), 50.0 * before["alpha"]), before["mean"], before["step"])
+    mid = ctx.state()
+    with pytest.raises(RuntimeError, match="singular"):
+        P.fkf_step(ctx, ys[1])
+    after = ctx.state()
+    assert after["alpha"] == mid["alpha"] and after["step"] == mid["step"]
+    assert np.array_equal(after["mean"], mid["mean"]) and np.array_equal(after["d"], mid["d"])
+    # recovery: restore a valid state and step again
+    ctx.set_state(before["alpha"], before["d"], before["mean"], before["step"])
+    st = P.fkf_step(ctx, ys[1])
+    assert st["alpha"] == before["alpha"] + 1.0
