@@ -179,9 +179,9 @@ int main() {
         float t = time_ms([&] { fl(); launch_stream_dot(n, r, r, U, XPlain{x}, EpiSt{y}, s, tb); }, reps, s) - tf;
         printf("U pass stream_dot tile %3lld KB: %.2f us  %.0f GB/s\n", tb >> 10, t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
     }
-    {
-        float t = time_ms([&] { fl(); launch_gemv_rowmajor(n, r, U, r, XPlain{x}, EpiSt{y}, s); }, reps, s) - tf;
-        printf("U pass gemv_rowmajor:          %.2f us  %.0f GB/s\n", t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
+    for (long long mc : {0LL, 592LL, 1184LL, 1776LL, 4096LL}) {
+        float t = time_ms([&] { fl(); launch_gemv_rowmajor(n, r, U, r, XPlain{x}, EpiSt{y}, s, mc); }, reps, s) - tf;
+        printf("U pass gemv_rowmajor max_ctas %5lld: %.2f us  %.0f GB/s\n", mc, t * 1e3, 8.0 * n * r / (t * 1e-3) / 1e9);
     }
     for (int ctas : {0}) {
         auto run = [&](auto rpw) {
