@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
         const int ix0 = blockIdx.x * 2 * RP;
         const int q0 = ix0 + 2 * p, q1 = q0 + 1;
         const int bl = L::blen(my);
-        double2* ap = sm + tl + p * bl;
+        double2* ap = sm + p * bl;  // twiddles come from the global per-pass table (fft_reg)
         double2 v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -245,18 +245,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
             v[q] = make_double2((iy < ny && q0 < nx) ? x[(long long)q0 * ny + iy] : 0.0,
                                 (iy < ny && q1 < nx) ? x[(long long)q1 * ny + iy] : 0.0);
         }
-        {  // twiddles: every load in flight before the first store (≤ 8 per thread)
-            double2 tv[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int e = t + q * int(blockDim.x);
-                tv[q] = e < tl ? fy.twp[e] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (t + q * int(blockDim.x) < tl) tw[t + q * int(blockDim.x)] = tv[q];
-        }
-        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, tw, j);  // ping-pong if alone
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, fy.twp, j);  // ping-pong if alone
         __syncthreads();  // last exchange loads done before the result overwrites the buffer
 #pragma unroll
         for (int q = 0; q < 8; ++q) ap[fpad(j + q * TPT)] = v[q];
@@ -266,7 +255,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
             const int ky = e / rows, rl = e - ky * rows;
             const int ix = ix0 + rl;
             if (ix >= nx) continue;
-            const double2* zt = sm + tl + (rl >> 1) * bl;
+            const double2* zt = sm + (rl >> 1) * bl;
             const double2 pp = zt[fpad(ky)];
             const double2 qq = cconj(zt[fpad(ky == 0 ? 0 : my - ky)]);
             W[(long long)ky * nx + ix] = (rl & 1) == 0 ? make_double2(0.5 * (pp.x + qq.x), 0.5 * (pp.y + qq.y))
@@ -315,22 +304,20 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
     const double* sp = spec_half + (long long)blockIdx.x * mx;
     if constexpr (reg_fft_len<NT>()) {  // forward → × spectrum → inverse, all in registers
         const int j = threadIdx.x;
-        double2 v[8], tv[8];
+        double2* ra = sm;  // no shared twiddle table on this path
+        double2* rb = sm + L::blen(mx);
+        double2 v[8];
         double spv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int ix = j + q * T;
-            tv[q] = ix < tl ? fx.twp[ix] : make_double2(0.0, 0.0);
             v[q] = ix < nx ? w[ix] : make_double2(0.0, 0.0);
             spv[q] = __ldg(sp + ix);
         }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (j + q * T < tl) tw[j + q * T] = tv[q];
-        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw, j);
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ra, rb, fx.twp, j);
 #pragma unroll
         for (int q = 0; q < 8; ++q) v[q] = cscale(v[q], spv[q]);
-        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, a, b, tw, j);
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ra, rb, fx.twp, j);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             if (j + q * T < nx) w[j + q * T] = v[q];
@@ -389,7 +376,7 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
         const int ix0 = blockIdx.x * 2 * RP;
         const int q0 = ix0 + 2 * p, q1 = q0 + 1;
         const int bl = L::blen(my);
-        double2* ap = sm + tl + p * bl;
+        double2* ap = sm + p * bl;  // twiddles come from the global per-pass table (fft_reg)
         double2 v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -401,18 +388,7 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
             if (hi) { u1 = cconj(u1); u2 = cconj(u2); }
             v[q] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
         }
-        {  // twiddles: every load in flight before the first store (≤ 8 per thread)
-            double2 tv[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int e = t + q * int(blockDim.x);
-                tv[q] = e < tl ? fy.twp[e] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (t + q * int(blockDim.x) < tl) tw[t + q * int(blockDim.x)] = tv[q];
-        }
-        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, tw, j);
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, fy.twp, j);
         if (acc_coef && gate && *gate) return;
         const double c = acc_coef ? *acc_coef : 0.0;
 #pragma unroll
@@ -714,12 +690,13 @@ std::vector<double> Cov::spectrum_host() const {
 static int threads_1(int n) { return std::max(32, ((n / kEpt + 31) / 32) * 32); }
 // shared bytes of a single-transform kernel of length n (see Lay1)
 static size_t smem_1(int n) {
+    if (n == 512) return 2 * size_t(n + n / 8 + 1) * sizeof(double2);  // register-resident: buffers only
     if (static_len(n)) return (size_t(static_tw_len(n)) + 2 * size_t(n + n / 8 + 1)) * sizeof(double2);
     return 3 * size_t(n) * sizeof(double2);
 }
 // rows passes: register-resident lengths hold kRowPairs single buffers
 static size_t smem_rows(int n, int rp) {
-    if (n == 512) return (size_t(static_tw_len(n)) + size_t(std::max(rp, 2)) * (n + n / 8 + 1)) * sizeof(double2);
+    if (n == 512) return size_t(std::max(rp, 2)) * (n + n / 8 + 1) * sizeof(double2);
     return smem_1(n);
 }
 

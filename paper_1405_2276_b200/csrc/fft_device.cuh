@@ -326,8 +326,22 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2*
                                         int j) {
     static_assert(reg_fft_len<N>(), "fft_reg: N must be a power of 8");
     constexpr int nb = N / 8;
+    constexpr int NX = N == 512 ? 2 : 3;  // exchanges (passes after the first)
+    // each pass needs ONE twiddle per thread (w = ω^k₂, the rest are its powers): fetched from
+    // the global per-pass table (L1-resident, 8 KB) before the first exchange — no shared-memory
+    // staging or loads for twiddles
+    double2 w1s[NX];
+    {
+        int off = 0, ns2 = 8;
+#pragma unroll
+        for (int p = 0; p < NX; ++p) {
+            w1s[p] = __ldg(tp + off + j % ns2);
+            off += 7 * ns2;
+            ns2 *= 8;
+        }
+    }
     dft<8, SIGN>(v);  // pass NS = 1: no twiddles
-    int off = 0;
+    int pidx = 0;
     double2* buf = bufA;
 #pragma unroll
     for (int ns = 1; ns < nb; ns *= 8) {
@@ -340,10 +354,8 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2*
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < 8; ++r) v[r] = buf[fpad(j + r * nb)];
-        const int ns2 = ns * 8, k2 = j % ns2;
-        {  // w^r from one shared-memory load: w² = w·w, w³ = w²·w, … (≤ 4 ulp; halves the
-           // pass's shared-memory wavefronts, the kernel's limiter)
-            double2 w1 = tp[off + k2];
+        {  // w^r from the pass's one twiddle: w² = w·w, w³ = w²·w, … (≤ 4 ulp)
+            double2 w1 = w1s[pidx++];
             if (SIGN > 0) w1.y = -w1.y;
             const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
             const double2 w5 = cmul(w4, w1), w6 = cmul(w3, w3), w7 = cmul(w6, w1);
@@ -355,7 +367,6 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2*
             v[6] = cmul(v[6], w6);
             v[7] = cmul(v[7], w7);
         }
-        off += 7 * ns2;
         dft<8, SIGN>(v);
         if (bufB) buf = (buf == bufA) ? bufB : bufA;
     }
