@@ -12,7 +12,6 @@
 #include <cstdlib>
 
 #include "dense.cuh"
-#include "gemv.cuh"
 
 namespace fkb {
 
@@ -463,60 +462,6 @@ size_t gram_ws_elems(int M, int N, int K) {
 }
 
 // --------------------------------------------------------------------------- GEMV
-__global__ void k_gemv_n(int n, int k, const double* __restrict__ A, long long lda, const double* __restrict__ x,
-                         double alpha, double beta, double* __restrict__ y) {
-    extern __shared__ double xs[];
-    for (int c = threadIdx.x; c < k; c += blockDim.x) xs[c] = x[c];
-    __syncthreads();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double s0 = 0.0, s1 = 0.0;
-        int c = 0;
-        for (; c + 1 < k; c += 2) {
-            s0 = fma(A[i + (long long)c * lda], xs[c], s0);
-            s1 = fma(A[i + (long long)(c + 1) * lda], xs[c + 1], s1);
-        }
-        if (c < k) s0 = fma(A[i + (long long)c * lda], xs[c], s0);
-        const double v = alpha * (s0 + s1);
-        y[i] = beta == 0.0 ? v : v + beta * y[i];
-    }
-}
-
-void gemv_n(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
-            cudaStream_t s) {
-    if (n <= 0) return;
-    if (k <= 0) {
-        if (beta != 1.0) {  // y = beta·y via a K=0 gemm epilogue
-            GemmArgs g;
-            g.M = n; g.N = 1; g.K = 0; g.A = A; g.lda = lda; g.B = x; g.ldb = 1;
-            g.alpha = 0.0; g.beta = beta; g.C = y; g.ldc = n;
-            gemm(g, nullptr, s);
-        }
-        return;
-    }
-    launch_gemv_rows(n, k, A, lda, XPlain{x}, EpiAxpby{y, alpha, beta}, s);
-}
-
-__global__ void k_gemv_t(int n, const double* __restrict__ A, long long lda, const double* __restrict__ x,
-                         double alpha, double beta, double* __restrict__ y) {
-    const int c = blockIdx.x;
-    const double* a = A + (long long)c * lda;
-    double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], x[i], s);
-    __shared__ double red[32];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) y[c] = beta == 0.0 ? alpha * s : alpha * s + beta * y[c];
-    }
-}
-
-void gemv_t(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
-            cudaStream_t s) {
-    launch_gemv_cols(n, k, A, lda, XPlain{x}, EpiAxpby{y, alpha, beta}, s);
-}
 
 // --------------------------------------------------------------------------- Cholesky
 constexpr int CNB = 64;

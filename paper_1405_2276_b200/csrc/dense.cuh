@@ -44,12 +44,6 @@ void gram_sym(const GemmArgs& g, cudaStream_t s);
 void gemm(const GemmArgs& g, double* ws, cudaStream_t s);
 int gemm_pick_splitk(int M, int N, int K);
 
-// y = alpha·A x + beta·y, A n×k column-major (tall-skinny, k small)
-void gemv_n(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
-            cudaStream_t s);
-// y = alpha·Aᵀ x (+ beta·y), A n×k column-major: one block per column, deterministic
-void gemv_t(int n, int k, const double* A, long long lda, const double* x, double alpha, double beta, double* y,
-            cudaStream_t s);
 
 // In-place lower Cholesky of the n×n SPD matrix A (column-major, lda).  Sets *info
 // (device int) to j+1 at the first non-positive pivot, leaves it 0 on success.

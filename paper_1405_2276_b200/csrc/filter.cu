@@ -502,7 +502,6 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     st.alloc(size_t(std::max(m, 1)));
     ucap.alloc(size_t(std::max(r, 1)));
     rdg.alloc(std::max<size_t>(chol_solve_scratch(r), 1));
-    gpart.alloc(size_t(592) * 32 + size_t(std::max(m, 1)) + 64);  // split-GEMV partials
     pcgwork.alloc(size_t(std::max(r, 1)) + 1);
     pcgflag.alloc(1);
     if (std::getenv("FKB_PCG_STAMPS")) pcg_ts.alloc(64);

@@ -39,7 +39,7 @@ struct Filter {
     // solver = 0 reproduces the reference order: form S and LLT it (m×m) every step.
     int solver = 1;
     int eig_sweeps = 0;
-    DBuf<double> P, Pt, theta, E, Erow, rt, ucap, st, rdg, gpart, pcgwork;
+    DBuf<double> P, Pt, theta, E, Erow, rt, ucap, st, rdg, pcgwork;
     // Per-step Woodbury scalars Λ_M⁻¹ (wsq), D^½ (sqd) and capacitance K, double-buffered by
     // step parity: step t reads buffer t&1 while its side branch forms step t+1's into the
     // other (they depend only on α and d, not on the observation).
