@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -279,6 +281,7 @@ int sym_eig_device(int m, double* A, long long lda, double* theta, double* V, cu
         FKB_CUDA(cudaStreamSynchronize(s));
         double mx = 0.0;
         for (double v : offh) mx = std::max(mx, v);
+        if (std::getenv("FKB_EIG_TRACE")) std::fprintf(stderr, "eig sweep %d: max rel offdiag %.3e\n", sweeps, mx);
         prev_mx = mx;
         if (mx <= tol) break;
     }
