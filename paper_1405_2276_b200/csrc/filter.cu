@@ -704,12 +704,12 @@ void Filter::enqueue_step(const double* d_y) {
     // run concurrently it starves the FFT passes of SMs.)
     // (measured: dc beside Hᵀz costs the step less than dc beside the FFT passes)
     const bool par = side() != s;
-    if (r > 0) {
+    if (r > 0 && solver == 0) {  // (the Woodbury solve already forked dc = d ⊙ Eᵀs̃ = d ⊙ Bᵀz)
         fork();
         launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
         mark_on(side(), "ctz_d_update");
         if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
-    } else {
+    } else if (r == 0) {
         k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α (reads α_dev[1] only)
         FKB_LAUNCH_CHECK();
         count_launch();
@@ -752,6 +752,14 @@ void Filter::enqueue_solve_woodbury() {
     FKB_LAUNCH_CHECK();
     count_launch();
     mark("woodbury_st");
+    if (r > 0) {
+        // side branch beside the Pᵀ stream of z = P·s̃: Bᵀz = EᵀPᵀP·s̃ = Eᵀs̃ (E is L2-resident),
+        // dc = d ⊙ Bᵀz with the d and α update in the same pass — done before Hᵀz needs the SMs
+        fork();
+        launch_coldot(m, r, E.p, m, XPlain{st.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
+        mark_on(side(), "ctz_d_update");
+        if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
+    }
     launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s);  // z = P·s̃ (rows of P)
     mark("rotate_out");
 }
