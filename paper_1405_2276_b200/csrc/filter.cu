@@ -161,22 +161,43 @@ struct EpiCtzD {
     const double* lam;
     double* alpha_dev;
     const int* info;
+    const unsigned long long* hout;  // [1]: mapped pinned host d (0 = none), see Filter::hostout
     __device__ __forceinline__ void operator()(long long j, double v) const {
         if (*info) return;
         const double alpha = alpha_dev[1];
         const double dj = d[j], l = lam[j], c = alpha - dj;
         dc[j] = dj * v;
-        d[j] = (dj + alpha * l * c) / (1.0 + l * c);
+        const double dn = (dj + alpha * l * c) / (1.0 + l * c);
+        d[j] = dn;
+        if (hout[1]) reinterpret_cast<double*>(hout[1])[j] = dn;
+        if (j == 0) alpha_dev[0] = alpha;
+    }
+    // dc_j = sqd_j·x_j given directly (Woodbury path), then the same d/α commit
+    __device__ __forceinline__ void operator()(long long j, double xj, double sqdj) const {
+        if (*info) return;
+        const double alpha = alpha_dev[1];
+        const double dj = d[j], l = lam[j], c = alpha - dj;
+        dc[j] = sqdj * xj;
+        const double dn = (dj + alpha * l * c) / (1.0 + l * c);
+        d[j] = dn;
+        if (hout[1]) reinterpret_cast<double*>(hout[1])[j] = dn;
         if (j == 0) alpha_dev[0] = alpha;
     }
 };
 
 // s̃_i = wsq_i · (r̃_i + Σ_j E_ij · (sqd_j · x_j))   ([Λ_M − EDEᵀ]⁻¹ r̃ via Woodbury); warp per
-// row of the row-major E copy, every load of the row in flight
+// row of the row-major E copy, every load of the row in flight.
+// The extra last CTA forms the mean update's coefficients and commits d and α: with
+// u = D^½EᵀΛ_M⁻¹r̃ and K = I − D^½EᵀΛ_M⁻¹ED^½, D^½Eᵀs̃ = u + (I − K)x = x, so
+// d ⊙ Bᵀz = d ⊙ EᵀPᵀP s̃ = D^½x — no pass over B or E (fast_filter.hpp:114-123)
 __global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double* __restrict__ Erow,
                                                     const double* __restrict__ sqd, const double* __restrict__ x,
                                                     const double* __restrict__ wsq, const double* __restrict__ rt,
-                                                    double* __restrict__ st) {
+                                                    double* __restrict__ st, EpiCtzD upd) {
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int j = threadIdx.x; j < r; j += blockDim.x) upd(j, x[j], sqd[j]);
+        return;
+    }
     const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (i >= m) return;
     const double* er = Erow + (long long)i * r;
@@ -196,15 +217,23 @@ __global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double*
     if (lane == 0) st[i] = wsq[i] * (rt[i] + acc);
 }
 
-// mean_i ← (mean_i + α·t_i) − Σ_j U_ij·dc_j  (fast_filter.hpp:114-116), skipped on a failed step
+// mean_i ← (mean_i + α·t_i) − Σ_j U_ij·dc_j  (fast_filter.hpp:114-116), skipped on a failed step;
+// the step's last kernel: with hout[0] set it also writes the
+// new mean straight into the caller's mapped pinned host buffer (and hout[2] the failure
+// flag), so the host-buffer step needs no device→host copies after the graph
 struct EpiMean {
     double* mean;
     const double* t;
     const double* alpha_dev;
     const int* info;
+    const unsigned long long* hout;
     __device__ __forceinline__ void operator()(long long i, double v) const {
-        if (*info) return;
-        mean[i] = (mean[i] + alpha_dev[1] * t[i]) - v;
+        const int bad = *info;
+        if (i == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+        if (bad) return;
+        const double nm = (mean[i] + alpha_dev[1] * t[i]) - v;
+        mean[i] = nm;
+        if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = nm;
     }
 };
 
@@ -516,6 +545,8 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
     info.alloc(1);
+    hostout.alloc(3);
+    FKB_CUDA(cudaMemset(hostout.p, 0, hostout.bytes()));
     flags.alloc(size_t(2 * ceil_div(std::max(m, 1), 64) + 2));
     reset();
 }
@@ -528,6 +559,7 @@ Filter::~Filter() {
     if (s3) cudaStreamSynchronize(s3);
     drop_graphs();
     if (h_info) cudaFreeHost(h_info);
+    if (h_hostout) cudaFreeHost(h_hostout);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join2) cudaEventDestroy(ev_join2);
@@ -699,14 +731,14 @@ void Filter::enqueue_step(const double* d_y) {
     mark("residual");
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
-    // side branch: dc = d ⊙ Bᵀz with d and α updated in the same pass; main branch:
-    // t = Γ(Hᵀz); then mean += α·t − U·dc (:114-123).  (The U pass stays on the main branch:
-    // run concurrently it starves the FFT passes of SMs.)
-    // (measured: dc beside Hᵀz costs the step less than dc beside the FFT passes)
+    // dc = d ⊙ Bᵀz with d and α updated in the same pass (solver 0: a side-branch pass over B;
+    // solver 1: D^½x inside k_woodbury_st); main branch: t = Γ(Hᵀz); then mean += α·t − U·dc
+    // (:114-123).  (The U pass stays on the main branch: run concurrently it starves the FFT
+    // passes of SMs and slows Hᵀz, which shares HBM with it.)
     const bool par = side() != s;
-    if (r > 0 && solver == 0) {  // (the Woodbury solve already forked dc = d ⊙ Eᵀs̃ = d ⊙ Bᵀz)
+    if (r > 0 && solver == 0) {
         fork();
-        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
+        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p}, side());
         mark_on(side(), "ctz_d_update");
         if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
     } else if (r == 0) {
@@ -718,8 +750,8 @@ void Filter::enqueue_step(const double* d_y) {
     mark("ht_z");
     cov->apply1(t.p, t.p);
     mark("gamma_apply");
-    if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
-    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p}, s);
+    if (r > 0 && par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
+    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p, hostout.p}, s);
     if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
@@ -748,18 +780,11 @@ void Filter::enqueue_solve_woodbury() {
         mark("cap_solve");
     }
     // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
-    k_woodbury_st<<<std::max(1, ceil_div(m, 8)), 256, 0, s>>>(m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p);
+    k_woodbury_st<<<std::max(1, ceil_div(m, 8)) + 1, 256, 0, s>>>(
+        m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p});
     FKB_LAUNCH_CHECK();
     count_launch();
     mark("woodbury_st");
-    if (r > 0) {
-        // side branch beside the Pᵀ stream of z = P·s̃: Bᵀz = EᵀPᵀP·s̃ = Eᵀs̃ (E is L2-resident),
-        // dc = d ⊙ Bᵀz with the d and α update in the same pass — done before Hᵀz needs the SMs
-        fork();
-        launch_coldot(m, r, E.p, m, XPlain{st.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p}, side());
-        mark_on(side(), "ctz_d_update");
-        if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
-    }
     launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s);  // z = P·s̃ (rows of P)
     mark("rotate_out");
 }
@@ -835,6 +860,7 @@ void Filter::launch_step() {
 }
 
 void Filter::step(const double* d_y) {
+    set_hostout(0, 0, 0);
     if (d_y != ybuf.p)
         FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
     launch_step();
@@ -847,13 +873,44 @@ void Filter::step(const double* d_y) {
 // One step from a host observation with the new state downloaded in the same round trip
 // (the reference's fkf_step returns the new LowRankState by value): H2D y, graph replay, D2H of
 // the failure flag, d and mean, ONE stream synchronization.
+// device address of a page-locked (mapped) host buffer, 0 for pageable memory
+static unsigned long long mapped_host(const void* p) {
+    if (!p) return 0;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return a.type == cudaMemoryTypeHost && a.devicePointer ? reinterpret_cast<unsigned long long>(a.devicePointer) : 0;
+}
+
+void Filter::set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi) {
+    if (hm == hostout_cache[0] && hd == hostout_cache[1] && hi == hostout_cache[2]) return;
+    if (!h_hostout)
+        FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_hostout), 3 * sizeof(unsigned long long),
+                               cudaHostAllocDefault));
+    FKB_CUDA(cudaStreamSynchronize(s));  // the staging slots may still feed an earlier copy
+    h_hostout[0] = hostout_cache[0] = hm;
+    h_hostout[1] = hostout_cache[1] = hd;
+    h_hostout[2] = hostout_cache[2] = hi;
+    FKB_CUDA(cudaMemcpyAsync(hostout.p, h_hostout, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+}
+
 void Filter::step_host_state(const double* h_y, double* h_d, double* h_mean) {
     if (!h_info) FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_info), sizeof(int), cudaHostAllocDefault));
+    // page-locked caller buffers: the graph's last kernels write d, the mean and the failure
+    // flag straight into them (mapped host memory), overlapped with the U pass
+    const unsigned long long hm = mapped_host(h_mean), hd = (h_d && r > 0) ? mapped_host(h_d) : 0;
+    const bool zc = h_mean && hm && (!(h_d && r > 0) || hd);
+    if (zc) set_hostout(hm, hd, mapped_host(h_info));
+    else set_hostout(0, 0, 0);
     if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_y, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
     launch_step();
-    FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
-    if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+    if (!zc) {
+        FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
+        if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+    }
     FKB_CUDA(cudaStreamSynchronize(s));
     if (*h_info) {
         k_valid = false;
@@ -871,6 +928,7 @@ void Filter::step_host(const double* h_y) {
 
 void Filter::steps_async(const double* d_ys, int nsteps, long long ldy) {
     // Device-resident observation sequence; one deferred singularity check at the end.
+    set_hostout(0, 0, 0);
     for (int k = 0; k < nsteps; ++k) {
         FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_ys + (long long)k * ldy, sizeof(double) * size_t(m),
                                  cudaMemcpyDeviceToDevice, s));

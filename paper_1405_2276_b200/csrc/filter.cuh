@@ -1,5 +1,6 @@
 // filter.cuh — the constant-H fast filter on the device (fkf_init / fkf_step / UQ).
 #pragma once
+#include <cstdlib>
 
 #include <string>
 #include <utility>
@@ -98,6 +99,11 @@ struct Filter {
     void step_host(const double* h_y);                   // same, y from host memory
     void step_host_state(const double* h_y, double* h_d, double* h_mean);  // + new state, one sync
     int* h_info = nullptr;                               // pinned failure-flag staging
+    // mapped host outputs of the step graph: [0] mean, [1] d, [2] failure flag (0 = none)
+    DBuf<unsigned long long> hostout;
+    unsigned long long hostout_cache[3] = {0, 0, 0};
+    unsigned long long* h_hostout = nullptr;
+    void set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi);
     // k steps over device-resident observations (column k at d_ys + k·ldy), no host sync;
     // finish_async() performs the deferred singularity check and commits host mirrors.
     void steps_async(const double* d_ys, int nsteps, long long ldy);

@@ -22,3 +22,7 @@ for q in range(1, it + 1):
         print(f" iter {q}: {int(st[1 + q]) - int(st[q])} ns")
 print("final check + exit:", int(st[63]) - int(st[1 + it]), "ns")
 print("total", int(st[63]) - t0, "ns")
+if st[39]:
+    b = int(st[39])
+    print("iter 3 phases (ns from start): send", int(st[40]) - b, "| wait", int(st[41]) - b,
+          "| reduce", int(st[42]) - b, "| matvec", int(st[43]) - b, "| update", int(st[1 + 4]) - b)

@@ -244,6 +244,56 @@ def test_step_state_round_trip_matches_step_then_state():
     assert lib().fkb_fkf_step_state(b._f, C.c_void_p(bad.ctypes.data), 3, None, None, None) == 1  # invalid_argument
 
 
+@pytest.mark.parametrize("solver", [0, 1])
+def test_step_state_pinned_buffers_written_by_the_graph(solver):
+    """Page-locked output buffers take the zero-copy path (the graph's last kernels write mean,
+    d and the failure flag into mapped host memory): identical to the copy path, also when
+    pinned, pageable and device-only steps alternate, and singularity still raises."""
+    import ctypes as C
+    import torch
+    from paper_1405_2276_b200._native import lib
+    w, h, ys, s2 = workload_inputs("c0", 6)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    a = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    b = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    a.set_solver(solver)
+    b.set_solver(solver)
+    pin_d = torch.empty(max(b.rank(), 1), dtype=torch.float64).pin_memory()
+    pin_m = torch.empty(w.N, dtype=torch.float64).pin_memory()
+    for i, y in enumerate(ys):
+        sa = P.fkf_step(a, y)
+        y = np.ascontiguousarray(y)
+        alpha = C.c_double()
+        if i % 3 == 2:  # device-side step entry point between host-buffer steps
+            sb = P.fkf_step(b, y)
+            assert np.array_equal(sb["mean"], sa["mean"]) and np.array_equal(sb["d"], sa["d"])
+            continue
+        if i % 3 == 0:
+            pin_d.fill_(np.nan)
+            pin_m.fill_(np.nan)
+            dptr, mptr = pin_d.data_ptr(), pin_m.data_ptr()
+        else:
+            d_np, m_np = np.empty(b.rank()), np.empty(w.N)
+            dptr, mptr = d_np.ctypes.data, m_np.ctypes.data
+        assert lib().fkb_fkf_step_state(b._f, C.c_void_p(y.ctypes.data), len(y), C.byref(alpha),
+                                        C.c_void_p(dptr), C.c_void_p(mptr)) == 0
+        d_out = pin_d.numpy()[: b.rank()] if i % 3 == 0 else d_np
+        m_out = pin_m.numpy() if i % 3 == 0 else m_np
+        assert alpha.value == sa["alpha"]
+        assert np.array_equal(d_out, sa["d"]) and np.array_equal(m_out, sa["mean"])
+    # a singular step through the zero-copy path raises and leaves the state untouched
+    st = b.state()
+    b.set_state(st["alpha"], np.full(b.rank(), 50.0 * st["alpha"]), st["mean"], st["step"])
+    mid = b.state()
+    bad_y = np.ascontiguousarray(ys[0])
+    rc = lib().fkb_fkf_step_state(b._f, C.c_void_p(bad_y.ctypes.data), len(bad_y), None,
+                                  C.c_void_p(pin_d.data_ptr()), C.c_void_p(pin_m.data_ptr()))
+    assert rc == 2  # runtime_error: singular
+    after = b.state()
+    assert after["alpha"] == mid["alpha"] and np.array_equal(after["mean"], mid["mean"])
+
+
 def _c0_ctx():
     w, h, ys, s2 = workload_inputs("c0", 4)
     kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
