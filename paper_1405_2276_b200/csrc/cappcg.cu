@@ -77,12 +77,18 @@ __device__ __forceinline__ void block_matvec(PcgShared& sh, const double* Ks, co
         double s0 = 0.0, s1 = 0.0;
         if (i < r1) {
             const double* Kc = kstage ? Ks + (long long)(i - r0) * n : K + (long long)i * ld;
+            // four independent FMA chains (FP64 latency dominates this short dot)
+            double s2 = 0.0, s3 = 0.0;
             int j = sub;
-            for (; j + 16 < n; j += 32) {
+            for (; j + 48 < n; j += 64) {
                 s0 = fma(Kc[j], v[j], s0);
                 s1 = fma(Kc[j + 16], v[j + 16], s1);
+                s2 = fma(Kc[j + 32], v[j + 32], s2);
+                s3 = fma(Kc[j + 48], v[j + 48], s3);
             }
-            if (j < n) s0 = fma(Kc[j], v[j], s0);
+            for (; j < n; j += 16) s0 = fma(Kc[j], v[j], s0);
+            s0 += s2;
+            s1 += s3;
         }
         double s = s0 + s1;
         for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -91,6 +97,23 @@ __device__ __forceinline__ void block_matvec(PcgShared& sh, const double* Ks, co
     __syncthreads();
 }
 
+// Same product with this thread's K entries held in registers (KR > 0: n ≤ 16·KR, one row
+// per 16-lane group, entries j = sub + 16k): per iteration only the exchanged vector is read
+// from shared memory (one broadcast wavefront per load) — the K block is read once per solve.
+template <int KR>
+__device__ __forceinline__ void block_matvec_reg(PcgShared& sh, const double (&kr)[KR], int r0, int r1, int buf) {
+    const int sub = threadIdx.x & 15, slot = threadIdx.x >> 4;
+    const double* v = sh.v[buf] + sub;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < KR; ++k) a[k & 3] = fma(kr[k], v[16 * k], a[k & 3]);
+    double s = (a[0] + a[1]) + (a[2] + a[3]);
+    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (sub == 0 && r0 + slot < r1) sh.q[slot] = s;
+    __syncthreads();
+}
+
+template <int KR>
 __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, long long ld, int n,
                                                  double* __restrict__ u, double* __restrict__ work,
                                                  int* __restrict__ fallback, int maxit, double tol, int kstage,
@@ -135,6 +158,8 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         for (int e = tid; e < cnt; e += PC_T) cp_async8(Ks + e, K + (long long)(r0 + e / n) * ld + e % n);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    if constexpr (KR > 0)  // entries n..16·KR−1 of both exchange buffers multiply zero K entries
+        for (int e = n + tid; e < 16 * KR; e += PC_T) sh.v[0][e] = sh.v[1][e] = 0.0;
     __syncthreads();  // mbarrier initialized before anyone waits on it
     // Pipelined Jacobi-PCG (Ghysels–Vanroose): the matvec n = K·m and the reductions
     // γ = rᵀu, δ = wᵀu of the same iteration are independent, so one cluster exchange per
@@ -169,63 +194,73 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     cl.sync();  // u₀ exchanged; also orders every thread's staged K before the first matvec
-    block_matvec(sh, Ks, K, ld, n, r0, r1, 1, kstage);  // w₀ = K u₀
+    double kr[KR > 0 ? KR : 1];
+    if constexpr (KR > 0) {
+        const int sub = tid & 15, i = r0 + (tid >> 4);
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int j = sub + 16 * k;
+            kr[k] = (i < r1 && j < n) ? Ks[(long long)(i - r0) * n + j] : 0.0;
+        }
+        block_matvec_reg<KR>(sh, kr, r0, r1, 1);  // w₀ = K u₀
+    } else {
+        block_matvec(sh, Ks, K, ld, n, r0, r1, 1, kstage);  // w₀ = K u₀
+    }
     if (own) w = sh.q[tid];
     if (stamp) ts[1] = gtimer();
-    double gamma_prev = 1.0, alpha_prev = 1.0, stop = 0.0;
+    double inv_gamma_prev = 1.0, inv_alpha_prev = 1.0, stop = 0.0;
     int it = 0;
     bool done = false;
     // exchange bytes every CTA receives per iteration: all n entries of m + 16×3 partials
     const unsigned xbytes = unsigned(n) * 8u + unsigned(PC_CL) * 32u;
+    // Roles: the owner warp(s) (rows r0..r1 live in threads 0..rb−1) push m and the partials,
+    // reduce the 16 slots and run the scalar recurrence; meanwhile every warp multiplies its
+    // rows of K by m.  The owners' verdict (continue / converged / give up) reaches the other
+    // warps through a per-parity shared flag published before the matvec's CTA barrier.
+    const bool scal = warp < ((rb + 31) >> 5);
+    __shared__ int xflag[2];
+    double mv = 0.0, gamma = 0.0, alpha = 0.0, beta = 0.0;
     while (true) {
         const int buf = it & 1;
         const unsigned parity = unsigned((it >> 1) & 1);
-        const double mv = dinv * w;
-        if (stamp && it == 3) ts[39] = gtimer();
-        if (tid == 0) {
-            const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[buf]));
-            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xa), "r"(xbytes) : "memory");
-        }
-        {
-            double a = own ? r * uu : 0.0, bq = own ? w * uu : 0.0, c = own ? r * r : 0.0;
-            double e = it == 0 ? nonpos : 0.0;
-            if (warp < 2) {
-                for (int o = 16; o > 0; o >>= 1) {
-                    a += __shfl_xor_sync(0xffffffffu, a, o);
-                    bq += __shfl_xor_sync(0xffffffffu, bq, o);
-                    c += __shfl_xor_sync(0xffffffffu, c, o);
-                    e += __shfl_xor_sync(0xffffffffu, e, o);
-                }
-            }
-            if (own)
+        const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[buf]));
+        if (stamp && it == 3) ts[39] = clock64();
+        if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xa), "r"(xbytes) : "memory");
+        if (scal) {
+            mv = dinv * w;
+            if (own)  // the vector first: its stores overlap the partial-sum shuffles below
 #pragma unroll
                 for (int cc = 0; cc < PC_CL; ++cc) st_async_cluster(&sh.v[buf][row], &xbar[buf], cc, mv);
-            if (rb <= 32) {  // one owning warp: its lanes 0..15 push the three sums to every CTA
-                if (warp == 0 && lane < PC_CL) {
-                    const double a0 = __shfl_sync(0x0000ffffu, a, 0), b0 = __shfl_sync(0x0000ffffu, bq, 0),
-                                 c0 = __shfl_sync(0x0000ffffu, c, 0), e0 = __shfl_sync(0x0000ffffu, e, 0);
-                    st_async_cluster(&sh.part[buf][crank][0], &xbar[buf], lane, a0);
-                    st_async_cluster(&sh.part[buf][crank][1], &xbar[buf], lane, b0);
-                    st_async_cluster(&sh.part[buf][crank][2], &xbar[buf], lane, c0);
-                    st_async_cluster(&sh.part[buf][crank][3], &xbar[buf], lane, e0);
-                }
-            } else {
-                if (warp < 2 && lane == 0) {
+            double a = own ? r * uu : 0.0, bq = own ? w * uu : 0.0, c = own ? r * r : 0.0;
+            double e = it == 0 ? nonpos : 0.0;
+            for (int o = 16; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                bq += __shfl_xor_sync(0xffffffffu, bq, o);
+                c += __shfl_xor_sync(0xffffffffu, c, o);
+                e += __shfl_xor_sync(0xffffffffu, e, o);
+            }
+            if (rb > 32) {  // two owner warps: combine through shared memory (named barrier)
+                if (lane == 0) {
                     sh.red[warp][0] = a;
                     sh.red[warp][1] = bq;
                     sh.red[warp][2] = c;
                     sh.red[warp][3] = e;
                 }
-                __syncthreads();
-                if (tid < 4 * PC_CL) {
-                    const int qq = tid % 4, dest = tid / 4;
-                    st_async_cluster(&sh.part[buf][crank][qq], &xbar[buf], dest, sh.red[0][qq] + sh.red[1][qq]);
-                }
+                asm volatile("bar.sync 1, 64;" ::: "memory");
+                a = sh.red[0][0] + sh.red[1][0];
+                bq = sh.red[0][1] + sh.red[1][1];
+                c = sh.red[0][2] + sh.red[1][2];
+                e = sh.red[0][3] + sh.red[1][3];
+            }
+            if (warp == 0 && lane < PC_CL) {  // lanes 0..15 push the sums to CTA `lane`
+                st_async_cluster(&sh.part[buf][crank][0], &xbar[buf], lane, a);
+                st_async_cluster(&sh.part[buf][crank][1], &xbar[buf], lane, bq);
+                st_async_cluster(&sh.part[buf][crank][2], &xbar[buf], lane, c);
+                st_async_cluster(&sh.part[buf][crank][3], &xbar[buf], lane, e);
             }
         }
-        if (stamp && it == 3) ts[40] = gtimer();
+        if (stamp && it == 3) ts[40] = clock64();
         {  // m and all partials delivered (this CTA's barrier of this parity)
-            const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[buf]));
             unsigned ok = 0;
             while (!ok)
                 asm volatile(
@@ -234,46 +269,69 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
                     : "r"(xa), "r"(parity)
                     : "memory");
         }
-        if (stamp && it == 3) ts[41] = gtimer();
-        double gamma = 0.0, delta = 0.0, rr = 0.0, bad = 0.0;
+        if (stamp && it == 3) ts[41] = clock64();
+        if (scal) {
+            // lane-parallel sum of the 16 CTA slots (lane l reads slot l & 15, xor butterfly):
+            // each add pairs the same two operands in every lane, warp and CTA (a + b = b + a
+            // exactly), so all CTAs hold bit-identical scalars and decide alike
+            const double* ps = sh.part[buf][lane & 15];
+            double g = ps[0], dl = ps[1], rr = ps[2], bad = ps[3];
 #pragma unroll
-        for (int c = 0; c < PC_CL; ++c) {
-            gamma += sh.part[buf][c][0];
-            delta += sh.part[buf][c][1];
-            rr += sh.part[buf][c][2];
-            bad += sh.part[buf][c][3];
+            for (int o = 8; o > 0; o >>= 1) {
+                g += __shfl_xor_sync(0xffffffffu, g, o);
+                dl += __shfl_xor_sync(0xffffffffu, dl, o);
+                rr += __shfl_xor_sync(0xffffffffu, rr, o);
+                bad += __shfl_xor_sync(0xffffffffu, bad, o);
+            }
+            if (stamp && it == 3) ts[45] = clock64();
+            int fl = 0;
+            // a non-positive pivot means K (hence S) is not SPD: leave it to the Cholesky,
+            // which reports "singular" exactly like the reference LLT (fast_filter.hpp:104-106)
+            if (bad > 0.0) {
+                fl = 2;
+            } else {
+                if (it == 0) stop = tol * tol * rr;  // r₀ = u
+                if (rr <= stop || rr == 0.0) fl = 1;
+                else if (it >= maxit) fl = 2;
+            }
+            if (fl == 0) {
+                // 1/γ_prev and 1/α_prev were formed last iteration: one division here
+                gamma = g;
+                beta = it == 0 ? 0.0 : g * inv_gamma_prev;
+                const double eta = it == 0 ? dl : dl - beta * g * inv_alpha_prev;  // = pᵀKp
+                if (!(eta > 0.0)) fl = 2;  // non-positive curvature: not SPD (or breakdown)
+                else alpha = g / eta;
+            }
+            if (stamp && it == 3) ts[46] = clock64();
+            if (tid == 0) xflag[buf] = fl;
         }
-        // a non-positive pivot means K (hence S) is not SPD: leave it to the Cholesky, which
-        // reports "singular" exactly like the reference LLT (fast_filter.hpp:104-106)
-        if (bad > 0.0) break;
-        if (it == 0) stop = tol * tol * rr;  // r₀ = u
-        if (rr <= stop || rr == 0.0) {
-            done = true;
+        if (stamp && it == 3) ts[42] = clock64();
+        if constexpr (KR > 0) block_matvec_reg<KR>(sh, kr, r0, r1, buf);  // n = K m (ends in a CTA barrier)
+        else block_matvec(sh, Ks, K, ld, n, r0, r1, buf, kstage);
+        if (stamp && it == 3) ts[43] = clock64();
+        const int fl = xflag[buf];
+        if (fl) {
+            done = fl == 1;
             break;
         }
-        if (it >= maxit) break;
-        if (stamp && it == 3) ts[42] = gtimer();
-        block_matvec(sh, Ks, K, ld, n, r0, r1, buf, kstage);  // n = K m
-        if (stamp && it == 3) ts[43] = gtimer();
-        const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
-        const double eta = it == 0 ? delta : delta - beta * gamma / alpha_prev;  // = pᵀKp
-        if (!(eta > 0.0)) break;  // non-positive curvature: K is not SPD (or breakdown) → Cholesky
-        const double alpha = gamma / eta;
-        if (own) {
-            const double nv = sh.q[tid];
-            zv = fma(beta, zv, nv);
-            qv = fma(beta, qv, mv);
-            sv = fma(beta, sv, w);
-            pv = fma(beta, pv, uu);
-            x = fma(alpha, pv, x);
-            r = fma(-alpha, sv, r);
-            uu = fma(-alpha, qv, uu);
-            w = fma(-alpha, zv, w);
+        if (scal) {
+            if (own) {
+                const double nv = sh.q[tid];
+                zv = fma(beta, zv, nv);
+                qv = fma(beta, qv, mv);
+                sv = fma(beta, sv, w);
+                pv = fma(beta, pv, uu);
+                x = fma(alpha, pv, x);
+                r = fma(-alpha, sv, r);
+                uu = fma(-alpha, qv, uu);
+                w = fma(-alpha, zv, w);
+            }
+            inv_gamma_prev = 1.0 / gamma;
+            inv_alpha_prev = 1.0 / alpha;
         }
-        gamma_prev = gamma;
-        alpha_prev = alpha;
         ++it;
         if (stamp && it < 60) ts[1 + it] = gtimer();
+        if (stamp && it == 4) ts[44] = clock64();
     }
     cl.sync();  // no CTA exits while a peer's asynchronous stores may still target it
     if (done) {
@@ -295,9 +353,10 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
     const size_t stage = sizeof(double) * size_t(rb) * n;
     const int kstage = stage <= 190 * 1024 ? 1 : 0;  // K columns resident in shared memory
     if (!g_pcg_attr) {
-        FKB_CUDA(cudaFuncSetAttribute((const void*)k_cap_pcg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        FKB_CUDA(cudaFuncSetAttribute((const void*)k_cap_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      190 * 1024));
+        for (const void* fn : {(const void*)k_cap_pcg<0>, (const void*)k_cap_pcg<20>, (const void*)k_cap_pcg<32>}) {
+            FKB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            FKB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 190 * 1024));
+        }
         g_pcg_attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -312,7 +371,12 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
+    if (kstage && n <= 16 * 20)
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<20>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
+    else if (kstage && n <= 16 * 32)
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<32>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
+    else
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<0>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
     count_launch();
 }
 

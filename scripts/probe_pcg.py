@@ -20,5 +20,6 @@ for k in range(1, min(it.value, 60)):
     print(f" iter {k}: {int(st[1 + k]) - int(st[k])} ns")
 print("total", int(st[63]) - t0, "ns")
 if it.value > 4:
-    print("iter 3 detail: top->pushed", int(st[40]) - int(st[39]), "sync", int(st[41]) - int(st[40]),
-          "sums", int(st[42]) - int(st[41]), "matvec", int(st[43]) - int(st[42]), "update+next top", int(st[5]) - int(st[43]))
+    b = int(st[39])
+    print("iter 3 (SM cycles): sent", int(st[40]) - b, "| waited", int(st[41]) - b, "| shuffled", int(st[45]) - b,
+          "| decided", int(st[46]) - b, "| flag", int(st[42]) - b, "| matvec", int(st[43]) - b, "| update", int(st[44]) - b)

@@ -24,5 +24,5 @@ print("final check + exit:", int(st[63]) - int(st[1 + it]), "ns")
 print("total", int(st[63]) - t0, "ns")
 if st[39]:
     b = int(st[39])
-    print("iter 3 phases (ns from start): send", int(st[40]) - b, "| wait", int(st[41]) - b,
-          "| reduce", int(st[42]) - b, "| matvec", int(st[43]) - b, "| update", int(st[1 + 4]) - b)
+    print("iter 3 phases (SM cycles from start): send", int(st[40]) - b, "| wait", int(st[41]) - b,
+          "| shuffled", int(st[45]) - b, "| decided", int(st[46]) - b, "| flag", int(st[42]) - b, "| matvec", int(st[43]) - b, "| update", int(st[44]) - b)
