@@ -24,6 +24,7 @@
 // numpy/scipy restatement (tests/golden/make_golden.py).
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -861,6 +862,279 @@ inline void realization(const State& st, const Ctx& ctx, const double* z, double
     for (Index i = 0; i < n; ++i) out[i] = st.mean[size_t(i)] + (ra * z[i] - ra * up[size_t(i)]);
 }
 
+
+// ---------------------------------------------------------------- boxcox.hpp:14-90
+struct BoxCox {
+    double alpha = 1.0;
+    void validate() const {  // :19-23
+        if (!(alpha > 0.0)) throw std::invalid_argument("boxcox: alpha must be positive, got " + std::to_string(alpha));
+    }
+    double forward(double s) const {  // :25-31
+        validate();
+        if (alpha == 1.0) return s - 1.0;
+        if (s < 0.0) throw std::domain_error("boxcox: forward transform requires s >= 0");
+        return alpha * (std::pow(s, 1.0 / alpha) - 1.0);
+    }
+    double inverse(double shat) const {  // :33-40
+        validate();
+        if (alpha == 1.0) return shat + 1.0;
+        const double base = (shat + alpha) / alpha;
+        if (base < 0.0) throw std::domain_error("boxcox: inverse transform requires (shat + alpha)/alpha >= 0");
+        return std::pow(base, alpha);
+    }
+    double derivative(double shat) const {  // :43-50
+        validate();
+        if (alpha == 1.0) return 1.0;
+        const double base = (shat + alpha) / alpha;
+        if (base < 0.0) throw std::domain_error("boxcox: derivative requires (shat + alpha)/alpha >= 0");
+        return std::pow(base, alpha - 1.0);
+    }
+    // vector map with the component index in the message (:58-75); which: 0 fwd, 1 inv, 2 der
+    void map(const double* x, double* out, Index n, int which) const {
+        static const char* what[3] = {"forward", "inverse", "derivative"};
+        for (Index i = 0; i < n; ++i) {
+            try {
+                out[i] = which == 0 ? forward(x[i]) : which == 1 ? inverse(x[i]) : derivative(x[i]);
+            } catch (const std::domain_error&) {
+                throw std::domain_error("boxcox: " + std::string(what[which]) + " domain violation at index " +
+                                        std::to_string(i) + " (value " + std::to_string(x[i]) + ")");
+            }
+            if (!std::isfinite(out[i]))
+                throw std::domain_error("boxcox: " + std::string(what[which]) +
+                                        " produced a non-finite value at index " + std::to_string(i));
+        }
+    }
+};
+
+// ekf_linearize boxcox.hpp:81-90: H_k = H·diag(∂s/∂ŝ), h(ŝ) = H·s(ŝ), same sparsity
+inline void ekf_linearize(const Csr& h, const double* mean, const BoxCox& t, Csr& hk, std::vector<double>& h_of_mean) {
+    const Index n = h.cols;
+    std::vector<double> jac(static_cast<size_t>(n)), s(static_cast<size_t>(n));
+    t.map(mean, jac.data(), n, 2);
+    hk = h;
+    for (size_t e = 0; e < hk.val.size(); ++e) hk.val[e] = h.val[e] * jac[size_t(h.col[e])];
+    t.map(mean, s.data(), n, 1);
+    h_of_mean.assign(size_t(h.rows), 0.0);
+    csr_mv(h, s.data(), h_of_mean.data());
+}
+
+// CovarianceOperator::inverse_apply in fft mode (covariance.hpp:145-152): CG on the fast
+// matvec (cg.hpp:20-50), tol 1e-12, max 10·√n + 10 iterations (:125), throwing on failure (:130-139)
+inline void cov_solve(Cov& cov, const double* b, double* x, double tol = 1e-12) {
+    const Index n = cov.size();
+    const int max_iter = static_cast<int>(10.0 * std::sqrt(double(n))) + 10;
+    std::fill(x, x + n, 0.0);
+    const double bnorm = std::sqrt(dot(b, b, n));
+    if (bnorm == 0.0) return;
+    std::vector<double> r(b, b + n), p(b, b + n), ap(static_cast<size_t>(n));
+    double rs = dot(r.data(), r.data(), n);
+    int it = 0;
+    double res = 0.0;
+    for (; it < max_iter; ++it) {
+        cov.apply(p.data(), ap.data());
+        const double a = rs / dot(p.data(), ap.data(), n);
+        axpy(a, p.data(), x, n);
+        axpy(-a, ap.data(), r.data(), n);
+        const double rs_next = dot(r.data(), r.data(), n);
+        if (std::sqrt(rs_next) <= tol * bnorm) return;
+        for (Index i = 0; i < n; ++i) p[size_t(i)] = r[size_t(i)] + (rs_next / rs) * p[size_t(i)];
+        rs = rs_next;
+        res = std::sqrt(rs) / bnorm;
+    }
+    std::ostringstream msg;
+    msg << "cov_solve: CG did not converge within " << it << " iterations; achieved relative residual " << res
+        << " (requested " << tol << ")";
+    throw std::runtime_error(msg.str());
+}
+
+using BApply = std::function<void(const double*, double*)>;
+
+// b_orthonormalize lowrank.hpp:53-106 with `against` and cached B·against
+struct BOrtho { Mat q, bq; };
+inline BOrtho b_orthonormalize_against(const Mat& v, const BApply& b_apply, const Mat& ag, const Mat& b_ag) {
+    const Index n = v.rows, m = v.cols;
+    BOrtho out;
+    out.q = Mat(n, m);
+    out.bq = Mat(n, m);
+    Index kept = 0;
+    std::vector<double> w(static_cast<size_t>(n)), bw(static_cast<size_t>(n));
+    for (Index j = 0; j < m; ++j) {
+        std::copy(v.col(j), v.col(j) + n, w.begin());
+        for (double x : w)
+            if (!std::isfinite(x))
+                throw std::invalid_argument("b_orthonormalize: column " + std::to_string(j) + " contains non-finite entries");
+        b_apply(w.data(), bw.data());
+        const double pre_norm = std::sqrt(std::max(dot(w.data(), bw.data(), n), 0.0));
+        double norm = 0.0;
+        for (int sweep = 0; sweep < 2; ++sweep) {
+            for (Index i = 0; i < ag.cols; ++i) axpy(-dot(b_ag.col(i), w.data(), n), ag.col(i), w.data(), n);
+            for (Index i = 0; i < kept; ++i) axpy(-dot(out.bq.col(i), w.data(), n), out.q.col(i), w.data(), n);
+            b_apply(w.data(), bw.data());
+            norm = std::sqrt(std::max(dot(w.data(), bw.data(), n), 0.0));
+        }
+        if (norm <= 1e-12 * pre_norm || norm == 0.0) continue;
+        for (Index i = 0; i < n; ++i) {
+            out.q(i, kept) = w[size_t(i)] / norm;
+            out.bq(i, kept) = bw[size_t(i)] / norm;
+        }
+        ++kept;
+    }
+    out.q.cols = out.bq.cols = kept;
+    out.q.a.resize(size_t(n * kept));
+    out.bq.a.resize(size_t(n * kept));
+    return out;
+}
+
+// add_low_rank lowrank.hpp:238-294: U D_U Uᵀ + V D_V Vᵀ in one B-orthonormal factorization
+struct LowRankSym { Mat w; std::vector<double> d; };
+inline LowRankSym add_low_rank(const Mat& u, const std::vector<double>& d_u, const Mat& v,
+                               const std::vector<double>& d_v, const BApply& b_apply, double tol) {
+    if (u.cols != Index(d_u.size()) || v.cols != Index(d_v.size()))
+        throw std::invalid_argument("add_low_rank: basis/diagonal size mismatch");
+    if (tol < 0.0) throw std::invalid_argument("add_low_rank: tol must be nonnegative");
+    if (v.cols == 0) return {u, d_u};
+    if (u.cols == 0) return {v, d_v};
+    const Index n = u.rows, ru = u.cols;
+    Mat bu(n, ru);
+    for (Index j = 0; j < ru; ++j) b_apply(u.col(j), bu.col(j));
+    BOrtho orth = b_orthonormalize_against(v, b_apply, u, bu);
+    const Index rv = orth.q.cols;
+    const Mat c = gemm_tn(bu, v);           // ru × kv
+    const Mat rh = gemm_tn(orth.bq, v);     // rv × kv
+    const Index nm = ru + rv, kv = v.cols;
+    Mat m(nm, nm);
+    auto zrow = [&](Index i, Index k) { return i < ru ? c(i, k) : rh(i - ru, k); };
+    for (Index j = 0; j < nm; ++j)
+        for (Index i = 0; i < nm; ++i) {
+            double sacc = 0.0;
+            for (Index k = 0; k < kv; ++k) sacc += zrow(i, k) * d_v[size_t(k)] * zrow(j, k);
+            m(i, j) = sacc + (i == j && i < ru ? d_u[size_t(i)] : 0.0);
+        }
+    for (Index j = 0; j < nm; ++j)
+        for (Index i = 0; i < j; ++i) m(i, j) = m(j, i) = 0.5 * (m(i, j) + m(j, i));
+    std::vector<double> ev;
+    Mat vec;
+    sym_eig(m, ev, vec);
+    double max_abs = 0.0;
+    for (double e : ev) max_abs = std::max(max_abs, std::fabs(e));
+    std::vector<Index> keep;
+    for (Index i = 0; i < nm; ++i)
+        if (std::fabs(ev[size_t(i)]) >= tol * max_abs && ev[size_t(i)] != 0.0) keep.push_back(i);
+    std::stable_sort(keep.begin(), keep.end(), [&](Index a, Index b) { return std::fabs(ev[size_t(a)]) > std::fabs(ev[size_t(b)]); });
+    LowRankSym out;
+    out.w = Mat(n, Index(keep.size()));
+    out.d.resize(keep.size());
+    for (size_t i = 0; i < keep.size(); ++i) {
+        out.d[i] = ev[size_t(keep[i])];
+        const double* e = vec.col(keep[i]);
+        double* o = out.w.col(Index(i));
+        for (Index k = 0; k < ru; ++k) axpy(e[k], u.col(k), o, n);
+        for (Index k = 0; k < rv; ++k) axpy(e[ru + k], orth.q.col(k), o, n);
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------- fast_filter.hpp:127-224 (extended filter)
+struct FekfOptions {  // :127-134
+    Index k_rank = -1;
+    Index oversampling = 20;
+    double trunc_tol = 1e-5;
+    int relinearizations = 1;
+    uint64_t seed = 0;
+};
+struct EState {  // LowRankState with its own W (fast_filter.hpp:21-37)
+    double alpha = 0.0;
+    int step = 0;
+    std::vector<double> mean, d;
+    Mat w;
+};
+inline EState fekf_step(const EState& st, Cov& cov, const Csr& h, const double* y, Index ylen, double sigma2,
+                        const BoxCox& t, const FekfOptions& opts) {
+    const Index n = cov.size();
+    if (h.cols != n || Index(st.mean.size()) != n || ylen != h.rows)
+        throw std::invalid_argument("fekf_step: dimension mismatch");
+    if (!(sigma2 > 0.0)) throw std::invalid_argument("fekf_step: sigma2 must be positive");
+    if (opts.relinearizations < 1 || opts.relinearizations > 5)
+        throw std::invalid_argument("fekf_step: relinearizations must lie in [1, 5]");
+    const double alpha = st.alpha + 1.0;
+    const Index r = Index(st.d.size());
+    std::vector<double> d_bar(static_cast<size_t>(r));
+    for (Index i = 0; i < r; ++i) {
+        if (!(st.d[size_t(i)] < alpha)) throw std::runtime_error("fekf_step: state diagonal exceeds alpha");
+        d_bar[size_t(i)] = st.d[size_t(i)] / (alpha * (alpha - st.d[size_t(i)]));
+    }
+    const Index m = h.rows;
+    std::vector<double> eta = st.mean;
+    Csr h_last;
+    for (int it = 0; it < opts.relinearizations; ++it) {  // :167-196
+        Csr hk;
+        std::vector<double> h_eta;
+        ekf_linearize(h, eta.data(), t, hk, h_eta);
+        Mat ght(n, m);  // ΓH_kᵀ column by column (:171-172)
+        {
+            std::vector<double> row(static_cast<size_t>(n));
+            for (Index i = 0; i < m; ++i) {
+                std::fill(row.begin(), row.end(), 0.0);
+                for (int e = hk.rowptr[size_t(i)]; e < hk.rowptr[size_t(i) + 1]; ++e) row[size_t(hk.col[size_t(e)])] = hk.val[size_t(e)];
+                cov.apply(row.data(), ght.col(i));
+            }
+        }
+        Mat hw(m, r);  // H_k W
+        for (Index j = 0; j < r; ++j) csr_mv(hk, st.w.col(j), hw.col(j));
+        Mat s(m, m);
+        for (Index j = 0; j < m; ++j) csr_mv(hk, ght.col(j), s.col(j));  // H_k ΓH_kᵀ
+        for (Index j = 0; j < m; ++j)
+            for (Index i = 0; i < m; ++i) {
+                double acc = alpha * s(i, j);
+                for (Index q = 0; q < r; ++q) acc -= hw(i, q) * st.d[size_t(q)] * hw(j, q);
+                s(i, j) = acc + (i == j ? sigma2 : 0.0);
+            }
+        for (Index j = 0; j < m; ++j)
+            for (Index i = 0; i < j; ++i) s(i, j) = s(j, i) = 0.5 * (s(i, j) + s(j, i));
+        if (!llt(s)) throw std::runtime_error("fekf_step: innovation system is singular");
+        std::vector<double> dm(static_cast<size_t>(n)), hdm(static_cast<size_t>(m)), z(static_cast<size_t>(m));
+        for (Index i = 0; i < n; ++i) dm[size_t(i)] = st.mean[size_t(i)] - eta[size_t(i)];
+        csr_mv(hk, dm.data(), hdm.data());
+        for (Index i = 0; i < m; ++i) z[size_t(i)] = y[i] - h_eta[size_t(i)] - hdm[size_t(i)];
+        llt_solve(s, z.data());
+        std::vector<double> eta_next(st.mean);
+        std::vector<double> gz(static_cast<size_t>(n));
+        gemv(ght, z.data(), gz.data());
+        axpy(alpha, gz.data(), eta_next.data(), n);
+        if (r > 0) {
+            std::vector<double> dc(static_cast<size_t>(r)), wdc(static_cast<size_t>(n));
+            for (Index q = 0; q < r; ++q) dc[size_t(q)] = st.d[size_t(q)] * dot(hw.col(q), z.data(), m);
+            gemv(st.w, dc.data(), wdc.data());
+            axpy(-1.0, wdc.data(), eta_next.data(), n);
+        }
+        std::vector<double> diff(static_cast<size_t>(n));
+        for (Index i = 0; i < n; ++i) diff[size_t(i)] = eta_next[size_t(i)] - eta[size_t(i)];
+        const double change = std::sqrt(dot(diff.data(), diff.data(), n));
+        h_last = std::move(hk);
+        eta = std::move(eta_next);
+        if (change <= 1e-6 * std::sqrt(dot(eta.data(), eta.data(), n))) break;
+    }
+    const Index k_rank = opts.k_rank < 0 ? m : opts.k_rank;  // :198-203
+    Gep gep = randomized_ghep(cov, h_last, sigma2, k_rank, opts.oversampling, opts.seed);
+    const BApply b_apply = [&cov](const double* x, double* out) { cov_solve(cov, x, out); };
+    LowRankSym sum = add_low_rank(st.w, d_bar, gep.u, gep.lambda, b_apply, opts.trunc_tol);
+    EState next;  // :210-222
+    next.alpha = alpha;
+    next.step = st.step + 1;
+    next.mean = std::move(eta);
+    std::vector<Index> keep;
+    for (Index i = 0; i < Index(sum.d.size()); ++i)
+        if (sum.d[size_t(i)] > 1e-14) keep.push_back(i);
+    next.w = Mat(n, Index(keep.size()));
+    next.d.resize(keep.size());
+    for (size_t i = 0; i < keep.size(); ++i) {
+        const double dhat = sum.d[size_t(keep[i])];
+        next.d[i] = alpha * alpha * dhat / (1.0 + alpha * dhat);
+        std::copy(sum.w.col(keep[i]), sum.w.col(keep[i]) + n, next.w.col(Index(i)));
+    }
+    return next;
+}
+
 }  // namespace orc
 
 // =================================================================== C API (ctypes)
@@ -874,6 +1148,9 @@ int guarded(F&& f) {
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return 1;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return 4;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 2;
@@ -1098,4 +1375,47 @@ int orc_realizations(void* f, uint64_t seed, int count, double* out) {
     });
 }
 
+}  // extern "C"
+
+// ---- extended filter (fast_filter.hpp:127-224), Box–Cox (boxcox.hpp), CG Γ⁻¹ (covariance.hpp:118-152)
+extern "C" {
+int orc_boxcox_map(double alpha, int which, const double* x, long long n, double* out) {
+    return guarded([&] { orc::BoxCox{alpha}.map(x, out, n, which); });
+}
+int orc_cov_solve(void* c, const double* b, double tol, double* x) {
+    return guarded([&] { orc::cov_solve(*static_cast<orc::Cov*>(c), b, x, tol); });
+}
+void* orc_fekf_create(long long n, const double* mean0) {
+    auto* st = new orc::EState;
+    st->mean.assign(mean0, mean0 + n);
+    st->w = orc::Mat(n, 0);
+    return st;
+}
+void orc_fekf_destroy(void* st) { delete static_cast<orc::EState*>(st); }
+int orc_fekf_step(void* st, void* cov, void* h, const double* y, long long ylen, double sigma2, double bc_alpha,
+                  long long k_rank, long long p, double trunc_tol, int relin, uint64_t seed) {
+    return guarded([&] {
+        orc::FekfOptions o;
+        o.k_rank = k_rank;
+        o.oversampling = p;
+        o.trunc_tol = trunc_tol;
+        o.relinearizations = relin;
+        o.seed = seed;
+        auto* s = static_cast<orc::EState*>(st);
+        *s = orc::fekf_step(*s, *static_cast<orc::Cov*>(cov), *static_cast<orc::Csr*>(h), y, ylen, sigma2,
+                            orc::BoxCox{bc_alpha}, o);
+    });
+}
+void orc_fekf_dims(void* st, double* alpha, int* step, long long* rank) {
+    auto* s = static_cast<orc::EState*>(st);
+    *alpha = s->alpha;
+    *step = s->step;
+    *rank = (long long)s->d.size();
+}
+void orc_fekf_read(void* st, double* mean, double* d, double* w) {
+    auto* s = static_cast<orc::EState*>(st);
+    std::copy(s->mean.begin(), s->mean.end(), mean);
+    std::copy(s->d.begin(), s->d.end(), d);
+    std::copy(s->w.a.begin(), s->w.a.end(), w);
+}
 }  // extern "C"

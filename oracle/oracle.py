@@ -83,6 +83,13 @@ def lib():
         "orc_trace_criterion": (_i, [_p, C.POINTER(_d)]),
         "orc_relative_entropy": (_i, [_p, C.POINTER(_d)]),
         "orc_realizations": (_i, [_p, _u64, _i, _dp]),
+        "orc_boxcox_map": (_i, [_d, _i, _dp, _ll, _dp]),
+        "orc_cov_solve": (_i, [_p, _dp, _d, _dp]),
+        "orc_fekf_create": (_p, [_ll, _dp]),
+        "orc_fekf_destroy": (None, [_p]),
+        "orc_fekf_step": (_i, [_p, _p, _p, _dp, _ll, _d, _d, _ll, _ll, _d, _i, _u64]),
+        "orc_fekf_dims": (None, [_p, C.POINTER(_d), C.POINTER(_i), C.POINTER(_ll)]),
+        "orc_fekf_read": (None, [_p, _dp, _dp, _dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -92,10 +99,16 @@ def lib():
     return L
 
 
+class DomainError(ValueError):
+    """std::domain_error (boxcox.hpp)."""
+
+
 def _raise(rc: int):
     msg = lib().orc_last_error().decode()
     if rc == 1:
         raise ValueError(msg)  # std::invalid_argument
+    if rc == 4:
+        raise DomainError(msg)  # std::domain_error
     raise RuntimeError(msg)  # std::runtime_error
 
 
@@ -369,3 +382,55 @@ class FastFilter:
         if rc:
             _raise(rc)
         return out.reshape(count, self.n).T
+
+
+# ---------------------------------------------------------------- extended filter
+def boxcox(alpha: float, x, which: str) -> np.ndarray:
+    """BoxCox::forward / inverse / derivative on a vector (boxcox.hpp:25-75)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    rc = lib().orc_boxcox_map(alpha, {"forward": 0, "inverse": 1, "derivative": 2}[which], x, x.size, out)
+    if rc:
+        _raise(rc)
+    return out
+
+
+def cov_solve(cov: CovarianceOperator, b, tol: float = 1e-12) -> np.ndarray:
+    """CovarianceOperator::solve by CG on the fast matvec (covariance.hpp:118-139)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty_like(b)
+    rc = lib().orc_cov_solve(cov._h, b, tol, x)
+    if rc:
+        _raise(rc)
+    return x
+
+
+class ExtendedFilter:
+    """LowRankState driven by fekf_step (fast_filter.hpp:127-224) from zero_start with a
+    given initial mean (driver.hpp:315-316)."""
+
+    def __init__(self, cov: CovarianceOperator, h: Csr, mean0):
+        self.cov, self.h = cov, h
+        mean0 = np.ascontiguousarray(mean0, dtype=np.float64)
+        self.n = mean0.size
+        self._s = lib().orc_fekf_create(self.n, mean0)
+
+    def __del__(self):
+        if getattr(self, "_s", None):
+            lib().orc_fekf_destroy(self._s)
+            self._s = None
+
+    def step(self, y, sigma2, bc_alpha, k_rank=-1, oversampling=20, trunc_tol=1e-5, relinearizations=1, seed=0):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        rc = lib().orc_fekf_step(self._s, self.cov._h, self.h._h, y, y.size, sigma2, bc_alpha, k_rank, oversampling,
+                                 trunc_tol, relinearizations, seed)
+        if rc:
+            _raise(rc)
+
+    def state(self):
+        a, st, r = _d(), _i(), _ll()
+        lib().orc_fekf_dims(self._s, C.byref(a), C.byref(st), C.byref(r))
+        mean, d, w = np.empty(self.n), np.empty(r.value), np.empty(self.n * r.value)
+        lib().orc_fekf_read(self._s, mean, d, w)
+        return {"alpha": a.value, "step": st.value, "mean": mean, "d": d,
+                "w": w.reshape(r.value, self.n).T if r.value else np.zeros((self.n, 0))}

@@ -292,14 +292,14 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
 }
 
 // --------------------------------------------------------------------------- host side
-static void check_nonneg_args(long long k, long long p, long long n) {  // lowrank.hpp:145-151
+void check_nonneg_args(long long k, long long p, long long n) {  // lowrank.hpp:145-151
     if (k < 0 || p < 0) throw std::invalid_argument("randomized_ghep: k and oversampling must be nonnegative");
     if (k + p > n)
         throw std::invalid_argument("randomized_ghep: k + oversampling = " + std::to_string(k + p) +
                                     " exceeds problem size " + std::to_string(n));
 }
 
-static std::vector<double> download(const double* p, size_t count, cudaStream_t s) {
+std::vector<double> download(const double* p, size_t count, cudaStream_t s) {
     std::vector<double> h(count);
     if (count) {
         FKB_CUDA(cudaMemcpyAsync(h.data(), p, count * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -307,12 +307,12 @@ static std::vector<double> download(const double* p, size_t count, cudaStream_t 
     }
     return h;
 }
-static void upload(double* p, const std::vector<double>& h, cudaStream_t s) {
+void upload(double* p, const std::vector<double>& h, cudaStream_t s) {
     if (!h.empty()) FKB_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s));
 }
 
 // Gram C = Aᵀ B for tall-skinny A (n×p), B (n×q) on DMMA with split-K
-static void gram_tn(long long n, int p, int q, const double* A, const double* B, double* C, DBuf<double>& ws,
+void gram_tn(long long n, int p, int q, const double* A, const double* B, double* C, DBuf<double>& ws,
                     cudaStream_t s) {
     GemmArgs g;
     g.M = p; g.N = q; g.K = int(n);
@@ -324,7 +324,7 @@ static void gram_tn(long long n, int p, int q, const double* A, const double* B,
     gram(g, ws.p, s);
 }
 // C (n×q) = A (n×p) · W (p×q), W on the device
-static void tall_times_small(long long n, int p, int q, const double* A, const double* W, double* C, cudaStream_t s) {
+void tall_times_small(long long n, int p, int q, const double* A, const double* W, double* C, cudaStream_t s) {
     GemmArgs g;
     g.M = int(n); g.N = q; g.K = p;
     g.A = A; g.lda = n;
@@ -335,7 +335,7 @@ static void tall_times_small(long long n, int p, int q, const double* A, const d
 
 // Symmetric eigen of a small device Gram: returns kept columns W = V·diag(w^{-1/2}) for
 // eigenvalues above tol·max (rank-revealing drop), ordered by ascending eigenvalue.
-static std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept) {
+std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept) {
     std::vector<double> G = Gh;
     for (int j = 0; j < p; ++j)
         for (int i = 0; i < j; ++i) G[size_t(i) + size_t(j) * p] = G[size_t(j) + size_t(i) * p] =
@@ -356,8 +356,17 @@ static std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, d
     return W;
 }
 
-void Filter::ghep(long long k, long long p, uint64_t seed) {
+void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double sigma2, long long k, long long p,
+                            uint64_t seed, DBuf<double>& ws, cudaStream_t s, GepDev& out) {
+    const long long n = cov->size();
+    const int m = H.rows;
     check_nonneg_args(k, p, n);
+    int& r = out.r;
+    int& kept_cols = out.kept_cols;
+    std::vector<double>& lambda_h = out.lambda_h;
+    DBuf<double>& lambda = out.lambda;
+    DBuf<double>& U = out.U;
+    DBuf<double>& Ubar = out.Ubar;
     r = 0;
     kept_cols = 0;
     lambda_h.clear();
@@ -445,6 +454,44 @@ void Filter::ghep(long long k, long long p, uint64_t seed) {
     FKB_CUDA(cudaStreamSynchronize(s));
 }
 
+void Filter::ghep(long long k, long long p, uint64_t seed) {
+    GepDev g;
+    randomized_ghep_device(cov, H, HT, sigma2, k, p, seed, ws, s, g);
+    r = g.r;
+    kept_cols = g.kept_cols;
+    lambda_h = std::move(g.lambda_h);
+    lambda = std::move(g.lambda);
+    U = std::move(g.U);
+    Ubar = std::move(g.Ubar);
+}
+
+// G = H·ΓHᵀ, symmetrized (fast_filter.hpp:68-72): ΓHᵀ streamed in column batches of ≤ 2²⁷/N
+// densified rows of H, never stored.
+void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s) {
+    const long long n = cov->size();
+    const int m = H.rows;
+    if (m <= 0) return;
+    const int bc = int(std::max<long long>(1, std::min<long long>(m, (1LL << 27) / std::max<long long>(n, 1))));
+    DBuf<double> Ec(size_t(n) * bc);
+    for (int c0 = 0; c0 < m; c0 += bc) {
+        const int nb = std::min(bc, m - c0);
+        FKB_CUDA(cudaMemsetAsync(Ec.p, 0, sizeof(double) * size_t(n) * nb, s));
+        k_densify_rows<<<dim3(1, nb), 128, 0, s>>>(H.rowptr.p, H.col.p, H.val.p, c0, nb, Ec.p, n);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        cov->apply(Ec.p, n, nb, Ec.p, n);
+        spmm(H, Ec.p, n, nb, G + (long long)c0 * m, m, 1.0, 0.0, s);
+    }
+    symmetrize(m, G, m, s);
+}
+
+void symmetrize(int n, double* A, long long lda, cudaStream_t s) {
+    if (n <= 1) return;
+    k_symmetrize<<<std::min(ceil_div((long long)n * n, 256), 4096), 256, 0, s>>>(A, n, lda);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
 Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, const double* val, double sig2,
                long long k, long long p, uint64_t seed)
     : cov(c), s(c->stream), n(c->size()), m(m_), sigma2(sig2) {
@@ -464,22 +511,7 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     ghep(k, p, seed);                                                                    // :63-66
     // G = H·ΓHᵀ, symmetrized (:68-72): ΓHᵀ streamed in column batches, never stored.
     G.alloc(size_t(std::max(m, 1)) * std::max(m, 1));
-    if (m > 0) {
-        const int bc = int(std::max<long long>(1, std::min<long long>(m, (1LL << 27) / std::max<long long>(n, 1))));
-        DBuf<double> Ec(size_t(n) * bc);
-        for (int c0 = 0; c0 < m; c0 += bc) {
-            const int nb = std::min(bc, m - c0);
-            FKB_CUDA(cudaMemsetAsync(Ec.p, 0, sizeof(double) * size_t(n) * nb, s));
-            k_densify_rows<<<dim3(1, nb), 128, 0, s>>>(H.rowptr.p, H.col.p, H.val.p, c0, nb, Ec.p, n);
-            FKB_LAUNCH_CHECK();
-            count_launch();
-            cov->apply(Ec.p, n, nb, Ec.p, n);
-            spmm(H, Ec.p, n, nb, G.p + (long long)c0 * m, m, 1.0, 0.0, s);
-        }
-        k_symmetrize<<<std::min(ceil_div((long long)m * m, 256), 4096), 256, 0, s>>>(G.p, m, m);
-        FKB_LAUNCH_CHECK();
-        count_launch();
-    }
+    build_hgh(cov, H, G.p, s);
     B.alloc(size_t(std::max(m, 1)) * std::max(r, 1));  // HU (:73)
     spmm(H, U.p, n, r, B.p, m, 1.0, 0.0, s);
     colsq.alloc(size_t(std::max(r, 1)));

@@ -12,6 +12,27 @@
 
 namespace fkb {
 
+// randomized_ghep (lowrank.hpp:132-213) with A = HᵀH/σ² and B = Γ on the device; U is
+// Γ⁻¹-orthonormal (N×r, column-major) and Ū = Γ⁻¹U comes with it.
+struct GepDev {
+    int r = 0, kept_cols = 0;
+    std::vector<double> lambda_h;
+    DBuf<double> lambda, U, Ubar;
+};
+void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double sigma2, long long k, long long p,
+                            uint64_t seed, DBuf<double>& ws, cudaStream_t s, GepDev& out);
+// G = H·Γ·Hᵀ (m×m, ld m), symmetrized
+void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s);
+void symmetrize(int n, double* A, long long lda, cudaStream_t s);
+// shared helpers (filter.cu)
+void check_nonneg_args(long long k, long long p, long long n);
+std::vector<double> download(const double* p, size_t count, cudaStream_t s);
+void upload(double* p, const std::vector<double>& h, cudaStream_t s);
+void gram_tn(long long n, int p, int q, const double* A, const double* B, double* C, DBuf<double>& ws,
+             cudaStream_t s);
+void tall_times_small(long long n, int p, int q, const double* A, const double* W, double* C, cudaStream_t s);
+std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept);
+
 struct Filter {
     Cov* cov = nullptr;
     cudaStream_t s = nullptr;

@@ -134,3 +134,46 @@ def csr_dense(h):
 def workload_inputs(name, steps=None):
     """BASELINE config inputs: (workload, H CsrMatrix (whitened for c3), ys, sigma2)."""
     return W.problem(name, steps)
+
+
+def boxcox_np(alpha, x, which):
+    """BoxCox (boxcox.hpp:25-50) restated in numpy (no domain checks)."""
+    x = np.asarray(x, dtype=np.float64)
+    if alpha == 1.0:
+        return {"forward": x - 1.0, "inverse": x + 1.0, "derivative": np.ones_like(x)}[which]
+    if which == "forward":
+        return alpha * (np.power(x, 1.0 / alpha) - 1.0)
+    base = (x + alpha) / alpha
+    return np.power(base, alpha) if which == "inverse" else np.power(base, alpha - 1.0)
+
+
+def dense_ekf(gamma, h_dense, obs, sigma2, bc_alpha, mean0, relinearizations=1):
+    """dense_ekf_step (dense_filter.hpp:68-106) restated in numpy, zero start with mean0."""
+    n = gamma.shape[0]
+    mean = np.array(mean0, dtype=np.float64)
+    cov = np.zeros((n, n))
+    out = []
+    for y in obs:
+        pred = cov + gamma
+        eta = mean.copy()
+        for _ in range(relinearizations):
+            hk = h_dense * boxcox_np(bc_alpha, eta, "derivative")[None, :]
+            h_eta = h_dense @ boxcox_np(bc_alpha, eta, "inverse")
+            hp = hk @ pred
+            s = hp @ hk.T + sigma2 * np.eye(hk.shape[0])
+            s = 0.5 * (s + s.T)
+            resid = y - h_eta - hk @ (mean - eta)
+            eta_next = mean + hp.T @ np.linalg.solve(s, resid)
+            change = np.linalg.norm(eta_next - eta)
+            eta = eta_next
+            if change <= 1e-6 * np.linalg.norm(eta):
+                break
+        mean = eta
+        cov = pred - hp.T @ np.linalg.solve(s, hp)
+        cov = 0.5 * (cov + cov.T)
+        out.append((mean.copy(), cov.copy()))
+    return out
+
+
+def low_rank_cov(alpha, w, d, gamma):  # oracles.hpp: Σ = αΓ − W·diag(d)·Wᵀ
+    return alpha * gamma - (w * d[None, :]) @ w.T
