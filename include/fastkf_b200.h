@@ -30,9 +30,11 @@ extern "C" {
 #define FKB_INVALID_ARGUMENT 1
 #define FKB_RUNTIME_ERROR 2
 #define FKB_CUDA_ERROR 3
+#define FKB_DOMAIN_ERROR 4 /* std::domain_error (Box-Cox maps, boxcox.hpp:58-75) */
 
 typedef struct fkb_cov fkb_cov;
 typedef struct fkb_filter fkb_filter;
+typedef struct fkb_ekf fkb_ekf;
 
 const char* fkb_last_error(void);
 unsigned long long fkb_launch_count(void); /* kernels launched by this library so far */
@@ -114,6 +116,27 @@ int fkb_realizations_device(fkb_filter* f, uint64_t seed, int count, double* d_o
 /* host buffers, one pass over U for both: out (N×count, may be null when count = 0) and var
  * (diag Σ, may be null) */
 int fkb_realizations_with_variance(fkb_filter* f, uint64_t seed, int count, double* out, double* var);
+
+/* ---- extended fast filter (fekf_step, fast_filter.hpp:127-224) --------------------- */
+/* Binds Γ and the ray operator H (the reference passes both to every fekf_step call,
+ * :142-144; all its callers keep them fixed, driver.hpp:305-333,555-580) and starts from
+ * LowRankState::zero_start with mean = 0.  The state (α, step, mean, W, d) and W̄ = Γ⁻¹W
+ * stay on the device. */
+int fkb_ekf_create(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val,
+                   fkb_ekf** out);
+void fkb_ekf_destroy(fkb_ekf* e);
+/* zero_start with the given initial mean (driver.hpp:315-316: mean = forward(init_slowness)) */
+int fkb_ekf_reset(fkb_ekf* e, const double* mean0);
+/* fekf_step with FekfOptions {k_rank (−1 = m), oversampling, trunc_tol, relinearizations,
+ * seed} (:127-134) and BoxCox{boxcox_alpha} (boxcox.hpp:14-17) */
+int fkb_ekf_step(fkb_ekf* e, const double* y, long long ylen, double sigma2, double boxcox_alpha, long long k_rank,
+                 long long oversampling, double trunc_tol, int relinearizations, uint64_t seed);
+/* state sizes: α, step count, rank r = W.cols() */
+int fkb_ekf_state(fkb_ekf* e, double* alpha, int* step, int* rank);
+/* host copies of mean (N), d (r), W (N×r column-major) and W̄ = Γ⁻¹W (N×r); any may be null */
+int fkb_ekf_read(fkb_ekf* e, double* mean, double* d, double* w, double* wbar);
+/* diagnostics of the last step: GHEP rank and relinearization sweeps run */
+int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps);
 
 /* ---- kernels exposed for parity tests / benchmarks (device pointers) ------------- */
 /* Y = H X (trans = 0) or Hᵀ X (trans = 1) with the filter's uploaded operator */

@@ -48,6 +48,13 @@ SIGNATURES = {
     "fkb_cov_stream": (_p, [_p]),
     "fkb_gaussian_matrix": (_i, [_ll, _i, _u64, _u64, _dp]),
     "fkb_fkf_init": (_i, [_p, _i, _i, _ip, _ip, _dp, _d, _ll, _ll, _u64, C.POINTER(_p)]),
+    "fkb_ekf_create": (_i, [_p, _i, _i, _ip, _ip, _dp, C.POINTER(_p)]),
+    "fkb_ekf_destroy": (None, [_p]),
+    "fkb_ekf_reset": (_i, [_p, _dp]),
+    "fkb_ekf_step": (_i, [_p, _dp, _ll, _d, _d, _ll, _ll, _d, _i, _u64]),
+    "fkb_ekf_state": (_i, [_p, C.POINTER(_d), C.POINTER(_i), C.POINTER(_i)]),
+    "fkb_ekf_read": (_i, [_p, _p, _p, _p, _p]),
+    "fkb_ekf_last": (_i, [_p, C.POINTER(_i), C.POINTER(_i)]),
     "fkb_filter_destroy": (None, [_p]),
     "fkb_filter_rank": (_i, [_p, _PI, _PI]),
     "fkb_filter_lambda": (_i, [_p, _dp]),
@@ -115,6 +122,10 @@ class CudaError(RuntimeError):
     pass
 
 
+class DomainError(ValueError):
+    """std::domain_error (the Box–Cox maps, boxcox.hpp:58-75)."""
+
+
 def check(rc: int):
     if rc == 0:
         return
@@ -123,6 +134,8 @@ def check(rc: int):
         raise ValueError(msg)
     if rc == 3:
         raise CudaError(msg)
+    if rc == 4:
+        raise DomainError(msg)
     raise RuntimeError(msg)
 
 

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../../include/fastkf_b200.h"
+#include "ekf.cuh"
 #include "filter.cuh"
 #include "host_linalg.h"
 
@@ -47,6 +48,10 @@ struct fkb_filter {
     fkb_cov* owner = nullptr;
     std::unique_ptr<fkb::Filter> f;
 };
+struct fkb_ekf {
+    fkb_cov* owner = nullptr;
+    std::unique_ptr<fkb::Ekf> e;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -59,6 +64,9 @@ int guarded(F&& fn) {
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return FKB_INVALID_ARGUMENT;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return FKB_DOMAIN_ERROR;
     } catch (const fkb::CudaError& e) {
         g_err = e.what();
         return FKB_CUDA_ERROR;
@@ -522,5 +530,73 @@ int fkb_d2h(void* dst, const void* src, size_t bytes) {
     });
 }
 int fkb_dsync(void) { return guarded([&] { FKB_CUDA(cudaDeviceSynchronize()); }); }
+
+
+int fkb_ekf_create(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val,
+                   fkb_ekf** out) {
+    return guarded([&] {
+        need(c, "cov");
+        need(out, "out");
+        need(rowptr, "rowptr");
+        *out = nullptr;
+        auto h = std::make_unique<fkb_ekf>();
+        h->owner = c;
+        h->e = std::make_unique<fkb::Ekf>(c->cov.get(), m, h_cols, rowptr, col, val);
+        *out = h.release();
+    });
+}
+void fkb_ekf_destroy(fkb_ekf* e) {
+    if (e && e->e && e->e->s) cudaStreamSynchronize(e->e->s);
+    delete e;
+}
+int fkb_ekf_reset(fkb_ekf* e, const double* mean0) {
+    return guarded([&] {
+        need(e, "ekf");
+        need(mean0, "mean0");
+        e->e->reset(mean0);
+    });
+}
+int fkb_ekf_step(fkb_ekf* e, const double* y, long long ylen, double sigma2, double boxcox_alpha, long long k_rank,
+                 long long oversampling, double trunc_tol, int relinearizations, uint64_t seed) {
+    return guarded([&] {
+        need(e, "ekf");
+        if (ylen != e->e->m) throw std::invalid_argument("fekf_step: dimension mismatch");  // :145-147
+        if (ylen) need(y, "y");
+        fkb::EkfOptions o;
+        o.k_rank = k_rank;
+        o.oversampling = oversampling;
+        o.trunc_tol = trunc_tol;
+        o.relinearizations = relinearizations;
+        o.seed = seed;
+        e->e->step(y, sigma2, boxcox_alpha, o);
+    });
+}
+int fkb_ekf_state(fkb_ekf* e, double* alpha, int* step, int* rank) {
+    return guarded([&] {
+        need(e, "ekf");
+        if (alpha) *alpha = e->e->alpha;
+        if (step) *step = e->e->step_no;
+        if (rank) *rank = e->e->r;
+    });
+}
+int fkb_ekf_read(fkb_ekf* e, double* mean, double* d, double* w, double* wbar) {
+    return guarded([&] {
+        need(e, "ekf");
+        auto& E = *e->e;
+        const size_t n = size_t(E.n), r = size_t(E.r);
+        if (mean) FKB_CUDA(cudaMemcpyAsync(mean, E.mean.p, sizeof(double) * n, cudaMemcpyDeviceToHost, E.s));
+        if (d && r) std::memcpy(d, E.d_h.data(), sizeof(double) * r);
+        if (w && r) FKB_CUDA(cudaMemcpyAsync(w, E.W.p, sizeof(double) * n * r, cudaMemcpyDeviceToHost, E.s));
+        if (wbar && r) FKB_CUDA(cudaMemcpyAsync(wbar, E.Wbar.p, sizeof(double) * n * r, cudaMemcpyDeviceToHost, E.s));
+        FKB_CUDA(cudaStreamSynchronize(E.s));
+    });
+}
+int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps) {
+    return guarded([&] {
+        need(e, "ekf");
+        if (gep_rank) *gep_rank = e->e->last_gep_rank;
+        if (sweeps) *sweeps = e->e->last_relin;
+    });
+}
 
 }  // extern "C"

@@ -12,7 +12,7 @@ import dataclasses
 
 import numpy as np
 
-from ._native import DeviceArray, check, lib, ptr
+from ._native import DeviceArray, DomainError, check, lib, ptr
 
 POWERED_EXPONENTIAL = 0
 MATERN = 1
@@ -403,6 +403,86 @@ class FkfContext:
         return dict(zip(keys, ms[: cnt.value].tolist()))
 
 
+@dataclasses.dataclass
+class FekfOptions:  # fast_filter.hpp:127-134
+    k_rank: int = -1  # −1: n_m
+    oversampling: int = 20
+    trunc_tol: float = 1e-5
+    relinearizations: int = 1
+    seed: int = 0
+
+
+@dataclasses.dataclass(frozen=True)
+class BoxCox:  # boxcox.hpp:14-17 (the maps run on the device inside fekf_step)
+    alpha: float = 1.0
+
+
+class ExtendedFilter:
+    """fekf_step (fast_filter.hpp:127-224) on a device-resident LowRankState.
+
+    Binds Γ (``cov``) and the ray operator ``h`` once (every reference caller keeps them
+    fixed across steps, driver.hpp:305-333); ``reset(mean0)`` is zero_start with the
+    initial mean of driver.hpp:315-316.  Besides W the state carries W̄ = Γ⁻¹W.
+    """
+
+    def __init__(self, cov: CovarianceOperator, h: CsrMatrix, mean0=None):
+        self.cov, self.h = cov, h
+        self.n, self.m = cov.size(), h.rows
+        e = C.c_void_p()
+        check(lib().fkb_ekf_create(cov._h, h.rows, h.cols, np.ascontiguousarray(h.rowptr, np.int32),
+                                   np.ascontiguousarray(h.col if len(h.col) else np.zeros(1, np.int32), np.int32),
+                                   np.ascontiguousarray(h.val if len(h.val) else np.zeros(1), np.float64),
+                                   C.byref(e)))
+        self._e = e
+        if mean0 is not None:
+            self.reset(mean0)
+
+    def __del__(self):
+        if getattr(self, "_e", None) and self._e.value:
+            lib().fkb_ekf_destroy(self._e)
+            self._e = None
+
+    def reset(self, mean0):
+        check(lib().fkb_ekf_reset(self._e, np.ascontiguousarray(np.broadcast_to(mean0, (self.n,)), np.float64)))
+
+    def step(self, y, sigma2: float, transform: BoxCox, opts: FekfOptions = FekfOptions()):
+        y = np.ascontiguousarray(y, np.float64)
+        check(lib().fkb_ekf_step(self._e, y, y.size, float(sigma2), float(transform.alpha), int(opts.k_rank),
+                                 int(opts.oversampling), float(opts.trunc_tol), int(opts.relinearizations),
+                                 int(opts.seed)))
+
+    def rank(self) -> int:
+        r = C.c_int()
+        check(lib().fkb_ekf_state(self._e, None, None, C.byref(r)))
+        return r.value
+
+    def state(self, with_w: bool = True):
+        a, st, r = C.c_double(), C.c_int(), C.c_int()
+        check(lib().fkb_ekf_state(self._e, C.byref(a), C.byref(st), C.byref(r)))
+        n, k = self.n, r.value
+        mean, d = np.empty(n), np.empty(k)
+        w = np.empty((k, n)) if with_w else None
+        wb = np.empty((k, n)) if with_w else None
+        check(lib().fkb_ekf_read(self._e, ptr(mean), ptr(d) if k else None, ptr(w) if with_w and k else None,
+                                 ptr(wb) if with_w and k else None))
+        out = {"alpha": a.value, "step": st.value, "mean": mean, "d": d}
+        if with_w:
+            out["w"] = w.T if k else np.zeros((n, 0))
+            out["wbar"] = wb.T if k else np.zeros((n, 0))
+        return out
+
+    def last_step_info(self):
+        g, sw = C.c_int(), C.c_int()
+        check(lib().fkb_ekf_last(self._e, C.byref(g), C.byref(sw)))
+        return {"gep_rank": g.value, "sweeps": sw.value}
+
+
+def fekf_step(filt: ExtendedFilter, y, sigma2, transform: BoxCox, opts: FekfOptions = FekfOptions()):
+    """Advances the extended filter's device state by one cycle (fast_filter.hpp:142-224)."""
+    filt.step(y, sigma2, transform, opts)
+    return filt.state()
+
+
 def fkf_init(cov, h, sigma2, k_rank, p_oversample, seed) -> FkfContext:
     return FkfContext(cov, h, sigma2, k_rank, p_oversample, seed)
 
@@ -427,4 +507,5 @@ def relative_entropy(ctx: FkfContext):
 
 __all__ = ["Grid", "KernelSpec", "kernel_eval", "next_smooth", "trace_ray", "SourceReceiverLayout", "CsrMatrix",
            "build_H", "sym_eig", "CovarianceOperator", "gaussian_matrix", "FkfContext", "fkf_init", "fkf_step",
-           "variance", "trace_criterion", "relative_entropy", "DeviceArray", "POWERED_EXPONENTIAL", "MATERN"]
+           "variance", "trace_criterion", "relative_entropy", "DeviceArray", "POWERED_EXPONENTIAL", "MATERN",
+           "FekfOptions", "BoxCox", "ExtendedFilter", "fekf_step", "DomainError"]
