@@ -57,6 +57,8 @@ int fkb_build_H(int nx, int ny, double lx, double ly, int n_src, const double* s
 /* small symmetric eigensolver used by the GHEP (stand-in for SelfAdjointEigenSolver,
  * lowrank.hpp:193): ascending eigenvalues w, eigenvectors Z (n×n column-major) */
 int fkb_sym_eig(int n, const double* A, double* w, double* Z);
+/* the same on the GPU (two-sided block Jacobi, eig.cu; ascending eigenvalues); *sweeps may be null */
+int fkb_sym_eig_device(int n, const double* A, double* w, double* Z, int* sweeps);
 
 /* ---- covariance operator Γ (CovarianceOperator FFT mode, covariance.hpp:69-353) ---- */
 /* constructor covariance.hpp:71-79 + build_fft :238-260 (padding loop, acceptance) */

@@ -48,6 +48,7 @@ SIGNATURES = {
     "fkb_cov_stream": (_p, [_p]),
     "fkb_gaussian_matrix": (_i, [_ll, _i, _u64, _u64, _dp]),
     "fkb_fkf_init": (_i, [_p, _i, _i, _ip, _ip, _dp, _d, _ll, _ll, _u64, C.POINTER(_p)]),
+    "fkb_sym_eig_device": (_i, [_i, _dp, _dp, _dp, C.POINTER(_i)]),
     "fkb_ekf_create": (_i, [_p, _i, _i, _ip, _ip, _dp, C.POINTER(_p)]),
     "fkb_ekf_destroy": (None, [_p]),
     "fkb_ekf_reset": (_i, [_p, _dp]),

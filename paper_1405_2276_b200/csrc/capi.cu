@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../../include/fastkf_b200.h"
+#include "eig.cuh"
 #include "ekf.cuh"
 #include "filter.cuh"
 #include "host_linalg.h"
@@ -130,6 +131,22 @@ int fkb_build_H(int nx, int ny, double lx, double ly, int n_src, const double* s
 
 int fkb_sym_eig(int n, const double* A, double* w, double* Z) {
     return guarded([&] { fkb::sym_eig_small(n, A, w, Z); });
+}
+int fkb_sym_eig_device(int n, const double* A, double* w, double* Z, int* sweeps) {
+    return guarded([&] {
+        if (n < 0) throw std::invalid_argument("sym_eig: negative size");
+        if (n == 0) return;
+        cudaStream_t s = nullptr;
+        FKB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct Guard { cudaStream_t s; ~Guard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } g{s};
+        fkb::DBuf<double> Ad(size_t(n) * n), th{size_t(n)}, V(size_t(n) * n);
+        FKB_CUDA(cudaMemcpyAsync(Ad.p, A, sizeof(double) * size_t(n) * n, cudaMemcpyHostToDevice, s));
+        const int sw = fkb::sym_eig_sorted_device(n, Ad.p, n, th.p, V.p, s);
+        if (sweeps) *sweeps = sw;
+        FKB_CUDA(cudaMemcpyAsync(w, th.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaMemcpyAsync(Z, V.p, sizeof(double) * size_t(n) * n, cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+    });
 }
 
 int fkb_cov_create(int nx, int ny, double lx, double ly, int family, double theta, double length, double power,

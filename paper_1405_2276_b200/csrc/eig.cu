@@ -291,4 +291,36 @@ int sym_eig_device(int m, double* A, long long lda, double* theta, double* V, cu
     return sweeps;
 }
 
+// gather eigenpairs into ascending order: θ_out[c] = θ[perm[c]], V_out[:, c] = V[:, perm[c]]
+__global__ void k_gather_pairs(int m, const int* __restrict__ perm, const double* __restrict__ th,
+                               const double* __restrict__ V, double* __restrict__ tho, double* __restrict__ Vo) {
+    const int c = blockIdx.y;
+    const int src = perm[c];
+    if (blockIdx.x == 0 && threadIdx.x == 0) tho[c] = th[src];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        Vo[i + (long long)c * m] = V[i + (long long)src * m];
+}
+
+int sym_eig_sorted_device(int m, double* A, long long lda, double* theta, double* V, cudaStream_t s, double tol,
+                          int max_sweeps) {
+    const int sw = sym_eig_device(m, A, lda, theta, V, s, tol, max_sweeps);
+    if (m <= 1) return sw;
+    std::vector<double> th(static_cast<size_t>(m));
+    FKB_CUDA(cudaMemcpyAsync(th.data(), theta, sizeof(double) * size_t(m), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> perm(static_cast<size_t>(m));
+    for (int i = 0; i < m; ++i) perm[size_t(i)] = i;
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return th[size_t(a)] < th[size_t(b)]; });
+    DBuf<int> pd(perm.size());
+    DBuf<double> tho{size_t(m)}, Vo(size_t(m) * m);
+    FKB_CUDA(cudaMemcpyAsync(pd.p, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice, s));
+    k_gather_pairs<<<dim3(ceil_div(m, 256), m), 256, 0, s>>>(m, pd.p, theta, V, tho.p, Vo.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    FKB_CUDA(cudaMemcpyAsync(theta, tho.p, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
+    FKB_CUDA(cudaMemcpyAsync(V, Vo.p, sizeof(double) * size_t(m) * m, cudaMemcpyDeviceToDevice, s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    return sw;
+}
+
 }  // namespace fkb

@@ -11,4 +11,9 @@ namespace fkb {
 int sym_eig_device(int m, double* A, long long lda, double* theta, double* V, cudaStream_t s, double tol = 1e-15,
                    int max_sweeps = 40);
 
+// The same, then eigenpairs sorted by ascending eigenvalue (θ, V reordered in place; A is
+// left diagonalized but unsorted).
+int sym_eig_sorted_device(int m, double* A, long long lda, double* theta, double* V, cudaStream_t s,
+                          double tol = 1e-15, int max_sweeps = 40);
+
 }  // namespace fkb

@@ -19,7 +19,10 @@
 //      follow :205-222.  W̄' = [W̄, V̂̄]·E is carried with W' = [W, V̂]·E.
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 #include <sstream>
@@ -94,6 +97,23 @@ __global__ void k_scale_columns(long long n, int p, double* A, const double* __r
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         A[i + (long long)j * n] *= sc[j];
 }
+
+// FKB_EKF_TRACE=1: per-phase wall times of each step on stderr (stream-synchronized)
+static bool ekf_trace() {
+    static const bool on = std::getenv("FKB_EKF_TRACE") != nullptr;
+    return on;
+}
+struct PhaseClock {
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void lap(const char* what) {
+        if (!ekf_trace()) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[ekf] %-18s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 static int grid_for(long long n) { return int(std::max<long long>(1, std::min<long long>((n + 255) / 256, 2048))); }
 
@@ -196,11 +216,14 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
     FKB_CUDA(cudaMemcpyAsync(eta.p, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, s));
     if (r > 0) HW.ensure(size_t(std::max(m, 1)) * r);
     last_relin = 0;
+    PhaseClock clk{s};
     for (int it = 0; it < o.relinearizations; ++it) {  // :163-196
         ++last_relin;
         linearize(a_bc);
+        clk.lap("linearize");
         if (m > 0) {
             build_hgh(cov, Hk, G.p, s);  // H_k Γ H_kᵀ (:171-176)
+            clk.lap("HkGHkT");
             if (r > 0) spmm(Hk, W.p, n, r, HW.p, m, 1.0, 0.0, s);  // H_k W (:173)
             GemmArgs g;  // S = αG_k − (H_kW) D (H_kW)ᵀ + σ²I (:175-178)
             g.M = m; g.N = m; g.K = r;
@@ -214,11 +237,13 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
             g.diag_add = sigma2;
             gemm(g, nullptr, s);
             symmetrize(m, S.p, m, s);
+            FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
             potrf_lower(m, S.p, m, info.p, nullptr, 0, s);  // LLT (:179-181)
             int h = 0;
             FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             FKB_CUDA(cudaStreamSynchronize(s));
             if (h) throw std::runtime_error("fekf_step: innovation system is singular");
+            clk.lap("S build + LLT");
             // z = S⁻¹(y − h(η) − H_k(mean − η)) (:183-184)
             k_sub<<<grid_for(n), 256, 0, s>>>(n, mean.p, eta.p, tv.p);
             FKB_LAUNCH_CHECK();
@@ -256,6 +281,7 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
         const double change = std::sqrt(sumsq(tv.p, n, ws.p, s));
         std::swap(eta, eta2);
         const double enorm = std::sqrt(sumsq(eta.p, n, ws.p, s));
+        clk.lap("mean update");
         if (change <= 1e-6 * enorm) break;
     }
     // GHEP of H_lastᵀH_last/σ² (:198-203); H_k holds the last linearization
@@ -263,7 +289,9 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
     GepDev g;
     randomized_ghep_device(cov, Hk, HkT, sigma2, k_rank, o.oversampling, o.seed, ws, s, g);
     last_gep_rank = g.r;
+    clk.lap("ghep");
     add_low_rank(d_bar, g, o.trunc_tol, a);
+    clk.lap("add_low_rank");
     std::swap(mean, eta);  // :212
     alpha = a;
     ++step_no;
@@ -271,6 +299,7 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
 
 void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, double a) {
     if (tol < 0.0) throw std::invalid_argument("add_low_rank: tol must be nonnegative");
+    PhaseClock ck{s};
     const int kv = g.r;
     std::vector<double> dsum;  // D̂ before the d̂ > 1e-14 filter (lowrank.hpp:248-249)
     DBuf<double> Wn, Wbn;
@@ -393,8 +422,9 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
             symmetrize(nm, Md.p, nm, s);
             FKB_CUDA(cudaStreamSynchronize(s));
         }
+        ck.lap("alr: project+core");
         std::vector<double> ev(static_cast<size_t>(nm)), vec(static_cast<size_t>(nm) * nm);
-        if (nm <= 1024) {
+        if (nm <= 2048) {  // host QL (ε-accurate); the device block Jacobi beyond
             std::vector<double> Mh = download(Md.p, size_t(nm) * nm, s);
             sym_eig_small(nm, Mh.data(), ev.data(), vec.data());
         } else {
@@ -403,6 +433,7 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
             ev = download(th.p, size_t(nm), s);
             vec = download(Vd.p, size_t(nm) * nm, s);
         }
+        ck.lap("alr: core eig");
         double max_abs = 0.0;
         for (double e : ev) max_abs = std::max(max_abs, std::fabs(e));
         std::vector<int> order;

@@ -3,7 +3,7 @@
 //  * build_H: straight-ray travel-time operator (tomography.hpp:29-146).  The survey
 //    keeps H construction on the host: it runs once, and the
 //    exact floating-point order of the reference decides cells on grid lines.
-//  * sym_eig_small: symmetric eigensolver for the ≤ 540×540 Gram/core matrices of
+//  * sym_eig_small: symmetric eigensolver for the Gram/core matrices of
 //    the randomized GHEP (lowrank.hpp:193 uses Eigen::SelfAdjointEigenSolver on the
 //    host too).  Householder tridiagonalization + implicit-shift QL, eigenvalues
 //    ascending with matching eigenvector columns.
@@ -114,116 +114,161 @@ void build_H(int nx, int ny, double lx, double ly, int ns, const double* src, in
 
 // --------------------------------------------------------------------------- small symmetric eig
 // A (n×n column-major, symmetric) → w ascending, Z eigenvectors (column j ↔ w[j]).
+// Householder tridiagonalization (unblocked, column-oriented: every inner loop runs down a
+// contiguous column; OpenMP over columns), explicit Q by backward accumulation, then
+// implicit-shift QL whose rotations are recorded per sweep and applied to Q by row chunks in
+// parallel.  The splitting test is relative to the neighbouring diagonal or to ‖T‖ (the
+// reduction is backward stable to ε‖A‖ only, so a graded tridiagonal can hold off-diagonals
+// at ε‖T‖ that never fall below ε(|d_m| + |d_m+1|)).
 void sym_eig_small(int n, const double* A, double* w, double* Z) {
-    std::vector<double> a(A, A + size_t(n) * n);  // working copy, becomes Q
-    std::vector<double> d(static_cast<size_t>(n)), e(static_cast<size_t>(n));
-    auto at = [&](int i, int j) -> double& { return a[size_t(i) + size_t(j) * n]; };
-    // Householder reduction to tridiagonal form, accumulating the orthogonal transform.
-    for (int i = n - 1; i > 0; --i) {
-        const int l = i - 1;
-        double h = 0.0, scale = 0.0;
-        if (l > 0) {
-            for (int k = 0; k <= l; ++k) scale += std::fabs(at(i, k));
-            if (scale == 0.0) {
-                e[size_t(i)] = at(i, l);
-            } else {
-                for (int k = 0; k <= l; ++k) {
-                    at(i, k) /= scale;
-                    h += at(i, k) * at(i, k);
-                }
-                double f = at(i, l);
-                double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
-                e[size_t(i)] = scale * g;
-                h -= f * g;
-                at(i, l) = f - g;
-                f = 0.0;
-                for (int j = 0; j <= l; ++j) {
-                    at(j, i) = at(i, j) / h;
-                    g = 0.0;
-                    for (int k = 0; k <= j; ++k) g += at(j, k) * at(i, k);
-                    for (int k = j + 1; k <= l; ++k) g += at(k, j) * at(i, k);
-                    e[size_t(j)] = g / h;
-                    f += e[size_t(j)] * at(i, j);
-                }
-                const double hh = f / (h + h);
-                for (int j = 0; j <= l; ++j) {
-                    f = at(i, j);
-                    e[size_t(j)] = g = e[size_t(j)] - hh * f;
-                    for (int k = 0; k <= j; ++k) at(j, k) -= (f * e[size_t(k)] + g * at(i, k));
-                }
-            }
-        } else {
-            e[size_t(i)] = at(i, l);
+    if (n <= 0) return;
+    const size_t N = size_t(n);
+    std::vector<double> a(A, A + N * N);
+    std::vector<double> d(N, 0.0), e(N, 0.0), tau(N, 0.0);
+    auto at = [&](int i, int j) -> double& { return a[size_t(i) + size_t(j) * N]; };
+    for (int j = 0; j < n; ++j)  // symmetrize into full storage from the lower triangle
+        for (int i = j + 1; i < n; ++i) at(j, i) = at(i, j);
+    const bool par = n >= 400;  // below this the OpenMP fork/join costs more than it saves
+    std::vector<double> p(N), wv(N);
+    for (int k = 0; k + 2 < n; ++k) {
+        // Householder v (v₀ = 1) with (I − τvvᵀ)x = βe₁ for x = A[k+1:, k]
+        double* x = &at(k + 1, k);
+        const int len = n - k - 1;
+        double sig = 0.0;
+        for (int i = 1; i < len; ++i) sig += x[i] * x[i];
+        const double x0 = x[0];
+        double t = 0.0, beta = x0;
+        if (sig != 0.0) {
+            const double mu = std::sqrt(x0 * x0 + sig);
+            beta = x0 <= 0.0 ? mu : -mu;
+            const double v0 = x0 - beta;
+            t = -v0 / beta;  // τ = (β − x₀)/β
+            for (int i = 1; i < len; ++i) x[i] /= v0;
         }
-        d[size_t(i)] = h;
-    }
-    d[0] = 0.0;
-    e[0] = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const int l = i - 1;
-        if (d[size_t(i)] != 0.0) {
-            for (int j = 0; j <= l; ++j) {
-                double g = 0.0;
-                for (int k = 0; k <= l; ++k) g += at(i, k) * at(k, j);
-                for (int k = 0; k <= l; ++k) at(k, j) -= g * at(k, i);
+        d[size_t(k)] = at(k, k);
+        e[size_t(k)] = beta;
+        tau[size_t(k)] = t;
+        x[0] = 1.0;  // v stored in place (v₀ = 1 explicitly during the update)
+        if (t != 0.0) {
+            // p = τ·A22·v (A22 symmetric, full storage: column sweeps)
+            const int o = k + 1;
+#pragma omp parallel for schedule(static) if (par)
+            for (int i = 0; i < len; ++i) {
+                const double* col = &at(o, o + i);  // A22[:, i] = A22[i, :]
+                double acc = 0.0;
+                for (int q = 0; q < len; ++q) acc += col[q] * x[q];
+                p[size_t(i)] = t * acc;
+            }
+            double pv = 0.0;
+            for (int i = 0; i < len; ++i) pv += p[size_t(i)] * x[i];
+            const double h = 0.5 * t * pv;
+            for (int i = 0; i < len; ++i) wv[size_t(i)] = p[size_t(i)] - h * x[i];
+            // A22 −= v wᵀ + w vᵀ
+#pragma omp parallel for schedule(static) if (par)
+            for (int j = 0; j < len; ++j) {
+                double* col = &at(o, o + j);
+                const double vj = x[j], wj = wv[size_t(j)];
+                for (int i = 0; i < len; ++i) col[i] -= x[i] * wj + wv[size_t(i)] * vj;
             }
         }
-        d[size_t(i)] = at(i, i);
-        at(i, i) = 1.0;
-        for (int j = 0; j <= l; ++j) at(j, i) = at(i, j) = 0.0;
     }
-    // Implicit-shift QL on the tridiagonal (d, e), rotating the columns of `a`.
-    for (int i = 1; i < n; ++i) e[size_t(i - 1)] = e[size_t(i)];
-    if (n > 0) e[size_t(n - 1)] = 0.0;
+    if (n >= 2) {
+        d[N - 2] = at(n - 2, n - 2);
+        e[N - 2] = at(n - 1, n - 2);
+    }
+    d[N - 1] = at(n - 1, n - 1);
+    // Q = H₀H₁…H_{n−3} by backward accumulation into q (column-major)
+    std::vector<double> q(N * N, 0.0);
+    auto qt = [&](int i, int j) -> double& { return q[size_t(i) + size_t(j) * N]; };
+    for (int i = 0; i < n; ++i) qt(i, i) = 1.0;
+    for (int k = n - 3; k >= 0; --k) {
+        const double t = tau[size_t(k)];
+        if (t == 0.0) continue;
+        const double* v = &at(k + 1, k);
+        const int o = k + 1, len = n - o;
+#pragma omp parallel for schedule(static) if (par)
+        for (int j = o; j < n; ++j) {
+            double* col = &qt(o, j);
+            double acc = 0.0;
+            for (int i = 0; i < len; ++i) acc += v[i] * col[i];
+            acc *= t;
+            for (int i = 0; i < len; ++i) col[i] -= acc * v[i];
+        }
+    }
+    // implicit-shift QL on (d, e); e[i] couples d[i] and d[i+1]
+    double tnorm = 0.0;
+    for (int i = 0; i < n; ++i) tnorm = std::max(tnorm, std::fabs(d[size_t(i)]) + std::fabs(e[size_t(i)]));
+    e[N - 1] = 0.0;
+    const double eps = 2.220446049250313e-16;
+    std::vector<double> rc(N), rs(N);
     for (int l = 0; l < n; ++l) {
         int iter = 0;
         int m;
         do {
             for (m = l; m < n - 1; ++m) {
                 const double dd = std::fabs(d[size_t(m)]) + std::fabs(d[size_t(m + 1)]);
-                if (std::fabs(e[size_t(m)]) <= 1e-300 + 2.220446049250313e-16 * dd) break;
+                const double em = std::fabs(e[size_t(m)]);
+                if (em <= 1e-300 + eps * dd || em <= 0.5 * eps * tnorm) break;
             }
             if (m != l) {
                 if (++iter > 60) throw std::runtime_error("sym_eig_small: QL iteration did not converge");
                 double g = (d[size_t(l + 1)] - d[size_t(l)]) / (2.0 * e[size_t(l)]);
                 double r = std::hypot(g, 1.0);
                 g = d[size_t(m)] - d[size_t(l)] + e[size_t(l)] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
-                double s = 1.0, c = 1.0, p = 0.0;
+                double sn = 1.0, c = 1.0, pp = 0.0;
                 int i;
+                int nrot = 0;
+                bool early = false;
                 for (i = m - 1; i >= l; --i) {
-                    double f = s * e[size_t(i)];
+                    double f = sn * e[size_t(i)];
                     const double b = c * e[size_t(i)];
                     e[size_t(i + 1)] = r = std::hypot(f, g);
                     if (r == 0.0) {
-                        d[size_t(i + 1)] -= p;
+                        d[size_t(i + 1)] -= pp;
                         e[size_t(m)] = 0.0;
+                        early = true;
                         break;
                     }
-                    s = f / r;
+                    sn = f / r;
                     c = g / r;
-                    g = d[size_t(i + 1)] - p;
-                    r = (d[size_t(i)] - g) * s + 2.0 * c * b;
-                    d[size_t(i + 1)] = g + (p = s * r);
+                    g = d[size_t(i + 1)] - pp;
+                    r = (d[size_t(i)] - g) * sn + 2.0 * c * b;
+                    d[size_t(i + 1)] = g + (pp = sn * r);
                     g = c * r - b;
-                    for (int k = 0; k < n; ++k) {
-                        f = at(k, i + 1);
-                        at(k, i + 1) = s * at(k, i) + c * f;
-                        at(k, i) = c * at(k, i) - s * f;
+                    rc[size_t(nrot)] = c;
+                    rs[size_t(nrot)] = sn;
+                    ++nrot;
+                }
+                // rotations (i = m−1 … l) on columns (i, i+1) of Q, row chunks in parallel
+                const int i_first = m - 1;
+#pragma omp parallel for schedule(static) if (par && nrot > 16)
+                for (int k0 = 0; k0 < n; k0 += 64) {
+                    const int k1 = std::min(n, k0 + 64);
+                    for (int t2 = 0; t2 < nrot; ++t2) {
+                        const int ii = i_first - t2;
+                        const double cc = rc[size_t(t2)], ss = rs[size_t(t2)];
+                        double* c0 = &qt(0, ii);
+                        double* c1 = &qt(0, ii + 1);
+                        for (int k = k0; k < k1; ++k) {
+                            const double f = c1[k];
+                            c1[k] = ss * c0[k] + cc * f;
+                            c0[k] = cc * c0[k] - ss * f;
+                        }
                     }
                 }
-                if (r == 0.0 && i >= l) continue;
-                d[size_t(l)] -= p;
+                if (early) continue;
+                d[size_t(l)] -= pp;
                 e[size_t(l)] = g;
                 e[size_t(m)] = 0.0;
             }
         } while (m != l);
     }
-    std::vector<int> order(static_cast<size_t>(n));
+    std::vector<int> order(N);
     for (int i = 0; i < n; ++i) order[size_t(i)] = i;
     std::sort(order.begin(), order.end(), [&](int x, int y) { return d[size_t(x)] < d[size_t(y)]; });
     for (int j = 0; j < n; ++j) {
         w[j] = d[size_t(order[size_t(j)])];
-        for (int i = 0; i < n; ++i) Z[size_t(i) + size_t(j) * n] = at(i, order[size_t(j)]);
+        std::copy(&qt(0, order[size_t(j)]), &qt(0, order[size_t(j)]) + n, Z + size_t(j) * N);
     }
 }
 

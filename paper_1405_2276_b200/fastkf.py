@@ -158,6 +158,17 @@ def sym_eig(a: np.ndarray):
     return w, Z.reshape(n, n).T
 
 
+def sym_eig_device(a: np.ndarray):
+    """The same on the GPU (block Jacobi, eig.cu): (ascending eigenvalues, eigenvectors, sweeps)."""
+    n = a.shape[0]
+    A = np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).ravel()
+    w = np.empty(n)
+    Z = np.empty(n * n)
+    sw = C.c_int()
+    check(lib().fkb_sym_eig_device(n, A, w, Z, C.byref(sw)))
+    return w, Z.reshape(n, n).T, sw.value
+
+
 # ------------------------------------------------------------------ covariance.hpp (FFT mode)
 class CovarianceOperator:
     """CovarianceOperator(grid, spec, CovMode::fft) — covariance.hpp:69-353 on the GPU."""
@@ -506,6 +517,6 @@ def relative_entropy(ctx: FkfContext):
 
 
 __all__ = ["Grid", "KernelSpec", "kernel_eval", "next_smooth", "trace_ray", "SourceReceiverLayout", "CsrMatrix",
-           "build_H", "sym_eig", "CovarianceOperator", "gaussian_matrix", "FkfContext", "fkf_init", "fkf_step",
+           "build_H", "sym_eig", "sym_eig_device", "CovarianceOperator", "gaussian_matrix", "FkfContext", "fkf_init", "fkf_step",
            "variance", "trace_criterion", "relative_entropy", "DeviceArray", "POWERED_EXPONENTIAL", "MATERN",
            "FekfOptions", "BoxCox", "ExtendedFilter", "fekf_step", "DomainError"]
