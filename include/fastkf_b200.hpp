@@ -7,7 +7,8 @@
 //   90-126), build_H (:130-146), GepResult (lowrank.hpp:26-31), randomized_ghep specialised to
 //   A = HᵀH/σ² (lowrank.hpp:208-213 with fast_filter.hpp:63-66), FkfContext/fkf_init
 //   (fast_filter.hpp:42-75), LowRankState/fkf_step (:21-37, :84-125), variance /
-//   trace_criterion / relative_entropy (uq.hpp:16-53).
+//   trace_criterion / relative_entropy (uq.hpp:16-53), BoxCox/FekfOptions/fekf_step
+//   (boxcox.hpp:14-17, fast_filter.hpp:127-224).
 // Eigen is not required: Vector/Matrix/SparseRowMatrix are thin column-major stand-ins with
 // the subset of API callers use (SURVEY.md §8b caveat 2).  Error codes map back to
 // std::invalid_argument (1) and std::runtime_error (2, 3).
@@ -35,6 +36,7 @@ inline void check(int rc) {
     if (rc == FKB_OK) return;
     const std::string msg = fkb_last_error();
     if (rc == FKB_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    if (rc == FKB_DOMAIN_ERROR) throw std::domain_error(msg);
     throw std::runtime_error(msg);
 }
 }  // namespace detail
@@ -199,6 +201,18 @@ struct GepResult {  // lowrank.hpp:26-31
     Index rank() const { return lambda.size(); }
 };
 
+namespace detail {
+struct EkfDevice {  // device-resident extended-filter state (W, W̄ = Γ⁻¹W) behind fekf_step
+    fkb_ekf* e = nullptr;
+    const void* cov = nullptr;
+    const void* h = nullptr;
+    long long generation = 0;
+    ~EkfDevice() {
+        if (e) fkb_ekf_destroy(e);
+    }
+};
+}  // namespace detail
+
 struct LowRankState {  // fast_filter.hpp:21-37 (W ≡ U lives on the device)
     double alpha = 0.0;
     Vector d;
@@ -206,7 +220,16 @@ struct LowRankState {  // fast_filter.hpp:21-37 (W ≡ U lives on the device)
     int step = 0;
     const void* token = nullptr;  // context whose device state this mirrors ...
     long long generation = -1;    // ... at this generation of that context
+    // extended filter (fekf_step): W and Γ⁻¹W stay on the device; w() downloads W
+    std::shared_ptr<detail::EkfDevice> ekf;
+    long long ekf_generation = -1;
     Index rank() const { return d.size(); }
+    Matrix w() const {
+        if (!ekf) throw std::invalid_argument("LowRankState::w: W is held by the filter context (W = U)");
+        Matrix W(mean.size(), rank());
+        if (rank()) detail::check(fkb_ekf_read(ekf->e, nullptr, nullptr, W.data(), nullptr));
+        return W;
+    }
     static LowRankState zero_start(Index n) {
         LowRankState s;
         s.mean = Vector::Zero(n);
@@ -306,6 +329,58 @@ inline double relative_entropy(const LowRankState& state, FkfContext& ctx) {
     double v = 0.0;
     detail::check(fkb_relative_entropy(ctx.handle(), &v));
     return v;
+}
+
+// ---- extended fast filter (fast_filter.hpp:127-224, boxcox.hpp:14-17)
+struct BoxCox {
+    double alpha = 1.0;
+};
+enum class GhepMode { two_pass, single_pass };
+struct FekfOptions {  // fast_filter.hpp:127-134
+    Index k_rank = -1;
+    Index oversampling = 20;
+    double trunc_tol = 1e-5;
+    int relinearizations = 1;
+    GhepMode mode = GhepMode::two_pass;
+    std::uint64_t seed = 0;
+};
+
+// fekf_step (fast_filter.hpp:142-224).  Value semantics as the reference: a new state is
+// returned.  States produced by this function keep W and Γ⁻¹W on the device (shared handle);
+// a rank-0 state (zero_start with any mean) starts a new device filter.  A state is stepped in
+// place when it is the latest one of its device filter, otherwise it is rejected (W̄ = Γ⁻¹W of an
+// older state is no longer held).
+inline LowRankState fekf_step(const LowRankState& state, const CovarianceOperator& cov, const SparseRowMatrix& h,
+                              const Vector& y, double sigma2, const BoxCox& transform, const FekfOptions& opts) {
+    if (h.cols() != cov.size() || state.mean.size() != cov.size() || y.size() != h.rows())
+        throw std::invalid_argument("fekf_step: dimension mismatch");
+    if (opts.mode != GhepMode::two_pass)
+        throw std::invalid_argument("fekf_step: only the two-pass GHEP is provided on the GPU");
+    std::shared_ptr<detail::EkfDevice> dev = state.ekf;
+    const bool live = dev && dev->cov == cov.handle() && dev->h == &h && state.ekf_generation == dev->generation;
+    if (!live) {
+        if (state.rank() != 0)
+            throw std::invalid_argument("fekf_step: a state with W must be the latest state of its device filter");
+        if (state.alpha != 0.0 || state.step != 0)
+            throw std::invalid_argument("fekf_step: a fresh device filter starts from zero_start (alpha = 0)");
+        dev = std::make_shared<detail::EkfDevice>();
+        detail::check(fkb_ekf_create(cov.handle(), h.m, h.n, h.rowptr.data(), h.col.empty() ? nullptr : h.col.data(),
+                                     h.val.empty() ? nullptr : h.val.data(), &dev->e));
+        dev->cov = cov.handle();
+        dev->h = &h;
+        detail::check(fkb_ekf_reset(dev->e, state.mean.data()));
+    }
+    detail::check(fkb_ekf_step(dev->e, y.data(), y.size(), sigma2, transform.alpha, opts.k_rank, opts.oversampling,
+                               opts.trunc_tol, opts.relinearizations, opts.seed));
+    LowRankState next;
+    int rank = 0;
+    detail::check(fkb_ekf_state(dev->e, &next.alpha, &next.step, &rank));
+    next.d = Vector(rank);
+    next.mean = Vector(state.mean.size());
+    detail::check(fkb_ekf_read(dev->e, next.mean.data(), rank ? next.d.data() : nullptr, nullptr, nullptr));
+    next.ekf = dev;
+    next.ekf_generation = ++dev->generation;
+    return next;
 }
 
 }  // namespace fastkf

@@ -20,10 +20,13 @@ def _pair(p, mean0):
     return cov, g, o
 
 
-def _compare(p, gs, os_, tol):
+def _compare(p, gs, os_, tol, mean0=None):
     gam = p.gamma()
     assert gs["alpha"] == os_["alpha"] and gs["step"] == os_["step"]
     e_mean = rel_err(gs["mean"], os_["mean"])
+    if mean0 is not None:  # the update itself (the means sit on a large constant offset)
+        e_inc = rel_err(gs["mean"] - mean0, os_["mean"] - mean0)
+        assert e_inc < tol, e_inc
     e_cov = rel_err(low_rank_cov(gs["alpha"], gs["w"], gs["d"], gam), low_rank_cov(os_["alpha"], os_["w"], os_["d"], gam))
     assert e_mean < tol, e_mean
     assert e_cov < tol, e_cov
@@ -57,7 +60,7 @@ def test_fekf_matches_oracle(case):
                                                           relinearizations=relin, seed=seed))
         o.step(y, p.sigma2, bc, k_rank=m, oversampling=20, trunc_tol=tol, relinearizations=relin, seed=seed)
         gs, os_ = g.state(), o.state()
-        _compare(p, gs, os_, 1e-8)
+        _compare(p, gs, os_, 1e-9, mean0)
         # carried W̄ = Γ⁻¹W and Γ⁻¹-orthonormality of W
         if gs["w"].shape[1]:
             gam = p.gamma()
@@ -92,7 +95,7 @@ def test_fekf_dense_ekf_mid_size():
         g.step(y, p.sigma2, P.BoxCox(3.0), P.FekfOptions(k_rank=48, trunc_tol=0.0, relinearizations=3, seed=seed))
         o.step(y, p.sigma2, 3.0, k_rank=48, trunc_tol=0.0, relinearizations=3, seed=seed)
         gs = g.state()
-        _compare(p, gs, o.state(), 1e-8)
+        _compare(p, gs, o.state(), 1e-9, mean0)
         assert rel_err(gs["mean"], dm) < 1e-6
 
 
