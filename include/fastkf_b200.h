@@ -35,6 +35,7 @@ extern "C" {
 typedef struct fkb_cov fkb_cov;
 typedef struct fkb_filter fkb_filter;
 typedef struct fkb_ekf fkb_ekf;
+typedef struct fkb_enkf fkb_enkf;
 
 const char* fkb_last_error(void);
 unsigned long long fkb_launch_count(void); /* kernels launched by this library so far */
@@ -139,6 +140,19 @@ int fkb_ekf_state(fkb_ekf* e, double* alpha, int* step, int* rank);
 int fkb_ekf_read(fkb_ekf* e, double* mean, double* d, double* w, double* wbar);
 /* diagnostics of the last step: GHEP rank and relinearization sweeps run */
 int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps);
+
+/* ---- ensemble Kalman filter (enkf.hpp:15-94) ---------------------------------------- */
+/* enkf_init (:30-34: n_members ≥ 2, all members zero) bound to Γ and H; members stay on the
+ * device (n×n_members column-major). */
+int fkb_enkf_init(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val,
+                  int n_members, fkb_enkf** out);
+void fkb_enkf_destroy(fkb_enkf* e);
+/* enkf_step (:49-94): forecast draws (seed, 1), perturbations (seed, 2) */
+int fkb_enkf_step(fkb_enkf* e, const double* y, long long ylen, double sigma2, uint64_t seed);
+/* Ensemble::members download / upload (n×n_members column-major), Ensemble::mean (:20) */
+int fkb_enkf_members(fkb_enkf* e, double* out);
+int fkb_enkf_set_members(fkb_enkf* e, const double* in);
+int fkb_enkf_mean(fkb_enkf* e, double* out);
 
 /* ---- kernels exposed for parity tests / benchmarks (device pointers) ------------- */
 /* Y = H X (trans = 0) or Hᵀ X (trans = 1) with the filter's uploaded operator */

@@ -1135,6 +1135,91 @@ inline EState fekf_step(const EState& st, Cov& cov, const Csr& h, const double* 
     return next;
 }
 
+
+// ---------------------------------------------------------------- enkf.hpp:43-94 (perturbed-observation EnKF)
+inline void enkf_step(Mat& members, const Csr& h, const double* y, Index ylen, Cov& cov, double sigma2,
+                      uint64_t seed) {
+    const Index n = members.rows, ne = members.cols;
+    if (ne < 2) throw std::invalid_argument("enkf_step: ensemble size must be at least 2");
+    if (h.cols != n || ylen != h.rows) throw std::invalid_argument("enkf_step: dimension mismatch");
+    if (sigma2 < 0.0) throw std::invalid_argument("enkf_step: sigma2 must be nonnegative");
+    const uint64_t seed_forecast = derive_seed(seed, 1), seed_perturb = derive_seed(seed, 2);  // :61-62
+    const Index m = h.rows;
+    {  // forecast increments (:64-70), pairs in parallel (independent streams)
+        const Index np = (ne + 1) / 2;
+#pragma omp parallel for schedule(dynamic)
+        for (Index j2 = 0; j2 < np; ++j2) {
+            std::vector<double> a(static_cast<size_t>(n)), b(static_cast<size_t>(n));
+            cov.sample_pair(seed_forecast, uint64_t(j2), a.data(), b.data());
+            axpy(1.0, a.data(), members.col(2 * j2), n);
+            if (2 * j2 + 1 < ne) axpy(1.0, b.data(), members.col(2 * j2 + 1), n);
+        }
+    }
+    Mat hm(m, ne);
+#pragma omp parallel for schedule(static)
+    for (Index j = 0; j < ne; ++j) csr_mv(h, members.col(j), hm.col(j));  // :72
+    std::vector<double> mmean(static_cast<size_t>(n), 0.0), hmean(static_cast<size_t>(m), 0.0);  // :73-74
+    for (Index j = 0; j < ne; ++j) {
+        axpy(1.0, members.col(j), mmean.data(), n);
+        axpy(1.0, hm.col(j), hmean.data(), m);
+    }
+    for (auto& v : mmean) v /= double(ne);
+    for (auto& v : hmean) v /= double(ne);
+    Mat dev(n, ne), hdev(m, ne);  // :75-76
+    for (Index j = 0; j < ne; ++j) {
+        for (Index i = 0; i < n; ++i) dev(i, j) = members(i, j) - mmean[size_t(i)];
+        for (Index i = 0; i < m; ++i) hdev(i, j) = hm(i, j) - hmean[size_t(i)];
+    }
+    Mat cyy(m, m);  // :78-80
+    {
+        Mat hdt(ne, m);
+        for (Index j = 0; j < ne; ++j)
+            for (Index i = 0; i < m; ++i) hdt(j, i) = hdev(i, j);
+#pragma omp parallel for schedule(static)
+        for (Index b = 0; b < m; ++b)
+            for (Index a = 0; a < m; ++a) cyy(a, b) = dot(hdt.col(a), hdt.col(b), ne) / double(ne - 1);
+    }
+    for (Index i = 0; i < m; ++i) cyy(i, i) += sigma2;
+    for (Index b = 0; b < m; ++b)
+        for (Index a = 0; a < b; ++a) cyy(a, b) = cyy(b, a) = 0.5 * (cyy(a, b) + cyy(b, a));
+    if (!llt(cyy))  // :81-85
+        throw std::runtime_error("enkf_step: sample innovation covariance is singular even with observation noise added");
+    // innovations (:89-96) solved in place: Z = C_yy⁻¹ (y + σ v_j − Hm_j)
+    Mat z(m, ne);
+    const double sigma = std::sqrt(sigma2);
+#pragma omp parallel for schedule(static)
+    for (Index j = 0; j < ne; ++j) {
+        double* c = z.col(j);
+        if (sigma2 > 0.0) {
+            gaussian_vector(m, seed_perturb, uint64_t(j), c);
+            for (Index i = 0; i < m; ++i) c[i] = y[i] + sigma * c[i] - hm(i, j);
+        } else {
+            for (Index i = 0; i < m; ++i) c[i] = y[i] - hm(i, j);
+        }
+        llt_solve(cyy, c);
+    }
+    // members += C_sy Z, C_sy = dev·hdevᵀ/(ne − 1) (:87, :97)
+    Mat csy(n, m);
+#pragma omp parallel for schedule(static)
+    for (Index b = 0; b < m; ++b) {
+        double* c = csy.col(b);
+        for (Index j = 0; j < ne; ++j) {
+            const double w = hdev(b, j) / double(ne - 1);
+            const double* d = dev.col(j);
+            for (Index i = 0; i < n; ++i) c[i] += d[i] * w;
+        }
+    }
+#pragma omp parallel for schedule(static)
+    for (Index j = 0; j < ne; ++j) {
+        double* x = members.col(j);
+        for (Index b = 0; b < m; ++b) {
+            const double w = z(b, j);
+            const double* c = csy.col(b);
+            for (Index i = 0; i < n; ++i) x[i] += c[i] * w;
+        }
+    }
+}
+
 }  // namespace orc
 
 // =================================================================== C API (ctypes)
@@ -1417,5 +1502,18 @@ void orc_fekf_read(void* st, double* mean, double* d, double* w) {
     std::copy(s->mean.begin(), s->mean.end(), mean);
     std::copy(s->d.begin(), s->d.end(), d);
     std::copy(s->w.a.begin(), s->w.a.end(), w);
+}
+}  // extern "C"
+
+extern "C" {
+// enkf_step (enkf.hpp:43-94) on a column-major n×ne member block, in place
+int orc_enkf_step(double* members, long long n, long long ne, void* h, const double* y, long long ylen, void* cov,
+                  double sigma2, uint64_t seed) {
+    return guarded([&] {
+        orc::Mat x(n, ne);
+        std::copy(members, members + n * ne, x.a.begin());
+        orc::enkf_step(x, *static_cast<orc::Csr*>(h), y, ylen, *static_cast<orc::Cov*>(cov), sigma2, seed);
+        std::copy(x.a.begin(), x.a.end(), members);
+    });
 }
 }  // extern "C"

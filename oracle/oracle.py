@@ -90,6 +90,7 @@ def lib():
         "orc_fekf_step": (_i, [_p, _p, _p, _dp, _ll, _d, _d, _ll, _ll, _d, _i, _u64]),
         "orc_fekf_dims": (None, [_p, C.POINTER(_d), C.POINTER(_i), C.POINTER(_ll)]),
         "orc_fekf_read": (None, [_p, _dp, _dp, _dp]),
+        "orc_enkf_step": (_i, [_dp, _ll, _ll, _p, _dp, _ll, _p, _d, _u64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -434,3 +435,16 @@ class ExtendedFilter:
         lib().orc_fekf_read(self._s, mean, d, w)
         return {"alpha": a.value, "step": st.value, "mean": mean, "d": d,
                 "w": w.reshape(r.value, self.n).T if r.value else np.zeros((self.n, 0))}
+
+
+# ---------------------------------------------------------------- EnKF (enkf.hpp)
+def enkf_step(members, h: Csr, y, cov: CovarianceOperator, sigma2: float, seed: int) -> np.ndarray:
+    """enkf_step (enkf.hpp:43-94): returns the new n×ne member matrix."""
+    x = np.asfortranarray(np.array(members, dtype=np.float64))
+    n, ne = x.shape
+    buf = np.ascontiguousarray(x.T).ravel()  # column-major flat
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    rc = lib().orc_enkf_step(buf, n, ne, h._h, y, y.size, cov._h, sigma2, seed)
+    if rc:
+        _raise(rc)
+    return buf.reshape(ne, n).T.copy()

@@ -49,6 +49,12 @@ SIGNATURES = {
     "fkb_gaussian_matrix": (_i, [_ll, _i, _u64, _u64, _dp]),
     "fkb_fkf_init": (_i, [_p, _i, _i, _ip, _ip, _dp, _d, _ll, _ll, _u64, C.POINTER(_p)]),
     "fkb_sym_eig_device": (_i, [_i, _dp, _dp, _dp, C.POINTER(_i)]),
+    "fkb_enkf_init": (_i, [_p, _i, _i, _ip, _ip, _dp, _i, C.POINTER(_p)]),
+    "fkb_enkf_destroy": (None, [_p]),
+    "fkb_enkf_step": (_i, [_p, _dp, _ll, _d, _u64]),
+    "fkb_enkf_members": (_i, [_p, _dp]),
+    "fkb_enkf_set_members": (_i, [_p, _dp]),
+    "fkb_enkf_mean": (_i, [_p, _dp]),
     "fkb_ekf_create": (_i, [_p, _i, _i, _ip, _ip, _dp, C.POINTER(_p)]),
     "fkb_ekf_destroy": (None, [_p]),
     "fkb_ekf_reset": (_i, [_p, _dp]),

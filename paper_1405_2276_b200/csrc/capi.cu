@@ -11,6 +11,7 @@
 #include "../../include/fastkf_b200.h"
 #include "eig.cuh"
 #include "ekf.cuh"
+#include "enkf.cuh"
 #include "filter.cuh"
 #include "host_linalg.h"
 
@@ -52,6 +53,10 @@ struct fkb_filter {
 struct fkb_ekf {
     fkb_cov* owner = nullptr;
     std::unique_ptr<fkb::Ekf> e;
+};
+struct fkb_enkf {
+    fkb_cov* owner = nullptr;
+    std::unique_ptr<fkb::Enkf> e;
 };
 
 namespace {
@@ -613,6 +618,61 @@ int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps) {
         need(e, "ekf");
         if (gep_rank) *gep_rank = e->e->last_gep_rank;
         if (sweeps) *sweeps = e->e->last_relin;
+    });
+}
+
+
+int fkb_enkf_init(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val,
+                  int n_members, fkb_enkf** out) {
+    return guarded([&] {
+        need(c, "cov");
+        need(out, "out");
+        need(rowptr, "rowptr");
+        *out = nullptr;
+        auto h = std::make_unique<fkb_enkf>();
+        h->owner = c;
+        h->e = std::make_unique<fkb::Enkf>(c->cov.get(), m, h_cols, rowptr, col, val, n_members);
+        *out = h.release();
+    });
+}
+void fkb_enkf_destroy(fkb_enkf* e) {
+    if (e && e->e && e->e->s) cudaStreamSynchronize(e->e->s);
+    delete e;
+}
+int fkb_enkf_step(fkb_enkf* e, const double* y, long long ylen, double sigma2, uint64_t seed) {
+    return guarded([&] {
+        need(e, "enkf");
+        if (ylen != e->e->m) throw std::invalid_argument("enkf_step: dimension mismatch");  // enkf.hpp:53-54
+        if (ylen) need(y, "y");
+        e->e->step(y, sigma2, seed);
+    });
+}
+int fkb_enkf_members(fkb_enkf* e, double* out) {
+    return guarded([&] {
+        need(e, "enkf");
+        need(out, "out");
+        auto& E = *e->e;
+        FKB_CUDA(cudaMemcpyAsync(out, E.X.p, E.X.bytes(), cudaMemcpyDeviceToHost, E.s));
+        FKB_CUDA(cudaStreamSynchronize(E.s));
+    });
+}
+int fkb_enkf_set_members(fkb_enkf* e, const double* in) {
+    return guarded([&] {
+        need(e, "enkf");
+        need(in, "in");
+        auto& E = *e->e;
+        FKB_CUDA(cudaMemcpyAsync(E.X.p, in, E.X.bytes(), cudaMemcpyHostToDevice, E.s));
+        FKB_CUDA(cudaStreamSynchronize(E.s));
+    });
+}
+int fkb_enkf_mean(fkb_enkf* e, double* out) {
+    return guarded([&] {
+        need(e, "enkf");
+        need(out, "out");
+        auto& E = *e->e;
+        E.member_mean(E.mean.p);
+        FKB_CUDA(cudaMemcpyAsync(out, E.mean.p, sizeof(double) * size_t(E.n), cudaMemcpyDeviceToHost, E.s));
+        FKB_CUDA(cudaStreamSynchronize(E.s));
     });
 }
 

@@ -450,11 +450,15 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
 
 // Sampler pass 1: draw amp·(n_re + i n_im) on the torus for a tile of ky columns,
 // inverse FFT along x, keep ix < nx → T[ky][ix] (full ky range).
+// blockIdx.y = pair p of a batch: streams (seed, 2(sid0+p)) and (seed, 2(sid0+p)+1), T offset by p·my·nx
 __global__ void __launch_bounds__(kThreads) k_sampler_cols(const double* __restrict__ amp, int my, int nx,
-                                                          FftLen fx, uint64_t st_re, uint64_t st_im,
+                                                          FftLen fx, uint64_t seed, uint64_t sid0,
                                                           double2* __restrict__ T, int kt) {
     extern __shared__ double2 sm[];
     const int mx = fx.n;
+    const uint64_t sid = sid0 + blockIdx.y;
+    const uint64_t st_re = splitmix64(seed ^ splitmix64(2 * sid)), st_im = splitmix64(seed ^ splitmix64(2 * sid + 1));
+    T += (long long)blockIdx.y * my * nx;
     double2* a = sm;
     double2* b = sm + kt * mx;
     const int ky0 = blockIdx.x * kt;
@@ -479,11 +483,18 @@ __global__ void __launch_bounds__(kThreads) k_sampler_cols(const double* __restr
 }
 
 // Sampler pass 2: per row ix, inverse c2c FFT along y, crop, Re → a, Im → b (×1/√M).
+// blockIdx.y = pair p: outputs da + p·ld_pair, db + p·ld_pair (db skipped when 2p+1 ≥ ncols);
+// accumulate: add into the outputs instead of storing
 __global__ void __launch_bounds__(kThreads) k_sampler_rows(const double2* __restrict__ T, int nx, int ny,
                                                           FftLen fy, double* __restrict__ da,
-                                                          double* __restrict__ db, int rows, double scale) {
+                                                          double* __restrict__ db, int rows, double scale,
+                                                          long long ld_pair, int ncols, int accumulate) {
     extern __shared__ double2 sm[];
     const int my = fy.n;
+    const int p = blockIdx.y;
+    T += (long long)p * my * nx;
+    da += p * ld_pair;
+    db = 2 * p + 1 < ncols ? db + p * ld_pair : nullptr;
     double2* a = sm;
     double2* b = sm + rows * my;
     const int ix0 = blockIdx.x * rows;
@@ -499,8 +510,14 @@ __global__ void __launch_bounds__(kThreads) k_sampler_rows(const double2* __rest
         const int ix = ix0 + t;
         if (ix < nx) {
             const double2 v = f[t * my + iy];
-            da[(long long)ix * ny + iy] = v.x * scale;
-            db[(long long)ix * ny + iy] = v.y * scale;
+            const long long o = (long long)ix * ny + iy;
+            if (accumulate) {
+                da[o] += v.x * scale;
+                if (db) db[o] += v.y * scale;
+            } else {
+                da[o] = v.x * scale;
+                if (db) db[o] = v.y * scale;
+            }
         }
     }
 }
@@ -809,14 +826,36 @@ void Cov::sample_pair(uint64_t seed, uint64_t sid, double* da, double* db) {
     const int rows = std::max(1, std::min(4, 4096 / my));
     set_smem((const void*)k_sampler_cols, smem_bytes(kt, mx));
     set_smem((const void*)k_sampler_rows, smem_bytes(rows, my));
-    const uint64_t st_re = derive_seed_host(seed, 2 * sid), st_im = derive_seed_host(seed, 2 * sid + 1);
-    k_sampler_cols<<<ceil_div(my, kt), kThreads, smem_bytes(kt, mx), stream>>>(amp_full.p, my, nx, fx, st_re, st_im,
+    k_sampler_cols<<<ceil_div(my, kt), kThreads, smem_bytes(kt, mx), stream>>>(amp_full.p, my, nx, fx, seed, sid,
                                                                              work.p, kt);
     FKB_LAUNCH_CHECK();
-    k_sampler_rows<<<ceil_div(nx, rows), kThreads, smem_bytes(rows, my), stream>>>(work.p, nx, ny, fy, da, db, rows,
-                                                                                   1.0 / std::sqrt(double(M())));
+    k_sampler_rows<<<ceil_div(nx, rows), kThreads, smem_bytes(rows, my), stream>>>(
+        work.p, nx, ny, fy, da, db, rows, 1.0 / std::sqrt(double(M())), 0, 2, 0);
     FKB_LAUNCH_CHECK();
     count_launch(2);
+}
+
+void Cov::sample_pairs_add(uint64_t seed, uint64_t sid0, double* X, long long ldx, int ncols) {
+    if (ncols <= 0) return;
+    const int kt = kt_for(mx);
+    const int rows = std::max(1, std::min(4, 4096 / my));
+    set_smem((const void*)k_sampler_cols, smem_bytes(kt, mx));
+    set_smem((const void*)k_sampler_rows, smem_bytes(rows, my));
+    const int npairs = (ncols + 1) / 2;
+    const size_t per = size_t(my) * size_t(nx);
+    const int bp = int(std::max<size_t>(1, std::min<size_t>(npairs, (size_t(1) << 26) / per)));  // ≤ 1 GiB
+    if (swork.n < per * size_t(bp)) swork.alloc(per * size_t(bp));
+    for (int p0 = 0; p0 < npairs; p0 += bp) {
+        const int np = std::min(bp, npairs - p0);
+        k_sampler_cols<<<dim3(ceil_div(my, kt), np), kThreads, smem_bytes(kt, mx), stream>>>(
+            amp_full.p, my, nx, fx, seed, sid0 + uint64_t(p0), swork.p, kt);
+        FKB_LAUNCH_CHECK();
+        double* xa = X + (long long)(2 * p0) * ldx;
+        k_sampler_rows<<<dim3(ceil_div(nx, rows), np), kThreads, smem_bytes(rows, my), stream>>>(
+            swork.p, nx, ny, fy, xa, xa + ldx, rows, 1.0 / std::sqrt(double(M())), 2 * ldx, ncols - 2 * p0, 1);
+        FKB_LAUNCH_CHECK();
+        count_launch(2);
+    }
 }
 
 }  // namespace fkb

@@ -28,6 +28,7 @@ struct Cov {
     DBuf<double> spec_half;  // [ky][kx], clipped ≥ 0 (covariance.hpp:295)
     DBuf<double> amp_full;   // √spectrum on the full torus, row-major mx×my (sampler :339)
     DBuf<double2> work;      // intermediate [col][ky][ix]
+    DBuf<double2> swork;     // batched sampler intermediate [pair][ky][ix]
     int batch_cap = 0;
     long long applies = 0;
 
@@ -45,6 +46,9 @@ struct Cov {
     void apply1_inv(double* dy, const double* acc_coef, const int* gate, int ncols = 1, long long ldy = 0);
     // Two N(0,Γ) draws (covariance.hpp:332-353) into device vectors.
     void sample_pair(uint64_t seed, uint64_t stream_id, double* da, double* db);
+    // X[:, j] += draw j of the pairs (seed, sid0 + j/2) (Re → even j, Im → odd j), j < ncols
+    // (the EnKF forecast, enkf.hpp:67-72), batched over pairs.
+    void sample_pairs_add(uint64_t seed, uint64_t sid0, double* X, long long ldx, int ncols);
     // Host copy of the full clipped spectrum (covariance.hpp:207-211), row-major mx×my.
     std::vector<double> spectrum_host() const;
 

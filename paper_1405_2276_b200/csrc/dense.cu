@@ -671,4 +671,82 @@ void potrs_lower(int n, const double* L, long long lda, double* x, int* flags, c
     count_launch(2);
 }
 
+// --------------------------------------------------------------------------- multi-RHS potrs
+// Diagonal-block solve for nrhs right-hand sides: the kb×kb block of L at (k0, k0) in shared
+// memory, 32 RHS columns per CTA staged transposed; one thread per column substitutes
+// sequentially (forward L·y = b, or backward Lᵀ·x = y when TRANS).
+constexpr int TRC = 16;  // right-hand sides per CTA of the multi-RHS diagonal solve
+template <bool TRANS>
+__global__ void __launch_bounds__(256) k_trsm_diag(const double* __restrict__ L, long long lda, int k0, int kb,
+                                                  double* __restrict__ B, long long ldb, int nrhs) {
+    __shared__ double D[CNB][CNB + 1];
+    __shared__ double Y[TRC][CNB + 1];
+    const int c0 = blockIdx.x * TRC;
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+        const int i = e % kb, j = e / kb;
+        D[i][j] = L[(k0 + i) + (long long)(k0 + j) * lda];
+    }
+    for (int e = threadIdx.x; e < TRC * kb; e += blockDim.x) {
+        const int i = e % kb, c = e / kb;
+        Y[c][i] = c0 + c < nrhs ? B[(k0 + i) + (long long)(c0 + c) * ldb] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < TRC) {
+        double* y = Y[threadIdx.x];
+        if (!TRANS) {
+            for (int i = 0; i < kb; ++i) {
+                double v = y[i];
+                for (int k = 0; k < i; ++k) v = fma(-D[i][k], y[k], v);
+                y[i] = v / D[i][i];
+            }
+        } else {
+            for (int i = kb - 1; i >= 0; --i) {
+                double v = y[i];
+                for (int k = i + 1; k < kb; ++k) v = fma(-D[k][i], y[k], v);
+                y[i] = v / D[i][i];
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < TRC * kb; e += blockDim.x) {
+        const int i = e % kb, c = e / kb;
+        if (c0 + c < nrhs) B[(k0 + i) + (long long)(c0 + c) * ldb] = Y[c][i];
+    }
+}
+
+void potrs_lower_multi(int n, const double* L, long long lda, double* B, long long ldb, int nrhs, cudaStream_t s) {
+    if (n <= 0 || nrhs <= 0) return;
+    const int nblk = ceil_div(n, CNB);
+    for (int b = 0; b < nblk; ++b) {  // L·Y = B, trailing updates on DMMA
+        const int k0 = b * CNB, kb = std::min(CNB, n - k0), k1 = k0 + kb;
+        k_trsm_diag<false><<<ceil_div(nrhs, TRC), 256, 0, s>>>(L, lda, k0, kb, B, ldb, nrhs);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        if (k1 < n) {
+            GemmArgs g;
+            g.M = n - k1; g.N = nrhs; g.K = kb;
+            g.A = L + k1 + (long long)k0 * lda; g.lda = lda;
+            g.B = B + k0; g.ldb = ldb;
+            g.alpha = -1.0; g.beta = 1.0;
+            g.C = B + k1; g.ldc = ldb;
+            gemm(g, nullptr, s);
+        }
+    }
+    for (int b = nblk - 1; b >= 0; --b) {  // Lᵀ·X = Y
+        const int k0 = b * CNB, kb = std::min(CNB, n - k0);
+        k_trsm_diag<true><<<ceil_div(nrhs, TRC), 256, 0, s>>>(L, lda, k0, kb, B, ldb, nrhs);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        if (k0 > 0) {
+            GemmArgs g;  // X[0:k0] −= L[k0:k1, 0:k0]ᵀ · X[k0:k1]
+            g.M = k0; g.N = nrhs; g.K = kb;
+            g.A = L + k0; g.lda = lda; g.transA = 1;
+            g.B = B + k0; g.ldb = ldb;
+            g.alpha = -1.0; g.beta = 1.0;
+            g.C = B; g.ldc = ldb;
+            gemm(g, nullptr, s);
+        }
+    }
+}
+
 }  // namespace fkb

@@ -51,5 +51,8 @@ void potrf_lower(int n, double* A, long long lda, int* info, double* ws, size_t 
 size_t potrf_ws_elems(int n);
 // Solves L Lᵀ x = b in place (x on entry holds b).  flags: device int[2·ceil(n/64)].
 void potrs_lower(int n, const double* L, long long lda, double* x, int* flags, cudaStream_t s);
+// The same for nrhs right-hand sides B (n×nrhs, ldb), blocked: 64×64 diagonal solves plus
+// DMMA trailing updates.
+void potrs_lower_multi(int n, const double* L, long long lda, double* B, long long ldb, int nrhs, cudaStream_t s);
 
 }  // namespace fkb

@@ -485,6 +485,13 @@ void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s) {
     symmetrize(m, G, m, s);
 }
 
+void transpose_cm(long long n, int r, const double* in, double* out, cudaStream_t s) {
+    if (n <= 0 || r <= 0) return;
+    k_transpose<<<dim3(ceil_div(n, 32), ceil_div(r, 32)), dim3(32, 8), 0, s>>>(n, r, in, out);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
 void symmetrize(int n, double* A, long long lda, cudaStream_t s) {
     if (n <= 1) return;
     k_symmetrize<<<std::min(ceil_div((long long)n * n, 256), 4096), 256, 0, s>>>(A, n, lda);

@@ -24,6 +24,8 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
 // G = H·Γ·Hᵀ (m×m, ld m), symmetrized
 void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s);
 void symmetrize(int n, double* A, long long lda, cudaStream_t s);
+// out (r×n column-major, i.e. row-major n×r) = in (n×r column-major)ᵀ
+void transpose_cm(long long n, int r, const double* in, double* out, cudaStream_t s);
 // shared helpers (filter.cu)
 void check_nonneg_args(long long k, long long p, long long n);
 std::vector<double> download(const double* p, size_t count, cudaStream_t s);

@@ -494,6 +494,66 @@ def fekf_step(filt: ExtendedFilter, y, sigma2, transform: BoxCox, opts: FekfOpti
     return filt.state()
 
 
+class Ensemble:
+    """Ensemble (enkf.hpp:15-28) resident on the GPU and bound to Γ and H: ``enkf_init``
+    (:30-34) at construction, ``step`` = enkf_step (:49-94)."""
+
+    def __init__(self, cov: CovarianceOperator, h: CsrMatrix, n_members: int):
+        self.cov, self.h = cov, h
+        self.n, self.m, self.n_members = cov.size(), h.rows, int(n_members)
+        e = C.c_void_p()
+        check(lib().fkb_enkf_init(cov._h, h.rows, h.cols, np.ascontiguousarray(h.rowptr, np.int32),
+                                  np.ascontiguousarray(h.col if len(h.col) else np.zeros(1, np.int32), np.int32),
+                                  np.ascontiguousarray(h.val if len(h.val) else np.zeros(1), np.float64),
+                                  self.n_members, C.byref(e)))
+        self._e = e
+
+    def __del__(self):
+        if getattr(self, "_e", None) and self._e.value:
+            lib().fkb_enkf_destroy(self._e)
+            self._e = None
+
+    def size(self) -> int:
+        return self.n_members
+
+    def step(self, y, sigma2: float, seed: int):
+        y = np.ascontiguousarray(y, np.float64)
+        check(lib().fkb_enkf_step(self._e, y, y.size, float(sigma2), int(seed)))
+
+    @property
+    def members(self) -> np.ndarray:  # n × N_e
+        out = np.empty(self.n * self.n_members)
+        check(lib().fkb_enkf_members(self._e, out))
+        return out.reshape(self.n_members, self.n).T
+
+    @members.setter
+    def members(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (self.n, self.n_members):
+            raise ValueError("ensemble: members must be n × N_e")
+        check(lib().fkb_enkf_set_members(self._e, np.ascontiguousarray(x.T).ravel()))
+
+    def mean(self) -> np.ndarray:
+        out = np.empty(self.n)
+        check(lib().fkb_enkf_mean(self._e, out))
+        return out
+
+    def covariance(self) -> np.ndarray:  # enkf.hpp:22-25 (host; desk scale)
+        x = self.members
+        dev = x - x.mean(axis=1, keepdims=True)
+        return dev @ dev.T / (self.n_members - 1)
+
+
+def enkf_init(cov, h, n_members) -> Ensemble:
+    return Ensemble(cov, h, n_members)
+
+
+def enkf_step(ens: Ensemble, y, sigma2, seed) -> Ensemble:
+    """Advances the device ensemble by one cycle (enkf.hpp:49-94)."""
+    ens.step(y, sigma2, seed)
+    return ens
+
+
 def fkf_init(cov, h, sigma2, k_rank, p_oversample, seed) -> FkfContext:
     return FkfContext(cov, h, sigma2, k_rank, p_oversample, seed)
 
@@ -519,4 +579,5 @@ def relative_entropy(ctx: FkfContext):
 __all__ = ["Grid", "KernelSpec", "kernel_eval", "next_smooth", "trace_ray", "SourceReceiverLayout", "CsrMatrix",
            "build_H", "sym_eig", "sym_eig_device", "CovarianceOperator", "gaussian_matrix", "FkfContext", "fkf_init", "fkf_step",
            "variance", "trace_criterion", "relative_entropy", "DeviceArray", "POWERED_EXPONENTIAL", "MATERN",
-           "FekfOptions", "BoxCox", "ExtendedFilter", "fekf_step", "DomainError"]
+           "FekfOptions", "BoxCox", "ExtendedFilter", "fekf_step", "DomainError", "Ensemble", "enkf_init",
+           "enkf_step"]
