@@ -8,7 +8,8 @@
 //   A = HᵀH/σ² (lowrank.hpp:208-213 with fast_filter.hpp:63-66), FkfContext/fkf_init
 //   (fast_filter.hpp:42-75), LowRankState/fkf_step (:21-37, :84-125), variance /
 //   trace_criterion / relative_entropy (uq.hpp:16-53), BoxCox/FekfOptions/fekf_step
-//   (boxcox.hpp:14-17, fast_filter.hpp:127-224).
+//   (boxcox.hpp:14-17, fast_filter.hpp:127-224), Field/write_field/read_field/write_state/
+//   read_state (field_io.hpp:18-135).
 // Eigen is not required: Vector/Matrix/SparseRowMatrix are thin column-major stand-ins with
 // the subset of API callers use (SURVEY.md §8b caveat 2).  Error codes map back to
 // std::invalid_argument (1) and std::runtime_error (2, 3).
@@ -18,7 +19,9 @@
 // upload, otherwise it is uploaded first (so arbitrary user-constructed states still work).
 #pragma once
 
+#include <bit>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -223,8 +226,10 @@ struct LowRankState {  // fast_filter.hpp:21-37 (W ≡ U lives on the device)
     // extended filter (fekf_step): W and Γ⁻¹W stay on the device; w() downloads W
     std::shared_ptr<detail::EkfDevice> ekf;
     long long ekf_generation = -1;
+    Matrix w_host;  // W of a state read from a FKS1 file (read_state)
     Index rank() const { return d.size(); }
     Matrix w() const {
+        if (w_host.cols() == rank() && w_host.rows() == mean.size() && (rank() || !ekf)) return w_host;
         if (!ekf) throw std::invalid_argument("LowRankState::w: W is held by the filter context (W = U)");
         Matrix W(mean.size(), rank());
         if (rank()) detail::check(fkb_ekf_read(ekf->e, nullptr, nullptr, W.data(), nullptr));
@@ -381,6 +386,107 @@ inline LowRankState fekf_step(const LowRankState& state, const CovarianceOperato
     next.ekf = dev;
     next.ekf_generation = ++dev->generation;
     return next;
+}
+
+// ---- field_io.hpp: FKF1 field and FKS1 state snapshots (little-endian, host I/O)
+static_assert(std::endian::native == std::endian::little,
+              "field formats are little-endian; big-endian hosts are unsupported");  // field_io.hpp:15-16
+struct Field {
+    int nx = 0;
+    int ny = 0;
+    Vector data;
+};
+
+namespace detail {
+inline std::FILE* open_file(const std::string& path, const char* mode) {
+    std::FILE* f = std::fopen(path.c_str(), mode);
+    if (!f) throw std::runtime_error(std::string(mode[0] == 'w' ? "cannot open for writing: " : "cannot open for reading: ") + path);
+    return f;
+}
+struct FileCloser {
+    std::FILE* f;
+    ~FileCloser() {
+        if (f) std::fclose(f);
+    }
+};
+inline void write_bytes(std::FILE* f, const void* p, size_t n, const std::string& path) {
+    if (n && std::fwrite(p, 1, n, f) != n) throw std::runtime_error("write failed: " + path);
+}
+inline void read_bytes(std::FILE* f, void* p, size_t n, const std::string& path) {
+    if (n && std::fread(p, 1, n, f) != n) throw std::runtime_error("truncated file: " + path);
+}
+}  // namespace detail
+
+// write_field field_io.hpp:66-79: "FKF1", uint32 nx, uint32 ny, nx·ny float64 (x-major)
+inline void write_field(const std::string& path, int nx, int ny, const Vector& data) {
+    if (data.size() != static_cast<Index>(nx) * ny)
+        throw std::invalid_argument("write_field: data length does not match " + std::to_string(nx) + "x" +
+                                    std::to_string(ny));
+    detail::FileCloser c{detail::open_file(path, "wb")};
+    const std::uint32_t dims[2] = {std::uint32_t(nx), std::uint32_t(ny)};
+    detail::write_bytes(c.f, "FKF1", 4, path);
+    detail::write_bytes(c.f, dims, sizeof dims, path);
+    detail::write_bytes(c.f, data.data(), sizeof(double) * size_t(data.size()), path);
+}
+
+// read_field field_io.hpp:81-95
+inline Field read_field(const std::string& path) {
+    detail::FileCloser c{detail::open_file(path, "rb")};
+    char magic[4] = {0, 0, 0, 0};
+    if (std::fread(magic, 1, 4, c.f) != 4 || std::string(magic, 4) != "FKF1")
+        throw std::runtime_error("not a FKF1 field file: " + path);
+    std::uint32_t dims[2];
+    detail::read_bytes(c.f, dims, sizeof dims, path);
+    Field f;
+    f.nx = int(dims[0]);
+    f.ny = int(dims[1]);
+    if (f.nx < 1 || f.ny < 1 || static_cast<long long>(f.nx) * f.ny > (1LL << 31))
+        throw std::runtime_error("implausible field dimensions in " + path);
+    f.data = Vector(Index(f.nx) * f.ny);
+    detail::read_bytes(c.f, f.data.data(), sizeof(double) * size_t(f.data.size()), path);
+    return f;
+}
+
+// write_state field_io.hpp:100-113: "FKS1", uint32 n, uint32 r, uint32 step, float64 α,
+// mean (n), D (r), W (n·r column-major).  W is fetched from the device only here.
+inline void write_state(const std::string& path, const LowRankState& state, const Matrix& w) {
+    if (w.rows() != state.mean.size() || w.cols() != state.rank())
+        throw std::invalid_argument("write_state: W does not match the state");
+    detail::FileCloser c{detail::open_file(path, "wb")};
+    const std::uint32_t hdr[3] = {std::uint32_t(state.mean.size()), std::uint32_t(state.rank()),
+                                  std::uint32_t(state.step)};
+    detail::write_bytes(c.f, "FKS1", 4, path);
+    detail::write_bytes(c.f, hdr, sizeof hdr, path);
+    detail::write_bytes(c.f, &state.alpha, sizeof(double), path);
+    detail::write_bytes(c.f, state.mean.data(), sizeof(double) * size_t(state.mean.size()), path);
+    detail::write_bytes(c.f, state.d.data(), sizeof(double) * size_t(state.d.size()), path);
+    detail::write_bytes(c.f, w.data(), sizeof(double) * w.a.size(), path);
+}
+// extended-filter states (and states read from disk) carry their own W
+inline void write_state(const std::string& path, const LowRankState& state) { write_state(path, state, state.w()); }
+// constant-H states: W = U of the context (fast_filter.hpp:113); a rank-0 state has no W
+inline void write_state(const std::string& path, const LowRankState& state, const FkfContext& ctx) {
+    write_state(path, state, state.rank() ? ctx.u() : Matrix(state.mean.size(), 0));
+}
+
+// read_state field_io.hpp:115-135
+inline LowRankState read_state(const std::string& path) {
+    detail::FileCloser c{detail::open_file(path, "rb")};
+    char magic[4] = {0, 0, 0, 0};
+    if (std::fread(magic, 1, 4, c.f) != 4 || std::string(magic, 4) != "FKS1")
+        throw std::runtime_error("not a FKS1 state file: " + path);
+    std::uint32_t hdr[3];
+    detail::read_bytes(c.f, hdr, sizeof hdr, path);
+    LowRankState s;
+    s.step = int(hdr[2]);
+    detail::read_bytes(c.f, &s.alpha, sizeof(double), path);
+    s.mean = Vector(Index(hdr[0]));
+    s.d = Vector(Index(hdr[1]));
+    s.w_host = Matrix(Index(hdr[0]), Index(hdr[1]));
+    detail::read_bytes(c.f, s.mean.data(), sizeof(double) * size_t(hdr[0]), path);
+    detail::read_bytes(c.f, s.d.data(), sizeof(double) * size_t(hdr[1]), path);
+    detail::read_bytes(c.f, s.w_host.data(), sizeof(double) * s.w_host.a.size(), path);
+    return s;
 }
 
 }  // namespace fastkf

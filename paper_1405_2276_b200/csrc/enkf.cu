@@ -13,7 +13,10 @@
 //              N_e ≤ m (2nN_e² flops instead of 4nmN_e), else in the reference order.
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "enkf.cuh"
 #include "rng_device.cuh"
@@ -44,6 +47,20 @@ __global__ void k_perturbed_innov(int m, int ne, const double* __restrict__ y, d
         Z[e] = sigma > 0.0 ? y[i] + sigma * Z[e] - HX[e] : y[i] - HX[e];
     }
 }
+
+// FKB_ENKF_TRACE=1: per-phase wall times of each step on stderr (stream-synchronized)
+struct EnkfClock {
+    cudaStream_t s;
+    bool on = std::getenv("FKB_ENKF_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void lap(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[enkf] %-14s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 static int grid_of(long long n) { return int(std::max<long long>(1, std::min<long long>((n + 255) / 256, 4096))); }
 
@@ -83,9 +100,11 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
     if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, y_h, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
     // the new members are formed in Xr (D, then X + update) so a singular C_yy leaves X untouched
     DBuf<double>& D = Xr;
+    EnkfClock clk{s};
     Xf.ensure(size_t(n) * ne);  // forecast members
     FKB_CUDA(cudaMemcpyAsync(Xf.p, X.p, X.bytes(), cudaMemcpyDeviceToDevice, s));
     cov->sample_pairs_add(seed_f, 0, Xf.p, n, ne);  // (:61-67)
+    clk.lap("forecast");
     if (m == 0) {
         FKB_CUDA(cudaMemcpyAsync(X.p, Xf.p, X.bytes(), cudaMemcpyDeviceToDevice, s));
         FKB_CUDA(cudaStreamSynchronize(s));
@@ -95,6 +114,7 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
     transpose_cm(n, ne, Xf.p, D.p, s);
     spmm_rm(H, D.p, ne, ne, HXr.p, ne, 1.0, s);
     transpose_cm(ne, m, HXr.p, HX.p, s);
+    clk.lap("HX");
     // anomalies (:70-73)
     k_row_mean<<<grid_of(n), 256, 0, s>>>(n, ne, Xf.p, n, mean.p);
     FKB_LAUNCH_CHECK();
@@ -106,6 +126,7 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
     FKB_LAUNCH_CHECK();
     count_launch(4);
     double* HD = HXr.p;
+    clk.lap("anomalies");
     const double inv = 1.0 / double(ne - 1);
     {  // C_yy = HD·HDᵀ/(N_e − 1) + σ²I (:75-77)
         GemmArgs g;
@@ -128,12 +149,14 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
     if (h)
         throw std::runtime_error(
             "enkf_step: sample innovation covariance is singular even with observation noise added");
+    clk.lap("Cyy + LLT");
     // perturbed innovations (:86-92) and Z = C_yy⁻¹·innovations
     if (sigma2 > 0.0) gaussian_matrix(m, ne, seed_p, 0, Z.p, m, s);
     k_perturbed_innov<<<grid_of((long long)m * ne), 256, 0, s>>>(m, ne, ybuf.p, std::sqrt(sigma2), HX.p, Z.p);
     FKB_LAUNCH_CHECK();
     count_launch();
     potrs_lower_multi(m, Cyy.p, m, Z.p, m, ne, s);
+    clk.lap("innov + TRSM");
     // X = X_f + C_sy·Z (:93)
     if (ne <= m) {
         T.ensure(size_t(ne) * ne);
@@ -172,6 +195,7 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
         u.C = X.p; u.ldc = n;
         gemm(u, nullptr, s);
     }
+    clk.lap("update");
     FKB_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -554,6 +554,64 @@ def enkf_step(ens: Ensemble, y, sigma2, seed) -> Ensemble:
     return ens
 
 
+# ------------------------------------------------------------------ field_io.hpp (FKF1 / FKS1)
+def write_field(path, nx: int, ny: int, data) -> None:
+    """write_field (field_io.hpp:66-79): "FKF1", uint32 nx, uint32 ny, float64 x-major."""
+    data = np.ascontiguousarray(data, dtype="<f8")
+    if data.size != nx * ny:
+        raise ValueError(f"write_field: data length does not match {nx}x{ny}")
+    with open(path, "wb") as f:
+        f.write(b"FKF1" + np.array([nx, ny], dtype="<u4").tobytes() + data.tobytes())
+
+
+def read_field(path):
+    """read_field (field_io.hpp:81-95) → (nx, ny, data)."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:4] != b"FKF1":
+        raise RuntimeError(f"not a FKF1 field file: {path}")
+    if len(raw) < 12:
+        raise RuntimeError(f"truncated file: {path}")
+    nx, ny = (int(v) for v in np.frombuffer(raw, "<u4", 2, 4))
+    if nx < 1 or ny < 1 or nx * ny > (1 << 31):
+        raise RuntimeError(f"implausible field dimensions in {path}")
+    if len(raw) < 12 + 8 * nx * ny:
+        raise RuntimeError(f"truncated file: {path}")
+    return nx, ny, np.frombuffer(raw, "<f8", nx * ny, 12).copy()
+
+
+def write_state(path, state: dict, w=None) -> None:
+    """write_state (field_io.hpp:100-113): "FKS1", uint32 n, r, step, float64 α, mean, D, W
+    (column-major).  ``w`` defaults to state["w"]; for an FkfContext state pass ctx.u()."""
+    mean = np.ascontiguousarray(state["mean"], "<f8")
+    d = np.ascontiguousarray(state["d"], "<f8")
+    w = np.asarray(state["w"] if w is None else w, dtype=np.float64)
+    if w.shape != (mean.size, d.size):
+        raise ValueError("write_state: W does not match the state")
+    with open(path, "wb") as f:
+        f.write(b"FKS1" + np.array([mean.size, d.size, int(state["step"])], "<u4").tobytes()
+                + np.array([state["alpha"]], "<f8").tobytes() + mean.tobytes() + d.tobytes()
+                + np.asfortranarray(w).astype("<f8").tobytes(order="F"))
+
+
+def read_state(path) -> dict:
+    """read_state (field_io.hpp:115-135) → {"alpha", "step", "mean", "d", "w"}."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:4] != b"FKS1":
+        raise RuntimeError(f"not a FKS1 state file: {path}")
+    if len(raw) < 24:
+        raise RuntimeError(f"truncated file: {path}")
+    n, r, step = (int(v) for v in np.frombuffer(raw, "<u4", 3, 4))
+    alpha = float(np.frombuffer(raw, "<f8", 1, 16)[0])
+    need = 24 + 8 * (n + r + n * r)
+    if len(raw) < need:
+        raise RuntimeError(f"truncated file: {path}")
+    vals = np.frombuffer(raw, "<f8", n + r + n * r, 24)
+    return {"alpha": alpha, "step": step, "mean": vals[:n].copy(), "d": vals[n:n + r].copy(),
+            "w": vals[n + r:].reshape(r, n).T.copy()}
+
+
 def fkf_init(cov, h, sigma2, k_rank, p_oversample, seed) -> FkfContext:
     return FkfContext(cov, h, sigma2, k_rank, p_oversample, seed)
 
@@ -580,4 +638,5 @@ __all__ = ["Grid", "KernelSpec", "kernel_eval", "next_smooth", "trace_ray", "Sou
            "build_H", "sym_eig", "sym_eig_device", "CovarianceOperator", "gaussian_matrix", "FkfContext", "fkf_init", "fkf_step",
            "variance", "trace_criterion", "relative_entropy", "DeviceArray", "POWERED_EXPONENTIAL", "MATERN",
            "FekfOptions", "BoxCox", "ExtendedFilter", "fekf_step", "DomainError", "Ensemble", "enkf_init",
-           "enkf_step"]
+           "enkf_step", "write_field",
+           "read_field", "write_state", "read_state"]
