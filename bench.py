@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-widened", action="store_true", help="skip the fekf/EnKF sub-measurements")
     return ap.parse_args()
 
 
@@ -457,9 +458,65 @@ def run_ours(args, rank, world, local_rank):
         "offline_s": offline_s,
         "eig_sweeps": ctx.eig_sweeps(),
     }
+    if not args.no_widened:
+        out["widened"] = widened_paths(args, w, h, ys, s2, cov, rank == 0 and world == 1 and not args.no_cpu_baseline)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, w, h, ys, s2)
     return out
+
+
+def widened_paths(args, w, h, ys, s2, cov, with_cpu):
+    """The SURVEY §8(f) rows built on top of the hot path, timed on the same workload:
+    the extended filter (fekf_step, Box–Cox 1 = the linear regime, rank cap and p of the
+    config, tol 1e-5) and the EnKF (enkf_step with the acceptance suite's 1,000 members,
+    acceptance.cpp:471).  Host-clock timing around synchronous calls (each step ends with a
+    stream sync); the reference CPU path is timed beside them only where it finishes: its
+    EnKF at c0 (1 thread per member block, all host threads), its fekf not at all (CG Γ⁻¹
+    per merged column, minutes per step at c0; it does not converge at c1+)."""
+    import paper_1405_2276_b200 as P
+    from paper_1405_2276_b200 import workloads as W
+    k, p = w.ghep_sizes()
+    res = {}
+    ekf = P.ExtendedFilter(cov, h, np.full(w.N, -1.0))
+    ts = []
+    for i, y in enumerate(ys[:4]):
+        t0 = time.perf_counter()
+        ekf.step(y, s2, P.BoxCox(1.0), P.FekfOptions(k_rank=k, oversampling=p, trunc_tol=1e-5, seed=i))
+        ts.append(time.perf_counter() - t0)
+    res["fekf"] = {"workload": args.config, "ms_per_step": 1e3 * float(np.median(ts[1:])),
+                   "steps_per_s": 1.0 / float(np.median(ts[1:])), "rank": ekf.rank(), "steps_timed": len(ts) - 1,
+                   "note": "per step: Box–Cox linearization, H_kΓH_kᵀ, m×m LLT, GHEP, add_low_rank (host eigensolves)"}
+    del ekf
+    ne = 1000
+    ens = P.Ensemble(cov, h, ne)
+    ts = []
+    for i, y in enumerate(ys[:4]):
+        t0 = time.perf_counter()
+        ens.step(y, s2, W.derive_seed(1011, i + 1))
+        ts.append(time.perf_counter() - t0)
+    res["enkf"] = {"workload": args.config, "members": ne, "ms_per_step": 1e3 * float(np.median(ts[1:])),
+                   "steps_per_s": 1.0 / float(np.median(ts[1:])), "steps_timed": len(ts) - 1}
+    del ens
+    if with_cpu:
+        from oracle import oracle as O
+        wc, hc, ysc, s2c = W.problem("c0", 1)
+        oc = O.CovarianceOperator(wc.n, wc.n, family=1, theta=wc.theta, length=wc.length, nu=wc.nu)
+        oh = O.Csr.from_arrays(hc.rows, hc.cols, hc.rowptr, hc.col, hc.val)
+        O.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        O.enkf_step(np.zeros((wc.N, ne)), oh, ysc[0], oc, s2c, W.derive_seed(1011, 1))
+        cpu_s = time.perf_counter() - t0
+        covc = P.CovarianceOperator(P.Grid(wc.n, wc.n), P.KernelSpec(family=1, theta=wc.theta, length=wc.length,
+                                                                      nu=wc.nu))
+        ens = P.Ensemble(covc, hc, ne)
+        ens.step(ysc[0], s2c, W.derive_seed(1011, 1))
+        t0 = time.perf_counter()
+        ens.step(ysc[0], s2c, W.derive_seed(1011, 2))
+        gpu_s = time.perf_counter() - t0
+        res["enkf_c0_vs_reference_cpu"] = {"members": ne, "gpu_ms": 1e3 * gpu_s, "cpu_ms": 1e3 * cpu_s,
+                                           "cpu_threads": O.max_threads(), "kind": "port",
+                                           "sample": "one enkf_step at c0 from the zero ensemble"}
+    return res
 
 
 def main():
