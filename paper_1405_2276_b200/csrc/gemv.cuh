@@ -128,53 +128,6 @@ __global__ void __launch_bounds__(256) k_coldot(int m, int n, const double* __re
     }
 }
 
-// y_i = epi(i, Σ_j A_ij·x_j) for COLUMN-MAJOR A (m×n): a CTA owns 16 rows and walks all
-// columns, a warp reading two 128-byte column segments per load, 8 loads in flight per
-// thread; fixed-order reduction over the 32 column groups (deterministic).  Used where A
-// was streamed earlier in the same step and is still L2-resident (z = P·s̃ after r̃ = Pᵀ·r).
-template <class Epi>
-__global__ void __launch_bounds__(512) k_gemv_cm(int m, int n, const double* __restrict__ A, long long lda,
-                                                 const double* __restrict__ x, Epi epi) {
-    extern __shared__ double xs[];
-    __shared__ double red[32][17];
-    for (int c = threadIdx.x; c < n; c += 512) xs[c] = x[c];
-    __syncthreads();
-    const int rr = threadIdx.x & 15, cg = threadIdx.x >> 4;
-    const int row = blockIdx.x * 16 + rr;
-    const bool ok = row < m;
-    const double* a = A + (ok ? row : 0);
-    double s0 = 0.0, s1 = 0.0;
-    int c = cg;
-    for (; c + 32 * 7 < n; c += 256) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = ok ? a[(long long)(c + 32 * u) * lda] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; u += 2) {
-            s0 = fma(v[u], xs[c + 32 * u], s0);
-            s1 = fma(v[u + 1], xs[c + 32 * (u + 1)], s1);
-        }
-    }
-    for (; c < n; c += 32) s0 = fma(ok ? a[(long long)c * lda] : 0.0, xs[c], s0);
-    red[cg][rr] = s0 + s1;
-    __syncthreads();
-    if (threadIdx.x < 16 && blockIdx.x * 16 + (int)threadIdx.x < m) {
-        double v = 0.0;
-#pragma unroll 8
-        for (int g = 0; g < 32; ++g) v += red[g][threadIdx.x];
-        epi(blockIdx.x * 16 + threadIdx.x, v);
-    }
-}
-
-template <class Epi>
-inline void launch_gemv_cm(int m, int n, const double* A, long long lda, const double* x, Epi epi, cudaStream_t s) {
-    if (m <= 0) return;
-    k_gemv_cm<Epi><<<(unsigned)((m + 15) / 16), 512, sizeof(double) * size_t(std::max(n, 1)), s>>>(m, n, A, lda, x,
-                                                                                                 epi);
-    FKB_LAUNCH_CHECK();
-    count_launch();
-}
-
 template <class XL, class Epi>
 inline void launch_coldot(int m, int n, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s) {
     if (n <= 0) return;
