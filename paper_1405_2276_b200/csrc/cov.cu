@@ -522,6 +522,81 @@ __global__ void __launch_bounds__(kThreads) k_sampler_rows(const double2* __rest
     }
 }
 
+// ---- fast sampler path for 512×512 tori (register-resident radix-8 transforms).
+// Pass 1: a CTA owns 4 consecutive ky columns (ky0 ≡ 0 mod 4): the 4×512 torus inputs
+// amp·(n_re + i·n_im) are generated into shared memory with one Box–Muller evaluation per
+// two normals (idx = kx·my + ky: ky0+2q and ky0+2q+1 share the pair idx/2), then each
+// 64-thread group runs an inverse 512-point transform along x in registers; rows ix < nx are
+// stored ix-major, T[ix][ky] (64-byte segments of the 4 columns).
+__global__ void __launch_bounds__(256) k_samp_cols512(const double* __restrict__ amp, int my, int nx,
+                                                      const double2* __restrict__ twp, uint64_t seed, uint64_t sid0,
+                                                      double2* __restrict__ T) {
+    constexpr int N = 512, BL = N + N / 8 + 1;
+    extern __shared__ double2 sm[];
+    double2* g = sm;                 // [4][512] generated inputs, reused as the output stage
+    double2* fb = sm + 4 * N;        // 4 transforms × 2 ping-pong buffers
+    const uint64_t sid = sid0 + blockIdx.y;
+    const uint64_t st_re = splitmix64(seed ^ splitmix64(2 * sid)), st_im = splitmix64(seed ^ splitmix64(2 * sid + 1));
+    T += (long long)blockIdx.y * nx * my;
+    const int ky0 = blockIdx.x * 4;
+    for (int e = threadIdx.x; e < N * 2; e += blockDim.x) {  // (kx, q): pair of columns ky0+2q, +1
+        const int kx = e >> 1, q = e & 1;
+        const unsigned long long idx = (unsigned long long)kx * my + ky0 + 2 * q;  // even
+        double r0, r1, i0, i1;
+        rng_normal_pair(st_re, idx >> 1, r0, r1);
+        rng_normal_pair(st_im, idx >> 1, i0, i1);
+        const double a0 = __ldg(amp + idx), a1 = __ldg(amp + idx + 1);
+        g[(2 * q) * N + kx] = make_double2(a0 * r0, a0 * i0);
+        g[(2 * q + 1) * N + kx] = make_double2(a1 * r1, a1 * i1);
+    }
+    __syncthreads();
+    const int t = threadIdx.x >> 6, j = threadIdx.x & 63;
+    double2 v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = g[t * N + j + 64 * r];
+    double2* ba = fb + t * 2 * BL;
+    fft_reg<+1, N>(v, ba, ba + BL, twp, j);
+    __syncthreads();  // every transform has consumed g
+#pragma unroll
+    for (int r = 0; r < 8; ++r) g[t * N + j + 64 * r] = v[r];
+    __syncthreads();
+    for (int e = threadIdx.x; e < nx * 4; e += blockDim.x) {
+        const int ix = e >> 2, c = e & 3;
+        T[(long long)ix * my + ky0 + c] = g[c * N + ix];
+    }
+}
+
+// Pass 2: a CTA owns 4 rows ix; each 64-thread group loads T[ix][0..512) coalesced, runs the
+// inverse transform along y in registers and adds Re → a, Im → b (×1/√M) for iy < ny.
+__global__ void __launch_bounds__(256) k_samp_rows512(const double2* __restrict__ T, int nx, int ny,
+                                                      const double2* __restrict__ twp, double* __restrict__ da,
+                                                      double* __restrict__ db, double scale, long long ld_pair,
+                                                      int ncols) {
+    constexpr int N = 512, BL = N + N / 8 + 1;
+    extern __shared__ double2 sm[];
+    const int p = blockIdx.y;
+    T += (long long)p * nx * N;
+    da += p * ld_pair;
+    db = 2 * p + 1 < ncols ? db + p * ld_pair : nullptr;
+    const int t = threadIdx.x >> 6, j = threadIdx.x & 63;
+    const int ix = blockIdx.x * 4 + t;
+    double2 v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = ix < nx ? T[(long long)ix * N + j + 64 * r] : make_double2(0.0, 0.0);
+    double2* ba = sm + t * 2 * BL;
+    fft_reg<+1, N>(v, ba, ba + BL, twp, j);
+    if (ix >= nx) return;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int iy = j + 64 * r;
+        if (iy < ny) {
+            const long long o = (long long)ix * ny + iy;
+            da[o] += v[r].x * scale;
+            if (db) db[o] += v[r].y * scale;
+        }
+    }
+}
+
 // --------------------------------------------------------------------------- host orchestration
 // lengths with a compile-time single-transform schedule (see with_len)
 static bool static_len(int n) { return n == 64 || n == 128 || n == 256 || n == 512 || n == 1024 || n == 2048; }
@@ -843,6 +918,26 @@ void Cov::sample_pairs_add(uint64_t seed, uint64_t sid0, double* X, long long ld
     set_smem((const void*)k_sampler_rows, smem_bytes(rows, my));
     const int npairs = (ncols + 1) / 2;
     const size_t per = size_t(my) * size_t(nx);
+    if (mx == 512 && my == 512 && fx8.twp && fy8.twp) {  // register-resident fast path
+        constexpr int N = 512, BL = N + N / 8 + 1;
+        const size_t sm1 = (4 * N + 4 * 2 * BL) * sizeof(double2), sm2 = 4 * 2 * BL * sizeof(double2);
+        FKB_CUDA(cudaFuncSetAttribute(k_samp_cols512, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1)));
+        FKB_CUDA(cudaFuncSetAttribute(k_samp_rows512, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2)));
+        const int bp = int(std::max<size_t>(1, std::min<size_t>(npairs, (size_t(1) << 26) / per)));
+        if (swork.n < per * size_t(bp)) swork.alloc(per * size_t(bp));
+        for (int p0 = 0; p0 < npairs; p0 += bp) {
+            const int np = std::min(bp, npairs - p0);
+            k_samp_cols512<<<dim3(my / 4, np), 256, sm1, stream>>>(amp_full.p, my, nx, fx8.twp, seed,
+                                                                  sid0 + uint64_t(p0), swork.p);
+            FKB_LAUNCH_CHECK();
+            double* xa = X + (long long)(2 * p0) * ldx;
+            k_samp_rows512<<<dim3(ceil_div(nx, 4), np), 256, sm2, stream>>>(
+                swork.p, nx, ny, fy8.twp, xa, xa + ldx, 1.0 / std::sqrt(double(M())), 2 * ldx, ncols - 2 * p0);
+            FKB_LAUNCH_CHECK();
+            count_launch(2);
+        }
+        return;
+    }
     const int bp = int(std::max<size_t>(1, std::min<size_t>(npairs, (size_t(1) << 26) / per)));  // ≤ 1 GiB
     if (swork.n < per * size_t(bp)) swork.alloc(per * size_t(bp));
     for (int p0 = 0; p0 < npairs; p0 += bp) {
