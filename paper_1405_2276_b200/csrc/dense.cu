@@ -466,19 +466,28 @@ size_t gram_ws_elems(int M, int N, int K) {
 // --------------------------------------------------------------------------- Cholesky
 constexpr int CNB = 64;
 
-__global__ void __launch_bounds__(256) k_potrf_diag(double* A, long long lda, int kb, int k0, int* info) {
-    __shared__ double s[CNB][CNB + 1];
+// Factor the kb×kb diagonal block at (k0, k0) in shared memory (right-looking, 256 threads,
+// each owning 16 fixed (i, c) entries so the rank-1 updates need no index division); write L11
+// back, and when dinv ≠ null also L11⁻¹ (kb×kb, ld CNB) to dinv + k0·CNB by the same
+// row-operation sweep on the identity.
+__global__ void __launch_bounds__(256) k_potrf_diag(double* A, long long lda, int kb, int k0, int* info,
+                                                   double* __restrict__ dinv) {
+    extern __shared__ double potrf_sm[];
+    double (*s)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(potrf_sm);
+    double (*x)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(potrf_sm + CNB * (CNB + 1));
+    __shared__ int bad;
     if (*info) return;
     double* a = A + k0 + (long long)k0 * lda;
-    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-        const int i = e % kb, j = e / kb;
-        if (i >= j) s[i][j] = a[i + (long long)j * lda];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < CNB * CNB; e += 256) {
+        const int i = e & (CNB - 1), j = e >> 6;
+        s[i][j] = (i < kb && j < kb && i >= j) ? a[i + (long long)j * lda] : 0.0;
+        x[i][j] = i == j ? 1.0 : 0.0;
     }
-    __shared__ int bad;
-    if (threadIdx.x == 0) bad = 0;
+    if (tid == 0) bad = 0;
     __syncthreads();
     for (int j = 0; j < kb; ++j) {
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             const double d = s[j][j];
             if (!(d > 0.0)) {
                 bad = 1;
@@ -490,18 +499,38 @@ __global__ void __launch_bounds__(256) k_potrf_diag(double* A, long long lda, in
         __syncthreads();
         if (bad) return;
         const double piv = s[j][j];
-        for (int i = j + 1 + threadIdx.x; i < kb; i += blockDim.x) s[i][j] /= piv;
+        if (tid < CNB && tid > j && tid < kb) s[tid][j] /= piv;
         __syncthreads();
-        const int rem = kb - j - 1;
-        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-            const int i = j + 1 + e % rem, c = j + 1 + e / rem;
-            if (i >= c) s[i][c] -= s[i][j] * s[c][j];
+#pragma unroll
+        for (int q = 0; q < CNB * CNB / 256; ++q) {
+            const int e = tid + 256 * q;
+            const int i = e & (CNB - 1), c = e >> 6;
+            if (c > j && i >= c && i < kb) s[i][c] = fma(-s[i][j], s[c][j], s[i][c]);
         }
         __syncthreads();
     }
-    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    for (int e = tid; e < kb * kb; e += 256) {
         const int i = e % kb, j = e / kb;
         if (i >= j) a[i + (long long)j * lda] = s[i][j];
+    }
+    if (!dinv) return;
+    // L X = I by row sweeps: row j ← row j / L_jj, then rows i > j −= L_ij · row j
+    for (int j = 0; j < kb; ++j) {
+        const double piv = s[j][j];
+        if (tid < kb) x[j][tid] /= piv;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < CNB * CNB / 256; ++q) {
+            const int e = tid + 256 * q;
+            const int i = e >> 6, c = e & (CNB - 1);
+            if (i > j && i < kb && c <= j) x[i][c] = fma(-s[i][j], x[j][c], x[i][c]);
+        }
+        __syncthreads();
+    }
+    double* di = dinv + (long long)k0 * CNB;  // block b at dinv + b·CNB·CNB (k0 = b·CNB)
+    for (int e = tid; e < CNB * CNB; e += 256) {
+        const int i = e & (CNB - 1), j = e >> 6;
+        di[i + j * CNB] = (i < kb && j < kb) ? x[i][j] : 0.0;
     }
 }
 
@@ -537,36 +566,54 @@ __global__ void __launch_bounds__(CNB) k_trsm_panel(double* A, long long lda, in
     }
 }
 
+static size_t potrf_inv_elems(int n) { return size_t(std::max(ceil_div(n, CNB), 1)) * CNB * CNB; }
 size_t potrf_ws_elems(int n) {
-    // worst split-K workspace of a trailing update (none: trailing updates have K = 64)
-    (void)n;
-    return 0;
+    // full 64×64 diagonal-block inverses (ceil(n/64)·64·64) + the panel product L21 (n·64)
+    return potrf_inv_elems(n) + size_t(std::max(n, 1)) * CNB;
 }
 
+// With a workspace (ws_elems ≥ potrf_ws_elems(n)) every panel is one DMMA product
+// L21 = A21·L11⁻ᵀ with the diagonal inverse formed beside L11, and the inverses stay in ws
+// for potrs_lower_multi; without one (graph-captured solver 0) the substitution panel kernel.
 void potrf_lower(int n, double* A, long long lda, int* info, double* ws, size_t ws_elems, cudaStream_t s) {
-    (void)ws;
-    (void)ws_elems;
     const size_t trsm_smem = 2 * sizeof(double) * CNB * (CNB + 1);
     static bool attr = false;
     if (!attr) {
         FKB_CUDA(cudaFuncSetAttribute((const void*)k_trsm_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(trsm_smem)));
+        FKB_CUDA(cudaFuncSetAttribute((const void*)k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(trsm_smem)));
         attr = true;
     }
+    const bool inv = ws && ws_elems >= potrf_ws_elems(n);
+    double* dinv = inv ? ws : nullptr;
+    double* pan = inv ? ws + potrf_inv_elems(n) : nullptr;
     for (int k0 = 0; k0 < n; k0 += CNB) {
         const int kb = std::min(CNB, n - k0);
-        k_potrf_diag<<<1, 256, 0, s>>>(A, lda, kb, k0, info);
+        k_potrf_diag<<<1, 256, trsm_smem, s>>>(A, lda, kb, k0, info, dinv);
         FKB_LAUNCH_CHECK();
         count_launch();
         const int rest = n - k0 - kb;
         if (rest <= 0) break;
-        k_trsm_panel<<<ceil_div(rest, CNB), CNB, trsm_smem, s>>>(A, lda, n, k0, kb, info);
-        FKB_LAUNCH_CHECK();
-        count_launch();
+        double* a21 = A + (k0 + kb) + (long long)k0 * lda;
+        if (inv) {
+            GemmArgs p;  // L21 = A21 · L11⁻ᵀ into the panel scratch (ld rest)
+            p.M = rest; p.N = kb; p.K = kb;
+            p.A = a21; p.lda = lda;
+            p.B = dinv + (long long)k0 * CNB; p.ldb = CNB; p.transB = 1;
+            p.C = pan; p.ldc = rest;
+            gemm(p, nullptr, s);
+            FKB_CUDA(cudaMemcpy2DAsync(a21, sizeof(double) * size_t(lda), pan, sizeof(double) * size_t(rest),
+                                       sizeof(double) * size_t(rest), size_t(kb), cudaMemcpyDeviceToDevice, s));
+        } else {
+            k_trsm_panel<<<ceil_div(rest, CNB), CNB, trsm_smem, s>>>(A, lda, n, k0, kb, info);
+            FKB_LAUNCH_CHECK();
+            count_launch();
+        }
         GemmArgs g;  // A22 −= L21 L21ᵀ (lower tiles)
         g.M = rest; g.N = rest; g.K = kb;
-        g.A = A + (k0 + kb) + (long long)k0 * lda; g.lda = lda; g.transA = 0;
-        g.B = g.A; g.ldb = lda; g.transB = 1;
+        g.A = inv ? pan : a21; g.lda = inv ? rest : lda; g.transA = 0;
+        g.B = g.A; g.ldb = g.lda; g.transB = 1;
         g.alpha = -1.0; g.beta = 1.0;
         g.C = A + (k0 + kb) + (long long)(k0 + kb) * lda; g.ldc = lda;
         g.lower_only = 1;
@@ -714,14 +761,27 @@ __global__ void __launch_bounds__(256) k_trsm_diag(const double* __restrict__ L,
     }
 }
 
-void potrs_lower_multi(int n, const double* L, long long lda, double* B, long long ldb, int nrhs, cudaStream_t s) {
+void potrs_lower_multi(int n, const double* L, long long lda, double* B, long long ldb, int nrhs, cudaStream_t s,
+                       const double* dinv, double* tmp) {
     if (n <= 0 || nrhs <= 0) return;
     const int nblk = ceil_div(n, CNB);
+    const bool inv = dinv && tmp;
     for (int b = 0; b < nblk; ++b) {  // L·Y = B, trailing updates on DMMA
         const int k0 = b * CNB, kb = std::min(CNB, n - k0), k1 = k0 + kb;
-        k_trsm_diag<false><<<ceil_div(nrhs, TRC), 256, 0, s>>>(L, lda, k0, kb, B, ldb, nrhs);
-        FKB_LAUNCH_CHECK();
-        count_launch();
+        if (inv) {
+            GemmArgs d;  // Y_b = L_bb⁻¹ · B_b
+            d.M = kb; d.N = nrhs; d.K = kb;
+            d.A = dinv + (long long)k0 * CNB; d.lda = CNB;
+            d.B = B + k0; d.ldb = ldb;
+            d.C = tmp; d.ldc = CNB;
+            gemm(d, nullptr, s);
+            FKB_CUDA(cudaMemcpy2DAsync(B + k0, sizeof(double) * size_t(ldb), tmp, sizeof(double) * CNB,
+                                       sizeof(double) * size_t(kb), size_t(nrhs), cudaMemcpyDeviceToDevice, s));
+        } else {
+            k_trsm_diag<false><<<ceil_div(nrhs, TRC), 256, 0, s>>>(L, lda, k0, kb, B, ldb, nrhs);
+            FKB_LAUNCH_CHECK();
+            count_launch();
+        }
         if (k1 < n) {
             GemmArgs g;
             g.M = n - k1; g.N = nrhs; g.K = kb;
@@ -734,9 +794,20 @@ void potrs_lower_multi(int n, const double* L, long long lda, double* B, long lo
     }
     for (int b = nblk - 1; b >= 0; --b) {  // Lᵀ·X = Y
         const int k0 = b * CNB, kb = std::min(CNB, n - k0);
-        k_trsm_diag<true><<<ceil_div(nrhs, TRC), 256, 0, s>>>(L, lda, k0, kb, B, ldb, nrhs);
-        FKB_LAUNCH_CHECK();
-        count_launch();
+        if (inv) {
+            GemmArgs d;  // X_b = L_bb⁻ᵀ · Y_b
+            d.M = kb; d.N = nrhs; d.K = kb;
+            d.A = dinv + (long long)k0 * CNB; d.lda = CNB; d.transA = 1;
+            d.B = B + k0; d.ldb = ldb;
+            d.C = tmp; d.ldc = CNB;
+            gemm(d, nullptr, s);
+            FKB_CUDA(cudaMemcpy2DAsync(B + k0, sizeof(double) * size_t(ldb), tmp, sizeof(double) * CNB,
+                                       sizeof(double) * size_t(kb), size_t(nrhs), cudaMemcpyDeviceToDevice, s));
+        } else {
+            k_trsm_diag<true><<<ceil_div(nrhs, TRC), 256, 0, s>>>(L, lda, k0, kb, B, ldb, nrhs);
+            FKB_LAUNCH_CHECK();
+            count_launch();
+        }
         if (k0 > 0) {
             GemmArgs g;  // X[0:k0] −= L[k0:k1, 0:k0]ᵀ · X[k0:k1]
             g.M = k0; g.N = nrhs; g.K = kb;

@@ -46,13 +46,18 @@ int gemm_pick_splitk(int M, int N, int K);
 
 
 // In-place lower Cholesky of the n×n SPD matrix A (column-major, lda).  Sets *info
-// (device int) to j+1 at the first non-positive pivot, leaves it 0 on success.
+// (device int) to j+1 at the first non-positive pivot, leaves it 0 on success.  A workspace
+// of potrf_ws_elems(n) selects the DMMA panel path and leaves the 64×64 diagonal-block
+// inverses at ws (block b at ws + b·64·64) for potrs_lower_multi.
 void potrf_lower(int n, double* A, long long lda, int* info, double* ws, size_t ws_elems, cudaStream_t s);
 size_t potrf_ws_elems(int n);
 // Solves L Lᵀ x = b in place (x on entry holds b).  flags: device int[2·ceil(n/64)].
 void potrs_lower(int n, const double* L, long long lda, double* x, int* flags, cudaStream_t s);
 // The same for nrhs right-hand sides B (n×nrhs, ldb), blocked: 64×64 diagonal solves plus
 // DMMA trailing updates.
-void potrs_lower_multi(int n, const double* L, long long lda, double* B, long long ldb, int nrhs, cudaStream_t s);
+// dinv (the inverses left by potrf_lower's workspace) and tmp (64·nrhs) make every block a
+// DMMA product; without them the 64×64 blocks are solved by substitution.
+void potrs_lower_multi(int n, const double* L, long long lda, double* B, long long ldb, int nrhs, cudaStream_t s,
+                       const double* dinv = nullptr, double* tmp = nullptr);
 
 }  // namespace fkb

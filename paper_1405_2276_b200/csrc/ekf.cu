@@ -238,7 +238,8 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
             gemm(g, nullptr, s);
             symmetrize(m, S.p, m, s);
             FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
-            potrf_lower(m, S.p, m, info.p, nullptr, 0, s);  // LLT (:179-181)
+            pws.ensure(potrf_ws_elems(m));
+            potrf_lower(m, S.p, m, info.p, pws.p, potrf_ws_elems(m), s);  // LLT (:179-181)
             int h = 0;
             FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             FKB_CUDA(cudaStreamSynchronize(s));

@@ -40,7 +40,7 @@ struct Ekf {
     DBuf<double> mean, W, Wbar, d;
     int last_gep_rank = 0, last_relin = 0;
 
-    DBuf<double> eta, eta2, jac, sinv, heta, G, S, HW, z, tv, gt, dc, ybuf, ws;
+    DBuf<double> eta, eta2, jac, sinv, heta, G, S, HW, z, tv, gt, dc, ybuf, ws, pws;
     DBuf<int> info, flags, bad;
 
     Ekf(Cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val);

@@ -142,7 +142,8 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
         symmetrize(m, Cyy.p, m, s);
     }
     FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
-    potrf_lower(m, Cyy.p, m, info.p, nullptr, 0, s);  // (:78-82)
+    pws.ensure(potrf_ws_elems(m) + size_t(64) * ne);
+    potrf_lower(m, Cyy.p, m, info.p, pws.p, potrf_ws_elems(m), s);  // (:78-82)
     int h = 0;
     FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FKB_CUDA(cudaStreamSynchronize(s));
@@ -155,7 +156,7 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
     k_perturbed_innov<<<grid_of((long long)m * ne), 256, 0, s>>>(m, ne, ybuf.p, std::sqrt(sigma2), HX.p, Z.p);
     FKB_LAUNCH_CHECK();
     count_launch();
-    potrs_lower_multi(m, Cyy.p, m, Z.p, m, ne, s);
+    potrs_lower_multi(m, Cyy.p, m, Z.p, m, ne, s, pws.p, pws.p + potrf_ws_elems(m));
     clk.lap("innov + TRSM");
     // X = X_f + C_sy·Z (:93)
     if (ne <= m) {

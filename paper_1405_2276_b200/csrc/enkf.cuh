@@ -12,7 +12,7 @@ struct Enkf {
     int m = 0, ne = 0;
     DevCsr H, HT;
     DBuf<double> X;  // members, n×ne column-major (Ensemble::members)
-    DBuf<double> Xf, Xr, HXr, HX, mean, hmean, Z, Cyy, T, ybuf, ws;
+    DBuf<double> Xf, Xr, HXr, HX, mean, hmean, Z, Cyy, T, ybuf, ws, pws;
     DBuf<int> info;
 
     Enkf(Cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val, int n_members);

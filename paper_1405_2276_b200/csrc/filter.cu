@@ -718,6 +718,7 @@ void Filter::set_solver(int mode) {
     solver = mode;
     k_valid = false;
     if (mode == 0 && S.n < size_t(m) * m) S.alloc(size_t(std::max(m, 1)) * std::max(m, 1));  // before any capture
+    if (mode == 0) potrf_ws.ensure(potrf_ws_elems(m));  // DMMA panel path inside the captured graph
     drop_graphs();
 }
 
@@ -846,7 +847,7 @@ void Filter::enqueue_solve_dense() {
     g.lower_only = 1;
     gemm(g, nullptr, s);
     mark("innovation_build");
-    potrf_lower(m, S.p, m, info.p, nullptr, 0, s);  // LLT (:104-106)
+    potrf_lower(m, S.p, m, info.p, potrf_ws.p, potrf_ws.n, s);  // LLT (:104-106)
     mark("llt");
     potrs_lower(m, S.p, m, z.p, flags.p, s);         // z = S⁻¹(y − H·mean) (:108)
     mark("llt_solve");

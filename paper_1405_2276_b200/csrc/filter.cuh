@@ -80,7 +80,7 @@ struct Filter {
     int pcg_maxit = 200;  // iteration cap before the exact Cholesky takes over (tests force 0)  // 1 when the capacitance PCG fell back to the cluster Cholesky
 
     // step workspaces
-    DBuf<double> S, z, t, cvec, ws, ws_step;
+    DBuf<double> S, z, t, cvec, ws, ws_step, potrf_ws;
     DBuf<int> info, flags;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one per step parity
     bool graph_ready[2] = {false, false};
