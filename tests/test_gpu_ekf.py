@@ -125,3 +125,28 @@ def test_fekf_errors_leave_state():
     # the same step succeeds afterwards and matches the oracle
     g.step(p.obs[1], p.sigma2, P.BoxCox(2.0), P.FekfOptions(k_rank=4, seed=2))
     assert g.state()["step"] == 2
+
+
+def test_fekf_c0_first_step_matches_oracle():
+    """BASELINE c0 size (N = 4,096, m = 256, rank cap 256 = full rank, Box–Cox 2 about s = 1):
+    the first extended step (linearization, m×m LLT, GHEP; add_low_rank returns (U, λ) from
+    the zero start, so the oracle's CG Γ⁻¹ is not needed) against the oracle."""
+    w, h, ys, s2 = W.problem("c0", 1)
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu))
+    mean0 = np.zeros(w.N)  # forward(1.0) = 0 for Box–Cox 2
+    k, p = w.ghep_sizes()
+    g = P.ExtendedFilter(cov, h, mean0)
+    g.step(ys[0], s2, P.BoxCox(2.0), P.FekfOptions(k_rank=k, oversampling=p, trunc_tol=1e-5, seed=w.ghep_seed))
+    o = O.ExtendedFilter(O.CovarianceOperator(w.n, w.n, family=1, theta=w.theta, length=w.length, nu=w.nu),
+                         O.Csr.from_arrays(h.rows, h.cols, h.rowptr, h.col, h.val), mean0)
+    o.step(ys[0], s2, 2.0, k_rank=k, oversampling=p, trunc_tol=1e-5, seed=w.ghep_seed)
+    gs, os_ = g.state(), o.state()
+    assert gs["alpha"] == os_["alpha"] == 1.0
+    assert rel_err(gs["mean"], os_["mean"]) < 1e-9
+    kk = min(len(gs["d"]), len(os_["d"]))
+    assert np.max(np.abs(gs["d"][:kk] - os_["d"][:kk])) <= 1e-9 * gs["alpha"]
+    # W D Wᵀ applied to probe vectors (N² is too large to form)
+    z = np.random.default_rng(0).standard_normal((w.N, 4))
+    wg = gs["w"] @ (gs["d"][:, None] * (gs["w"].T @ z))
+    wo = os_["w"] @ (os_["d"][:, None] * (os_["w"].T @ z))
+    assert rel_err(wg, wo) < 1e-9

@@ -29,7 +29,7 @@ def _run(p, ne, ys, sigma2, seeds):
     return ens, x, max(errs)
 
 
-@pytest.mark.parametrize("case", ["desk6_50", "desk10_2000", "c0_100", "c1_12"])
+@pytest.mark.parametrize("case", ["desk6_50", "desk10_2000", "c0_100", "c1_12", "c2_20", "c4_10"])
 def test_enkf_matches_oracle(case):
     if case == "desk6_50":  # test_enkf.cpp:42-53 geometry, three cycles
         p = Problem(6, 6, 2, 3, 0, 2e-4, kernel=UNIT)
@@ -39,6 +39,28 @@ def test_enkf_matches_oracle(case):
         p = Problem(10, 10, 3, 8, 0, 2e-4, kernel=dict(UNIT, theta=1e-4, power=0.5))
         ys = [simulate_observations(p.h, plume_field(10, 10, 3.0 * k), 2e-4, W.derive_seed(55, k)) for k in (1, 2, 3)]
         ne, sigma2, seeds = 2000, 2e-4, [W.derive_seed(56, k) for k in (1, 2, 3)]
+    elif case in ("c2_20", "c4_10"):  # full BASELINE sizes (c2: two ray blocks; c4: 1024² torus), few members
+        cfg, ne = case.split("_")
+        w, h, ys_all, s2 = W.problem(cfg, 1)
+
+        class _P:  # the workload's own operator (c2 stacks two layouts, beyond cross_well)
+            nx = ny = w.n
+            grid = P.Grid(w.n, w.n)
+            sigma2 = s2
+
+            def __init__(self):
+                self.h = h
+
+            def spec(self):
+                return P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+
+            def oracle_cov(self):
+                return O.CovarianceOperator(w.n, w.n, family=1, theta=w.theta, length=w.length, nu=w.nu)
+
+            def oracle_h(self):
+                return O.Csr.from_arrays(h.rows, h.cols, h.rowptr, h.col, h.val)
+        p = _P()
+        ys, ne, sigma2, seeds = ys_all[:1], int(ne), s2, [W.derive_seed(1011, 1)]
     elif case == "c1_12":  # BASELINE c1 (512² torus: the register-resident sampler path), odd pair count
         w, h, ys_all, s2 = W.problem("c1", 1)
         p = Problem(128, 128, 32, 32, 0, s2, kernel=dict(family=1, theta=w.theta, length=w.length, nu=w.nu))
