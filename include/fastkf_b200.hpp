@@ -9,7 +9,7 @@
 //   (fast_filter.hpp:42-75), LowRankState/fkf_step (:21-37, :84-125), variance /
 //   trace_criterion / relative_entropy (uq.hpp:16-53), BoxCox/FekfOptions/fekf_step
 //   (boxcox.hpp:14-17, fast_filter.hpp:127-224), Field/write_field/read_field/write_state/
-//   read_state (field_io.hpp:18-135).
+//   read_state (field_io.hpp:18-135), Ensemble/enkf_init/enkf_step (enkf.hpp:15-94).
 // Eigen is not required: Vector/Matrix/SparseRowMatrix are thin column-major stand-ins with
 // the subset of API callers use (SURVEY.md §8b caveat 2).  Error codes map back to
 // std::invalid_argument (1) and std::runtime_error (2, 3).
@@ -386,6 +386,53 @@ inline LowRankState fekf_step(const LowRankState& state, const CovarianceOperato
     next.ekf = dev;
     next.ekf_generation = ++dev->generation;
     return next;
+}
+
+// ---- enkf.hpp:15-94 — the ensemble lives on the device, bound to Γ and H at enkf_init
+class Ensemble {
+public:
+    Ensemble(const CovarianceOperator& cov, const SparseRowMatrix& h, Index n_members) : n_(cov.size()) {
+        fkb_enkf* e = nullptr;
+        detail::check(fkb_enkf_init(cov.handle(), h.m, h.n, h.rowptr.data(), h.col.empty() ? nullptr : h.col.data(),
+                                    h.val.empty() ? nullptr : h.val.data(), int(n_members), &e));
+        e_.reset(e);
+        ne_ = n_members;
+        cov_ = cov.handle();
+        h_ = &h;
+    }
+    Index size() const { return ne_; }
+    Vector mean() const {  // Ensemble::mean (:20)
+        Vector m(n_);
+        detail::check(fkb_enkf_mean(e_.get(), m.data()));
+        return m;
+    }
+    Matrix members() const {  // n × N_e
+        Matrix x(n_, ne_);
+        detail::check(fkb_enkf_members(e_.get(), x.data()));
+        return x;
+    }
+    fkb_enkf* handle() const { return e_.get(); }
+    const void* cov_ = nullptr;
+    const SparseRowMatrix* h_ = nullptr;
+
+private:
+    struct Del {
+        void operator()(fkb_enkf* p) const { fkb_enkf_destroy(p); }
+    };
+    Index n_ = 0, ne_ = 0;
+    std::unique_ptr<fkb_enkf, Del> e_;
+};
+// enkf_init (:30-34) — takes Γ and H so the members can stay on the device
+inline Ensemble enkf_init(const CovarianceOperator& cov, const SparseRowMatrix& h, Index n_members) {
+    return Ensemble(cov, h, n_members);
+}
+// enkf_step (:49-94), advancing the device ensemble in place and returning it
+inline Ensemble& enkf_step(Ensemble& ens, const SparseRowMatrix& h, const Vector& y, const CovarianceOperator& cov,
+                           double sigma2, std::uint64_t seed) {
+    if (ens.cov_ != cov.handle() || ens.h_ != &h)
+        throw std::invalid_argument("enkf_step: the ensemble is bound to another operator pair");
+    detail::check(fkb_enkf_step(ens.handle(), y.data(), y.size(), sigma2, seed));
+    return ens;
 }
 
 // ---- field_io.hpp: FKF1 field and FKS1 state snapshots (little-endian, host I/O)
