@@ -129,10 +129,12 @@ def replica_throughput(local_ms: float, steps: int, world: int, device) -> float
 
 
 # ----------------------------------------------------------------------------- work accounting
-def phase_work(w, r, fft_flops, nnz):
+def phase_work(w, r, fft_flops, nnz, uq_count=-1):
     """Algorithmic work per launch of each step phase: unique bytes a
-    kernel must move for HBM-bound phases, minimal flops for arithmetic phases."""
+    kernel must move for HBM-bound phases, minimal flops for arithmetic phases.  uq_count ≥ 0:
+    the U pass also reads the count draws and writes diag Σ and the count realizations."""
     N, m = w.N, w.m
+    uq_bytes = 0.0 if uq_count < 0 else 8.0 * N * (1 + 2 * uq_count) + 8.0 * r * (2 + uq_count)
     return {
         "residual": ("hbm", 12.0 * nnz + 4.0 * (m + 1) + 8.0 * N + 16.0 * m),
         "capacitance": ("tensor", 1.0 * m * r * (r + 1)),  # symmetric Eᵀ·diag·E (lower half)
@@ -144,7 +146,7 @@ def phase_work(w, r, fft_flops, nnz):
         "ctz_d_update": ("hbm", 8.0 * m * r + 8.0 * m + 48.0 * r),
         "ht_z": ("hbm", 12.0 * nnz + 4.0 * (N + 1) + 8.0 * (N + m)),
         "gamma_apply": ("tensor", fft_flops),
-        "mean_update": ("hbm", 8.0 * N * r + 24.0 * N + 8.0 * r),
+        "mean_update": ("hbm", 8.0 * N * r + 24.0 * N + 8.0 * r + uq_bytes),
     }
 
 
@@ -263,9 +265,10 @@ def run_ours(args, rank, world, local_rank):
         UQV = torch.empty(w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
 
     def step_dev(i):
-        ctx.steps_async(yptr(i), 1, w.m)
-        if uq:
-            ctx.realizations_device(w.sample_seed, uq_count, C.c_void_p(UQX.data_ptr()), C.c_void_p(UQV.data_ptr()))
+        if uq:  # the step's U pass fused with diag Σ and the realizations of the new state
+            ctx.step_uq_device(yptr(i), w.sample_seed, uq_count, C.c_void_p(UQX.data_ptr()), C.c_void_p(UQV.data_ptr()))
+        else:
+            ctx.steps_async(yptr(i), 1, w.m)
 
     # ---- warm-up
     for i in range(args.warmup):
@@ -332,11 +335,13 @@ def run_ours(args, rank, world, local_rank):
 
     def step_e2e(i):
         # fkf_step returns the new state (fast_filter.hpp:84-125): y in, α/d/mean out, one round trip
-        check(L.fkb_fkf_step_state(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m, C.byref(a_),
-                                   C.c_void_p(pin_d.data_ptr()), C.c_void_p(pin_mean.data_ptr())))
-        if uq:
-            check(L.fkb_realizations_with_variance(ctx._f, w.sample_seed, uq_count, C.c_void_p(pin_x.data_ptr()),
-                                                   C.c_void_p(pin_v.data_ptr())))
+        if uq:  # + diag Σ and the realizations of the new state from the same fused U pass
+            check(L.fkb_fkf_step_uq(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m, w.sample_seed, uq_count,
+                                    C.c_void_p(pin_x.data_ptr()), C.c_void_p(pin_v.data_ptr()), C.byref(a_),
+                                    C.c_void_p(pin_d.data_ptr()), C.c_void_p(pin_mean.data_ptr())))
+        else:
+            check(L.fkb_fkf_step_state(ctx._f, C.c_void_p(pin_y[i % S].data_ptr()), w.m, C.byref(a_),
+                                       C.c_void_p(pin_d.data_ptr()), C.c_void_p(pin_mean.data_ptr())))
 
     for i in range(args.warmup):
         step_e2e(i)
@@ -397,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
     hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
     # ---- roofline of the dominant step phase
-    work = phase_work(w, r, fcol, float(h.nnz))
+    work = phase_work(w, r, fcol, float(h.nnz), uq_count if uq else -1)
     tsrc = kernel_ms if kernel_ms else phases
     # Side-branch kernels (the next step's K, dc/d-update) overlap the main branch and do not
     # bound the step; the roofline reports the dominant kernel on the step's critical path and

@@ -96,6 +96,14 @@ int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen);
  * fkf_step returns the new LowRankState by value (fast_filter.hpp:84-125); d/mean may be null */
 int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* alpha, double* d, double* mean);
 int fkb_fkf_step_device(fkb_filter* f, const double* d_y);
+/* one step plus the UQ of the new state — diag Σ (var, N) and `count` ≤ 8 conditional
+ * realizations (x, N×count; RealizationPropagator draws (seed, s/2), uq.hpp:86-112) — from ONE
+ * pass over U fused with the mean update (the reference's fkf_step + variance +
+ * RealizationPropagator::at calls, driver.hpp:292-300); host buffers, any output may be null */
+int fkb_fkf_step_uq(fkb_filter* f, const double* y, long long ylen, uint64_t seed, int count, double* x, double* var,
+                    double* alpha, double* d, double* mean);
+/* device buffers, enqueued without a host sync like fkb_fkf_steps_async (fkb_fkf_sync checks and commits) */
+int fkb_fkf_step_uq_device(fkb_filter* f, const double* d_y, uint64_t seed, int count, double* d_x, double* d_var);
 /* nsteps device-resident observations (column k at d_ys + k*ldy) without host syncs;
  * fkb_fkf_sync performs the deferred singularity check and commits the state. */
 int fkb_fkf_steps_async(fkb_filter* f, const double* d_ys, int nsteps, long long ldy);

@@ -55,6 +55,8 @@ SIGNATURES = {
     "fkb_enkf_members": (_i, [_p, _dp]),
     "fkb_enkf_set_members": (_i, [_p, _dp]),
     "fkb_enkf_mean": (_i, [_p, _dp]),
+    "fkb_fkf_step_uq": (_i, [_p, _p, _ll, _u64, _i, _p, _p, _p, _p, _p]),
+    "fkb_fkf_step_uq_device": (_i, [_p, _p, _u64, _i, _p, _p]),
     "fkb_ekf_create": (_i, [_p, _i, _i, _ip, _ip, _dp, C.POINTER(_p)]),
     "fkb_ekf_destroy": (None, [_p]),
     "fkb_ekf_reset": (_i, [_p, _dp]),

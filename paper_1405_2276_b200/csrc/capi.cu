@@ -286,6 +286,7 @@ int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen) {
         if (ylen != F.m)
             throw std::invalid_argument("fkf_step: observation length " + std::to_string(ylen) + " does not match " +
                                         std::to_string(F.m) + " measurements");
+        F.set_step_uq(false);
         F.step_host(y);
     });
 }
@@ -296,6 +297,7 @@ int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* a
         if (ylen != F.m)
             throw std::invalid_argument("fkf_step: observation length " + std::to_string(ylen) + " does not match " +
                                         std::to_string(F.m) + " measurements");
+        F.set_step_uq(false);
         F.step_host_state(y, d, mean);
         if (alpha) *alpha = F.alpha;
     });
@@ -303,13 +305,47 @@ int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* a
 int fkb_fkf_step_device(fkb_filter* f, const double* d_y) {
     return guarded([&] {
         need(f, "filter");
+        f->f->set_step_uq(false);
         f->f->step(d_y);
     });
 }
 int fkb_fkf_steps_async(fkb_filter* f, const double* d_ys, int nsteps, long long ldy) {
     return guarded([&] {
         need(f, "filter");
+        f->f->set_step_uq(false);
         f->f->steps_async(d_ys, nsteps, ldy);
+    });
+}
+int fkb_fkf_step_uq_device(fkb_filter* f, const double* d_y, uint64_t seed, int count, double* d_x, double* d_var) {
+    return guarded([&] {
+        need(f, "filter");
+        f->f->step_uq(d_y, seed, count, d_x, d_var);
+    });
+}
+int fkb_fkf_step_uq(fkb_filter* f, const double* y, long long ylen, uint64_t seed, int count, double* x, double* var,
+                    double* alpha, double* d, double* mean) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (ylen != F.m)
+            throw std::invalid_argument("fkf_step: observation length " + std::to_string(ylen) + " does not match " +
+                                        std::to_string(F.m) + " measurements");
+        F.set_step_uq(true, seed, count);
+        F.step_host_state(y, d, mean);
+        if (alpha) *alpha = F.alpha;
+        if (F.r == 0) {  // rank-0 GEP: the separate UQ pass
+            F.host_out.ensure(size_t(F.n) * (count + 1));
+            F.realizations(seed, count, F.host_out.p + F.n, F.host_out.p);
+            if (var) FKB_CUDA(cudaMemcpyAsync(var, F.host_out.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
+            if (x && count)
+                FKB_CUDA(cudaMemcpyAsync(x, F.host_out.p + F.n, sizeof(double) * size_t(F.n) * count,
+                                         cudaMemcpyDeviceToHost, F.s));
+        } else {
+            if (var) FKB_CUDA(cudaMemcpyAsync(var, F.uq_var.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
+            if (x && count)
+                FKB_CUDA(cudaMemcpyAsync(x, F.uq_x.p, sizeof(double) * size_t(F.n) * count, cudaMemcpyDeviceToHost, F.s));
+        }
+        FKB_CUDA(cudaStreamSynchronize(F.s));
     });
 }
 int fkb_fkf_sync(fkb_filter* f, int nsteps) {

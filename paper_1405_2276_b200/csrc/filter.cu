@@ -273,7 +273,21 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
         double acc[8];
 #pragma unroll
         for (int s = 0; s < 8; ++s) acc[s] = 0.0;
-        for (int j = 0; j < r; ++j) {
+        int j0 = 0;
+        for (; j0 + 8 <= r; j0 += 8) {  // 8 coalesced column loads in flight per thread
+            double u[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) u[q] = __ldcs(U + i + (long long)(j0 + q) * n);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = j0 + q;
+                vs = fma(u[q] * u[q], ds[j], vs);
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    if (s < count) acc[s] = fma(u[q], P[j * count + s], acc[s]);
+            }
+        }
+        for (int j = j0; j < r; ++j) {
             const double u = U[i + (long long)j * n];
             vs = fma(u * u, ds[j], vs);
 #pragma unroll
@@ -287,6 +301,78 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
             if (s < count) {
                 const double z = Z[i + (long long)s * n];
                 X[i + (long long)s * n] = alpha == 0.0 ? mi : mi + (ra * z - ra * acc[s]);
+            }
+    }
+}
+
+// The step's U pass fused with the UQ of the new state (c3-style workloads: diag Σ and
+// `count` conditional realizations after every step): per row i of the column-major U,
+//   mean_i ← (mean_i + α·t_i) − Σ_j U_ij dc_j                      (fast_filter.hpp:114-116)
+//   var_i = αθ − Σ_j d_j U_ij²,  x_s,i = mean_i + √α(z_s,i − Σ_j U_ij Σ₋_j (Ūᵀz_s)_j)
+// with α, d already updated for this step (α_dev[1]; d by the Woodbury epilogue), one thread
+// per row and 8 coalesced column loads in flight.  The failure flag gates every write, as
+// EpiMean, and is published to the mapped host slot.
+__global__ void __launch_bounds__(256, 2) k_mean_uq(long long n, int r, const double* __restrict__ U,
+                                                const double* __restrict__ dc, const double* __restrict__ d,
+                                                const double* __restrict__ alpha_dev, double theta,
+                                                const double* __restrict__ t, double* __restrict__ mean, int count,
+                                                const double* __restrict__ Z, const double* __restrict__ proj,
+                                                double* __restrict__ X, double* __restrict__ var,
+                                                const int* __restrict__ info,
+                                                const unsigned long long* __restrict__ hout) {
+    extern __shared__ double sh[];
+    double* cs = sh;           // dc (r)
+    double* ds = sh + r;       // d  (r)
+    double* P = sh + 2 * r;    // Σ₋ ⊙ Ūᵀz_s (r × count)
+    const int bad = *info;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+    if (bad) return;
+    const double alpha = alpha_dev[1];
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        cs[j] = dc[j];
+        ds[j] = d[j];
+        const double sm = 1.0 - sqrt(fmax(1.0 - d[j] / alpha, 0.0));  // uq.hpp:59-64
+        for (int s = 0; s < count; ++s) P[j * count + s] = sm * proj[j + (long long)s * r];
+    }
+    __syncthreads();
+    const double ra = sqrt(alpha);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double vm = 0.0, vs = 0.0;
+        double acc[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[s] = 0.0;
+        int j0 = 0;
+        for (; j0 + 8 <= r; j0 += 8) {
+            double u[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) u[q] = __ldcs(U + i + (long long)(j0 + q) * n);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = j0 + q;
+                vm = fma(u[q], cs[j], vm);
+                vs = fma(u[q] * u[q], ds[j], vs);
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    if (s < count) acc[s] = fma(u[q], P[j * count + s], acc[s]);
+            }
+        }
+        for (int j = j0; j < r; ++j) {
+            const double u = U[i + (long long)j * n];
+            vm = fma(u, cs[j], vm);
+            vs = fma(u * u, ds[j], vs);
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+                if (s < count) acc[s] = fma(u, P[j * count + s], acc[s]);
+        }
+        const double mi = (mean[i] + alpha * t[i]) - vm;
+        mean[i] = mi;
+        if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = mi;
+        if (var) var[i] = alpha * theta - vs;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if (s < count) {
+                const double z = Z[i + (long long)s * n];
+                X[i + (long long)s * n] = mi + (ra * z - ra * acc[s]);
             }
     }
 }
@@ -791,7 +877,17 @@ void Filter::enqueue_step(const double* d_y) {
     cov->apply1(t.p, t.p);
     mark("gamma_apply");
     if (r > 0 && par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
-    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p, hostout.p}, s);
+    if (uq_count >= 0 && r > 0) {  // U pass + diag Σ + realizations of the new state
+        const size_t shm = sizeof(double) * size_t(r) * (2 + std::max(uq_count, 1));
+        k_mean_uq<<<ceil_div(n, 256), 256, shm, s>>>(n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
+                                                     uq_count, uq_count ? draws.p : nullptr,
+                                                     uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
+                                                     hostout.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    } else {
+        launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p, hostout.p}, s);
+    }
     if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
@@ -988,7 +1084,7 @@ void Filter::finish_async(int nsteps) {
 std::vector<double> Filter::d_host() const { return download(d.p, size_t(r), s); }
 
 void Filter::variance(double* d_out) {
-    const int blocks = std::min(ceil_div(n, 256), 148 * 4);
+    const int blocks = ceil_div(n, 256);
     k_uq<<<blocks, 256, sizeof(double) * size_t(std::max(r, 1)), s>>>(n, state_rank ? r : 0, U.p, d.p, alpha_dev.p,
                                                                      cov->spec.theta, mean.p, 0, nullptr, nullptr,
                                                                      nullptr, d_out);
@@ -1026,33 +1122,69 @@ double Filter::relative_entropy() {  // uq.hpp:39-53
 // count realizations x_s = mean + √α(z_s − U Σ₋ Ūᵀ z_s); draw s = sample_pair(seed, s/2),
 // Re for even s, Im for odd.  Draws and Ūᵀz_s are cached per (seed, count) so each later
 // state costs one pass over U (RealizationPropagator, uq.hpp:86-112).
+void Filter::prepare_draws(uint64_t seed, int count) {
+    if (count <= 0 || (draw_count == count && draw_seed == seed)) return;
+    draws.alloc(size_t(n) * count);
+    DBuf<double> spare(static_cast<size_t>(n));
+    for (int sidx = 0; sidx < count; sidx += 2) {
+        double* a = draws.p + (long long)sidx * n;
+        double* b = sidx + 1 < count ? draws.p + (long long)(sidx + 1) * n : spare.p;
+        cov->sample_pair(seed, uint64_t(sidx / 2), a, b);
+    }
+    draw_proj.alloc(size_t(std::max(r, 1)) * count);
+    if (r > 0) {
+        GemmArgs g;
+        g.M = r; g.N = count; g.K = int(n);
+        g.A = Ubar.p; g.lda = n; g.transA = 1;
+        g.B = draws.p; g.ldb = n;
+        g.C = draw_proj.p; g.ldc = r;
+        g.splitk = gemm_pick_splitk(r, count, int(n));
+        ws.ensure(gemm_ws_elems(g));
+        gemm(g, ws.p, s);
+    }
+    FKB_CUDA(cudaStreamSynchronize(s));
+    draw_seed = seed;
+    draw_count = count;
+    if (uq_count > 0) drop_graphs();  // the fused step graph holds the draw buffers
+}
+
+void Filter::set_step_uq(bool on, uint64_t seed, int count) {
+    if (on && (count < 0 || count > 8)) throw std::invalid_argument("realizations: count must lie in [0, 8]");
+    const int want = on ? count : -1;
+    if (on) {
+        prepare_draws(seed, count);
+        uq_x.ensure(size_t(n) * std::max(count, 1));
+        uq_var.ensure(size_t(n));
+    }
+    if (want != uq_count) {
+        uq_count = want;
+        drop_graphs();
+    }
+}
+
+// One step on device y with diag Σ and `count` realizations of the new state from the fused
+// U pass, enqueued without a host sync (as steps_async; finish_async() checks and commits);
+// outputs copied to d_x (N×count) / d_var when given.  A rank-0 GEP runs the separate UQ kernel.
+void Filter::step_uq(const double* d_y, uint64_t seed, int count, double* d_x, double* d_var) {
+    set_step_uq(true, seed, count);
+    set_hostout(0, 0, 0);
+    if (d_y != ybuf.p)
+        FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_y, sizeof(double) * size_t(m), cudaMemcpyDeviceToDevice, s));
+    launch_step();
+    if (r == 0) {
+        realizations(seed, count, d_x, d_var);
+        return;
+    }
+    if (d_x && count)
+        FKB_CUDA(cudaMemcpyAsync(d_x, uq_x.p, sizeof(double) * size_t(n) * count, cudaMemcpyDeviceToDevice, s));
+    if (d_var) FKB_CUDA(cudaMemcpyAsync(d_var, uq_var.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, s));
+}
+
 void Filter::realizations(uint64_t seed, int count, double* d_out, double* d_var) {
     if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
     if (count == 0 && !d_var) return;
-    if (count > 0 && (draw_count != count || draw_seed != seed)) {
-        draws.alloc(size_t(n) * count);
-        DBuf<double> spare(static_cast<size_t>(n));
-        for (int sidx = 0; sidx < count; sidx += 2) {
-            double* a = draws.p + (long long)sidx * n;
-            double* b = sidx + 1 < count ? draws.p + (long long)(sidx + 1) * n : spare.p;
-            cov->sample_pair(seed, uint64_t(sidx / 2), a, b);
-        }
-        draw_proj.alloc(size_t(std::max(r, 1)) * count);
-        if (r > 0) {
-            GemmArgs g;
-            g.M = r; g.N = count; g.K = int(n);
-            g.A = Ubar.p; g.lda = n; g.transA = 1;
-            g.B = draws.p; g.ldb = n;
-            g.C = draw_proj.p; g.ldc = r;
-            g.splitk = gemm_pick_splitk(r, count, int(n));
-            ws.ensure(gemm_ws_elems(g));
-            gemm(g, ws.p, s);
-        }
-        FKB_CUDA(cudaStreamSynchronize(s));
-        draw_seed = seed;
-        draw_count = count;
-    }
-    const int blocks = std::min(ceil_div(n, 256), 148 * 4);
+    prepare_draws(seed, count);
+    const int blocks = ceil_div(n, 256);
     const int rr = state_rank ? r : 0;
     const size_t shm = sizeof(double) * size_t(std::max(rr, 1)) * (1 + std::max(count, 1));
     k_uq<<<blocks, 256, shm, s>>>(n, rr, U.p, d.p, alpha_dev.p, cov->spec.theta, mean.p, count,

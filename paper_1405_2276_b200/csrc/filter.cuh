@@ -109,6 +109,13 @@ struct Filter {
     uint64_t draw_seed = 0;
     int draw_count = 0;
     DBuf<double> draws, draw_proj;  // N×count, r×count (Ūᵀz)
+    void prepare_draws(uint64_t seed, int count);
+    // fused step + UQ (c3-style workloads): −1 = plain step graphs; 0..8 = the captured step's U
+    // pass also writes diag Σ (uq_var) and uq_count realizations (uq_x) of the new state
+    int uq_count = -1;
+    DBuf<double> uq_x, uq_var;
+    void set_step_uq(bool on, uint64_t seed = 0, int count = 0);
+    void step_uq(const double* d_y, uint64_t seed, int count, double* d_x, double* d_var);
     DBuf<double> sig_minus;
 
     DBuf<double> ybuf;

@@ -304,6 +304,22 @@ class FkfContext:
     def step_device(self, d_y):
         check(lib().fkb_fkf_step_device(self._f, d_y))
 
+    def step_uq(self, y, seed: int, count: int):
+        """One step + diag Σ and `count` realizations of the new state from one fused U pass
+        (fkf_step + variance + RealizationPropagator::at, uq.hpp:16-112).  Returns
+        (state dict, realizations N×count, variance)."""
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        x, var = np.empty(max(self.n * count, 1)), np.empty(self.n)
+        a = C.c_double()
+        d, mean = np.empty(max(self.r, 1)), np.empty(self.n)
+        check(lib().fkb_fkf_step_uq(self._f, ptr(y), len(y), int(seed), int(count), ptr(x), ptr(var), C.byref(a), ptr(d),
+                                    ptr(mean)))
+        st = self.state()
+        return st, x[: self.n * count].reshape(count, self.n).T.copy(), var
+
+    def step_uq_device(self, d_y, seed, count, d_x, d_var):
+        check(lib().fkb_fkf_step_uq_device(self._f, d_y, int(seed), int(count), d_x, d_var))
+
     def steps_async(self, d_ys, nsteps, ldy):
         check(lib().fkb_fkf_steps_async(self._f, d_ys, nsteps, ldy))
 

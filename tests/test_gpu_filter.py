@@ -336,3 +336,35 @@ def test_singular_innovation_raises_and_keeps_state(solver):
     ctx.set_state(before["alpha"], before["d"], before["mean"], before["step"])
     st = P.fkf_step(ctx, ys[1])
     assert st["alpha"] == before["alpha"] + 1.0
+
+
+@pytest.mark.parametrize("name,count,steps", [("c0", 4, 4), ("c3", 8, 2)])
+def test_fused_step_uq_matches_separate_calls(name, count, steps):
+    """fkb_fkf_step_uq (the step's U pass fused with diag Σ and the realizations of the new
+    state) against fkf_step followed by the separate UQ calls on a twin filter, plus a
+    plain step in between (graph mode switch) and the device entry point."""
+    from paper_1405_2276_b200._native import DeviceArray
+    w, h, ys, s2 = workload_inputs(name, steps + 1)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    a = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    b = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    for i, y in enumerate(ys[:steps]):
+        st, x, var = a.step_uq(y, w.sample_seed, count)
+        sb = P.fkf_step(b, y)
+        assert np.array_equal(st["d"], sb["d"]) and st["alpha"] == sb["alpha"]
+        # the fused pass sums U·dc per row sequentially, the plain U pass by warp reductions
+        assert rel_err(st["mean"], sb["mean"]) < 1e-11
+        assert rel_err(var, b.variance()) < 1e-13
+        xb = b.realizations(w.sample_seed, count)
+        assert rel_err(x - st["mean"][:, None], xb - sb["mean"][:, None]) < 1e-11
+        if i == 0:  # a plain step on both, then back to the fused graphs
+            P.fkf_step(a, ys[steps])
+            P.fkf_step(b, ys[steps])
+    dy = DeviceArray.from_host(np.ascontiguousarray(ys[0]))
+    dx, dv = DeviceArray(w.N * count), DeviceArray(w.N)
+    a.step_uq_device(dy.ptr, w.sample_seed, count, dx.ptr, dv.ptr)
+    a.sync(1)
+    b.step_device(dy.ptr)
+    assert rel_err(dv.to_host(), b.variance()) < 1e-13
+    assert rel_err(dx.to_host().reshape(count, w.N).T, b.realizations(w.sample_seed, count)) < 1e-11
