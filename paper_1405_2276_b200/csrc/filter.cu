@@ -312,14 +312,14 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
 // with α, d already updated for this step (α_dev[1]; d by the Woodbury epilogue), one thread
 // per row and 8 coalesced column loads in flight.  The failure flag gates every write, as
 // EpiMean, and is published to the mapped host slot.
-__global__ void __launch_bounds__(256, 2) k_mean_uq(long long n, int r, const double* __restrict__ U,
-                                                const double* __restrict__ dc, const double* __restrict__ d,
-                                                const double* __restrict__ alpha_dev, double theta,
-                                                const double* __restrict__ t, double* __restrict__ mean, int count,
-                                                const double* __restrict__ Z, const double* __restrict__ proj,
-                                                double* __restrict__ X, double* __restrict__ var,
-                                                const int* __restrict__ info,
-                                                const unsigned long long* __restrict__ hout) {
+__global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const double* __restrict__ U,
+                                                   const double* __restrict__ dc, const double* __restrict__ d,
+                                                   const double* __restrict__ alpha_dev, double theta,
+                                                   const double* __restrict__ t, double* __restrict__ mean, int count,
+                                                   const double* __restrict__ Z, const double* __restrict__ proj,
+                                                   double* __restrict__ X, double* __restrict__ var,
+                                                   const int* __restrict__ info,
+                                                   const unsigned long long* __restrict__ hout) {
     extern __shared__ double sh[];
     double* cs = sh;           // dc (r)
     double* ds = sh + r;       // d  (r)
@@ -342,12 +342,12 @@ __global__ void __launch_bounds__(256, 2) k_mean_uq(long long n, int r, const do
 #pragma unroll
         for (int s = 0; s < 8; ++s) acc[s] = 0.0;
         int j0 = 0;
-        for (; j0 + 8 <= r; j0 += 8) {
-            double u[8];
+        for (; j0 + 16 <= r; j0 += 16) {  // 16 coalesced column loads in flight per thread
+            double u[16];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) u[q] = __ldcs(U + i + (long long)(j0 + q) * n);
+            for (int q = 0; q < 16; ++q) u[q] = __ldcs(U + i + (long long)(j0 + q) * n);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 16; ++q) {
                 const int j = j0 + q;
                 vm = fma(u[q], cs[j], vm);
                 vs = fma(u[q] * u[q], ds[j], vs);
@@ -879,7 +879,7 @@ void Filter::enqueue_step(const double* d_y) {
     if (r > 0 && par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
     if (uq_count >= 0 && r > 0) {  // U pass + diag Σ + realizations of the new state
         const size_t shm = sizeof(double) * size_t(r) * (2 + std::max(uq_count, 1));
-        k_mean_uq<<<ceil_div(n, 256), 256, shm, s>>>(n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
+        k_mean_uq<<<ceil_div(n, 128), 128, shm, s>>>(n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
                                                      uq_count, uq_count ? draws.p : nullptr,
                                                      uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
                                                      hostout.p);
