@@ -760,9 +760,12 @@ bool Cov::try_spectrum(double& worst) {  // covariance.hpp:264-298
     FKB_CUDA(cudaMemcpyAsync(spec_half.p, sh.data(), sh.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
     FKB_CUDA(cudaMemcpyAsync(amp_full.p, amp.data(), amp.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
     FKB_CUDA(cudaStreamSynchronize(stream));
-    // Batch so the intermediate stays well inside the 126 MB L2.
+    // Column batches of the blocked Γ·X: larger batches shorten the per-launch wave tails of
+    // the three passes, and that outweighs keeping the intermediate L2-resident (measured at
+    // c2: 45 columns (48 MB) 9.9 TF/s, 128 10.6, 256 11.2, 592 11.6).  Budget 640 MB, ≤ 1024.
     const size_t per_col = size_t(nky) * size_t(nx) * sizeof(double2);
-    batch_cap = int(std::max<size_t>(1, std::min<size_t>(256, (48u << 20) / per_col)));
+    batch_cap = int(std::max<size_t>(1, std::min<size_t>(1024, (size_t(640) << 20) / per_col)));
+    if (const char* e = std::getenv("FKB_GX_BATCH")) batch_cap = std::max(1, std::atoi(e));  // tuning aid
     // One workspace for the whole lifetime (graph-captured steps hold its address):
     // batched Γ-apply intermediate or the sampler's my×nx column pass.
     work.release();
