@@ -14,6 +14,7 @@
 #include <cmath>
 #include <stdexcept>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "host_linalg.h"
@@ -128,7 +129,8 @@ void sym_eig_small(int n, const double* A, double* w, double* Z) {
     auto at = [&](int i, int j) -> double& { return a[size_t(i) + size_t(j) * N]; };
     for (int j = 0; j < n; ++j)  // symmetrize into full storage from the lower triangle
         for (int i = j + 1; i < n; ++i) at(j, i) = at(i, j);
-    const bool par = n >= 400;  // below this the OpenMP fork/join costs more than it saves
+    static const int par_min = std::getenv("FKB_EIG_PAR") ? std::atoi(std::getenv("FKB_EIG_PAR")) : 400;
+    const bool par = n >= par_min;  // below this the OpenMP fork/join costs more than it saves
     std::vector<double> p(N), wv(N);
     for (int k = 0; k + 2 < n; ++k) {
         // Householder v (v₀ = 1) with (I − τvvᵀ)x = βe₁ for x = A[k+1:, k]
