@@ -222,7 +222,7 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
         linearize(a_bc);
         clk.lap("linearize");
         if (m > 0) {
-            build_hgh(cov, Hk, G.p, s);  // H_k Γ H_kᵀ (:171-176)
+            build_hgh(cov, Hk, G.p, s, &hgh_ws);  // H_k Γ H_kᵀ (:171-176)
             clk.lap("HkGHkT");
             if (r > 0) spmm(Hk, W.p, n, r, HW.p, m, 1.0, 0.0, s);  // H_k W (:173)
             GemmArgs g;  // S = αG_k − (H_kW) D (H_kW)ᵀ + σ²I (:175-178)
@@ -287,7 +287,7 @@ void Ekf::step(const double* y_h, double sigma2, double a_bc, const EkfOptions& 
     }
     // GHEP of H_lastᵀH_last/σ² (:198-203); H_k holds the last linearization
     const long long k_rank = o.k_rank < 0 ? m : o.k_rank;
-    GepDev g;
+    GepDev& g = gep;  // device temporaries persist across steps
     randomized_ghep_device(cov, Hk, HkT, sigma2, k_rank, o.oversampling, o.seed, ws, s, g);
     last_gep_rank = g.r;
     clk.lap("ghep");
@@ -303,11 +303,9 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
     PhaseClock ck{s};
     const int kv = g.r;
     std::vector<double> dsum;  // D̂ before the d̂ > 1e-14 filter (lowrank.hpp:248-249)
-    DBuf<double> Wn, Wbn;
     std::vector<int> keep;
     std::vector<double> Ek;  // (r + kh) × |keep| combination of [W, V̂], column-major
     int nm = 0, kh = 0;
-    DBuf<double> Vh, Vhb;
     if (kv == 0 || r == 0) {
         if (kv == 0) dsum = d_bar;
         else dsum = g.lambda_h;
@@ -317,8 +315,8 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
         const int src_r = kv == 0 ? r : kv;
         const double* src = kv == 0 ? W.p : g.U.p;
         const double* srcb = kv == 0 ? Wbar.p : g.Ubar.p;
-        Wn.alloc(size_t(n) * std::max(rk, 1));
-        Wbn.alloc(size_t(n) * std::max(rk, 1));
+        Wn.ensure(size_t(n) * std::max(rk, 1));
+        Wbn.ensure(size_t(n) * std::max(rk, 1));
         for (int i = 0; i < rk; ++i) {
             FKB_CUDA(cudaMemcpyAsync(Wn.p + (long long)i * n, src + (long long)keep[size_t(i)] * n, sizeof(double) * n,
                                      cudaMemcpyDeviceToDevice, s));
@@ -328,14 +326,17 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
         (void)src_r;
     } else {
         // ---- b_orthonormalize(V = U, Γ⁻¹, against = W) by block CGS2 (lowrank.hpp:53-106, :254)
-        DBuf<double> C(size_t(r) * kv), C2(size_t(r) * kv), V(size_t(n) * kv), Vb(size_t(n) * kv);
+        DBuf<double>& C = tmp(0, size_t(r) * kv);
+        DBuf<double>& C2 = tmp(1, size_t(r) * kv);
+        DBuf<double>& V = tmp(2, size_t(n) * kv);
+        DBuf<double>& Vb = tmp(3, size_t(n) * kv);
         gram_tn(n, r, kv, Wbar.p, g.U.p, C.p, ws, s);                                // C = W̄ᵀV (:258)
         gemm_nn(n, kv, r, -1.0, W.p, C.p, r, 1.0, g.U.p, V.p, s);                    // V₁ = V − WC
         gemm_nn(n, kv, r, -1.0, Wbar.p, C.p, r, 1.0, g.Ubar.p, Vb.p, s);             // V̄₁ = V̄ − W̄C
         gram_tn(n, r, kv, Wbar.p, V.p, C2.p, ws, s);                                 // second pass
         gemm_nn(n, kv, r, -1.0, W.p, C2.p, r, 1.0, V.p, V.p, s);
         gemm_nn(n, kv, r, -1.0, Wbar.p, C2.p, r, 1.0, Vb.p, Vb.p, s);
-        DBuf<double> Gd(size_t(kv) * kv);
+        DBuf<double>& Gd = tmp(4, size_t(kv) * kv);
         gram_tn(n, kv, kv, V.p, Vb.p, Gd.p, ws, s);
         std::vector<double> Gh = download(Gd.p, size_t(kv) * kv, s);
         // projected Γ⁻¹-norms (pre-norms are 1: U is Γ⁻¹-orthonormal); MGS drops ≤ 1e-12 (:92-95)
@@ -363,22 +364,24 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
                 for (int c = 0; c < k1; ++c)
                     for (int p = 0; p < kl; ++p)
                         T1[size_t(live[size_t(p)]) + size_t(c) * kv] = W1[size_t(p) + size_t(c) * kl] * sc[size_t(live[size_t(p)])];
-                DBuf<double> Td(T1.size());
+                DBuf<double>& Td = tmp(5, T1.size());
                 upload(Td.p, T1, s);
-                DBuf<double> Q(size_t(n) * k1), Qb(size_t(n) * k1), C3(size_t(r) * k1);
+                DBuf<double>& Q = tmp(6, size_t(n) * k1);
+                DBuf<double>& Qb = tmp(7, size_t(n) * k1);
+                DBuf<double>& C3 = tmp(8, size_t(r) * k1);
                 tall_times_small(n, kv, k1, V.p, Td.p, Q.p, s);
                 tall_times_small(n, kv, k1, Vb.p, Td.p, Qb.p, s);
                 gram_tn(n, r, k1, Wbar.p, Q.p, C3.p, ws, s);  // third projection after normalization
                 gemm_nn(n, k1, r, -1.0, W.p, C3.p, r, 1.0, Q.p, Q.p, s);
                 gemm_nn(n, k1, r, -1.0, Wbar.p, C3.p, r, 1.0, Qb.p, Qb.p, s);
-                DBuf<double> G2(size_t(k1) * k1);
+                DBuf<double>& G2 = tmp(9, size_t(k1) * k1);
                 gram_tn(n, k1, k1, Q.p, Qb.p, G2.p, ws, s);
                 std::vector<double> W2 = gram_inv_sqrt(k1, download(G2.p, size_t(k1) * k1, s), 1e-13, kh);
                 if (kh > 0) {
-                    DBuf<double> T2(W2.size());
+                    DBuf<double>& T2 = tmp(10, W2.size());
                     upload(T2.p, W2, s);
-                    Vh.alloc(size_t(n) * kh);
-                    Vhb.alloc(size_t(n) * kh);
+                    Vh.ensure(size_t(n) * kh);
+                    Vhb.ensure(size_t(n) * kh);
                     tall_times_small(n, k1, kh, Q.p, T2.p, Vh.p, s);   // V̂
                     tall_times_small(n, k1, kh, Qb.p, T2.p, Vhb.p, s); // Γ⁻¹V̂
                 }
@@ -386,7 +389,9 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
         }
         // ---- core matrix M = diag(D̄, 0) + [C; R̂] Λ [C; R̂]ᵀ (:257-265)
         nm = r + kh;
-        DBuf<double> Z(size_t(nm) * kv), Md(size_t(nm) * nm), lam{size_t(kv)};
+        DBuf<double>& Z = tmp(11, size_t(nm) * kv);
+        DBuf<double>& Md = tmp(12, size_t(nm) * nm);
+        DBuf<double>& lam = tmp(13, size_t(kv));
         {
             GemmArgs gc;  // rows 0..r-1: C = W̄ᵀV (recomputed into Z's rows)
             gc.M = r; gc.N = kv; gc.K = int(n);
@@ -415,7 +420,7 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
             gm.dA = lam.p;
             gm.C = Md.p; gm.ldc = nm;
             gemm(gm, nullptr, s);
-            DBuf<double> db{size_t(r)};
+            DBuf<double>& db = tmp(14, size_t(r));
             upload(db.p, d_bar, s);
             k_add_diag<<<ceil_div(r, 256), 256, 0, s>>>(r, db.p, Md.p, nm);
             FKB_LAUNCH_CHECK();
@@ -429,7 +434,8 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
             std::vector<double> Mh = download(Md.p, size_t(nm) * nm, s);
             sym_eig_small(nm, Mh.data(), ev.data(), vec.data());
         } else {
-            DBuf<double> th{size_t(nm)}, Vd(size_t(nm) * nm);
+            DBuf<double>& th = tmp(15, size_t(nm));
+            DBuf<double>& Vd = tmp(16, size_t(nm) * nm);
             sym_eig_device(nm, Md.p, nm, th.p, Vd.p, s);
             ev = download(th.p, size_t(nm), s);
             vec = download(Vd.p, size_t(nm) * nm, s);
@@ -451,10 +457,10 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
             const int src = order[size_t(keep[size_t(c)])];
             std::copy(vec.begin() + size_t(src) * nm, vec.begin() + size_t(src + 1) * nm, Ek.begin() + size_t(c) * nm);
         }
-        Wn.alloc(size_t(n) * std::max(rk, 1));
-        Wbn.alloc(size_t(n) * std::max(rk, 1));
+        Wn.ensure(size_t(n) * std::max(rk, 1));
+        Wbn.ensure(size_t(n) * std::max(rk, 1));
         if (rk > 0) {
-            DBuf<double> Ed(Ek.size());
+            DBuf<double>& Ed = tmp(17, Ek.size());
             upload(Ed.p, Ek, s);
             gemm_nn(n, rk, r, 1.0, W.p, Ed.p, nm, 0.0, nullptr, Wn.p, s);      // W' = [W, V̂]·E (:272-277)
             gemm_nn(n, rk, r, 1.0, Wbar.p, Ed.p, nm, 0.0, nullptr, Wbn.p, s);
@@ -472,9 +478,9 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
         dn[size_t(i)] = a * a * dh / (1.0 + a * dh);
     }
     FKB_CUDA(cudaStreamSynchronize(s));
-    W = std::move(Wn);
-    Wbar = std::move(Wbn);
-    d.alloc(size_t(std::max(rk, 1)));
+    std::swap(W, Wn);  // the previous W/W̄ buffers become the next step's output buffers
+    std::swap(Wbar, Wbn);
+    d.ensure(size_t(std::max(rk, 1)));
     upload(d.p, dn, s);
     d_h = std::move(dn);
     r = rk;

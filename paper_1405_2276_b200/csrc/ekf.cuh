@@ -1,6 +1,7 @@
 // ekf.cuh — the fast extended filter (fekf_step, fast_filter.hpp:127-224) on the device.
 #pragma once
 
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,15 @@ struct Ekf {
     int last_gep_rank = 0, last_relin = 0;
 
     DBuf<double> eta, eta2, jac, sinv, heta, G, S, HW, z, tv, gt, dc, ybuf, ws, pws;
+    // persistent temporaries of the per-step GHEP and add_low_rank (no per-step cudaMalloc/Free)
+    GepDev gep;
+    DBuf<double> Wn, Wbn, Vh, Vhb, hgh_ws;
+    std::deque<DBuf<double>> scratch;  // deque: growing keeps references to earlier slots valid
+    DBuf<double>& tmp(size_t slot, size_t count) {
+        if (scratch.size() <= slot) scratch.resize(slot + 1);
+        scratch[slot].ensure(std::max<size_t>(count, 1));
+        return scratch[slot];
+    }
     DBuf<int> info, flags, bad;
 
     Ekf(Cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val);

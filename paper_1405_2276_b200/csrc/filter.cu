@@ -13,6 +13,8 @@
 // Two-pass core T = Qᵀ(AQ) = (HQ)ᵀ(HQ)/σ².
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -419,9 +421,45 @@ void tall_times_small(long long n, int p, int q, const double* A, const double* 
     gemm(g, nullptr, s);
 }
 
-// Symmetric eigen of a small device Gram: returns kept columns W = V·diag(w^{-1/2}) for
-// eigenvalues above tol·max (rank-revealing drop), ordered by ascending eigenvalue.
+// Orthonormalizing transform of a small Gram G (p×p): returns W (p×kept) with WᵀGW = I.
+// Well-conditioned G (every Cholesky pivot² ≥ 1e-10·max G_jj, i.e. far from the tol·max
+// eigenvalue drop): W = L⁻ᵀ from G = LLᵀ (CholQR; ~p³/1.5 flops).  Otherwise the symmetric
+// eigendecomposition: W = V·diag(w^{-1/2}) over eigenvalues above tol·max (rank-revealing
+// drop), ordered by ascending eigenvalue.  Both span the same columns when nothing is dropped.
 std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept) {
+    if (p > 0) {
+        std::vector<double> L(Gh);
+        auto at = [&](int i, int j) -> double& { return L[size_t(i) + size_t(j) * p]; };
+        double dmax = 0.0;
+        for (int j = 0; j < p; ++j) dmax = std::max(dmax, Gh[size_t(j) + size_t(j) * p]);
+        bool ok = dmax > 0.0;
+        for (int j = 0; j < p && ok; ++j) {  // left-looking Cholesky on the lower triangle
+            double dj = at(j, j);
+            for (int k = 0; k < j; ++k) dj -= at(j, k) * at(j, k);
+            if (!(dj >= 1e-10 * dmax)) { ok = false; break; }
+            const double ljj = std::sqrt(dj);
+            at(j, j) = ljj;
+            for (int i = j + 1; i < p; ++i) {
+                double v = 0.5 * (at(i, j) + Gh[size_t(j) + size_t(i) * p]);  // symmetrized entry
+                for (int k = 0; k < j; ++k) v -= at(i, k) * at(j, k);
+                at(i, j) = v / ljj;
+            }
+        }
+        if (ok) {
+            // W = L⁻ᵀ (upper triangular): solve Lᵀ W = I column by column
+            std::vector<double> W(static_cast<size_t>(p) * p, 0.0);
+            for (int c = 0; c < p; ++c) {
+                double* w = W.data() + size_t(c) * p;
+                for (int i = c; i >= 0; --i) {
+                    double v = i == c ? 1.0 : 0.0;
+                    for (int k = i + 1; k <= c; ++k) v -= at(k, i) * w[k];
+                    w[i] = v / at(i, i);
+                }
+            }
+            kept = p;
+            return W;
+        }
+    }
     std::vector<double> G = Gh;
     for (int j = 0; j < p; ++j)
         for (int i = 0; i < j; ++i) G[size_t(i) + size_t(j) * p] = G[size_t(j) + size_t(i) * p] =
@@ -442,11 +480,26 @@ std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double t
     return W;
 }
 
+// FKB_EKF_TRACE=1: phase times of the GHEP on stderr (stream-synchronized)
+struct GhepClock {
+    cudaStream_t s;
+    bool on = std::getenv("FKB_EKF_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void lap(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[ekf]   %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double sigma2, long long k, long long p,
                             uint64_t seed, DBuf<double>& ws, cudaStream_t s, GepDev& out) {
     const long long n = cov->size();
     const int m = H.rows;
     check_nonneg_args(k, p, n);
+    GhepClock gclk{s};
     int& r = out.r;
     int& kept_cols = out.kept_cols;
     std::vector<double>& lambda_h = out.lambda_h;
@@ -458,7 +511,9 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
     lambda_h.clear();
     if (k == 0) return;
     const int l = int(k + p);
-    DBuf<double> A(size_t(n) * l), Y(static_cast<size_t>(n) * l), HO(static_cast<size_t>(m) * l);
+    DBuf<double>& A = out.tmp(0, size_t(n) * l);
+    DBuf<double>& Y = out.tmp(1, size_t(n) * l);
+    DBuf<double>& HO = out.tmp(2, size_t(std::max(m, 1)) * l);
     gaussian_matrix(n, l, seed, 0, A.p, n, s);                    // Ω (lowrank.hpp:157)
     {
         // Ȳ = Hᵀ(HΩ)/σ² (:158-159) on row-major blocks: every nonzero then streams one
@@ -475,22 +530,27 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
     }
     ws.ensure(4096);
     if (sumsq(Y.p, (long long)n * l, ws.p, s) == 0.0) return;     // A = 0 (:161)
+    gclk.lap("ghep: sketch");
     DBuf<double>& Z = A;                                           // Ω no longer needed
     cov->apply(Y.p, n, l, Z.p, n);                                 // Z = ΓȲ
-    DBuf<double> Gd(size_t(l) * l);
+    DBuf<double>& Gd = out.tmp(3, size_t(l) * l);
     gram_tn(n, l, l, Y.p, Z.p, Gd.p, ws, s);                       // G₁ = ȲᵀΓȲ
+    gclk.lap("ghep: gamma_x + gram1");
     int k1 = 0;
     std::vector<double> W1 = gram_inv_sqrt(l, download(Gd.p, size_t(l) * l, s), 1e-13, k1);
+    gclk.lap("ghep: orth1 (host)");
     if (k1 == 0)
         throw std::runtime_error("randomized_ghep: rank collapse — every sketch column was dropped during orthonormalization");
-    DBuf<double> Wd(W1.size());
+    DBuf<double>& Wd = out.tmp(4, W1.size());
     upload(Wd.p, W1, s);
-    DBuf<double> Q1(size_t(n) * k1), Z1(static_cast<size_t>(n) * k1);
+    DBuf<double>& Q1 = out.tmp(5, size_t(n) * k1);
+    DBuf<double>& Z1 = out.tmp(6, size_t(n) * k1);
     tall_times_small(n, l, k1, Y.p, Wd.p, Q1.p, s);                // Q̄₁ = Ȳ W₁
     tall_times_small(n, l, k1, Z.p, Wd.p, Z1.p, s);                // ΓQ̄₁ = Z W₁
     gram_tn(n, k1, k1, Q1.p, Z1.p, Gd.p, ws, s);                   // G₂ = Q̄₁ᵀ Γ Q̄₁
     int k2 = 0;
     std::vector<double> W2 = gram_inv_sqrt(k1, download(Gd.p, size_t(k1) * k1, s), 1e-13, k2);
+    gclk.lap("ghep: orth2 (host)");
     if (k2 == 0)
         throw std::runtime_error("randomized_ghep: rank collapse — every sketch column was dropped during orthonormalization");
     kept_cols = k2;
@@ -498,11 +558,9 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
     // Q̄ = Q̄₁W₂ (into Y), Q = ΓQ̄ = Z₁W₂ (into Z)
     tall_times_small(n, k1, k2, Q1.p, Wd.p, Y.p, s);
     tall_times_small(n, k1, k2, Z1.p, Wd.p, Z.p, s);
-    Q1.release();
-    Z1.release();
     // T = Qᵀ(AQ) = (HQ)ᵀ(HQ)/σ², symmetrized (:186-191)
     spmm(H, Z.p, n, k2, HO.p, m, 1.0, 0.0, s);
-    DBuf<double> Td(size_t(k2) * k2);
+    DBuf<double>& Td = out.tmp(7, size_t(k2) * k2);
     {
         GemmArgs g;
         g.M = k2; g.N = k2; g.K = m;
@@ -520,6 +578,7 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
                                         0.5 * (T[size_t(i) + size_t(j) * k2] + T[size_t(j) + size_t(i) * k2]);
     std::vector<double> ev(static_cast<size_t>(k2)), Sv(static_cast<size_t>(k2) * k2);
     sym_eig_small(k2, T.data(), ev.data(), Sv.data());             // (:193)
+    gclk.lap("ghep: T eig (host)");
     const int kk = int(std::min<long long>(k, k2));                // (:197-205)
     r = kk;
     lambda_h.resize(size_t(kk));
@@ -531,10 +590,10 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
     }
     Wd.ensure(Sk.size());
     upload(Wd.p, Sk, s);
-    lambda.alloc(size_t(kk));
+    lambda.ensure(size_t(std::max(kk, 1)));
     upload(lambda.p, lambda_h, s);
-    U.alloc(size_t(n) * kk);
-    Ubar.alloc(size_t(n) * kk);
+    U.ensure(size_t(n) * std::max(kk, 1));
+    Ubar.ensure(size_t(n) * std::max(kk, 1));
     tall_times_small(n, k2, kk, Z.p, Wd.p, U.p, s);                // U = Q S
     tall_times_small(n, k2, kk, Y.p, Wd.p, Ubar.p, s);             // Ū = Q̄ S = Γ⁻¹U
     FKB_CUDA(cudaStreamSynchronize(s));
@@ -553,12 +612,14 @@ void Filter::ghep(long long k, long long p, uint64_t seed) {
 
 // G = H·ΓHᵀ, symmetrized (fast_filter.hpp:68-72): ΓHᵀ streamed in column batches of ≤ 2²⁷/N
 // densified rows of H, never stored.
-void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s) {
+void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s, DBuf<double>* scratch) {
     const long long n = cov->size();
     const int m = H.rows;
     if (m <= 0) return;
     const int bc = int(std::max<long long>(1, std::min<long long>(m, (1LL << 27) / std::max<long long>(n, 1))));
-    DBuf<double> Ec(size_t(n) * bc);
+    DBuf<double> own;
+    DBuf<double>& Ec = scratch ? *scratch : own;
+    Ec.ensure(size_t(n) * bc);
     for (int c0 = 0; c0 < m; c0 += bc) {
         const int nb = std::min(bc, m - c0);
         FKB_CUDA(cudaMemsetAsync(Ec.p, 0, sizeof(double) * size_t(n) * nb, s));

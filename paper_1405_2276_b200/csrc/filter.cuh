@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdlib>
 
+#include <deque>
 #include <string>
 #include <utility>
 #include <vector>
@@ -18,11 +19,19 @@ struct GepDev {
     int r = 0, kept_cols = 0;
     std::vector<double> lambda_h;
     DBuf<double> lambda, U, Ubar;
+    // device temporaries, kept across calls (the extended filter runs a GHEP every step)
+    std::deque<DBuf<double>> scratch;  // deque: growing keeps references to earlier slots valid
+    DBuf<double>& tmp(size_t slot, size_t count) {
+        if (scratch.size() <= slot) scratch.resize(slot + 1);
+        scratch[slot].ensure(std::max<size_t>(count, 1));
+        return scratch[slot];
+    }
 };
 void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double sigma2, long long k, long long p,
                             uint64_t seed, DBuf<double>& ws, cudaStream_t s, GepDev& out);
 // G = H·Γ·Hᵀ (m×m, ld m), symmetrized
-void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s);
+// (scratch: a persistent N×batch workspace for repeated calls; else a temporary)
+void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s, DBuf<double>* scratch = nullptr);
 void symmetrize(int n, double* A, long long lda, cudaStream_t s);
 // out (r×n column-major, i.e. row-major n×r) = in (n×r column-major)ᵀ
 void transpose_cm(long long n, int r, const double* in, double* out, cudaStream_t s);
