@@ -136,10 +136,10 @@ void Enkf::step(const double* y_h, double sigma2, uint64_t seed) {
         g.alpha = inv;
         g.diag_add = sigma2;
         g.C = Cyy.p; g.ldc = m;
+        g.lower_only = 1;  // the LLT reads the lower triangle only; symmetric by construction
         g.splitk = gemm_pick_splitk(m, m, ne);
         ws.ensure(std::max<size_t>(gemm_ws_elems(g), 1));
         gemm(g, ws.p, s);
-        symmetrize(m, Cyy.p, m, s);
     }
     FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
     pws.ensure(potrf_ws_elems(m) + size_t(64) * ne);
