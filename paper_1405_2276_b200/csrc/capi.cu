@@ -330,22 +330,8 @@ int fkb_fkf_step_uq(fkb_filter* f, const double* y, long long ylen, uint64_t see
         if (ylen != F.m)
             throw std::invalid_argument("fkf_step: observation length " + std::to_string(ylen) + " does not match " +
                                         std::to_string(F.m) + " measurements");
-        F.set_step_uq(true, seed, count);
-        F.step_host_state(y, d, mean);
+        F.step_uq_host(y, seed, count, x, var, d, mean);
         if (alpha) *alpha = F.alpha;
-        if (F.r == 0) {  // rank-0 GEP: the separate UQ pass
-            F.host_out.ensure(size_t(F.n) * (count + 1));
-            F.realizations(seed, count, F.host_out.p + F.n, F.host_out.p);
-            if (var) FKB_CUDA(cudaMemcpyAsync(var, F.host_out.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
-            if (x && count)
-                FKB_CUDA(cudaMemcpyAsync(x, F.host_out.p + F.n, sizeof(double) * size_t(F.n) * count,
-                                         cudaMemcpyDeviceToHost, F.s));
-        } else {
-            if (var) FKB_CUDA(cudaMemcpyAsync(var, F.uq_var.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
-            if (x && count)
-                FKB_CUDA(cudaMemcpyAsync(x, F.uq_x.p, sizeof(double) * size_t(F.n) * count, cudaMemcpyDeviceToHost, F.s));
-        }
-        FKB_CUDA(cudaStreamSynchronize(F.s));
     });
 }
 int fkb_fkf_sync(fkb_filter* f, int nsteps) {

@@ -369,12 +369,14 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const do
         const double mi = (mean[i] + alpha * t[i]) - vm;
         mean[i] = mi;
         if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = mi;
-        if (var) var[i] = alpha * theta - vs;
+        double* vo = hout[4] ? reinterpret_cast<double*>(hout[4]) : var;  // mapped host or device
+        double* xo = hout[3] ? reinterpret_cast<double*>(hout[3]) : X;
+        if (vo) vo[i] = alpha * theta - vs;
 #pragma unroll
         for (int s = 0; s < 8; ++s)
             if (s < count) {
                 const double z = Z[i + (long long)s * n];
-                X[i + (long long)s * n] = mi + (ra * z - ra * acc[s]);
+                xo[i + (long long)s * n] = mi + (ra * z - ra * acc[s]);
             }
     }
 }
@@ -731,7 +733,7 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
     info.alloc(1);
-    hostout.alloc(3);
+    hostout.alloc(5);
     FKB_CUDA(cudaMemset(hostout.p, 0, hostout.bytes()));
     flags.alloc(size_t(2 * ceil_div(std::max(m, 1), 64) + 2));
     reset();
@@ -1083,16 +1085,58 @@ static unsigned long long mapped_host(const void* p) {
     return a.type == cudaMemoryTypeHost && a.devicePointer ? reinterpret_cast<unsigned long long>(a.devicePointer) : 0;
 }
 
-void Filter::set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi) {
-    if (hm == hostout_cache[0] && hd == hostout_cache[1] && hi == hostout_cache[2]) return;
+void Filter::set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi, unsigned long long hx,
+                         unsigned long long hv) {
+    const unsigned long long want[5] = {hm, hd, hi, hx, hv};
+    if (std::equal(want, want + 5, hostout_cache)) return;
     if (!h_hostout)
-        FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_hostout), 3 * sizeof(unsigned long long),
+        FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_hostout), 5 * sizeof(unsigned long long),
                                cudaHostAllocDefault));
     FKB_CUDA(cudaStreamSynchronize(s));  // the staging slots may still feed an earlier copy
-    h_hostout[0] = hostout_cache[0] = hm;
-    h_hostout[1] = hostout_cache[1] = hd;
-    h_hostout[2] = hostout_cache[2] = hi;
-    FKB_CUDA(cudaMemcpyAsync(hostout.p, h_hostout, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < 5; ++i) h_hostout[i] = hostout_cache[i] = want[i];
+    FKB_CUDA(cudaMemcpyAsync(hostout.p, h_hostout, 5 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+}
+
+// step + fused UQ from host y: page-locked x/var buffers are written by the fused U pass
+// straight through mapped host memory (the PCIe writes overlap the pass); others are copied
+void Filter::step_uq_host(const double* h_y, uint64_t seed, int count, double* h_x, double* h_var, double* h_d,
+                          double* h_mean) {
+    set_step_uq(true, seed, count);
+    if (!h_info) FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_info), sizeof(int), cudaHostAllocDefault));
+    const unsigned long long hm = mapped_host(h_mean), hd = (h_d && r > 0) ? mapped_host(h_d) : 0;
+    const unsigned long long hx = (h_x && count) ? mapped_host(h_x) : 0, hv = h_var ? mapped_host(h_var) : 0;
+    const bool zc = h_mean && hm && (!(h_d && r > 0) || hd) && r > 0;
+    const bool zx = zc && (!(h_x && count) || hx) && (!h_var || hv);
+    if (zc) set_hostout(hm, hd, mapped_host(h_info), zx ? hx : 0, zx ? hv : 0);
+    else set_hostout(0, 0, 0);
+    if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_y, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+    launch_step();
+    if (!zc) {
+        FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
+        if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+    }
+    if (r > 0 && !zx) {
+        if (h_var) FKB_CUDA(cudaMemcpyAsync(h_var, uq_var.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        if (h_x && count)
+            FKB_CUDA(cudaMemcpyAsync(h_x, uq_x.p, sizeof(double) * size_t(n) * count, cudaMemcpyDeviceToHost, s));
+    }
+    FKB_CUDA(cudaStreamSynchronize(s));
+    if (*h_info) {
+        k_valid = false;
+        throw std::runtime_error("fkf_step: innovation system is singular");
+    }
+    alpha += 1.0;
+    ++step_no;
+    state_rank = r;
+    if (r == 0) {  // rank-0 GEP: the separate UQ pass
+        host_out.ensure(size_t(n) * (count + 1));
+        realizations(seed, count, host_out.p + n, host_out.p);
+        if (h_var) FKB_CUDA(cudaMemcpyAsync(h_var, host_out.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        if (h_x && count)
+            FKB_CUDA(cudaMemcpyAsync(h_x, host_out.p + n, sizeof(double) * size_t(n) * count, cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+    }
 }
 
 void Filter::step_host_state(const double* h_y, double* h_d, double* h_mean) {

@@ -140,9 +140,13 @@ struct Filter {
     int* h_info = nullptr;                               // pinned failure-flag staging
     // mapped host outputs of the step graph: [0] mean, [1] d, [2] failure flag (0 = none)
     DBuf<unsigned long long> hostout;
-    unsigned long long hostout_cache[3] = {0, 0, 0};
+    // [3] realizations, [4] diag Σ of the fused step + UQ
+    unsigned long long hostout_cache[5] = {0, 0, 0, 0, 0};
     unsigned long long* h_hostout = nullptr;
-    void set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi);
+    void set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi, unsigned long long hx = 0,
+                     unsigned long long hv = 0);
+    void step_uq_host(const double* h_y, uint64_t seed, int count, double* h_x, double* h_var, double* h_d,
+                      double* h_mean);
     // k steps over device-resident observations (column k at d_ys + k·ldy), no host sync;
     // finish_async() performs the deferred singularity check and commits host mirrors.
     void steps_async(const double* d_ys, int nsteps, long long ldy);

@@ -368,3 +368,31 @@ def test_fused_step_uq_matches_separate_calls(name, count, steps):
     b.step_device(dy.ptr)
     assert rel_err(dv.to_host(), b.variance()) < 1e-13
     assert rel_err(dx.to_host().reshape(count, w.N).T, b.realizations(w.sample_seed, count)) < 1e-11
+
+
+def test_fused_step_uq_mapped_host_outputs():
+    """fkb_fkf_step_uq with page-locked output buffers (the fused U pass writes x, diag Σ and
+    the mean through mapped host memory) ≡ the same call with pageable buffers."""
+    import ctypes as C
+    import torch
+    from paper_1405_2276_b200._native import lib
+    w, h, ys, s2 = workload_inputs("c0", 3)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    a = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    b = P.fkf_init(P.CovarianceOperator(P.Grid(w.n, w.n), kern), h, s2, k, p, w.ghep_seed)
+    cnt = 4
+    px = torch.empty(cnt * w.N, dtype=torch.float64).pin_memory()
+    pv = torch.empty(w.N, dtype=torch.float64).pin_memory()
+    pm = torch.empty(w.N, dtype=torch.float64).pin_memory()
+    pd = torch.empty(max(a.rank(), 1), dtype=torch.float64).pin_memory()
+    al = C.c_double()
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    for y in ys:
+        yv = np.ascontiguousarray(y)
+        assert lib().fkb_fkf_step_uq(a._f, C.c_void_p(yv.ctypes.data), w.m, w.sample_seed, cnt, vp(px), vp(pv),
+                                     C.byref(al), vp(pd), vp(pm)) == 0
+        st, x, var = b.step_uq(y, w.sample_seed, cnt)
+        assert np.array_equal(pm.numpy(), st["mean"]) and np.array_equal(pv.numpy(), var)
+        assert np.array_equal(px.numpy().reshape(cnt, w.N).T, x)
+        assert np.array_equal(pd.numpy()[: a.rank()], st["d"]) and al.value == st["alpha"]
