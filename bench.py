@@ -463,7 +463,7 @@ def run_ours(args, rank, world, local_rank):
         "offline_s": offline_s,
         "eig_sweeps": ctx.eig_sweeps(),
     }
-    if not args.no_widened:
+    if not args.no_widened and world == 1:  # replicas (N > 1) report the headline path only
         out["widened"] = widened_paths(args, w, h, ys, s2, cov, rank == 0 and world == 1 and not args.no_cpu_baseline)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, w, h, ys, s2)
