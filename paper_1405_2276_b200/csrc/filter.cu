@@ -621,7 +621,8 @@ void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s, DBuf<double
     const int bc = int(std::max<long long>(1, std::min<long long>(m, (1LL << 27) / std::max<long long>(n, 1))));
     DBuf<double> own;
     DBuf<double>& Ec = scratch ? *scratch : own;
-    Ec.ensure(size_t(n) * bc);
+    Ec.ensure(2 * size_t(n) * bc);  // ΓHᵀ batch (column-major) and its row-major copy
+    double* Er = Ec.p + size_t(n) * bc;
     for (int c0 = 0; c0 < m; c0 += bc) {
         const int nb = std::min(bc, m - c0);
         FKB_CUDA(cudaMemsetAsync(Ec.p, 0, sizeof(double) * size_t(n) * nb, s));
@@ -629,7 +630,11 @@ void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s, DBuf<double
         FKB_LAUNCH_CHECK();
         count_launch();
         cov->apply(Ec.p, n, nb, Ec.p, n);
-        spmm(H, Ec.p, n, nb, G + (long long)c0 * m, m, 1.0, 0.0, s);
+        // H·(ΓHᵀ) on row-major blocks: every nonzero streams one contiguous 8·nb-byte row (the
+        // column-major SpMM would gather 8-byte pieces); the m×nb result lands transposed in
+        // rows c0… of G, which is symmetric (averaged below)
+        transpose_cm(n, nb, Ec.p, Er, s);
+        spmm_rm(H, Er, nb, nb, G + c0, m, 1.0, s);
     }
     symmetrize(m, G, m, s);
 }
