@@ -561,13 +561,16 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
     tall_times_small(n, k1, k2, Q1.p, Wd.p, Y.p, s);
     tall_times_small(n, k1, k2, Z1.p, Wd.p, Z.p, s);
     // T = Qᵀ(AQ) = (HQ)ᵀ(HQ)/σ², symmetrized (:186-191)
-    spmm(H, Z.p, n, k2, HO.p, m, 1.0, 0.0, s);
+    // HQ on row-major blocks (Q transposed into the free Q̄₁ buffer, streaming ray SpMM); the
+    // m×k₂ row-major result is (HQ)ᵀ column-major, so T = XXᵀ/σ² with X = (HQ)ᵀ
+    transpose_cm(n, k2, Z.p, Q1.p, s);
+    spmm_rm(H, Q1.p, k2, k2, HO.p, k2, 1.0, s);
     DBuf<double>& Td = out.tmp(7, size_t(k2) * k2);
     {
         GemmArgs g;
         g.M = k2; g.N = k2; g.K = m;
-        g.A = HO.p; g.lda = m; g.transA = 1;
-        g.B = HO.p; g.ldb = m;
+        g.A = HO.p; g.lda = k2; g.transA = 0;
+        g.B = HO.p; g.ldb = k2; g.transB = 1;
         g.alpha = 1.0 / sigma2;
         g.C = Td.p; g.ldc = k2;
         g.splitk = gemm_pick_splitk(k2, k2, m);
