@@ -88,6 +88,9 @@ int fkb_fkf_init(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* co
 void fkb_filter_destroy(fkb_filter* f);
 int fkb_filter_rank(const fkb_filter* f, int* rank, int* kept_cols);
 int fkb_filter_lambda(fkb_filter* f, double* out); /* GepResult::lambda, descending */
+/* ghep_residual, lowrank.hpp:215-228: per pair ‖A u − λ Γ⁻¹u‖ / max(λ‖Γ⁻¹u‖, ε) with
+ * A = HᵀH/σ², Γ⁻¹u taken from the GHEP's Ū = Γ⁻¹U (exact; the reference solves by CG) */
+int fkb_filter_ghep_residual(fkb_filter* f, double* out);
 /* which: 0 U (N×r), 1 Ū = Γ⁻¹U (N×r), 2 G = HΓHᵀ (m×m), 3 B = HU (m×r) — host copies */
 int fkb_filter_get(fkb_filter* f, int which, double* out);
 /* fkf_step, fast_filter.hpp:84-125, advancing the device-resident state */

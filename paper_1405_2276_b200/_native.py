@@ -57,6 +57,7 @@ SIGNATURES = {
     "fkb_enkf_mean": (_i, [_p, _dp]),
     "fkb_fkf_step_uq": (_i, [_p, _p, _ll, _u64, _i, _p, _p, _p, _p, _p]),
     "fkb_fkf_step_uq_device": (_i, [_p, _p, _u64, _i, _p, _p]),
+    "fkb_filter_ghep_residual": (_i, [_p, _dp]),
     "fkb_ekf_create": (_i, [_p, _i, _i, _ip, _ip, _dp, C.POINTER(_p)]),
     "fkb_ekf_destroy": (None, [_p]),
     "fkb_ekf_reset": (_i, [_p, _dp]),

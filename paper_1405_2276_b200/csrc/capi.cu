@@ -254,6 +254,13 @@ int fkb_filter_rank(const fkb_filter* f, int* rank, int* kept_cols) {
         if (kept_cols) *kept_cols = f->f->kept_cols;
     });
 }
+int fkb_filter_ghep_residual(fkb_filter* f, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        const auto res = f->f->ghep_residual();
+        if (!res.empty()) std::memcpy(out, res.data(), res.size() * sizeof(double));
+    });
+}
 int fkb_filter_lambda(fkb_filter* f, double* out) {
     return guarded([&] {
         need(f, "filter");

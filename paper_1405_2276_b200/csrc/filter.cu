@@ -381,6 +381,34 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const do
     }
 }
 
+// ghep_residual (lowrank.hpp:215-228) per pair j: ‖A u_j − λ_j Γ⁻¹u_j‖ / max(λ_j‖Γ⁻¹u_j‖, ε)
+// with A u_j = Hᵀ(H u_j)/σ² (= Hᵀ B_j/σ², B = HU) and Γ⁻¹u_j = Ū_j exactly (no CG solve)
+__global__ void k_gep_resid(long long n, const double* __restrict__ AU, const double* __restrict__ Ub,
+                            const double* __restrict__ lam, double* __restrict__ out) {
+    const int j = blockIdx.x;
+    const double l = lam[j];
+    const double* a = AU + (long long)j * n;
+    const double* u = Ub + (long long)j * n;
+    double sr = 0.0, su = 0.0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = a[i] - l * u[i];
+        sr = fma(v, v, sr);
+        su = fma(u[i], u[i], su);
+    }
+    __shared__ double red[2][32];
+    for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_down_sync(0xffffffffu, sr, o);
+        su += __shfl_down_sync(0xffffffffu, su, o);
+    }
+    if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = sr; red[1][threadIdx.x >> 5] = su; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a2 = 0.0, u2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a2 += red[0][w]; u2 += red[1][w]; }
+        out[j] = sqrt(a2) / fmax(l * sqrt(u2), 2.220446049250313e-16);
+    }
+}
+
 // --------------------------------------------------------------------------- host side
 void check_nonneg_args(long long k, long long p, long long n) {  // lowrank.hpp:145-151
     if (k < 0 || p < 0) throw std::invalid_argument("randomized_ghep: k and oversampling must be nonnegative");
@@ -1195,6 +1223,17 @@ void Filter::finish_async(int nsteps) {
 }
 
 std::vector<double> Filter::d_host() const { return download(d.p, size_t(r), s); }
+
+std::vector<double> Filter::ghep_residual() {
+    std::vector<double> res(static_cast<size_t>(r));
+    if (r == 0) return res;
+    DBuf<double> AU(size_t(n) * r), out{size_t(r)};
+    spmm(HT, B.p, m, r, AU.p, n, 1.0 / sigma2, 0.0, s);  // Hᵀ(HU)/σ²
+    k_gep_resid<<<r, 256, 0, s>>>(n, AU.p, Ubar.p, lambda.p, out.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+    return download(out.p, size_t(r), s);
+}
 
 void Filter::variance(double* d_out) {
     const int blocks = ceil_div(n, 256);

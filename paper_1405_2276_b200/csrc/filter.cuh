@@ -176,6 +176,7 @@ struct Filter {
     void check_info();                                   // throws on a singular innovation system
     void reset();                                        // zero_start (:30-36)
     void variance(double* d_out);                        // uq.hpp:16-23
+    std::vector<double> ghep_residual();                 // lowrank.hpp:215-228 with Γ⁻¹U = Ū
     double trace_criterion();                            // uq.hpp:27-34
     double relative_entropy();                           // uq.hpp:39-53
     void realizations(uint64_t seed, int count, double* d_out, double* d_var);

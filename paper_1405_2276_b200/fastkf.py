@@ -342,6 +342,12 @@ class FkfContext:
     def reset(self):
         check(lib().fkb_filter_reset(self._f))
 
+    def ghep_residual(self):
+        """lowrank.hpp:215-228 for the context's GEP (Γ⁻¹U from Ū, no CG)."""
+        out = np.empty(max(self.r, 1))
+        check(lib().fkb_filter_ghep_residual(self._f, out))
+        return out[: self.r]
+
     # -- UQ
     def variance(self):
         out = np.empty(self.n)

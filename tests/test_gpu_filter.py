@@ -396,3 +396,20 @@ def test_fused_step_uq_mapped_host_outputs():
         assert np.array_equal(pm.numpy(), st["mean"]) and np.array_equal(pv.numpy(), var)
         assert np.array_equal(px.numpy().reshape(cnt, w.N).T, x)
         assert np.array_equal(pd.numpy()[: a.rank()], st["d"]) and al.value == st["alpha"]
+
+
+def test_ghep_residual_matches_dense():  # lowrank.hpp:215-228, test_lowrank.cpp:159-167
+    """Per-pair GHEP residuals on the device (Γ⁻¹U = Ū) against a dense numpy evaluation with
+    a dense Γ solve; a full-range sketch leaves residuals at rounding level."""
+    p = Problem(20, 20, 4, 6, 1, 2e-4)
+    cov = P.CovarianceOperator(p.grid, p.spec())
+    ctx = P.fkf_init(cov, p.h, p.sigma2, 24, 20, 5)
+    res = ctx.ghep_residual()
+    Hd = csr_dense(p.h)
+    A = Hd.T @ Hd / p.sigma2
+    U = ctx.U()
+    gu = np.linalg.solve(p.gamma(), U)
+    want = np.linalg.norm(A @ U - gu * ctx.lam[None, :], axis=0) / (ctx.lam * np.linalg.norm(gu, axis=0))
+    assert res.shape == (ctx.rank(),)
+    assert np.max(np.abs(res - want)) < 1e-7
+    assert res.max() < 1e-7  # the reference's sketched bound (test_lowrank.cpp:167)
