@@ -149,6 +149,8 @@ int fkb_ekf_step(fkb_ekf* e, const double* y, long long ylen, double sigma2, dou
 int fkb_ekf_state(fkb_ekf* e, double* alpha, int* step, int* rank);
 /* host copies of mean (N), d (r), W (N×r column-major) and W̄ = Γ⁻¹W (N×r); any may be null */
 int fkb_ekf_read(fkb_ekf* e, double* mean, double* d, double* w, double* wbar);
+/* trace_criterion (uq.hpp:25-34) and relative_entropy (uq.hpp:36-53) of the extended state */
+int fkb_ekf_uq(fkb_ekf* e, double* trace, double* entropy);
 /* diagnostics of the last step: GHEP rank and relinearization sweeps run */
 int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps);
 

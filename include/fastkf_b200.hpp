@@ -536,4 +536,18 @@ inline LowRankState read_state(const std::string& path) {
     return s;
 }
 
+// trace_criterion / relative_entropy of an extended-filter state (uq.hpp:25-53), W on the device
+inline double trace_criterion(const LowRankState& state, const CovarianceOperator&) {
+    if (!state.ekf) throw std::invalid_argument("trace_criterion: use the FkfContext overload for constant-H states");
+    double t = 0.0;
+    detail::check(fkb_ekf_uq(state.ekf->e, &t, nullptr));
+    return t;
+}
+inline double relative_entropy(const LowRankState& state) {
+    if (!state.ekf) throw std::invalid_argument("relative_entropy: use the FkfContext overload for constant-H states");
+    double h = 0.0;
+    detail::check(fkb_ekf_uq(state.ekf->e, nullptr, &h));
+    return h;
+}
+
 }  // namespace fastkf

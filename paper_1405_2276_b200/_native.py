@@ -65,6 +65,7 @@ SIGNATURES = {
     "fkb_ekf_state": (_i, [_p, C.POINTER(_d), C.POINTER(_i), C.POINTER(_i)]),
     "fkb_ekf_read": (_i, [_p, _p, _p, _p, _p]),
     "fkb_ekf_last": (_i, [_p, C.POINTER(_i), C.POINTER(_i)]),
+    "fkb_ekf_uq": (_i, [_p, C.POINTER(_d), C.POINTER(_d)]),
     "fkb_filter_destroy": (None, [_p]),
     "fkb_filter_rank": (_i, [_p, _PI, _PI]),
     "fkb_filter_lambda": (_i, [_p, _dp]),

@@ -642,6 +642,15 @@ int fkb_ekf_read(fkb_ekf* e, double* mean, double* d, double* w, double* wbar) {
         FKB_CUDA(cudaStreamSynchronize(E.s));
     });
 }
+int fkb_ekf_uq(fkb_ekf* e, double* trace, double* entropy) {
+    return guarded([&] {
+        need(e, "ekf");
+        double t = 0.0, h = 0.0;
+        e->e->uq_scalars(t, h);
+        if (trace) *trace = t;
+        if (entropy) *entropy = h;
+    });
+}
 int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps) {
     return guarded([&] {
         need(e, "ekf");

@@ -487,4 +487,26 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
     FKB_CUDA(cudaStreamSynchronize(s));
 }
 
+// trace_criterion (uq.hpp:25-34) and relative_entropy (uq.hpp:36-53) of the extended state:
+// φ = αNθ − Σ_j d_j‖W_j‖² (column norms on the device), ½[(N − r)ln α + Σ ln(α − d_j)]
+void Ekf::uq_scalars(double& trace, double& entropy) {
+    trace = alpha * double(n) * cov->spec.theta;
+    if (r > 0) {
+        DBuf<double>& cs = tmp(18, size_t(r));
+        column_sumsq(n, r, W.p, cs.p, s);
+        const std::vector<double> c = download(cs.p, size_t(r), s);
+        for (int j = 0; j < r; ++j) trace -= d_h[size_t(j)] * c[size_t(j)];
+    }
+    if (!(alpha > 0.0)) throw std::invalid_argument("relative_entropy: requires alpha > 0");
+    double sum = (double(n) - double(r)) * std::log(alpha);
+    for (int i = 0; i < r; ++i) {
+        const double gap = alpha - d_h[size_t(i)];
+        if (!(gap > 0.0))
+            throw std::runtime_error("relative_entropy: D_" + std::to_string(i) + " = " + std::to_string(d_h[size_t(i)]) +
+                                     " is not below alpha = " + std::to_string(alpha));
+        sum += std::log(gap);
+    }
+    entropy = 0.5 * sum;
+}
+
 }  // namespace fkb

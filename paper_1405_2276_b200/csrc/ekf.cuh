@@ -56,6 +56,7 @@ struct Ekf {
     Ekf(Cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val);
     void reset(const double* mean0_host);
     void step(const double* y_host, double sigma2, double bc_alpha, const EkfOptions& o);
+    void uq_scalars(double& trace, double& entropy);  // trace_criterion / relative_entropy
 
   private:
     void linearize(double bc_alpha);

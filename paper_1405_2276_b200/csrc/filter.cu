@@ -670,6 +670,13 @@ void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s, DBuf<double
     symmetrize(m, G, m, s);
 }
 
+void column_sumsq(long long n, int r, const double* A, double* out, cudaStream_t s) {
+    if (r <= 0) return;
+    k_colsq<<<r, 256, 0, s>>>(n, A, out);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
 void transpose_cm(long long n, int r, const double* in, double* out, cudaStream_t s) {
     if (n <= 0 || r <= 0) return;
     k_transpose<<<dim3(ceil_div(n, 32), ceil_div(r, 32)), dim3(32, 8), 0, s>>>(n, r, in, out);

@@ -33,6 +33,8 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
 // (scratch: a persistent N×batch workspace for repeated calls; else a temporary)
 void build_hgh(Cov* cov, const DevCsr& H, double* G, cudaStream_t s, DBuf<double>* scratch = nullptr);
 void symmetrize(int n, double* A, long long lda, cudaStream_t s);
+// out[j] = ‖A[:, j]‖² for the n×r column-major A
+void column_sumsq(long long n, int r, const double* A, double* out, cudaStream_t s);
 // out (r×n column-major, i.e. row-major n×r) = in (n×r column-major)ᵀ
 void transpose_cm(long long n, int r, const double* in, double* out, cudaStream_t s);
 // shared helpers (filter.cu)

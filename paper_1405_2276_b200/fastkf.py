@@ -504,6 +504,16 @@ class ExtendedFilter:
             out["wbar"] = wb.T if k else np.zeros((n, 0))
         return out
 
+    def trace_criterion(self) -> float:  # uq.hpp:25-34
+        t = C.c_double()
+        check(lib().fkb_ekf_uq(self._e, C.byref(t), None))
+        return t.value
+
+    def relative_entropy(self) -> float:  # uq.hpp:36-53
+        h = C.c_double()
+        check(lib().fkb_ekf_uq(self._e, None, C.byref(h)))
+        return h.value
+
     def last_step_info(self):
         g, sw = C.c_int(), C.c_int()
         check(lib().fkb_ekf_last(self._e, C.byref(g), C.byref(sw)))

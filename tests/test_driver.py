@@ -80,6 +80,9 @@ def test_driver_ekf_and_enkf(tmp_path):
         _, _, mean = P.read_field(os.path.join(out, f"mean_step{step:03d}.fkf"))
         assert rel_err(mean, g.state(with_w=False)["mean"] + 1.0) < 1e-12
     assert P.read_state(os.path.join(out, "state_step002.fks"))["w"].shape[1] == g.rank()
+    last = open(os.path.join(out, "metrics.csv")).read().splitlines()[-1].split(",")
+    assert abs(float(last[4]) - g.trace_criterion()) <= 1e-12 * abs(g.trace_criterion())
+    assert abs(float(last[5]) - g.relative_entropy()) <= 1e-12 * abs(g.relative_entropy())
     out = str(tmp_path / "enkf")
     r = subprocess.run([exe, d, out, "enkf", "--members", "64"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr

@@ -150,3 +150,19 @@ def test_fekf_c0_first_step_matches_oracle():
     wg = gs["w"] @ (gs["d"][:, None] * (gs["w"].T @ z))
     wo = os_["w"] @ (os_["d"][:, None] * (os_["w"].T @ z))
     assert rel_err(wg, wo) < 1e-9
+
+
+def test_fekf_trace_and_entropy():  # uq.hpp:25-53 on the extended state
+    p = Problem(12, 12, 3, 8, 3, 2e-4, kernel=dict(EXPERIMENT, theta=1e-5, power=1.0))
+    mean0 = np.full(144, O.boxcox(2.0, [1e-4], "forward")[0])
+    cov, g, o = _pair(p, mean0)
+    theta = p.kernel["theta"]
+    for k, y in enumerate(p.obs):
+        seed = W.derive_seed(906, k)
+        g.step(y, p.sigma2, P.BoxCox(2.0), P.FekfOptions(k_rank=p.h.rows, trunc_tol=1e-5, seed=seed))
+        o.step(y, p.sigma2, 2.0, k_rank=p.h.rows, trunc_tol=1e-5, seed=seed)
+        so = o.state()
+        tr = so["alpha"] * 144 * theta - np.sum(so["d"] * np.sum(so["w"] ** 2, axis=0))
+        ent = 0.5 * ((144 - len(so["d"])) * np.log(so["alpha"]) + np.sum(np.log(so["alpha"] - so["d"])))
+        assert abs(g.trace_criterion() - tr) <= 1e-9 * abs(tr)
+        assert abs(g.relative_entropy() - ent) <= 1e-9 * abs(ent)

@@ -181,14 +181,13 @@ int main(int argc, char** argv) {
             write_field(step_file(out, "mean_step", 0, ".fkf"), nx, ny, physical(st.mean));
             for (int k = 1; k <= n_steps; ++k) {
                 opts.seed = derive_seed(seed, 4000 + std::uint64_t(k));  // ekf_seed (driver.hpp:84-86)
-                Row r{k, 0, 0, 0, nan, 0};
+                Row r{k, 0, 0, 0, 0, 0};
                 r.wall = timed([&] { st = fekf_step(st, cov, h, obs[size_t(k - 1)], sigma2, t, opts); });
                 const Vector phys = physical(st.mean);
                 r.rel = rel_l2(phys, read_field(step_file(data, "truth_step", k, ".fkf")).data);
                 r.rank = double(st.rank());
-                double ent = 0.0;  // relative_entropy (uq.hpp:39-53) from α and d
-                for (Index i = 0; i < st.d.size(); ++i) ent += std::log(st.alpha - st.d[i]);
-                r.entropy = 0.5 * (double(grid.size() - st.rank()) * std::log(st.alpha) + ent);
+                r.trace = trace_criterion(st, cov);  // driver.hpp:328-329
+                r.entropy = relative_entropy(st);
                 rows.push_back(r);
                 write_field(step_file(out, "mean_step", k, ".fkf"), nx, ny, phys);
                 if (states == "all" || (states == "final" && k == n_steps))
