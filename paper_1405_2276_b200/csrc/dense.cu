@@ -466,64 +466,58 @@ size_t gram_ws_elems(int M, int N, int K) {
 // --------------------------------------------------------------------------- Cholesky
 constexpr int CNB = 64;
 
-// Factor the kb×kb diagonal block at (k0, k0) in shared memory (right-looking, 256 threads,
-// each owning 16 fixed (i, c) entries so the rank-1 updates need no index division); write L11
-// back, and when dinv ≠ null also L11⁻¹ (kb×kb, ld CNB) to dinv + k0·CNB by the same
-// row-operation sweep on the identity.
+// Factor the kb×kb diagonal block at (k0, k0) in shared memory (right-looking, 256 threads as a
+// 16×16 grid that sweeps only the shrinking trailing triangle; every thread derives the pivot
+// itself, so a step costs two barriers); write L11 back, and when dinv ≠ null also L11⁻¹ (kb×kb,
+// ld CNB) to dinv + k0·CNB by the same row-operation sweep on the identity.
 __global__ void __launch_bounds__(256) k_potrf_diag(double* A, long long lda, int kb, int k0, int* info,
                                                    double* __restrict__ dinv) {
     extern __shared__ double potrf_sm[];
     double (*s)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(potrf_sm);
     double (*x)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(potrf_sm + CNB * (CNB + 1));
-    __shared__ int bad;
+    __shared__ double ld[CNB];
     if (*info) return;
     double* a = A + k0 + (long long)k0 * lda;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     for (int e = tid; e < CNB * CNB; e += 256) {
         const int i = e & (CNB - 1), j = e >> 6;
         s[i][j] = (i < kb && j < kb && i >= j) ? a[i + (long long)j * lda] : 0.0;
         x[i][j] = i == j ? 1.0 : 0.0;
     }
-    if (tid == 0) bad = 0;
     __syncthreads();
     for (int j = 0; j < kb; ++j) {
-        if (tid == 0) {
-            const double d = s[j][j];
-            if (!(d > 0.0)) {
-                bad = 1;
-                atomicCAS(info, 0, k0 + j + 1);
-            } else {
-                s[j][j] = sqrt(d);
-            }
+        const double djj = s[j][j];  // final: updated by step j−1 before the last barrier
+        if (!(djj > 0.0)) {
+            if (tid == 0) atomicCAS(info, 0, k0 + j + 1);
+            return;  // uniform: every thread read the same pivot
         }
+        const double ljj = sqrt(djj), rinv = 1.0 / ljj;
+        if (tid == 0) ld[j] = ljj;
+        if (tid > j && tid < kb) s[tid][j] *= rinv;
         __syncthreads();
-        if (bad) return;
-        const double piv = s[j][j];
-        if (tid < CNB && tid > j && tid < kb) s[tid][j] /= piv;
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < CNB * CNB / 256; ++q) {
-            const int e = tid + 256 * q;
-            const int i = e & (CNB - 1), c = e >> 6;
-            if (c > j && i >= c && i < kb) s[i][c] = fma(-s[i][j], s[c][j], s[i][c]);
+        // trailing triangle rows/cols j+1..kb−1: s[i][c] −= L_ij·L_cj (i ≥ c)
+        for (int c = j + 1 + tx; c < kb; c += 16) {
+            const double lc = s[c][j];
+            for (int i = c + ty; i < kb; i += 16) s[i][c] = fma(-s[i][j], lc, s[i][c]);
         }
         __syncthreads();
     }
     for (int e = tid; e < kb * kb; e += 256) {
         const int i = e % kb, j = e / kb;
-        if (i >= j) a[i + (long long)j * lda] = s[i][j];
+        if (i > j) a[i + (long long)j * lda] = s[i][j];
+        else if (i == j) a[i + (long long)j * lda] = ld[j];
     }
     if (!dinv) return;
-    // L X = I by row sweeps: row j ← row j / L_jj, then rows i > j −= L_ij · row j
+    if (tid < kb) s[tid][tid] = ld[tid];
+    __syncthreads();
+    // L X = I by row sweeps: row j ← row j / L_jj, then rows i > j −= L_ij · row j (cols ≤ j)
     for (int j = 0; j < kb; ++j) {
-        const double piv = s[j][j];
-        if (tid < kb) x[j][tid] /= piv;
+        const double rinv = 1.0 / s[j][j];
+        if (tid <= j) x[j][tid] *= rinv;
         __syncthreads();
-#pragma unroll
-        for (int q = 0; q < CNB * CNB / 256; ++q) {
-            const int e = tid + 256 * q;
-            const int i = e >> 6, c = e & (CNB - 1);
-            if (i > j && i < kb && c <= j) x[i][c] = fma(-s[i][j], x[j][c], x[i][c]);
+        for (int c = tx; c <= j; c += 16) {
+            const double xj = x[j][c];
+            for (int i = j + 1 + ty; i < kb; i += 16) x[i][c] = fma(-s[i][j], xj, x[i][c]);
         }
         __syncthreads();
     }
