@@ -27,9 +27,11 @@ struct EpiAxpby {  // y_i = α·v + β·y_i
     }
 };
 
-// y_i = epi(i, Σ_j A_ij·x_j) for ROW-MAJOR A (m×k, ld ≥ k): each warp owns 4 rows and reads
-// each row as contiguous 256-B chunks, so the matrix streams linearly from HBM (the
-// step's U-pass; U is stored once more row-major for this).
+// y_i = epi(i, Σ_j A_ij·x_j) for ROW-MAJOR A (m×k, ld ≥ k): each warp reads rows as contiguous
+// 256-B chunks, 4 rows at a time, so the matrix streams linearly from HBM (the step's U-pass;
+// U is stored once more row-major for this).  The grid is persistent (one wave
+// of resident CTAs) and each warp owns a contiguous, balanced slice of rows — no second
+// partial wave, every warp finishes within one 4-row group of the others.
 template <class XL, class Epi>
 __global__ void __launch_bounds__(256) k_gemv_rowmajor(long long m, int k, const double* __restrict__ A,
                                                       long long ld, XL xl, Epi epi) {
@@ -37,11 +39,12 @@ __global__ void __launch_bounds__(256) k_gemv_rowmajor(long long m, int k, const
     for (int c = threadIdx.x; c < k; c += blockDim.x) xs[c] = xl(c);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;  // grid-stride over 4-row groups
-    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w * 4 < m; w += nw) {
-    const long long r0 = w * 4;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long lo = m * w / nw, hi = m * (w + 1) / nw;  // this warp's contiguous rows
+    for (long long r0 = lo; r0 < hi; r0 += 4) {
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    const int nq = (int)min(4LL, m - r0);
+    const int nq = (int)min(4LL, hi - r0);
     int c = lane;
     for (; c + 96 < k; c += 128) {  // 16 independent loads in flight per lane
         double v[4][4];
@@ -65,22 +68,89 @@ __global__ void __launch_bounds__(256) k_gemv_rowmajor(long long m, int k, const
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
-    if (lane < 4 && r0 + lane < m) {
+    if (lane < nq) {
         const double v = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
         epi(r0 + lane, v);
     }
     }
 }
 
+// Short-row variant (k ≤ 32·KC): a lane holds its KC row chunks of 4 rows in registers, so a
+// whole 4-row group (4·k doubles per warp) is one round trip to HBM instead of one per
+// 128-column slice plus the 32-wide tail; x lives in registers too.
+template <int KC, class XL, class Epi>
+__global__ void __launch_bounds__(256, 2) k_gemv_rowmajor_reg(long long m, int k, const double* __restrict__ A,
+                                                             long long ld, XL xl, Epi epi) {
+    const int lane = threadIdx.x & 31;
+    double xv[KC];
+#pragma unroll
+    for (int u = 0; u < KC; ++u) xv[u] = lane + 32 * u < k ? xl(lane + 32 * u) : 0.0;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long lo = m * w / nw, hi = m * (w + 1) / nw;
+    for (long long r0 = lo; r0 < hi; r0 += 4) {
+        const int nq = (int)min(4LL, hi - r0);
+        double v[4][KC];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int u = 0; u < KC; ++u)
+                v[q][u] = (q < nq && lane + 32 * u < k) ? __ldcs(A + (r0 + q) * ld + lane + 32 * u) : 0.0;
+        double s[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            s[q] = 0.0;
+#pragma unroll
+            for (int u = 0; u < KC; ++u) s[q] = fma(v[q][u], xv[u], s[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+        if (lane < nq) epi(r0 + lane, lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3]);
+    }
+}
+
+template <int KC, class XL, class Epi>
+inline void launch_gemv_rowmajor_reg(long long m, int k, const double* A, long long ld, XL xl, Epi epi,
+                                     cudaStream_t s) {
+    int dev = 0, sms = 0, per_sm = 0;
+    FKB_CUDA(cudaGetDevice(&dev));
+    FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor_reg<KC, XL, Epi>, 256, 0));
+    const long long ctas = std::min((m + 31) / 32, (long long)std::max(sms, 1) * std::max(per_sm, 1));
+    k_gemv_rowmajor_reg<KC, XL, Epi><<<(unsigned)ctas, 256, 0, s>>>(m, k, A, ld, xl, epi);
+}
+
 template <class XL, class Epi>
 inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long ld, XL xl, Epi epi, cudaStream_t s,
                                  long long max_ctas = 0) {
     if (m <= 0) return;
-    const long long warps = (m + 3) / 4;
-    long long ctas = (warps + 7) / 8;
+    if (k >= 1 && k <= 320 && max_ctas == 0) {  // the step's U pass: rank ≤ 320 held in registers
+        switch ((k + 31) / 32) {
+            case 1: launch_gemv_rowmajor_reg<1>(m, k, A, ld, xl, epi, s); break;
+            case 2: launch_gemv_rowmajor_reg<2>(m, k, A, ld, xl, epi, s); break;
+            case 3: launch_gemv_rowmajor_reg<3>(m, k, A, ld, xl, epi, s); break;
+            case 4: launch_gemv_rowmajor_reg<4>(m, k, A, ld, xl, epi, s); break;
+            case 5: launch_gemv_rowmajor_reg<5>(m, k, A, ld, xl, epi, s); break;
+            case 6: launch_gemv_rowmajor_reg<6>(m, k, A, ld, xl, epi, s); break;
+            case 7: launch_gemv_rowmajor_reg<7>(m, k, A, ld, xl, epi, s); break;
+            case 8: launch_gemv_rowmajor_reg<8>(m, k, A, ld, xl, epi, s); break;
+            case 9: launch_gemv_rowmajor_reg<9>(m, k, A, ld, xl, epi, s); break;
+            default: launch_gemv_rowmajor_reg<10>(m, k, A, ld, xl, epi, s); break;
+        }
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
+    const size_t shm = sizeof(double) * size_t(std::max(k, 1));
+    int dev = 0, sms = 0, per_sm = 0;
+    FKB_CUDA(cudaGetDevice(&dev));
+    FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor<XL, Epi>, 256, shm));
+    const long long warps = (m + 3) / 4;  // at least one 4-row group per warp
+    long long ctas = std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
     if (max_ctas > 0) ctas = std::min(ctas, max_ctas);
-    k_gemv_rowmajor<XL, Epi><<<(unsigned)ctas, 256, sizeof(double) * size_t(std::max(k, 1)), s>>>(m, k, A, ld, xl,
-                                                                                                 epi);
+    k_gemv_rowmajor<XL, Epi><<<(unsigned)ctas, 256, shm, s>>>(m, k, A, ld, xl, epi);
     FKB_LAUNCH_CHECK();
     count_launch();
 }
