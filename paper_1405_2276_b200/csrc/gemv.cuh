@@ -161,9 +161,9 @@ inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long 
 // first FMA, so a chunk costs one memory latency.  Fixed-order reductions (deterministic),
 // no split partials and no second kernel.
 template <class XL, class Epi, int CPC>
-__global__ void __launch_bounds__(256) k_coldot(int m, int n, const double* __restrict__ A, long long lda, XL xl,
+__global__ void __launch_bounds__(256, CPC == 4 ? 4 : 1) k_coldot(int m, int n, const double* __restrict__ A, long long lda, XL xl,
                                                Epi epi) {
-    constexpr int EPT = 8;
+    constexpr int EPT = CPC == 4 ? 4 : 8;  // CPC 4: ≤ 64 regs, 4 CTAs/SM, n = 2048 in one wave
     const int j0 = blockIdx.x * CPC;
     double acc[CPC];
 #pragma unroll
