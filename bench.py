@@ -129,12 +129,19 @@ def replica_throughput(local_ms: float, steps: int, world: int, device) -> float
 
 
 # ----------------------------------------------------------------------------- work accounting
-def phase_work(w, r, fft_flops, nnz, uq_count=-1):
+def phase_work(w, r, fft_flops, nnz, uq_count=-1, fft_split=None):
     """Algorithmic work per launch of each step phase: unique bytes a
     kernel must move for HBM-bound phases, minimal flops for arithmetic phases.  uq_count ≥ 0:
-    the U pass also reads the count draws and writes diag Σ and the count realizations."""
+    the U pass also reads the count draws and writes diag Σ and the count realizations (fused
+    into mean_update); otherwise the U pass (u_pass, side branch) writes v = U·dc and the last
+    FFT pass (mean_update) applies mean ← (mean + α·Γt) − v."""
     N, m = w.N, w.m
     uq_bytes = 0.0 if uq_count < 0 else 8.0 * N * (1 + 2 * uq_count) + 8.0 * r * (2 + uq_count)
+    f_fwd, f_inv, w_bytes = fft_split or (fft_flops, 0.0, 0.0)
+    if uq_count < 0:
+        mean_upd = ("hbm", w_bytes + 24.0 * N)  # W half-spectrum in, mean in/out, v in
+    else:
+        mean_upd = ("hbm", 8.0 * N * r + 24.0 * N + 8.0 * r + uq_bytes)
     return {
         "residual": ("hbm", 12.0 * nnz + 4.0 * (m + 1) + 8.0 * N + 16.0 * m),
         "capacitance": ("tensor", 1.0 * m * r * (r + 1)),  # symmetric Eᵀ·diag·E (lower half)
@@ -146,7 +153,9 @@ def phase_work(w, r, fft_flops, nnz, uq_count=-1):
         "ctz_d_update": ("hbm", 8.0 * m * r + 8.0 * m + 48.0 * r),
         "ht_z": ("hbm", 12.0 * nnz + 4.0 * (N + 1) + 8.0 * (N + m)),
         "gamma_apply": ("tensor", fft_flops),
-        "mean_update": ("hbm", 8.0 * N * r + 24.0 * N + 8.0 * r + uq_bytes),
+        "gamma_fwd": ("tensor", f_fwd),
+        "u_pass": ("hbm", 8.0 * N * r + 8.0 * N + 16.0 * r),
+        "mean_update": mean_upd,
     }
 
 
@@ -154,6 +163,15 @@ def gamma_x_flops(w, mx, my):
     """Pruned-R2C '5 n log2 n' count per column."""
     nx = w.n
     return (5 * nx * my * math.log2(my) + 10 * (my // 2 + 1) * mx * math.log2(mx) + 2 * mx * (my // 2 + 1))
+
+
+def gamma_split(w, mx, my):
+    """The single-vector Γ-apply split as the step runs it: (forward rows + column pass flops,
+    inverse rows flops, bytes of the W[ky][ix] intermediate the inverse rows pass reads)."""
+    nx, nky = w.n, my // 2 + 1
+    rows = 2.5 * nx * my * math.log2(my)
+    cols = 10 * nky * mx * math.log2(mx) + 2 * mx * nky
+    return rows + cols, rows, 16.0 * nky * nx
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -195,10 +213,25 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": k,
                    "parallelism": "host cores"},
-        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model(),
+                         "note": "the oracle's line-by-line C++ restatement of the reference CPU path with OpenMP "
+                                 "over all host threads (the reference itself is single-threaded and needs "
+                                 "Eigen3+FFTW3, absent here); not the reference binary"},
         "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "offline_s": offline,
     }
+
+
+def cpu_model():
+    """The host CPU model (lscpu 'Model name', from /proc/cpuinfo) for the baseline lines."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline(args, w, h, ys, s2):
@@ -219,7 +252,8 @@ def cpu_baseline(args, w, h, ys, s2):
         f.step(ys[(1 + i) % len(ys)])
     dt = time.perf_counter() - t0
     O.set_threads(os.cpu_count() or 1)
-    return {"value": n / dt, "unit": "steps/s", "cores": 1, "kind": "port",
+    return {"value": n / dt, "unit": "steps/s", "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+            "host_threads_available": os.cpu_count(),
             "sample": f"{n} oracle fkf_step on {args.config} (1 thread) after 1 warm step; oracle fkf_init "
                       f"{init_s:.1f}s with {os.cpu_count()} threads, untimed"}
 
@@ -346,16 +380,23 @@ def run_ours(args, rank, world, local_rank):
     for i in range(args.warmup):
         step_e2e(i)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    # each call bracketed by events on the library stream (the calls are synchronous, so the
+    # interval is the call's wall time: H2D of y, the step graph, D2H of the state, host
+    # overhead); L2 flushed before every call, outside the bracket, as in the device loop
+    eps = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            torch.sum(sweep, dim=0, keepdim=True, out=sweep_out)
+        eps[i][0].record(stream)
         step_e2e(args.warmup + i)
-    e1.record(stream)
+        eps[i][1].record(stream)
     torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), f"cuda:{local_rank}")
+    e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in eps), f"cuda:{local_rank}")
     d2h = 8 * (w.N + r) + 8 + 4 + 4 + ((8 * w.N * (1 + uq_count)) if uq else 0)
     e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": 8 * w.m,
-           "d2h_bytes_per_step": d2h}
+           "d2h_bytes_per_step": d2h, "l2": "flushed before every call (outside the per-call event bracket)",
+           "api": "fkb_fkf_step_uq" if uq else "fkb_fkf_step_state"}
 
     # ---- offline kernels: Γ·X on the m + l offline columns, H·X SpMM with l columns
     ncols = w.m + k + p
@@ -393,6 +434,29 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     sp_ms = ga.elapsed_time(gb) / reps
     sp_bytes = 12 * h.nnz + 4 * (h.rows + 1) + 8 * (w.N + w.m) * l
+    # W-block products of the offline GHEP on the DMMA path (lowrank.hpp:53-106, :197-205):
+    # the Γ-metric Gram Ȳᵀ(ΓȲ) (N×l)ᵀ(N×l) and the basis rotation U = Q·S (N×l)(l×k)
+    wprod = {}
+    cur = torch.cuda.current_stream()
+    Yb = torch.randn(l, w.N, dtype=torch.float64, device=f"cuda:{local_rank}")  # column-major N×l
+    Zb = torch.randn(l, w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
+    Gb = torch.empty(l, l, dtype=torch.float64, device=f"cuda:{local_rank}")
+    Sb = torch.randn(k, l, dtype=torch.float64, device=f"cuda:{local_rank}")     # column-major l×k
+    Ub = torch.empty(k, w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    for name, which, args, flops in (
+            ("gram", 0, (w.N, l, l, ptr(Yb), ptr(Zb), ptr(Gb)), 2.0 * w.N * l * l),
+            ("basis", 1, (w.N, l, k, ptr(Yb), ptr(Sb), ptr(Ub)), 2.0 * w.N * l * k)):
+        check(L.fkb_dense_product(which, *args, C.c_void_p(cur.cuda_stream)))
+        torch.cuda.synchronize()
+        ga.record(cur)
+        for _ in range(reps):
+            check(L.fkb_dense_product(which, *args, C.c_void_p(cur.cuda_stream)))
+        gb.record(cur)
+        torch.cuda.synchronize()
+        ms = ga.elapsed_time(gb) / reps
+        wprod[name] = {"tflops": flops / (ms * 1e-3) / 1e12, "ms": ms, "gflop": flops / 1e9}
+    del Yb, Zb, Gb, Sb, Ub
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -402,11 +466,11 @@ def run_ours(args, rank, world, local_rank):
     hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
     # ---- roofline of the dominant step phase
-    work = phase_work(w, r, fcol, float(h.nnz), uq_count if uq else -1)
+    work = phase_work(w, r, fcol, float(h.nnz), uq_count if uq else -1, gamma_split(w, cov.mx, cov.my))
     tsrc = kernel_ms if kernel_ms else phases
-    # Side-branch kernels (the next step's K, dc/d-update) overlap the main branch and do not
-    # bound the step; the roofline reports the dominant kernel on the step's critical path and
-    # the side-branch Gram separately (roofline_side).
+    # The next step's K and the solver-0 dc/d-update overlap the main branch and do not bound the
+    # step; the roofline reports the dominant kernel by in-graph time (the U pass) and the
+    # side-branch Gram separately (roofline_side).
     side = ("capacitance", "ctz_d_update")
     dom = max((kk for kk in tsrc if kk in work and kk not in side), key=lambda kk: tsrc[kk])
     bound, amount = work[dom]
@@ -422,7 +486,8 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                 "kernel": dom, "algorithmic_per_launch": amount, "launch_ms": dom_ms,
                 "timing": "in-graph CUDA events over a timed region of --steps steps",
-                "scope": "dominant kernel on the step's critical path",
+                "scope": "dominant kernel of the step by in-graph time (the U pass runs on a side branch "
+                         "beside the main chain when the step carries no UQ)",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"}
     else:
         ach = amount / (dom_ms * 1e-3) / 1e12
@@ -459,6 +524,9 @@ def run_ours(args, rank, world, local_rank):
                  "columns": l, "us": sp_ms * 1e3, "bytes": sp_bytes, "layout": "row-major X (N×l), Y (m×l)",
                  "note": "each nonzero streams an 8·l-byte X row from L2: bound by the L2 bandwidth cap, "
                          "L2→SM traffic = 8·nnz·l bytes"},
+        "w_products": {**{kk: {**v, "frac": v["tflops"] / fp64_peak} for kk, v in wprod.items()},
+                       "shapes": f"gram: ({w.N}x{l})^T({w.N}x{l}); basis: ({w.N}x{l})({l}x{k})",
+                       "kernels": "k_gram (split-K DMMA, 16-byte cp.async), k_gemm (DMMA)"},
         "fp64_peak_tflops": {"dmma": fp64_dmma.value, "dfma": fp64_dfma.value},
         "offline_s": offline_s,
         "eig_sweeps": ctx.eig_sweeps(),

@@ -36,6 +36,7 @@ typedef struct fkb_cov fkb_cov;
 typedef struct fkb_filter fkb_filter;
 typedef struct fkb_ekf fkb_ekf;
 typedef struct fkb_enkf fkb_enkf;
+typedef struct fkb_ghep fkb_ghep;
 
 const char* fkb_last_error(void);
 unsigned long long fkb_launch_count(void); /* kernels launched by this library so far */
@@ -91,7 +92,7 @@ int fkb_filter_lambda(fkb_filter* f, double* out); /* GepResult::lambda, descend
 /* ghep_residual, lowrank.hpp:215-228: per pair ‖A u − λ Γ⁻¹u‖ / max(λ‖Γ⁻¹u‖, ε) with
  * A = HᵀH/σ², Γ⁻¹u taken from the GHEP's Ū = Γ⁻¹U (exact; the reference solves by CG) */
 int fkb_filter_ghep_residual(fkb_filter* f, double* out);
-/* which: 0 U (N×r), 1 Ū = Γ⁻¹U (N×r), 2 G = HΓHᵀ (m×m), 3 B = HU (m×r) — host copies */
+/* which: 0 U (N×r), 1 Ū = Γ⁻¹U (N×r), 2 G = HΓHᵀ (m×m), 3 B = HU (m×r), 4 ‖U_j‖² (r) — host copies */
 int fkb_filter_get(fkb_filter* f, int which, double* out);
 /* fkf_step, fast_filter.hpp:84-125, advancing the device-resident state */
 int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen);
@@ -130,6 +131,29 @@ int fkb_realizations_device(fkb_filter* f, uint64_t seed, int count, double* d_o
 /* host buffers, one pass over U for both: out (N×count, may be null when count = 0) and var
  * (diag Σ, may be null) */
 int fkb_realizations_with_variance(fkb_filter* f, uint64_t seed, int count, double* out, double* var);
+/* RealizationPropagator::at / conditional_sample (uq.hpp:68-112) for draw `draw` alone:
+ * sample_pair(seed, draw/2), Re for even draw, Im for odd, on the filter's current state */
+int fkb_realization_at(fkb_filter* f, uint64_t seed, uint64_t draw, double* out);
+/* variance (uq.hpp:16-23) and the column norms ‖W_j‖² that trace_criterion needs (:27-34) for a
+ * state with an explicit W (e.g. read_state, field_io.hpp:115-135): Σ = αΓ − W·diag(d)·Wᵀ,
+ * W host N×r column-major (ld ≥ N); var (N) and colsq (r) may be null.  Computed on the GPU. */
+int fkb_lowrank_uq(fkb_cov* c, long long n, int r, double alpha, const double* d, const double* w, long long ldw,
+                   double* var, double* colsq);
+
+/* The GHEP's W-block products on the DMMA path (device pointers, column-major, on `stream`):
+ * which 0 — Gram C (p×q) = AᵀB, A n×p, B n×q (Ȳᵀ(ΓȲ), lowrank.hpp:53-106 block form);
+ * which 1 — C (n×q) = A (n×p)·B (p×q) (U = Q·S, Ū = Q̄·S, lowrank.hpp:197-205). */
+int fkb_dense_product(int which, long long n, int p, int q, const double* dA, const double* dB, double* dC,
+                      void* stream);
+
+/* ---- standalone randomized GHEP (lowrank.hpp:132-213 with A = HᵀH/σ², the a_apply of
+ * fast_filter.hpp:63-66; the generic-LinOp overload is served for this operator only) ---- */
+int fkb_ghep_run(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,
+                 long long k, long long p, uint64_t seed, fkb_ghep** out);
+void fkb_ghep_destroy(fkb_ghep* g);
+int fkb_ghep_info(const fkb_ghep* g, int* rank, int* kept_cols);
+/* which: 0 λ (rank, descending), 1 U (N×rank, Γ⁻¹-orthonormal), 2 Ū = Γ⁻¹U (N×rank) */
+int fkb_ghep_get(fkb_ghep* g, int which, double* out);
 
 /* ---- extended fast filter (fekf_step, fast_filter.hpp:127-224) --------------------- */
 /* Binds Γ and the ray operator H (the reference passes both to every fekf_step call,
@@ -151,6 +175,9 @@ int fkb_ekf_state(fkb_ekf* e, double* alpha, int* step, int* rank);
 int fkb_ekf_read(fkb_ekf* e, double* mean, double* d, double* w, double* wbar);
 /* trace_criterion (uq.hpp:25-34) and relative_entropy (uq.hpp:36-53) of the extended state */
 int fkb_ekf_uq(fkb_ekf* e, double* trace, double* entropy);
+/* diag Σ (var, N) and `count` ≤ 8 realizations (out, N×count; draws first_draw… as
+ * fkb_realization_at) of the extended state, in the transformed (Box–Cox) space; either may be null */
+int fkb_ekf_realizations(fkb_ekf* e, uint64_t seed, uint64_t first_draw, int count, double* out, double* var);
 /* diagnostics of the last step: GHEP rank and relinearization sweeps run */
 int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps);
 

@@ -109,6 +109,14 @@ SIGNATURES = {
     "fkb_h2d": (_i, [_p, _p, _sz]),
     "fkb_d2h": (_i, [_p, _p, _sz]),
     "fkb_dsync": (_i, []),
+    "fkb_realization_at": (_i, [_p, _u64, _u64, _dp]),
+    "fkb_lowrank_uq": (_i, [_p, _ll, _i, _d, _p, _p, _ll, _p, _p]),
+    "fkb_ekf_realizations": (_i, [_p, _u64, _u64, _i, _p, _p]),
+    "fkb_dense_product": (_i, [_i, _ll, _i, _i, _p, _p, _p, _p]),
+    "fkb_ghep_run": (_i, [_p, _i, _i, _ip, _ip, _dp, _d, _ll, _ll, _u64, C.POINTER(_p)]),
+    "fkb_ghep_destroy": (None, [_p]),
+    "fkb_ghep_info": (_i, [_p, _PI, _PI]),
+    "fkb_ghep_get": (_i, [_p, _i, _dp]),
 }
 
 _lib = None

@@ -37,7 +37,11 @@ __attribute__((noinline)) void sync_check(const char*) {
 }
 }  // namespace fkb
 
+// The operator is reference counted: every filter / ensemble / GHEP result built on it holds
+// a reference, so fkb_cov_destroy before them only drops the caller's reference (the device
+// objects run on the operator's stream and Γ-apply).
 struct fkb_cov {
+    int refs = 1;
     cudaStream_t stream = nullptr;
     std::unique_ptr<fkb::Cov> cov;
     ~fkb_cov() {
@@ -46,17 +50,43 @@ struct fkb_cov {
         if (stream) cudaStreamDestroy(stream);
     }
 };
+namespace {
+void cov_release(fkb_cov* c) {
+    if (c && --c->refs == 0) delete c;
+}
+// a reference to the operator held by a device object (released after the object's members)
+struct CovRef {
+    fkb_cov* c = nullptr;
+    CovRef() = default;
+    CovRef(const CovRef&) = delete;
+    CovRef& operator=(fkb_cov* p) {
+        cov_release(c);
+        c = p;
+        if (c) ++c->refs;
+        return *this;
+    }
+    ~CovRef() { cov_release(c); }
+    fkb_cov* operator->() const { return c; }
+    explicit operator bool() const { return c != nullptr; }
+};
+}  // namespace
 struct fkb_filter {
-    fkb_cov* owner = nullptr;
+    CovRef owner;  // declared first: released after f
     std::unique_ptr<fkb::Filter> f;
 };
 struct fkb_ekf {
-    fkb_cov* owner = nullptr;
+    CovRef owner;
     std::unique_ptr<fkb::Ekf> e;
 };
 struct fkb_enkf {
-    fkb_cov* owner = nullptr;
+    CovRef owner;
     std::unique_ptr<fkb::Enkf> e;
+};
+struct fkb_ghep {  // a standalone randomized_ghep result (lowrank.hpp:132-213), device resident
+    CovRef owner;
+    fkb::DevCsr H, HT;
+    fkb::GepDev g;
+    double sigma2 = 0.0;
 };
 
 namespace {
@@ -167,7 +197,7 @@ int fkb_cov_create(int nx, int ny, double lx, double ly, int family, double thet
         *out = h.release();
     });
 }
-void fkb_cov_destroy(fkb_cov* c) { delete c; }
+void fkb_cov_destroy(fkb_cov* c) { cov_release(c); }
 int fkb_cov_dims(const fkb_cov* c, int* mx, int* my) {
     return guarded([&] {
         need(c, "cov");
@@ -278,6 +308,7 @@ int fkb_filter_get(fkb_filter* f, int which, double* out) {
             case 1: src = F.Ubar.p; count = size_t(F.n) * F.r; break;
             case 2: src = F.G.p; count = size_t(F.m) * F.m; break;
             case 3: src = F.B.p; count = size_t(F.m) * F.r; break;
+            case 4: src = F.colsq.p; count = size_t(F.r); break;
             default: throw std::invalid_argument("filter_get: unknown product");
         }
         if (count) {
@@ -367,6 +398,7 @@ int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const 
             throw std::invalid_argument(
                 "fkf_step: state rank does not match the eigendecomposition (constant-H regime requires W = U)");
         const double a2[2] = {alpha, alpha};
+        FKB_CUDA(cudaMemsetAsync(F.info.p, 0, sizeof(int), F.s));  // a new state starts unflagged
         FKB_CUDA(cudaMemcpyAsync(F.alpha_dev.p, a2, sizeof(a2), cudaMemcpyHostToDevice, F.s));
         if (rank) FKB_CUDA(cudaMemcpyAsync(F.d.p, d, sizeof(double) * F.r, cudaMemcpyHostToDevice, F.s));
         else FKB_CUDA(cudaMemsetAsync(F.d.p, 0, F.d.bytes(), F.s));
@@ -435,6 +467,104 @@ int fkb_realizations(fkb_filter* f, uint64_t seed, int count, double* out) {
         F.realizations(seed, count, F.host_out.p, nullptr);
         FKB_CUDA(cudaMemcpyAsync(out, F.host_out.p, sizeof(double) * size_t(F.n) * count, cudaMemcpyDeviceToHost, F.s));
         FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+int fkb_realization_at(fkb_filter* f, uint64_t seed, uint64_t draw, double* out) {
+    return guarded([&] {
+        need(f, "filter");
+        need(out, "out");
+        auto& F = *f->f;
+        F.host_out.ensure(size_t(F.n));
+        F.realization_at(seed, draw, F.host_out.p);
+        FKB_CUDA(cudaMemcpyAsync(out, F.host_out.p, sizeof(double) * size_t(F.n), cudaMemcpyDeviceToHost, F.s));
+        FKB_CUDA(cudaStreamSynchronize(F.s));
+    });
+}
+int fkb_lowrank_uq(fkb_cov* c, long long n, int r, double alpha, const double* d, const double* w, long long ldw,
+                   double* var, double* colsq) {
+    return guarded([&] {
+        need(c, "cov");
+        auto& C = *c->cov;
+        if (n != C.size()) throw std::invalid_argument("variance: state does not match operator size");  // uq.hpp:17-18
+        if (r < 0 || ldw < n) throw std::invalid_argument("lowrank_uq: bad W dimensions");
+        if (r) { need(d, "d"); need(w, "w"); }
+        cudaStream_t s = C.stream;
+        fkb::DBuf<double> dW{size_t(n) * std::max(r, 1)}, dd{size_t(std::max(r, 1))}, da{1}, dv{size_t(n)},
+            dc{size_t(std::max(r, 1))}, scratch;
+        if (r) {
+            FKB_CUDA(cudaMemcpy2DAsync(dW.p, sizeof(double) * size_t(n), w, sizeof(double) * size_t(ldw),
+                                       sizeof(double) * size_t(n), size_t(r), cudaMemcpyHostToDevice, s));
+            FKB_CUDA(cudaMemcpyAsync(dd.p, d, sizeof(double) * size_t(r), cudaMemcpyHostToDevice, s));
+        }
+        FKB_CUDA(cudaMemcpyAsync(da.p, &alpha, sizeof(double), cudaMemcpyHostToDevice, s));
+        fkb::lowrank_uq(&C, n, r, da.p, dd.p, dW.p, nullptr, nullptr, 0, 0, 0, nullptr, var ? dv.p : nullptr,
+                        (colsq && r) ? dc.p : nullptr, scratch);
+        if (var) FKB_CUDA(cudaMemcpyAsync(var, dv.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        if (colsq && r) FKB_CUDA(cudaMemcpyAsync(colsq, dc.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+int fkb_dense_product(int which, long long n, int p, int q, const double* dA, const double* dB, double* dC,
+                      void* stream) {
+    return guarded([&] {
+        if (n < 0 || p < 0 || q < 0) throw std::invalid_argument("dense_product: negative size");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        static fkb::DBuf<double> ws;
+        if (which == 0) fkb::gram_tn(n, p, q, dA, dB, dC, ws, s);
+        else if (which == 1) fkb::tall_times_small(n, p, q, dA, dB, dC, s);
+        else throw std::invalid_argument("dense_product: which must be 0 (AᵀB) or 1 (A·B)");
+    });
+}
+int fkb_ghep_run(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,
+                 long long k, long long p, uint64_t seed, fkb_ghep** out) {
+    return guarded([&] {
+        need(c, "cov");
+        need(out, "out");
+        need(rowptr, "rowptr");
+        *out = nullptr;
+        auto& C = *c->cov;
+        if ((long long)h_cols != C.size()) throw std::invalid_argument("randomized_ghep: H columns do not match state dimension");
+        if (!(sigma2 > 0.0)) throw std::invalid_argument("randomized_ghep: sigma2 must be positive");
+        for (int i = 0; i < m; ++i)
+            for (int e = rowptr[i]; e < rowptr[i + 1]; ++e)
+                if (col[e] < 0 || col[e] >= h_cols) throw std::invalid_argument("randomized_ghep: H column index out of range");
+        auto g = std::make_unique<fkb_ghep>();
+        g->owner = c;
+        g->sigma2 = sigma2;
+        fkb::upload_csr_pair(m, h_cols, rowptr, col, val, g->H, g->HT);
+        fkb::DBuf<double> ws;
+        fkb::randomized_ghep_device(&C, g->H, g->HT, sigma2, k, p, seed, ws, C.stream, g->g);
+        g->g.scratch.clear();  // the sketch temporaries are not needed after the call
+        *out = g.release();
+    });
+}
+void fkb_ghep_destroy(fkb_ghep* g) {
+    if (!g) return;
+    if (g->owner && g->owner->stream) cudaStreamSynchronize(g->owner->stream);
+    delete g;
+}
+int fkb_ghep_info(const fkb_ghep* g, int* rank, int* kept_cols) {
+    return guarded([&] {
+        need(g, "ghep");
+        if (rank) *rank = g->g.r;
+        if (kept_cols) *kept_cols = g->g.kept_cols;
+    });
+}
+int fkb_ghep_get(fkb_ghep* g, int which, double* out) {
+    return guarded([&] {
+        need(g, "ghep");
+        need(out, "out");
+        const long long n = g->owner->cov->size();
+        const int r = g->g.r;
+        cudaStream_t s = g->owner->stream;
+        if (which == 0) {
+            std::copy(g->g.lambda_h.begin(), g->g.lambda_h.end(), out);
+            return;
+        }
+        const double* src = which == 1 ? g->g.U.p : which == 2 ? g->g.Ubar.p : nullptr;
+        if (!src && r) throw std::invalid_argument("ghep_get: unknown product");
+        if (r) FKB_CUDA(cudaMemcpyAsync(out, src, sizeof(double) * size_t(n) * r, cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
     });
 }
 int fkb_realizations_with_variance(fkb_filter* f, uint64_t seed, int count, double* out, double* var) {
@@ -649,6 +779,19 @@ int fkb_ekf_uq(fkb_ekf* e, double* trace, double* entropy) {
         e->e->uq_scalars(t, h);
         if (trace) *trace = t;
         if (entropy) *entropy = h;
+    });
+}
+int fkb_ekf_realizations(fkb_ekf* e, uint64_t seed, uint64_t first_draw, int count, double* out, double* var) {
+    return guarded([&] {
+        need(e, "ekf");
+        auto& E = *e->e;
+        if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
+        fkb::DBuf<double> buf(size_t(E.n) * (count + 1));
+        E.uq(seed, first_draw, count, buf.p + E.n, var ? buf.p : nullptr);
+        if (var) FKB_CUDA(cudaMemcpyAsync(var, buf.p, sizeof(double) * size_t(E.n), cudaMemcpyDeviceToHost, E.s));
+        if (count && out)
+            FKB_CUDA(cudaMemcpyAsync(out, buf.p + E.n, sizeof(double) * size_t(E.n) * count, cudaMemcpyDeviceToHost, E.s));
+        FKB_CUDA(cudaStreamSynchronize(E.s));
     });
 }
 int fkb_ekf_last(fkb_ekf* e, int* gep_rank, int* sweeps) {

@@ -113,11 +113,59 @@ __device__ __forceinline__ void block_matvec_reg(PcgShared& sh, const double (&k
     __syncthreads();
 }
 
+// sh.q[c] = sqd_j · Σ_i E_ij·wsq_i·rt_i for this CTA's rows j = r0 + c (the fused capacitance
+// RHS): the CTA's threads split the m rows of E, every column's loads in flight together,
+// warp shuffles then one pass over per-warp partials in fixed order (deterministic)
+__device__ __forceinline__ void fused_rhs(PcgShared& sh, const PcgRhs& ra, int r0, int r1) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double part[PC_T / 32][8];
+    for (int c0 = r0; c0 < r1; c0 += 8) {
+        const int nc = min(8, r1 - c0);
+        double acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+        int i = tid;
+        for (; i + 3 * PC_T < ra.m; i += 4 * PC_T) {  // 4 rows × 8 columns of loads in flight
+            double w[4], e[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int iq = i + q * PC_T;
+                w[q] = __ldg(ra.wsq + iq) * __ldg(ra.rt + iq);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) e[q][c] = c < nc ? __ldg(ra.E + iq + (long long)(c0 + c) * ra.lde) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[c] = fma(e[q][c], w[q], acc[c]);
+        }
+        for (; i < ra.m; i += PC_T) {
+            const double w = __ldg(ra.wsq + i) * __ldg(ra.rt + i);
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < nc) acc[c] = fma(__ldg(ra.E + i + (long long)(c0 + c) * ra.lde), w, acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            double v = acc[c];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) part[warp][c] = v;
+        }
+        __syncthreads();
+        if (tid < nc) {
+            double v = 0.0;
+            for (int w = 0; w < PC_T / 32; ++w) v += part[w][tid];
+            sh.q[c0 - r0 + tid] = __ldg(ra.sqd + c0 + tid) * v;
+        }
+        __syncthreads();
+    }
+}
+
 template <int KR>
 __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, long long ld, int n,
                                                  double* __restrict__ u, double* __restrict__ work,
                                                  int* __restrict__ fallback, int maxit, double tol, int kstage,
-                                                 unsigned long long* __restrict__ ts) {
+                                                 unsigned long long* __restrict__ ts, double vtol, PcgRhs ra) {
     __shared__ PcgShared sh;
     extern __shared__ double Ks[];  // this CTA's columns of K (rb × n) when kstage
     const bool stamp = ts && blockIdx.x == 0 && threadIdx.x == 0;
@@ -161,6 +209,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     if constexpr (KR > 0)  // entries n..16·KR−1 of both exchange buffers multiply zero K entries
         for (int e = n + tid; e < 16 * KR; e += PC_T) sh.v[0][e] = sh.v[1][e] = 0.0;
     __syncthreads();  // mbarrier initialized before anyone waits on it
+    if (ra.E) fused_rhs(sh, ra, r0, r1);  // overlaps the K staging copy
     // Pipelined Jacobi-PCG (Ghysels–Vanroose): the matvec n = K·m and the reductions
     // γ = rᵀu, δ = wᵀu of the same iteration are independent, so one cluster exchange per
     // iteration carries both: owners push m into every CTA and every CTA pushes its
@@ -170,14 +219,20 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     // ahead never overwrites data a peer is still reading.
     const int row = r0 + tid;
     const bool own = row < r1;
-    double dinv = 0.0, x = 0.0, r = 0.0, uu = 0.0, w = 0.0;
+    double dinv = 0.0, x = 0.0, r = 0.0, uu = 0.0, w = 0.0, u0 = 0.0;
     double zv = 0.0, qv = 0.0, sv = 0.0, pv = 0.0;
     double nonpos = 0.0;  // K_ii ≤ 0: K (hence S) is not positive definite
     if (own) {
         const double kii = K[row + (long long)row * ld];
         nonpos = kii > 0.0 ? 0.0 : 1.0;
         dinv = 1.0 / kii;
-        r = u[row];
+        if (ra.E) {
+            r = sh.q[tid];
+            u[row] = r;  // the Cholesky fallback's right-hand side
+        } else {
+            r = u[row];
+        }
+        u0 = r;
         uu = dinv * r;
 #pragma unroll
         for (int c = 0; c < PC_CL; ++c) st_cluster(&sh.v[1][row], c, uu);
@@ -333,6 +388,77 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         if (stamp && it < 60) ts[1 + it] = gtimer();
         if (stamp && it == 4) ts[44] = clock64();
     }
+    // True-residual check: the pipelined recursion for r can drift from u − Kx, so a converged
+    // x is exchanged once more, multiplied by this CTA's K rows, and ‖u − Kx‖² and ‖u‖² are
+    // summed in rank order (two more exchanges on the same parity sequence: iterations it+1 and
+    // it+2).  A miss beyond vtol·‖u‖ hands the solve to the exact Cholesky.
+    if (done && it > 0 && vtol > 0.0) {
+        {
+            const int b1 = (it + 1) & 1;
+            const unsigned par1 = unsigned(((it + 1) >> 1) & 1);
+            const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[b1]));
+            if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xa), "r"(unsigned(n) * 8u) : "memory");
+            if (own)
+#pragma unroll
+                for (int cc = 0; cc < PC_CL; ++cc) st_async_cluster(&sh.v[b1][row], &xbar[b1], cc, x);
+            unsigned ok = 0;
+            while (!ok)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(ok)
+                    : "r"(xa), "r"(par1)
+                    : "memory");
+            if constexpr (KR > 0) block_matvec_reg<KR>(sh, kr, r0, r1, b1);  // q = K x (CTA barrier)
+            else block_matvec(sh, Ks, K, ld, n, r0, r1, b1, kstage);
+        }
+        const int b2 = (it + 2) & 1;
+        const unsigned par2 = unsigned(((it + 2) >> 1) & 1);
+        const unsigned xa = static_cast<unsigned>(__cvta_generic_to_shared(&xbar[b2]));
+        if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xa), "r"(unsigned(PC_CL) * 16u) : "memory");
+        if (scal) {
+            const double e = own ? u0 - sh.q[tid] : 0.0;
+            double a = e * e, c = own ? u0 * u0 : 0.0;
+            for (int o = 16; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                c += __shfl_xor_sync(0xffffffffu, c, o);
+            }
+            if (rb > 32) {
+                if (lane == 0) {
+                    sh.red[warp][0] = a;
+                    sh.red[warp][2] = c;
+                }
+                asm volatile("bar.sync 1, 64;" ::: "memory");
+                a = sh.red[0][0] + sh.red[1][0];
+                c = sh.red[0][2] + sh.red[1][2];
+            }
+            if (warp == 0 && lane < PC_CL) {
+                st_async_cluster(&sh.part[b2][crank][0], &xbar[b2], lane, a);
+                st_async_cluster(&sh.part[b2][crank][2], &xbar[b2], lane, c);
+            }
+        }
+        {
+            unsigned ok = 0;
+            while (!ok)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(ok)
+                    : "r"(xa), "r"(par2)
+                    : "memory");
+        }
+        if (scal) {
+            const double* ps = sh.part[b2][lane & 15];
+            double e2 = ps[0], u2 = ps[2];
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {
+                e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+                u2 += __shfl_xor_sync(0xffffffffu, u2, o);
+            }
+            if (tid == 0) xflag[b2] = (e2 <= vtol * vtol * u2) ? 1 : 2;
+        }
+        __syncthreads();
+        done = xflag[b2] == 1;
+        if (crank == 0 && tid == 0 && !done) work[n + 1] = 1.0;  // diagnostics: the check failed
+    }
     cl.sync();  // no CTA exits while a peer's asynchronous stores may still target it
     if (done) {
         if (own) u[row] = x;
@@ -346,7 +472,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
 static bool g_pcg_attr = false;
 
 void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int* fallback, cudaStream_t s, int maxit,
-             double tol, unsigned long long* ts) {
+             double tol, unsigned long long* ts, double vtol, PcgRhs rhs) {
     if (n <= 0) return;
     if (n > PC_MAXN) throw std::invalid_argument("cap_pcg: n exceeds 1024");
     const int rb = (n + PC_CL - 1) / PC_CL;
@@ -372,11 +498,11 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (kstage && n <= 16 * 20)
-        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<20>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<20>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs));
     else if (kstage && n <= 16 * 32)
-        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<32>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<32>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs));
     else
-        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<0>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts));
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<0>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs));
     count_launch();
 }
 
@@ -387,14 +513,14 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
 extern "C" int fkb_cap_pcg_test(int n, const double* K, const double* b, double* x, int* iters,
                                 unsigned long long* stamps) {
     try {
-        fkb::DBuf<double> dK(static_cast<size_t>(n) * n), du(static_cast<size_t>(n)), w(static_cast<size_t>(n) + 1);
+        fkb::DBuf<double> dK(static_cast<size_t>(n) * n), du(static_cast<size_t>(n)), w(static_cast<size_t>(n) + 2);
         fkb::DBuf<int> fb(1);
         fkb::DBuf<unsigned long long> ts(64);
         FKB_CUDA(cudaMemcpy(dK.p, K, sizeof(double) * size_t(n) * n, cudaMemcpyHostToDevice));
         FKB_CUDA(cudaMemcpy(du.p, b, sizeof(double) * size_t(n), cudaMemcpyHostToDevice));
         FKB_CUDA(cudaMemset(fb.p, 0, sizeof(int)));
         FKB_CUDA(cudaMemset(ts.p, 0, ts.bytes()));
-        fkb::cap_pcg(n, dK.p, n, du.p, w.p, fb.p, nullptr, 200, 1e-14, stamps ? ts.p : nullptr);
+        fkb::cap_pcg(n, dK.p, n, du.p, w.p, fb.p, nullptr, 200, 1e-14, stamps ? ts.p : nullptr, 1e-13);
         FKB_CUDA(cudaDeviceSynchronize());
         int h = 0;
         double itd = 0.0;

@@ -351,12 +351,24 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
     for (int ix = threadIdx.x; ix < nx; ix += T) w[ix] = f[L::ix(ix)];
 }
 
-// Pass C: CTA = rows 2b, 2b+1 rebuilt from the Hermitian half, ×scale, crop.
-template <int NT>
+// Pass C: CTA = rows 2b, 2b+1 rebuilt from the Hermitian half, ×scale, crop.  With
+// upd.coef set the pass is the filter step's mean update instead of a plain store:
+// y_i ← (y_i + c·(Γx)_i) − sub_i (fast_filter.hpp:114-116, sub = U·dc from the concurrent U
+// pass), skipped when *upd.gate (failed step); the new value also goes to the mapped host
+// buffer upd.hout[0] and the failure flag to upd.hout[2] when set.
+template <int NT, bool UPD>
 __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ W, int nx, int ny, FftLen fy,
-                                                   double* __restrict__ y, double scale,
-                                                   const double* __restrict__ acc_coef, const int* __restrict__ gate,
+                                                   double* __restrict__ y, double scale, MeanUpd upd,
                                                    long long ldw, long long ldy) {
+    const double* __restrict__ acc_coef = UPD ? upd.coef : nullptr;
+    const int* __restrict__ gate = upd.gate;
+    const double* __restrict__ sub = upd.sub;
+    double* hm = nullptr;
+    if (acc_coef && upd.hout) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && upd.hout[2])
+            *reinterpret_cast<volatile int*>(upd.hout[2]) = gate ? *gate : 0;
+        hm = reinterpret_cast<double*>(upd.hout[0]);
+    }
     using L = Lay1<NT>;
     extern __shared__ double2 sm[];
     W += blockIdx.y * ldw;
@@ -377,6 +389,19 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
         const int q0 = ix0 + 2 * p, q1 = q0 + 1;
         const int bl = L::blen(my);
         double2* ap = sm + p * bl;  // twiddles come from the global per-pass table (fft_reg)
+        // mean-update operands loaded up front (independent of the transform, their latency
+        // hides under it; loaded after the stores below they would serialize on aliasing)
+        double2 ym[8], ys[8];
+        if (acc_coef) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int iy = j + q * TPT;
+                const bool in = iy < ny;
+                const long long i0 = (long long)q0 * ny + iy, i1 = (long long)q1 * ny + iy;
+                ym[q] = make_double2(in && q0 < nx ? y[i0] : 0.0, in && q1 < nx ? y[i1] : 0.0);
+                ys[q] = make_double2(in && q0 < nx && sub ? sub[i0] : 0.0, in && q1 < nx && sub ? sub[i1] : 0.0);
+            }
+        }
         double2 v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -396,12 +421,18 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
             const int iy = j + q * TPT;
             if (iy >= ny) continue;
             if (q0 < nx) {
-                double* y0 = y + (long long)q0 * ny + iy;
-                *y0 = acc_coef ? *y0 + c * (v[q].x * scale) : v[q].x * scale;
+                const long long i0 = (long long)q0 * ny + iy;
+                double nv = acc_coef ? ym[q].x + c * (v[q].x * scale) : v[q].x * scale;
+                if (sub) nv -= ys[q].x;
+                y[i0] = nv;
+                if (hm) hm[i0] = nv;
             }
             if (q1 < nx) {
-                double* y1 = y + (long long)q1 * ny + iy;
-                *y1 = acc_coef ? *y1 + c * (v[q].y * scale) : v[q].y * scale;
+                const long long i1 = (long long)q1 * ny + iy;
+                double nv = acc_coef ? ym[q].y + c * (v[q].y * scale) : v[q].y * scale;
+                if (sub) nv -= ys[q].y;
+                y[i1] = nv;
+                if (hm) hm[i1] = nv;
             }
         }
         return;
@@ -427,16 +458,22 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
     }
     __syncthreads();
     const double2* z = L::template fft<+1>(a, b, fy, tw);
-    if (acc_coef) {  // y += c·Γx (the mean update's α·Γ(Hᵀz) term), skipped when *gate
+    if (acc_coef) {  // y = (y + c·Γx) − sub (the mean update), skipped when *gate
         if (gate && *gate) return;
         const double c = *acc_coef;
         for (int iy = threadIdx.x; iy < ny; iy += T) {
             const double2 v = z[L::ix(iy)];
-            double* y0 = y + (long long)r0 * ny + iy;
-            *y0 = *y0 + c * (v.x * scale);
+            const long long i0 = (long long)r0 * ny + iy;
+            double nv = y[i0] + c * (v.x * scale);
+            if (sub) nv -= sub[i0];
+            y[i0] = nv;
+            if (hm) hm[i0] = nv;
             if (r1 < nx) {
-                double* y1 = y + (long long)r1 * ny + iy;
-                *y1 = *y1 + c * (v.y * scale);
+                const long long i1 = (long long)r1 * ny + iy;
+                double nw = y[i1] + c * (v.y * scale);
+                if (sub) nw -= sub[i1];
+                y[i1] = nw;
+                if (hm) hm[i1] = nw;
             }
         }
         return;
@@ -799,7 +836,8 @@ template <int NT>
 static void set_smem_1() {
     set_smem((const void*)k_rows_fwd_1<NT>, 0);
     set_smem((const void*)k_cols_1<NT>, 0);
-    set_smem((const void*)k_rows_inv_1<NT>, 0);
+    set_smem((const void*)k_rows_inv_1<NT, false>, 0);
+    set_smem((const void*)k_rows_inv_1<NT, true>, 0);
 }
 
 // launch one of the three single-vector passes with a compile-time length when n is a
@@ -819,7 +857,7 @@ static void with_len(int n, F&& f) {
 
 void Cov::apply1(const double* dx, double* dy) {
     apply1_fwd(dx);
-    apply1_inv(dy, nullptr, nullptr);
+    apply1_inv(dy, MeanUpd{});
 }
 
 void Cov::apply1_fwd(const double* dx, int ncols, long long ldx) {
@@ -847,14 +885,18 @@ void Cov::apply1_fwd(const double* dx, int ncols, long long ldx) {
     count_launch(2);
 }
 
-void Cov::apply1_inv(double* dy, const double* acc_coef, const int* gate, int ncols, long long ldy) {
+void Cov::apply1_inv(double* dy, const MeanUpd& upd, int ncols, long long ldy) {
     const size_t sy = smem_1(my);
     const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
         constexpr int NT = decltype(c)::value;
         const int rp = reg_fft_len<NT>() ? (ncols >= 8 ? kRowPairs : kRowPairs1) : 1;
-        k_rows_inv_1<NT><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
-            work.p, nx, ny, fy8, dy, 1.0 / double(M()), acc_coef, gate, ldw, ldy);
+        if (upd.coef)
+            k_rows_inv_1<NT, true><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
+                work.p, nx, ny, fy8, dy, 1.0 / double(M()), upd, ldw, ldy);
+        else
+            k_rows_inv_1<NT, false><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
+                work.p, nx, ny, fy8, dy, 1.0 / double(M()), upd, ldw, ldy);
     });
     FKB_LAUNCH_CHECK();
     count_launch();
@@ -874,7 +916,7 @@ void Cov::apply(const double* dX, long long ldx, int ncols, double* dY, long lon
         for (int c0 = 0; c0 < ncols; c0 += batch_cap) {
             const int bc = std::min(batch_cap, ncols - c0);
             apply1_fwd(dX + (long long)c0 * ldx, bc, ldx);
-            apply1_inv(dY + (long long)c0 * ldy, nullptr, nullptr, bc, ldy);
+            apply1_inv(dY + (long long)c0 * ldy, MeanUpd{}, bc, ldy);
         }
         return;
     }

@@ -15,6 +15,16 @@ struct KernelSpec {  // kernel.hpp:19-48
 double kernel_eval(const KernelSpec& s, double r);  // kernel.hpp:51-63
 int next_smooth(int n);                             // covariance.hpp:35-43
 
+// Epilogue of the single-vector inverse pass when it carries the filter step's mean update
+// (fast_filter.hpp:114-116): y ← (y + (*coef)·Γx) − sub, gated on *gate; hout (device copy
+// of the mapped host pointers, Filter::hostout): [0] new mean, [2] failure flag.
+struct MeanUpd {
+    const double* coef = nullptr;
+    const int* gate = nullptr;
+    const double* sub = nullptr;
+    const unsigned long long* hout = nullptr;
+};
+
 struct Cov {
     int nx = 0, ny = 0;
     double lx = 1.0, ly = 1.0;
@@ -40,10 +50,10 @@ struct Cov {
     void apply(const double* dX, long long ldx, int ncols, double* dY, long long ldy);
     void apply1(const double* dx, double* dy);  // single vector (CTA-per-transform kernels)
     // the single-vector apply split at its last pass: forward rows + column pass into the work
-    // buffer, then the inverse rows pass storing Γx into dy, or (acc_coef ≠ null) adding
-    // (*acc_coef)·Γx to dy unless *gate
+    // buffer, then the inverse rows pass storing Γx into dy, or (upd.coef ≠ null) the filter's
+    // mean update dy ← (dy + (*upd.coef)·Γx) − upd.sub unless *upd.gate (see MeanUpd)
     void apply1_fwd(const double* dx, int ncols = 1, long long ldx = 0);
-    void apply1_inv(double* dy, const double* acc_coef, const int* gate, int ncols = 1, long long ldy = 0);
+    void apply1_inv(double* dy, const MeanUpd& upd, int ncols = 1, long long ldy = 0);
     // Two N(0,Γ) draws (covariance.hpp:332-353) into device vectors.
     void sample_pair(uint64_t seed, uint64_t stream_id, double* da, double* db);
     // X[:, j] += draw j of the pairs (seed, sid0 + j/2) (Re → even j, Im → odd j), j < ncols

@@ -487,6 +487,14 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
     FKB_CUDA(cudaStreamSynchronize(s));
 }
 
+// diag Σ and realizations of the extended state (uq.hpp:16-23, :86-112 in FFT mode, SURVEY
+// App. A.4): the carried W̄ = Γ⁻¹W plays Γ^{−1/2}-projected draws, no solve is needed
+void Ekf::uq(uint64_t seed, uint64_t first, int count, double* X, double* var) {
+    DBuf<double>& ad = tmp(19, 1);
+    upload(ad.p, std::vector<double>{alpha}, s);
+    lowrank_uq(cov, n, r, ad.p, d.p, W.p, Wbar.p, mean.p, seed, first, count, X, var, nullptr, tmp(20, 1));
+}
+
 // trace_criterion (uq.hpp:25-34) and relative_entropy (uq.hpp:36-53) of the extended state:
 // φ = αNθ − Σ_j d_j‖W_j‖² (column norms on the device), ½[(N − r)ln α + Σ ln(α − d_j)]
 void Ekf::uq_scalars(double& trace, double& entropy) {

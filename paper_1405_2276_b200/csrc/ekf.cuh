@@ -57,6 +57,8 @@ struct Ekf {
     void reset(const double* mean0_host);
     void step(const double* y_host, double sigma2, double bc_alpha, const EkfOptions& o);
     void uq_scalars(double& trace, double& entropy);  // trace_criterion / relative_entropy
+    // diag Σ (var) and `count` realizations (draws first…first+count−1) into device buffers
+    void uq(uint64_t seed, uint64_t first, int count, double* X, double* var);
 
   private:
     void linearize(double bc_alpha);

@@ -81,24 +81,29 @@ __global__ void k_transpose(long long n, int r, const double* __restrict__ in, d
     }
 }
 
-// Step prologue fused with the residual (fast_filter.hpp:97, :108): α ← α + 1, failure flags
-// cleared, Woodbury scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j (when wsq ≠ null),
-// and z_i = y_i − H_i·mean with one warp per ray: every lane prefetches 16 (col, val) pairs,
-// then gathers the 16 mean values — two memory latencies per 512 nonzeros.
+// Step prologue fused with the residual (fast_filter.hpp:97, :108): α ← α + 1, the PCG fallback
+// flag cleared, Woodbury scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j (when wsq ≠
+// null), a snapshot of the committed d for the side branch that forms the next step's
+// capacitance (dsnap ≠ null; the step's own epilogue overwrites d concurrently), and
+// z_i = y_i − H_i·mean with one warp per ray: every lane prefetches 16 (col, val) pairs, then
+// gathers the 16 mean values — two memory latencies per 512 nonzeros.
+// The failure flag *info is sticky: a failed step leaves it set, so every later step of an
+// asynchronous batch is a no-op (its epilogues are gated on it) until the host clears it.
 __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* __restrict__ rp,
                                                       const int* __restrict__ ci, const double* __restrict__ hv,
                                                       const double* __restrict__ mean, const double* __restrict__ y,
                                                       double* __restrict__ z, double* alpha_dev,
                                                       const double* __restrict__ theta, const double* __restrict__ d,
                                                       double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
-                                                      int* __restrict__ info, int* __restrict__ pcgflag) {
+                                                      double* __restrict__ dsnap, int* __restrict__ pcgflag) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const double alpha = alpha_dev[0] + 1.0;
     if (gid == 0) {
         alpha_dev[1] = alpha;
-        *info = 0;
         if (pcgflag) *pcgflag = 0;
     }
+    if (dsnap)
+        for (int j = gid; j < r; j += nthreads) dsnap[j] = d[j];
     if (wsq) {
         for (int i = gid; i < m; i += nthreads) wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
         for (int j = gid; j < r; j += nthreads) sqd[j] = sqrt(d[j]);
@@ -219,26 +224,6 @@ __global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double*
     if (lane == 0) st[i] = wsq[i] * (rt[i] + acc);
 }
 
-// mean_i ← (mean_i + α·t_i) − Σ_j U_ij·dc_j  (fast_filter.hpp:114-116), skipped on a failed step;
-// the step's last kernel: with hout[0] set it also writes the
-// new mean straight into the caller's mapped pinned host buffer (and hout[2] the failure
-// flag), so the host-buffer step needs no device→host copies after the graph
-struct EpiMean {
-    double* mean;
-    const double* t;
-    const double* alpha_dev;
-    const int* info;
-    const unsigned long long* hout;
-    __device__ __forceinline__ void operator()(long long i, double v) const {
-        const int bad = *info;
-        if (i == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
-        if (bad) return;
-        const double nm = (mean[i] + alpha_dev[1] * t[i]) - v;
-        mean[i] = nm;
-        if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = nm;
-    }
-};
-
 // d'_i = (d_i + αλ_i(α − d_i)) / (1 + λ_i(α − d_i))  (fast_filter.hpp:118-123); commits α
 __global__ void k_d_update(int r, double* __restrict__ d, const double* __restrict__ lam, double* alpha_dev,
                            const int* __restrict__ info) {
@@ -297,6 +282,7 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
                 if (s < count) acc[s] = fma(u, P[j * count + s], acc[s]);
         }
         if (var) var[i] = alpha * theta - vs;
+        if (count == 0) continue;  // variance only (mean may be null)
         const double mi = mean[i];
 #pragma unroll
         for (int s = 0; s < 8; ++s)
@@ -762,7 +748,8 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     st.alloc(size_t(std::max(m, 1)));
     ucap.alloc(size_t(std::max(r, 1)));
     rdg.alloc(std::max<size_t>(chol_solve_scratch(r), 1));
-    pcgwork.alloc(size_t(std::max(r, 1)) + 1);
+    pcgwork.alloc(size_t(std::max(r, 1)) + 2);
+    dsnap.alloc(size_t(std::max(r, 1)));
     pcgflag.alloc(1);
     if (std::getenv("FKB_PCG_STAMPS")) pcg_ts.alloc(64);
     {
@@ -773,6 +760,13 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     }
     z.alloc(size_t(std::max(m, 1)));
     t.alloc(size_t(n));
+    vsub.alloc(size_t(n));
+    if (const char* e = std::getenv("FKB_UPASS_CTAS")) upass_per_sm = std::atoi(e);
+    if (const char* e = std::getenv("FKB_UPASS_THREADS")) upass_threads = std::atoi(e) == 128 ? 128 : 256;
+    if (const char* e = std::getenv("FKB_KFORK")) kfork = std::atoi(e);
+    if (const char* e = std::getenv("FKB_UFORK")) ufork = std::atoi(e);
+    if (const char* e = std::getenv("FKB_FUSE_RHS")) fuse_rhs = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FKB_UPASS_GRID")) upass_per_sm = -std::atoi(e);  // total CTAs
     cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
     info.alloc(1);
@@ -800,6 +794,7 @@ Filter::~Filter() {
 }
 
 void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
+    FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
     FKB_CUDA(cudaMemsetAsync(alpha_dev.p, 0, 2 * sizeof(double), s));
     FKB_CUDA(cudaMemsetAsync(d.p, 0, d.bytes(), s));
     FKB_CUDA(cudaMemsetAsync(mean.p, 0, mean.bytes(), s));
@@ -872,6 +867,7 @@ std::vector<std::pair<std::string, double>> Filter::graph_phase_times() {
 
 std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
     std::vector<std::pair<std::string, double>> acc;
+    set_hostout(0, 0, 0);  // the diagnostic steps must not write through a caller's stale mapped buffers
     for (int rep = 0; rep < reps; ++rep) {
         std::vector<cudaEvent_t> ev;
         phase_events = &ev;
@@ -928,8 +924,10 @@ void Filter::join(cudaEvent_t ev) {
 
 void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double* sqd_o, double* K_o) {
     if (solver != 1 || r <= 0) return;
+    // mode 1 (inside the step graph) reads the snapshot of the committed d taken by the step's
+    // first kernel: the step's own epilogue commits the new d concurrently with this branch
     k_woodbury_scalars<<<std::max(1, std::min(ceil_div(std::max(m, r), 256), 148)), 256, 0, b>>>(
-        m, r, mode, alpha_dev.p, theta.p, d.p, lambda.p, sigma2, wsq_o, sqd_o);
+        m, r, mode, alpha_dev.p, theta.p, mode == 1 ? dsnap.p : d.p, lambda.p, sigma2, wsq_o, sqd_o);
     FKB_LAUNCH_CHECK();
     count_launch();
     GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
@@ -956,7 +954,8 @@ void Filter::enqueue_step(const double* d_y) {
         const int blocks = std::max(1, ceil_div((long long)std::max(m, 1) * 32, 256));
         k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
                                                theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq_c : nullptr,
-                                               sqd_c, info.p, solver == 1 ? pcgflag.p : nullptr);
+                                               sqd_c, (solver == 1 && r > 0) ? dsnap.p : nullptr,
+                                               solver == 1 ? pcgflag.p : nullptr);
         FKB_LAUNCH_CHECK();
         count_launch();
     }
@@ -964,14 +963,19 @@ void Filter::enqueue_step(const double* d_y) {
     if (solver == 0) enqueue_solve_dense();
     else enqueue_solve_woodbury();
     // dc = d ⊙ Bᵀz with d and α updated in the same pass (solver 0: a side-branch pass over B;
-    // solver 1: D^½x inside k_woodbury_st); main branch: t = Γ(Hᵀz); then mean += α·t − U·dc
-    // (:114-123).  (The U pass stays on the main branch: run concurrently it starves the FFT
-    // passes of SMs and slows Hᵀz, which shares HBM with it.)
+    // solver 1: D^½x inside k_woodbury_st) and the U pass v = U·dc on the side branch (solver 1
+    // forks it right after the capacitance solve); main branch: t = Γ(Hᵀz), whose last FFT
+    // pass applies mean ← (mean + α·t) − v (:114-123) once the side branch has joined.
     const bool par = side() != s;
+    const bool fused_uq = uq_count >= 0 && r > 0;
     if (r > 0 && solver == 0) {
         fork();
         launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p}, side());
         mark_on(side(), "ctz_d_update");
+        if (!fused_uq) {
+            launch_u_pass(XPlain{cvec.p}, side());
+            mark_on(side(), "u_pass");
+        }
         if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
     } else if (r == 0) {
         k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α (reads α_dev[1] only)
@@ -980,10 +984,10 @@ void Filter::enqueue_step(const double* d_y) {
     }
     spmv_short(HT, z.p, t.p, 1.0, s);
     mark("ht_z");
-    cov->apply1(t.p, t.p);
-    mark("gamma_apply");
-    if (r > 0 && par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
-    if (uq_count >= 0 && r > 0) {  // U pass + diag Σ + realizations of the new state
+    if (fused_uq) {  // U pass + diag Σ + realizations of the new state (needs t: stays on the main branch)
+        cov->apply1(t.p, t.p);
+        mark("gamma_apply");
+        if (par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
         const size_t shm = sizeof(double) * size_t(r) * (2 + std::max(uq_count, 1));
         k_mean_uq<<<ceil_div(n, 128), 128, shm, s>>>(n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
                                                      uq_count, uq_count ? draws.p : nullptr,
@@ -991,23 +995,32 @@ void Filter::enqueue_step(const double* d_y) {
                                                      hostout.p);
         FKB_LAUNCH_CHECK();
         count_launch();
-    } else {
-        launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), XPlain{cvec.p}, EpiMean{mean.p, t.p, alpha_dev.p, info.p, hostout.p}, s);
+        if (solver == 1 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
+        mark("mean_update");
+        return;
     }
+    cov->apply1_fwd(t.p);
+    mark("gamma_fwd");
+    if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // v = U·dc ready
+    cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hostout.p});
     if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
 
+// v = U·dc (the mean update's low-rank term) streaming the row-major U, limited to
+// upass_per_sm resident CTAs per SM so the latency-bound main chain it overlaps keeps room
+template <class XL>
+void Filter::launch_u_pass(XL xl, cudaStream_t st) {
+    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), xl, EpiStore{vsub.p}, st, upass_per_sm, upass_threads);
+}
+
 // z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
 void Filter::enqueue_solve_woodbury() {
-    launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
-    mark("rotate_in");
-    if (r > 0) {
-        // u = D^½·Eᵀ·Λ_M⁻¹·r̃
-        launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
-        mark("cap_rhs");
-        // side branch (runs beside the 16-SM PCG cluster; measured better than after it): the
-        // NEXT step's Woodbury scalars and K into the other parity's buffers
+    // side branch: the NEXT step's Woodbury scalars and K into the other parity's buffers (they
+    // depend on α and d only); forked at kfork: 0 after cap_rhs (beside the 16-SM PCG cluster),
+    // 1 at the start of the step, 2 after the capacitance solve
+    auto fork_next_k = [&] {
+        if (r <= 0) return;
         if (side() != s) {
             FKB_CUDA(cudaEventRecord(ev_ctz, s));
             FKB_CUDA(cudaStreamWaitEvent(s3, ev_ctz, 0));
@@ -1016,12 +1029,39 @@ void Filter::enqueue_solve_woodbury() {
         enqueue_capacitance(side() != s ? s3 : s, 1, wsq_n, sqd_n, K_n);
         mark_on(side() != s ? s3 : s, "capacitance");
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join2, s3));
-        // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap
+    };
+    // the U pass v = U·(D^½x) beside the rest of the chain (ufork 0: after the capacitance
+    // solve, 1: after k_woodbury_st)
+    auto fork_u = [&] {
+        if (r <= 0 || uq_count >= 0) return;
+        fork();
+        launch_u_pass(XProd{sqd_c, ucap.p}, side());
+        mark_on(side(), "u_pass");
+        if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
+    };
+    if (kfork == 1) fork_next_k();
+    launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
+    mark("rotate_in");
+    if (r > 0) {
+        // u = D^½·Eᵀ·Λ_M⁻¹·r̃: formed by the PCG kernel itself (fuse_rhs) or as column dots
+        PcgRhs rhs;
+        if (fuse_rhs) {
+            rhs.E = E.p; rhs.lde = m; rhs.m = m; rhs.wsq = wsq_c; rhs.rt = rt.p; rhs.sqd = sqd_c;
+        } else {
+            launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
+            mark("cap_rhs");
+        }
+        if (kfork == 0) fork_next_k();
+        // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap.
         // ‖Kx − u‖ ≤ 1e-12‖u‖: the solve's error reaches the mean through U·D^½x at ~1e-12
-        // relative, three orders below the 1e-9 parity bar; one PCG iteration less than 1e-14
-        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p);
+        // relative, three orders below the 1e-9 parity bar.  A converged x is re-checked
+        // against the true residual ‖u − Kx‖ ≤ 1e-11‖u‖ inside the kernel (the pipelined
+        // recursion can drift); a miss routes to the Cholesky.
+        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs);
         chol_solve_small(r, K_c, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
         mark("cap_solve");
+        if (kfork == 2) fork_next_k();
+        if (ufork == 0) fork_u();
     }
     // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
     k_woodbury_st<<<std::max(1, ceil_div(m, 8)) + 1, 256, 0, s>>>(
@@ -1029,6 +1069,7 @@ void Filter::enqueue_solve_woodbury() {
     FKB_LAUNCH_CHECK();
     count_launch();
     mark("woodbury_st");
+    if (ufork == 1) fork_u();
     launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s);  // z = P·s̃ (rows of P)
     mark("rotate_out");
 }
@@ -1059,10 +1100,17 @@ void Filter::check_info() {
     int h = 0;
     FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FKB_CUDA(cudaStreamSynchronize(s));
-    if (h) {
-        k_valid = false;  // the side branch assumed the step would commit its d update
-        throw std::runtime_error("fkf_step: innovation system is singular");
-    }
+    if (h) fail_step("fkf_step: innovation system is singular");
+}
+
+// A failed step: clear the sticky device flag (so the next step can run), invalidate the
+// precomputed capacitance (the side branch assumed the step would commit its d update) and
+// raise the reference's error (fast_filter.hpp:104-106).
+void Filter::fail_step(const std::string& msg) {
+    FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    k_valid = false;
+    throw std::runtime_error(msg);
 }
 
 void Filter::launch_step() {
@@ -1165,10 +1213,7 @@ void Filter::step_uq_host(const double* h_y, uint64_t seed, int count, double* h
             FKB_CUDA(cudaMemcpyAsync(h_x, uq_x.p, sizeof(double) * size_t(n) * count, cudaMemcpyDeviceToHost, s));
     }
     FKB_CUDA(cudaStreamSynchronize(s));
-    if (*h_info) {
-        k_valid = false;
-        throw std::runtime_error("fkf_step: innovation system is singular");
-    }
+    if (*h_info) fail_step("fkf_step: innovation system is singular");
     alpha += 1.0;
     ++step_no;
     state_rank = r;
@@ -1198,10 +1243,7 @@ void Filter::step_host_state(const double* h_y, double* h_d, double* h_mean) {
         if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
     }
     FKB_CUDA(cudaStreamSynchronize(s));
-    if (*h_info) {
-        k_valid = false;
-        throw std::runtime_error("fkf_step: innovation system is singular");
-    }
+    if (*h_info) fail_step("fkf_step: innovation system is singular");
     alpha += 1.0;
     ++step_no;
     state_rank = r;
@@ -1222,11 +1264,23 @@ void Filter::steps_async(const double* d_ys, int nsteps, long long ldy) {
     }
 }
 
+// The deferred check of an asynchronous batch: the device α counts the committed steps (a
+// failed step and, through the sticky flag, every later step of the batch leave the state
+// untouched), so the host mirrors advance by exactly that many and the error names the
+// first failed step of the batch.
 void Filter::finish_async(int nsteps) {
-    check_info();
-    alpha += double(nsteps);
-    step_no += nsteps;
-    if (nsteps > 0) state_rank = r;
+    int h = 0;
+    double a = 0.0;
+    FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaMemcpyAsync(&a, alpha_dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    const int done = int(std::lround(a - alpha));
+    alpha = a;
+    step_no += done;
+    if (done > 0) state_rank = r;
+    if (h)
+        fail_step("fkf_step: innovation system is singular (step " + std::to_string(done + 1) + " of " +
+                  std::to_string(nsteps) + " in the batch)");
 }
 
 std::vector<double> Filter::d_host() const { return download(d.p, size_t(r), s); }
@@ -1276,6 +1330,56 @@ double Filter::relative_entropy() {  // uq.hpp:39-53
         }
     }
     return 0.5 * sum;
+}
+
+// UQ of an arbitrary low-rank state Σ = αΓ − W·diag(d)·Wᵀ in device buffers (uq.hpp:16-34 and
+// the FFT-mode realization formula of SURVEY App. A.4): diag Σ (var), the column norms ‖W_j‖²
+// (colsq, for trace_criterion) and `count` realizations mean + √α(z_s − W(Σ₋ ⊙ W̄ᵀz_s)) with
+// W̄ = Γ⁻¹W, draws z_s, s = first … first+count−1, as sample_pair(seed, s/2) (Re even, Im odd).
+// α is read from alpha_dev[0].  Runs on the operator's stream (sample_pair uses it).
+void lowrank_uq(Cov* cov, long long n, int r, const double* alpha_dev, const double* d, const double* W,
+                const double* Wbar, const double* mean, uint64_t seed, uint64_t first, int count, double* X,
+                double* var, double* colsq, DBuf<double>& scratch) {
+    cudaStream_t s = cov->stream;
+    if (count < 0 || count > 8) throw std::invalid_argument("realizations: count must lie in [0, 8]");
+    if (colsq) column_sumsq(n, r, W, colsq, s);
+    if (count == 0 && !var) return;
+    const size_t nd = size_t(n) * std::max(count + 1, 1);
+    scratch.ensure(nd + size_t(std::max(r, 1)) * std::max(count, 1));
+    double* Z = scratch.p;                  // count draws (+ the spare of an odd tail)
+    double* proj = scratch.p + nd;          // W̄ᵀZ (r × count)
+    for (int c = 0; c < count;) {
+        const uint64_t j = first + uint64_t(c);
+        double* a = Z + (long long)c * n;
+        if (j % 2 == 0) {  // pair (seed, j/2): Re → draw j, Im → draw j+1
+            double* b = c + 1 < count ? Z + (long long)(c + 1) * n : Z + (long long)count * n;
+            cov->sample_pair(seed, j / 2, a, b);
+            c += 2;
+        } else {           // odd first draw: the Im half of pair (seed, j/2)
+            cov->sample_pair(seed, j / 2, Z + (long long)count * n, a);
+            c += 1;
+        }
+    }
+    if (r > 0 && count > 0) {
+        GemmArgs g;
+        g.M = r; g.N = count; g.K = int(n);
+        g.A = Wbar; g.lda = n; g.transA = 1;
+        g.B = Z; g.ldb = n;
+        g.C = proj; g.ldc = r;
+        g.splitk = gemm_pick_splitk(r, count, int(n));
+        DBuf<double> gws(std::max<size_t>(gemm_ws_elems(g), 1));
+        gemm(g, gws.p, s);
+    }
+    const size_t shm = sizeof(double) * size_t(std::max(r, 1)) * (1 + std::max(count, 1));
+    k_uq<<<ceil_div(n, 256), 256, shm, s>>>(n, r, W, d, alpha_dev, cov->spec.theta, mean, count,
+                                            count ? Z : nullptr, count ? proj : nullptr, X, var);
+    FKB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void Filter::realization_at(uint64_t seed, uint64_t draw, double* d_out) {
+    lowrank_uq(cov, n, state_rank ? r : 0, alpha_dev.p, d.p, U.p, Ubar.p, mean.p, seed, draw, 1, d_out, nullptr, nullptr,
+               uq_scratch);
 }
 
 // count realizations x_s = mean + √α(z_s − U Σ₋ Ūᵀ z_s); draw s = sample_pair(seed, s/2),

@@ -46,6 +46,11 @@ void gram_tn(long long n, int p, int q, const double* A, const double* B, double
 void tall_times_small(long long n, int p, int q, const double* A, const double* W, double* C, cudaStream_t s);
 std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept);
 
+// diag Σ, ‖W_j‖² and realizations of Σ = αΓ − W·diag(d)·Wᵀ (device buffers, filter.cu)
+void lowrank_uq(Cov* cov, long long n, int r, const double* alpha_dev, const double* d, const double* W,
+                const double* Wbar, const double* mean, uint64_t seed, uint64_t first, int count, double* X,
+                double* var, double* colsq, DBuf<double>& scratch);
+
 struct Filter {
     Cov* cov = nullptr;
     cudaStream_t s = nullptr;
@@ -75,6 +80,7 @@ struct Filter {
     int solver = 1;
     int eig_sweeps = 0;
     DBuf<double> P, Pt, theta, E, Erow, rt, ucap, st, rdg, pcgwork;
+    DBuf<double> dsnap;  // committed d at the start of the step (read by the next-K side branch)
     // Per-step Woodbury scalars Λ_M⁻¹ (wsq), D^½ (sqd) and capacitance K, double-buffered by
     // step parity: step t reads buffer t&1 while its side branch forms step t+1's into the
     // other (they depend only on α and d, not on the observation).
@@ -90,8 +96,16 @@ struct Filter {
     DBuf<int> pcgflag;
     int pcg_maxit = 200;  // iteration cap before the exact Cholesky takes over (tests force 0)  // 1 when the capacitance PCG fell back to the cluster Cholesky
 
-    // step workspaces
-    DBuf<double> S, z, t, cvec, ws, ws_step, potrf_ws;
+    // step workspaces (vsub = U·dc from the side-branch U pass)
+    DBuf<double> S, z, t, cvec, vsub, ws, ws_step, potrf_ws;
+    int upass_per_sm = 1;     // resident U-pass CTAs per SM beside the main chain (FKB_UPASS_CTAS);
+                              // negative: a total CTA count (FKB_UPASS_GRID)
+    int upass_threads = 256;  // threads per U-pass CTA (FKB_UPASS_THREADS: 128 or 256)
+    int kfork = 1;            // where the next-K side branch forks (FKB_KFORK, enqueue_solve_woodbury)
+    int ufork = 1;            // where the U pass forks (FKB_UFORK)
+    bool fuse_rhs = true;     // capacitance RHS formed inside the PCG kernel (FKB_FUSE_RHS)
+    template <class XL>
+    void launch_u_pass(XL xl, cudaStream_t st);
     DBuf<int> info, flags;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one per step parity
     bool graph_ready[2] = {false, false};
@@ -176,12 +190,16 @@ struct Filter {
     std::vector<std::pair<std::string, double>> graph_phase_times();
     void launch_step();                                  // graph replay of enqueue_step(ybuf)
     void check_info();                                   // throws on a singular innovation system
+    [[noreturn]] void fail_step(const std::string& msg); // clears the sticky flag, throws
     void reset();                                        // zero_start (:30-36)
     void variance(double* d_out);                        // uq.hpp:16-23
     std::vector<double> ghep_residual();                 // lowrank.hpp:215-228 with Γ⁻¹U = Ū
     double trace_criterion();                            // uq.hpp:27-34
     double relative_entropy();                           // uq.hpp:39-53
     void realizations(uint64_t seed, int count, double* d_out, double* d_var);
+    // draw `draw` alone (RealizationPropagator(cov, seed, draw).at(state), uq.hpp:86-112)
+    void realization_at(uint64_t seed, uint64_t draw, double* d_out);
+    DBuf<double> uq_scratch;
     std::vector<double> d_host() const;
 };
 

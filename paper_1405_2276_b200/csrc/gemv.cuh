@@ -19,6 +19,10 @@ struct XProd {  // x_c = a_c · b_c
     const double* b;
     __device__ __forceinline__ double operator()(long long c) const { return __ldg(a + c) * __ldg(b + c); }
 };
+struct EpiStore {  // y_i = v
+    double* y;
+    __device__ __forceinline__ void operator()(long long i, double v) const { y[i] = v; }
+};
 struct EpiAxpby {  // y_i = α·v + β·y_i
     double* y;
     double alpha, beta;
@@ -112,31 +116,37 @@ __global__ void __launch_bounds__(256, 2) k_gemv_rowmajor_reg(long long m, int k
 
 template <int KC, class XL, class Epi>
 inline void launch_gemv_rowmajor_reg(long long m, int k, const double* A, long long ld, XL xl, Epi epi,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, int per_sm_cap, int threads) {
     int dev = 0, sms = 0, per_sm = 0;
     FKB_CUDA(cudaGetDevice(&dev));
     FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor_reg<KC, XL, Epi>, 256, 0));
-    const long long ctas = std::min((m + 31) / 32, (long long)std::max(sms, 1) * std::max(per_sm, 1));
-    k_gemv_rowmajor_reg<KC, XL, Epi><<<(unsigned)ctas, 256, 0, s>>>(m, k, A, ld, xl, epi);
+    FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor_reg<KC, XL, Epi>, threads, 0));
+    long long cap = (long long)std::max(sms, 1) * std::max(per_sm, 1);
+    if (per_sm_cap > 0) cap = std::min(cap, (long long)std::max(sms, 1) * per_sm_cap);
+    if (per_sm_cap < 0) cap = std::min(cap, (long long)-per_sm_cap);  // negative: a total CTA count
+    const long long ctas = std::min((m + threads / 8 - 1) / (threads / 8), cap);
+    k_gemv_rowmajor_reg<KC, XL, Epi><<<(unsigned)ctas, threads, 0, s>>>(m, k, A, ld, xl, epi);
 }
 
+// per_sm_cap > 0 limits the resident CTAs per SM (the step runs the U pass beside the
+// latency-bound main chain, which needs room on every SM)
 template <class XL, class Epi>
 inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long ld, XL xl, Epi epi, cudaStream_t s,
-                                 long long max_ctas = 0) {
+                                 int per_sm_cap = 0, int threads = 256) {
     if (m <= 0) return;
-    if (k >= 1 && k <= 320 && max_ctas == 0) {  // the step's U pass: rank ≤ 320 held in registers
+    if (k >= 1 && k <= 320) {  // the step's U pass: rank ≤ 320 held in registers
+        const int c = per_sm_cap, t = threads;
         switch ((k + 31) / 32) {
-            case 1: launch_gemv_rowmajor_reg<1>(m, k, A, ld, xl, epi, s); break;
-            case 2: launch_gemv_rowmajor_reg<2>(m, k, A, ld, xl, epi, s); break;
-            case 3: launch_gemv_rowmajor_reg<3>(m, k, A, ld, xl, epi, s); break;
-            case 4: launch_gemv_rowmajor_reg<4>(m, k, A, ld, xl, epi, s); break;
-            case 5: launch_gemv_rowmajor_reg<5>(m, k, A, ld, xl, epi, s); break;
-            case 6: launch_gemv_rowmajor_reg<6>(m, k, A, ld, xl, epi, s); break;
-            case 7: launch_gemv_rowmajor_reg<7>(m, k, A, ld, xl, epi, s); break;
-            case 8: launch_gemv_rowmajor_reg<8>(m, k, A, ld, xl, epi, s); break;
-            case 9: launch_gemv_rowmajor_reg<9>(m, k, A, ld, xl, epi, s); break;
-            default: launch_gemv_rowmajor_reg<10>(m, k, A, ld, xl, epi, s); break;
+            case 1: launch_gemv_rowmajor_reg<1>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 2: launch_gemv_rowmajor_reg<2>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 3: launch_gemv_rowmajor_reg<3>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 4: launch_gemv_rowmajor_reg<4>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 5: launch_gemv_rowmajor_reg<5>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 6: launch_gemv_rowmajor_reg<6>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 7: launch_gemv_rowmajor_reg<7>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 8: launch_gemv_rowmajor_reg<8>(m, k, A, ld, xl, epi, s, c, t); break;
+            case 9: launch_gemv_rowmajor_reg<9>(m, k, A, ld, xl, epi, s, c, t); break;
+            default: launch_gemv_rowmajor_reg<10>(m, k, A, ld, xl, epi, s, c, t); break;
         }
         FKB_LAUNCH_CHECK();
         count_launch();
@@ -147,9 +157,9 @@ inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long 
     FKB_CUDA(cudaGetDevice(&dev));
     FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor<XL, Epi>, 256, shm));
+    if (per_sm_cap > 0) per_sm = std::min(per_sm, per_sm_cap);
     const long long warps = (m + 3) / 4;  // at least one 4-row group per warp
-    long long ctas = std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
-    if (max_ctas > 0) ctas = std::min(ctas, max_ctas);
+    const long long ctas = std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
     k_gemv_rowmajor<XL, Epi><<<(unsigned)ctas, 256, shm, s>>>(m, k, A, ld, xl, epi);
     FKB_LAUNCH_CHECK();
     count_launch();

@@ -2,6 +2,7 @@
 // Mirrors the fkf branch of cmd_run (driver.hpp:278-303): build H, CovarianceOperator,
 // fkf_init, then fkf_step per observation with UQ.  Reads observations from stdin
 // (n_steps rows of m values), prints alpha, trace, entropy, and the mean per step.
+#include <cmath>
 #include <cstdio>
 #include <iostream>
 
@@ -18,7 +19,7 @@ int main(int argc, char** argv) {
     spec.power = 0.5;
     const CovarianceOperator cov(grid, spec, CovMode::fft);
     const SparseRowMatrix h = build_H(grid, SourceReceiverLayout::cross_well(grid, 3, 8));
-    FkfContext ctx = fkf_init(cov, h, 2e-4, 16, 20, 11);
+    const FkfContext ctx = fkf_init(cov, h, 2e-4, 16, 20, 11);
     LowRankState state = LowRankState::zero_start(grid.size());
     try {  // mismatched observation length must raise std::invalid_argument
         fkf_step(state, ctx, Vector(h.rows() + 1));
@@ -31,8 +32,23 @@ int main(int argc, char** argv) {
         for (Index i = 0; i < y.size(); ++i) std::cin >> y[i];
         state = fkf_step(state, ctx, y);
         std::printf("step %d alpha %.17g trace %.17g entropy %.17g\n", state.step, state.alpha,
-                    trace_criterion(state, ctx), relative_entropy(state, ctx));
+                    trace_criterion(state, cov), relative_entropy(state));
         for (Index i = 0; i < state.mean.size(); ++i) std::printf("%.17g\n", state.mean[i]);
     }
+    // value semantics (fast_filter.hpp:84-125): an edited copy, then the unedited state again
+    Vector y(h.rows());
+    for (Index i = 0; i < y.size(); ++i) y[i] = 1e-3 * double(i % 7);
+    const LowRankState s1 = fkf_step(state, ctx, y);
+    LowRankState edited = state;
+    edited.mean[0] += 1.0;
+    edited.alpha += 0.5;
+    const LowRankState s2 = fkf_step(edited, ctx, y);
+    const LowRankState s3 = fkf_step(state, ctx, y);
+    if (s3.mean.v != s1.mean.v || s3.d.v != s1.d.v || s3.alpha != s1.alpha) return 7;
+    if (s2.mean.v == s1.mean.v || s2.alpha != state.alpha + 1.5) return 8;
+    const FkfContext& cctx = ctx;  // const context, reference signatures
+    if (std::abs(trace_criterion(s3, cov) - trace_criterion(s3, cctx)) > 1e-12 * std::abs(trace_criterion(s3, cctx)))
+        return 9;
+    std::printf("edit ok\n");
     return 0;
 }

@@ -50,7 +50,7 @@ int main(int argc, char** argv) {
         std::cin >> seed;
         opts.seed = seed;
         state = fekf_step(state, cov, h, y, 2e-4, transform, opts);
-        const Matrix w = state.w();
+        const Matrix w = state.w;
         std::printf("step %d alpha %.17g rank %lld wcols %lld\n", state.step, state.alpha, state.rank(), w.cols());
         for (Index i = 0; i < state.mean.size(); ++i) std::printf("%.17g\n", state.mean[i]);
     }

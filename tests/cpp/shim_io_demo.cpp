@@ -26,7 +26,7 @@ int main(int argc, char** argv) {
         for (Index i = 0; i < 20; ++i) w(i, j) = double(i + 1) / double(j + 2);
     write_state(spath, st, w);
     const LowRankState rb = read_state(spath);
-    if (rb.alpha != 3.0 || rb.step != 3 || rb.mean.v != st.mean.v || rb.d.v != st.d.v || rb.w().a != w.a) return 4;
+    if (rb.alpha != 3.0 || rb.step != 3 || rb.mean.v != st.mean.v || rb.d.v != st.d.v || rb.w.get().a != w.a) return 4;
     int errors = 0;
     try { read_field(spath); } catch (const std::runtime_error&) { ++errors; }          // wrong magic
     try { read_field(fpath + ".missing"); } catch (const std::runtime_error&) { ++errors; }

@@ -45,6 +45,7 @@ def test_cpp_shim_matches_oracle(tmp_path):
         assert rel_err(mean, of.state()["mean"]) < 1e-9
         assert abs(float(hdr[5]) - of.trace_criterion()) <= 1e-9 * abs(of.trace_criterion())
         assert abs(float(hdr[7]) - of.relative_entropy()) <= 1e-9 * abs(of.relative_entropy())
+    assert out[i].strip() == "edit ok"
 
 
 def _compile_fekf(tmp_path):
