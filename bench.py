@@ -136,12 +136,12 @@ def phase_work(w, r, fft_flops, nnz, uq_count=-1, fft_split=None):
     into mean_update); otherwise the U pass (u_pass, side branch) writes v = U·dc and the last
     FFT pass (mean_update) applies mean ← (mean + α·Γt) − v."""
     N, m = w.N, w.m
-    uq_bytes = 0.0 if uq_count < 0 else 8.0 * N * (1 + 2 * uq_count) + 8.0 * r * (2 + uq_count)
+    cnt = max(uq_count, 0)
     f_fwd, f_inv, w_bytes = fft_split or (fft_flops, 0.0, 0.0)
-    if uq_count < 0:
-        mean_upd = ("hbm", w_bytes + 24.0 * N)  # W half-spectrum in, mean in/out, v in
-    else:
-        mean_upd = ("hbm", 8.0 * N * r + 24.0 * N + 8.0 * r + uq_bytes)
+    # last FFT pass: W half-spectrum in, mean in/out, v in (+ xp in, x out per realization)
+    mean_upd = ("hbm", w_bytes + 24.0 * N + 16.0 * N * cnt)
+    # U pass: U in, v out, the step's r-vectors (+ diag Σ out, draws in, xp out)
+    u_pass = 8.0 * N * r + 8.0 * N + 16.0 * r + (0.0 if uq_count < 0 else 8.0 * N + 16.0 * N * cnt + 8.0 * r * cnt)
     return {
         "residual": ("hbm", 12.0 * nnz + 4.0 * (m + 1) + 8.0 * N + 16.0 * m),
         "capacitance": ("tensor", 1.0 * m * r * (r + 1)),  # symmetric Eᵀ·diag·E (lower half)
@@ -154,7 +154,7 @@ def phase_work(w, r, fft_flops, nnz, uq_count=-1, fft_split=None):
         "ht_z": ("hbm", 12.0 * nnz + 4.0 * (N + 1) + 8.0 * (N + m)),
         "gamma_apply": ("tensor", fft_flops),
         "gamma_fwd": ("tensor", f_fwd),
-        "u_pass": ("hbm", 8.0 * N * r + 8.0 * N + 16.0 * r),
+        "u_pass": ("hbm", u_pass),
         "mean_update": mean_upd,
     }
 
@@ -444,14 +444,14 @@ def run_ours(args, rank, world, local_rank):
     Sb = torch.randn(k, l, dtype=torch.float64, device=f"cuda:{local_rank}")     # column-major l×k
     Ub = torch.empty(k, w.N, dtype=torch.float64, device=f"cuda:{local_rank}")
     ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
-    for name, which, args, flops in (
+    for name, which, pargs, flops in (
             ("gram", 0, (w.N, l, l, ptr(Yb), ptr(Zb), ptr(Gb)), 2.0 * w.N * l * l),
             ("basis", 1, (w.N, l, k, ptr(Yb), ptr(Sb), ptr(Ub)), 2.0 * w.N * l * k)):
-        check(L.fkb_dense_product(which, *args, C.c_void_p(cur.cuda_stream)))
+        check(L.fkb_dense_product(which, *pargs, C.c_void_p(cur.cuda_stream)))
         torch.cuda.synchronize()
         ga.record(cur)
         for _ in range(reps):
-            check(L.fkb_dense_product(which, *args, C.c_void_p(cur.cuda_stream)))
+            check(L.fkb_dense_product(which, *pargs, C.c_void_p(cur.cuda_stream)))
         gb.record(cur)
         torch.cuda.synchronize()
         ms = ga.elapsed_time(gb) / reps

@@ -61,6 +61,9 @@ int fkb_build_H(int nx, int ny, double lx, double ly, int n_src, const double* s
 int fkb_sym_eig(int n, const double* A, double* w, double* Z);
 /* the same on the GPU (two-sided block Jacobi, eig.cu; ascending eigenvalues); *sweeps may be null */
 int fkb_sym_eig_device(int n, const double* A, double* w, double* Z, int* sweeps);
+/* the same by GPU Householder tridiagonalization + QL (rotations applied on the GPU):
+ * w ascending, Z column-major (the GHEP and add_low_rank core eigensolves, lowrank.hpp:193, :265) */
+int fkb_sym_eig_tridiag(int n, const double* A, double* w, double* Z);
 
 /* ---- covariance operator Γ (CovarianceOperator FFT mode, covariance.hpp:69-353) ---- */
 /* constructor covariance.hpp:71-79 + build_fft :238-260 (padding loop, acceptance) */

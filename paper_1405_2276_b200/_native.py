@@ -49,6 +49,7 @@ SIGNATURES = {
     "fkb_gaussian_matrix": (_i, [_ll, _i, _u64, _u64, _dp]),
     "fkb_fkf_init": (_i, [_p, _i, _i, _ip, _ip, _dp, _d, _ll, _ll, _u64, C.POINTER(_p)]),
     "fkb_sym_eig_device": (_i, [_i, _dp, _dp, _dp, C.POINTER(_i)]),
+    "fkb_sym_eig_tridiag": (_i, [_i, _dp, _dp, _dp]),
     "fkb_enkf_init": (_i, [_p, _i, _i, _ip, _ip, _dp, _i, C.POINTER(_p)]),
     "fkb_enkf_destroy": (None, [_p]),
     "fkb_enkf_step": (_i, [_p, _dp, _ll, _d, _u64]),

@@ -16,7 +16,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++20", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-I" + os.path.join(HERE, "..", "include"), "-ccbin", shutil.which("g++") or "g++"]
-SOURCES = ["cov.cu", "dense.cu", "sparse.cu", "eig.cu", "smallchol.cu", "cappcg.cu", "filter.cu", "ekf.cu", "enkf.cu", "capi.cu",
+SOURCES = ["cov.cu", "dense.cu", "sparse.cu", "eig.cu", "tdeig.cu", "smallchol.cu", "cappcg.cu", "filter.cu", "ekf.cu", "enkf.cu", "capi.cu",
            "peak.cu", "host_linalg.cpp"]
 
 

@@ -190,7 +190,11 @@ int fkb_cov_create(int nx, int ny, double lx, double ly, int family, double thet
         need(out, "out");
         *out = nullptr;
         auto h = std::make_unique<fkb_cov>();
-        FKB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        // the operator's stream carries the filter step's main chain: highest priority, so its
+        // CTAs are dispatched ahead of the step's low-priority side branch (the U pass)
+        int lo = 0, hi = 0;
+        FKB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FKB_CUDA(cudaStreamCreateWithPriority(&h->stream, cudaStreamNonBlocking, hi));
         fkb::KernelSpec s;
         s.family = family; s.theta = theta; s.length = length; s.power = power; s.nu = nu; s.alpha_scale = alpha_scale;
         h->cov = std::make_unique<fkb::Cov>(nx, ny, lx, ly, s, h->stream);

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
             v[q] = make_double2((iy < ny && q0 < nx) ? x[(long long)q0 * ny + iy] : 0.0,
                                 (iy < ny && q1 < nx) ? x[(long long)q1 * ny + iy] : 0.0);
         }
-        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, fy.twp, j);  // ping-pong if alone
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, fy.twp, j, fy.tw);  // ping-pong if alone
         __syncthreads();  // last exchange loads done before the result overwrites the buffer
 #pragma unroll
         for (int q = 0; q < 8; ++q) ap[fpad(j + q * TPT)] = v[q];
@@ -314,10 +314,10 @@ __global__ void __launch_bounds__(256) k_cols_1(double2* __restrict__ W, int nx,
             v[q] = ix < nx ? w[ix] : make_double2(0.0, 0.0);
             spv[q] = __ldg(sp + ix);
         }
-        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ra, rb, fx.twp, j);
+        fft_reg<-1, (reg_fft_len<NT>() ? NT : 512)>(v, ra, rb, fx.twp, j, fx.tw);
 #pragma unroll
         for (int q = 0; q < 8; ++q) v[q] = cscale(v[q], spv[q]);
-        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ra, rb, fx.twp, j);
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ra, rb, fx.twp, j, fx.tw);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             if (j + q * T < nx) w[j + q * T] = v[q];
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
             if (hi) { u1 = cconj(u1); u2 = cconj(u2); }
             v[q] = make_double2(u1.x - u2.y, u1.y + u2.x);  // X1 + i·X2
         }
-        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, fy.twp, j);
+        fft_reg<+1, (reg_fft_len<NT>() ? NT : 512)>(v, ap, RP == 1 ? ap + bl : nullptr, fy.twp, j, fy.tw);
         if (acc_coef && gate && *gate) return;
         const double c = acc_coef ? *acc_coef : 0.0;
 #pragma unroll
@@ -822,14 +822,22 @@ std::vector<double> Cov::spectrum_host() const {
 static int threads_1(int n) { return std::max(32, ((n / kEpt + 31) / 32) * 32); }
 // shared bytes of a single-transform kernel of length n (see Lay1)
 static size_t smem_1(int n) {
-    if (n == 512) return 2 * size_t(n + n / 8 + 1) * sizeof(double2);  // register-resident: buffers only
+    if (n == 512 || n == 1024) return 2 * size_t(n + n / 8 + 1) * sizeof(double2);  // register-resident: buffers only
     if (static_len(n)) return (size_t(static_tw_len(n)) + 2 * size_t(n + n / 8 + 1)) * sizeof(double2);
     return 3 * size_t(n) * sizeof(double2);
 }
 // rows passes: register-resident lengths hold kRowPairs single buffers
 static size_t smem_rows(int n, int rp) {
-    if (n == 512) return size_t(std::max(rp, 2)) * (n + n / 8 + 1) * sizeof(double2);
+    if (n == 512 || n == 1024) return size_t(std::max(rp, 2)) * (n + n / 8 + 1) * sizeof(double2);
     return smem_1(n);
+}
+
+// transforms (row pairs) per CTA of the register-resident rows passes: ≤ 256 threads per CTA
+template <int NT>
+static int rows_rp(int ncols) {
+    if (!reg_fft_len<NT>()) return 1;
+    const int cap = 256 / (NT / 8);
+    return std::min(ncols >= 8 ? kRowPairs : kRowPairs1, std::max(cap, 1));
 }
 
 template <int NT>
@@ -872,7 +880,7 @@ void Cov::apply1_fwd(const double* dx, int ncols, long long ldx) {
     const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
         constexpr int NT = decltype(c)::value;
-        const int rp = reg_fft_len<NT>() ? (ncols >= 8 ? kRowPairs : kRowPairs1) : 1;  // coalescing vs CTA count
+        const int rp = rows_rp<NT>(ncols);  // coalescing vs CTA count
         k_rows_fwd_1<NT><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
             dx, nx, ny, fy8, work.p, ldx, ldw);
     });
@@ -890,7 +898,7 @@ void Cov::apply1_inv(double* dy, const MeanUpd& upd, int ncols, long long ldy) {
     const long long ldw = (long long)nky * nx;
     with_len(my, [&](auto c) {
         constexpr int NT = decltype(c)::value;
-        const int rp = reg_fft_len<NT>() ? (ncols >= 8 ? kRowPairs : kRowPairs1) : 1;
+        const int rp = rows_rp<NT>(ncols);
         if (upd.coef)
             k_rows_inv_1<NT, true><<<dim3(ceil_div(nx, 2 * rp), ncols), threads_1(my) * rp, smem_rows(my, rp), stream>>>(
                 work.p, nx, ny, fy8, dy, 1.0 / double(M()), upd, ldw, ldy);

@@ -16,4 +16,9 @@ int sym_eig_device(int m, double* A, long long lda, double* theta, double* V, cu
 int sym_eig_sorted_device(int m, double* A, long long lda, double* theta, double* V, cudaStream_t s,
                           double tol = 1e-15, int max_sweeps = 40);
 
+// Householder tridiagonalization + QL with the O(n³) parts on the GPU (tdeig.cu): A (device,
+// n×n column-major symmetric, overwritten) → eigenvalues ascending (host w) and eigenvector
+// columns (device Z, n×n column-major).  For the GHEP core and the add_low_rank core.
+void sym_eig_tridiag_device(int n, double* A, double* w_host, double* Z, cudaStream_t s);
+
 }  // namespace fkb

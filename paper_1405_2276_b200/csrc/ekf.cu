@@ -430,9 +430,10 @@ void Ekf::add_low_rank(const std::vector<double>& d_bar, GepDev& g, double tol, 
         }
         ck.lap("alr: project+core");
         std::vector<double> ev(static_cast<size_t>(nm)), vec(static_cast<size_t>(nm) * nm);
-        if (nm <= 2048) {  // host QL (ε-accurate); the device block Jacobi beyond
-            std::vector<double> Mh = download(Md.p, size_t(nm) * nm, s);
-            sym_eig_small(nm, Mh.data(), ev.data(), vec.data());
+        if (nm <= 2048) {  // Householder + QL, O(n³) on the GPU (tdeig.cu); block Jacobi beyond
+            DBuf<double>& Vd = tmp(16, size_t(nm) * nm);
+            sym_eig_tridiag_device(nm, Md.p, ev.data(), Vd.p, s);
+            vec = download(Vd.p, size_t(nm) * nm, s);
         } else {
             DBuf<double>& th = tmp(15, size_t(nm));
             DBuf<double>& Vd = tmp(16, size_t(nm) * nm);

@@ -316,15 +316,82 @@ __device__ __forceinline__ double2* fft_block_p(double2* a, double2* b, const do
 // last pass no store — a forward and an inverse transform chain through registers.  Passes
 // exchange through two padded ping-pong buffers (one barrier each); twiddles as fft_block_p.
 template <int N>
-constexpr bool reg_fft_len() { return N == 512 || N == 4096; }  // N/8 threads: ≥ 64
+constexpr bool reg_fft_len() { return N == 512 || N == 1024 || N == 4096; }  // N/8 threads: ≥ 64
+
+// N = 1024 = 2·8·8·8 with 128 threads, thread j holding v[r] = x[j + 128r]: a register
+// radix-2 pass (its pairs (x[j'], x[j'+512]) are (v[q], v[q+4]) for j' = j + 128q), then three
+// radix-8 Stockham passes with one exchange before each; the last pass leaves X[j + 128r] in
+// v[r] like the 8^a kernel.  One twiddle per radix-8 pass from the base table
+// tw[q] = exp(−2πi·q/1024) (k = j mod ns, angle k/(8·ns)), its powers by products.
+template <int SIGN>
+__device__ __forceinline__ void fft_reg1024(double2 (&v)[8], double2* bufA, double2* bufB, const double2* __restrict__ tw,
+                                            int j) {
+    constexpr int N = 1024, nb = N / 8;
+    double2 w1s[3];
+    w1s[0] = __ldg(tw + (j % 2) * (N / 16));
+    w1s[1] = __ldg(tw + (j % 16) * (N / 128));
+    w1s[2] = __ldg(tw + j % 128);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // pass NS = 1, R = 2 (no twiddles)
+        const double2 a = v[q], b = v[q + 4];
+        v[q] = cadd(a, b);
+        v[q + 4] = csub(a, b);
+    }
+    double2* buf = bufA;
+    // three exchanges end on bufA, where a preceding transform of the same threads (the
+    // column pass's forward before its inverse) made its last reads: wait for them
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // outputs y[2j' + t]
+        const int jj = j + nb * q;
+        buf[fpad(2 * jj)] = v[q];
+        buf[fpad(2 * jj + 1)] = v[q + 4];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = buf[fpad(j + r * nb)];
+    int ns = 2;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        {
+            double2 w1 = w1s[p];
+            if (SIGN > 0) w1.y = -w1.y;
+            const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
+            const double2 w5 = cmul(w4, w1), w6 = cmul(w3, w3), w7 = cmul(w6, w1);
+            v[1] = cmul(v[1], w1);
+            v[2] = cmul(v[2], w2);
+            v[3] = cmul(v[3], w3);
+            v[4] = cmul(v[4], w4);
+            v[5] = cmul(v[5], w5);
+            v[6] = cmul(v[6], w6);
+            v[7] = cmul(v[7], w7);
+        }
+        dft<8, SIGN>(v);
+        if (p < 2) {
+            if (bufB) buf = (buf == bufA) ? bufB : bufA;
+            else __syncthreads();  // single buffer: the previous loads are done
+            const int k = j % ns, d = (j / ns) * ns * 8 + k;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) buf[fpad(d + r * ns)] = v[r];
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = buf[fpad(j + r * nb)];
+            ns *= 8;
+        }
+    }
+}
 
 // j = index within the transform (0..N/8−1); several transforms may share a CTA (every
 // thread of the CTA must call with the same N).  bufB == nullptr: one buffer per transform
 // and a second barrier per exchange.
 template <int SIGN, int N>
 __device__ __forceinline__ void fft_reg(double2 (&v)[8], double2* bufA, double2* bufB, const double2* __restrict__ tp,
-                                        int j) {
-    static_assert(reg_fft_len<N>(), "fft_reg: N must be a power of 8");
+                                        int j, const double2* __restrict__ tw_base = nullptr) {
+    static_assert(reg_fft_len<N>(), "fft_reg: N must be 1024 or a power of 8");
+    if constexpr (N == 1024) {
+        fft_reg1024<SIGN>(v, bufA, bufB, tw_base, j);
+        return;
+    }
     constexpr int nb = N / 8;
     constexpr int NX = N == 512 ? 2 : 3;  // exchanges (passes after the first)
     // each pass needs ONE twiddle per thread (w = ω^k₂, the rest are its powers): fetched from

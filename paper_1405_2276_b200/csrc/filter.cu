@@ -48,6 +48,12 @@ __global__ void k_symmetrize(double* A, int n, long long lda) {  // A = ½(A + A
     }
 }
 
+// out[:, i] = in[:, ncol − 1 − i] (n rows, ld n; blockIdx.y = i; ncol = n here)
+__global__ void k_reverse_cols(int n, const double* __restrict__ in, int ncol, double* __restrict__ out) {
+    const int i = blockIdx.y, r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) out[r + (long long)i * n] = in[r + (long long)(ncol - 1 - i) * n];
+}
+
 __global__ void k_colsq(long long n, const double* __restrict__ U, double* __restrict__ out) {
     const double* u = U + (long long)blockIdx.x * n;
     double s = 0.0;
@@ -591,24 +597,20 @@ void randomized_ghep_device(Cov* cov, const DevCsr& H, const DevCsr& HT, double 
         ws.ensure(gemm_ws_elems(g));
         gemm(g, ws.p, s);
     }
-    std::vector<double> T = download(Td.p, size_t(k2) * k2, s);
-    for (int j = 0; j < k2; ++j)
-        for (int i = 0; i < j; ++i) T[size_t(i) + size_t(j) * k2] = T[size_t(j) + size_t(i) * k2] =
-                                        0.5 * (T[size_t(i) + size_t(j) * k2] + T[size_t(j) + size_t(i) * k2]);
-    std::vector<double> ev(static_cast<size_t>(k2)), Sv(static_cast<size_t>(k2) * k2);
-    sym_eig_small(k2, T.data(), ev.data(), Sv.data());             // (:193)
-    gclk.lap("ghep: T eig (host)");
+    symmetrize(k2, Td.p, k2, s);
+    std::vector<double> ev(static_cast<size_t>(k2));
+    DBuf<double>& Svd = out.tmp(8, size_t(k2) * k2);
+    sym_eig_tridiag_device(k2, Td.p, ev.data(), Svd.p, s);         // (:193)
+    gclk.lap("ghep: T eig");
     const int kk = int(std::min<long long>(k, k2));                // (:197-205)
     r = kk;
     lambda_h.resize(size_t(kk));
-    std::vector<double> Sk(static_cast<size_t>(k2) * kk);
-    for (int i = 0; i < kk; ++i) {
-        const int src = k2 - 1 - i;
-        lambda_h[size_t(i)] = std::max(ev[size_t(src)], 0.0);
-        std::copy(Sv.begin() + size_t(src) * k2, Sv.begin() + size_t(src + 1) * k2, Sk.begin() + size_t(i) * k2);
-    }
-    Wd.ensure(Sk.size());
-    upload(Wd.p, Sk, s);
+    for (int i = 0; i < kk; ++i) lambda_h[size_t(i)] = std::max(ev[size_t(k2 - 1 - i)], 0.0);
+    Wd.ensure(size_t(k2) * std::max(kk, 1));
+    if (kk > 0)  // S = eigenvectors in descending order: columns k2−1 … k2−kk
+        k_reverse_cols<<<dim3(ceil_div(k2, 256), kk), 256, 0, s>>>(k2, Svd.p, k2, Wd.p);
+    FKB_LAUNCH_CHECK();
+    count_launch();
     lambda.ensure(size_t(std::max(kk, 1)));
     upload(lambda.p, lambda_h, s);
     U.ensure(size_t(n) * std::max(kk, 1));
@@ -680,7 +682,11 @@ void symmetrize(int n, double* A, long long lda, cudaStream_t s) {
 Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, const double* val, double sig2,
                long long k, long long p, uint64_t seed)
     : cov(c), s(c->stream), n(c->size()), m(m_), sigma2(sig2) {
-    FKB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    {  // side branches at the lowest priority (the main chain is on the operator's high-priority stream)
+        int lo = 0, hi = 0;
+        FKB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FKB_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, lo));
+    }
     FKB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     FKB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     FKB_CUDA(cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming));
@@ -763,10 +769,14 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     vsub.alloc(size_t(n));
     if (const char* e = std::getenv("FKB_UPASS_CTAS")) upass_per_sm = std::atoi(e);
     if (const char* e = std::getenv("FKB_UPASS_THREADS")) upass_threads = std::atoi(e) == 128 ? 128 : 256;
+    // the next-K Gram forks at the step's start when it is short (rank ≤ 320: ≈ 40 µs, hidden
+    // beside the early main chain); at larger rank (c3/c4: 50–100 µs) beside the 16-SM PCG
+    kfork = r <= 320 ? 1 : 0;
     if (const char* e = std::getenv("FKB_KFORK")) kfork = std::atoi(e);
     if (const char* e = std::getenv("FKB_UFORK")) ufork = std::atoi(e);
     if (const char* e = std::getenv("FKB_FUSE_RHS")) fuse_rhs = std::atoi(e) != 0;
     if (const char* e = std::getenv("FKB_UPASS_GRID")) upass_per_sm = -std::atoi(e);  // total CTAs
+    if (const char* e = std::getenv("FKB_UPASS_SIDE")) upass_side_mode = std::atoi(e);
     cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
     info.alloc(1);
@@ -972,8 +982,8 @@ void Filter::enqueue_step(const double* d_y) {
         fork();
         launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p}, side());
         mark_on(side(), "ctz_d_update");
-        if (!fused_uq) {
-            launch_u_pass(XPlain{cvec.p}, side());
+        if (upass_side()) {
+            launch_u_pass(XPlain{cvec.p}, side(), true);
             mark_on(side(), "u_pass");
         }
         if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
@@ -984,7 +994,7 @@ void Filter::enqueue_step(const double* d_y) {
     }
     spmv_short(HT, z.p, t.p, 1.0, s);
     mark("ht_z");
-    if (fused_uq) {  // U pass + diag Σ + realizations of the new state (needs t: stays on the main branch)
+    if (fused_uq) {  // U pass + diag Σ + realizations of the new state in one pass (needs t)
         cov->apply1(t.p, t.p);
         mark("gamma_apply");
         if (par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
@@ -1001,17 +1011,25 @@ void Filter::enqueue_step(const double* d_y) {
     }
     cov->apply1_fwd(t.p);
     mark("gamma_fwd");
-    if (r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // v = U·dc ready
+    if (r > 0 && par && (upass_side() || solver == 0))
+        FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // v = U·dc (or solver 0's dc) ready
+    if (r > 0 && !upass_side()) {  // the long U pass (rank > 320 or fused UQ) on the whole GPU
+        if (solver == 0) launch_u_pass(XPlain{cvec.p}, s, false);
+        else launch_u_pass(XProd{sqd_c, ucap.p}, s, false);
+        mark("u_pass");
+    }
     cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hostout.p});
     if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
 
-// v = U·dc (the mean update's low-rank term) streaming the row-major U, limited to
-// upass_per_sm resident CTAs per SM so the latency-bound main chain it overlaps keeps room
+// v = U·dc (the mean update's low-rank term) streaming the row-major U: beside the main chain
+// at upass_per_sm CTAs per SM (so the latency-bound chain it overlaps keeps room), or on the
+// main stream with the whole GPU
 template <class XL>
-void Filter::launch_u_pass(XL xl, cudaStream_t st) {
-    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), xl, EpiStore{vsub.p}, st, upass_per_sm, upass_threads);
+void Filter::launch_u_pass(XL xl, cudaStream_t st, bool beside) {
+    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), xl, EpiStore{vsub.p}, st, beside ? upass_per_sm : 0,
+                         upass_threads);
 }
 
 // z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
@@ -1033,9 +1051,9 @@ void Filter::enqueue_solve_woodbury() {
     // the U pass v = U·(D^½x) beside the rest of the chain (ufork 0: after the capacitance
     // solve, 1: after k_woodbury_st)
     auto fork_u = [&] {
-        if (r <= 0 || uq_count >= 0) return;
+        if (r <= 0 || !upass_side()) return;
         fork();
-        launch_u_pass(XProd{sqd_c, ucap.p}, side());
+        launch_u_pass(XProd{sqd_c, ucap.p}, side(), true);
         mark_on(side(), "u_pass");
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
     };
@@ -1139,7 +1157,8 @@ void Filter::launch_step() {
         }
         capturing = false;
         FKB_CUDA(cudaStreamEndCapture(s, &gr));
-        FKB_CUDA(cudaGraphInstantiate(&graph[q], gr, 0));
+        // per-node priorities as captured: the main chain's CTAs go ahead of the U pass's
+        FKB_CUDA(cudaGraphInstantiate(&graph[q], gr, cudaGraphInstantiateFlagUseNodePriority));
         cudaGraphDestroy(gr);
         launches_per_step = int(g_launches - before);
         g_launches = before;

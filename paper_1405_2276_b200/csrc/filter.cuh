@@ -103,9 +103,15 @@ struct Filter {
     int upass_threads = 256;  // threads per U-pass CTA (FKB_UPASS_THREADS: 128 or 256)
     int kfork = 1;            // where the next-K side branch forks (FKB_KFORK, enqueue_solve_woodbury)
     int ufork = 1;            // where the U pass forks (FKB_UFORK)
-    bool fuse_rhs = true;     // capacitance RHS formed inside the PCG kernel (FKB_FUSE_RHS)
+    bool fuse_rhs = false;    // capacitance RHS formed inside the PCG kernel (FKB_FUSE_RHS; measured slower)
     template <class XL>
-    void launch_u_pass(XL xl, cudaStream_t st);
+    void launch_u_pass(XL xl, cudaStream_t st, bool beside);
+    // the U pass runs beside the main chain (side branch) when it is short enough to hide
+    // there: rank ≤ 320 (c2); otherwise after the forward FFT passes on the whole GPU (c4).
+    // The fused step + UQ (c3) keeps its single pass k_mean_uq after Γ(Hᵀz).  FKB_UPASS_SIDE
+    // = 0/1 forces either placement of the plain pass.
+    int upass_side_mode = -1;
+    bool upass_side() const { return upass_side_mode >= 0 ? upass_side_mode == 1 : (uq_count < 0 && r <= 320); }
     DBuf<int> info, flags;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one per step parity
     bool graph_ready[2] = {false, false};

@@ -10,6 +10,16 @@
 
 namespace fkb {
 
+// preferred shared-memory carveout (%) of the kernels that run beside the step's FFT passes
+// (FKB_CARVEOUT, default 50: ~100 KB shared memory, the rest L1 for the in-flight loads)
+inline int carveout_pct() {
+    static const int v = [] {
+        const char* e = std::getenv("FKB_CARVEOUT");
+        return e ? std::atoi(e) : 50;
+    }();
+    return v;
+}
+
 struct XPlain {
     const double* x;
     __device__ __forceinline__ double operator()(long long c) const { return __ldg(x + c); }
@@ -122,7 +132,8 @@ inline void launch_gemv_rowmajor_reg(long long m, int k, const double* A, long l
     FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor_reg<KC, XL, Epi>, threads, 0));
     long long cap = (long long)std::max(sms, 1) * std::max(per_sm, 1);
-    if (per_sm_cap > 0) cap = std::min(cap, (long long)std::max(sms, 1) * per_sm_cap);
+    if (per_sm_cap >= 1000) cap = 1LL << 40;  // non-persistent: one CTA per row block
+    else if (per_sm_cap > 0) cap = std::min(cap, (long long)std::max(sms, 1) * per_sm_cap);
     if (per_sm_cap < 0) cap = std::min(cap, (long long)-per_sm_cap);  // negative: a total CTA count
     const long long ctas = std::min((m + threads / 8 - 1) / (threads / 8), cap);
     k_gemv_rowmajor_reg<KC, XL, Epi><<<(unsigned)ctas, threads, 0, s>>>(m, k, A, ld, xl, epi);
@@ -156,10 +167,16 @@ inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long 
     int dev = 0, sms = 0, per_sm = 0;
     FKB_CUDA(cudaGetDevice(&dev));
     FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    static bool carve = false;  // beside the step's FFT kernels: room for their CTAs, L1 kept
+    if (!carve) {
+        FKB_CUDA(cudaFuncSetAttribute(k_gemv_rowmajor<XL, Epi>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct()));
+        carve = true;
+    }
     FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor<XL, Epi>, 256, shm));
-    if (per_sm_cap > 0) per_sm = std::min(per_sm, per_sm_cap);
+    if (per_sm_cap > 0 && per_sm_cap < 1000) per_sm = std::min(per_sm, per_sm_cap);
     const long long warps = (m + 3) / 4;  // at least one 4-row group per warp
-    const long long ctas = std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
+    const long long ctas = per_sm_cap >= 1000 ? (warps + 7) / 8  // non-persistent
+                                              : std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
     k_gemv_rowmajor<XL, Epi><<<(unsigned)ctas, 256, shm, s>>>(m, k, A, ld, xl, epi);
     FKB_LAUNCH_CHECK();
     count_launch();

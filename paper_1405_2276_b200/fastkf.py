@@ -169,6 +169,16 @@ def sym_eig_device(a: np.ndarray):
     return w, Z.reshape(n, n).T, sw.value
 
 
+def sym_eig_tridiag(a: np.ndarray):
+    """GPU Householder tridiagonalization + QL (tdeig.cu): (ascending eigenvalues, eigenvectors)."""
+    n = a.shape[0]
+    A = np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).ravel()
+    w = np.empty(n)
+    Z = np.empty(n * n)
+    check(lib().fkb_sym_eig_tridiag(n, A, w, Z))
+    return w, Z.reshape(n, n).T
+
+
 # ------------------------------------------------------------------ covariance.hpp (FFT mode)
 class CovarianceOperator:
     """CovarianceOperator(grid, spec, CovMode::fft) — covariance.hpp:69-353 on the GPU."""

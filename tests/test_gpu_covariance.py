@@ -109,3 +109,34 @@ def test_sample_pair_matches_oracle():
         a, b = gpu.sample_pair(99, 3)
         ao, bo = orc.sample_pair(99, 3)
         assert rel_err(a, ao) < 1e-10 and rel_err(b, bo) < 1e-10
+
+
+@pytest.mark.parametrize("nx,ny", [(512, 8), (8, 512), (512, 64), (64, 512)])
+@pytest.mark.parametrize("ncols", [1, 9])
+def test_register_resident_1024_passes(nx, ny, ncols):
+    """1024-point register transforms in one direction only (the other is a short
+    compile-time or generic schedule), single vector and batched, against the oracle."""
+    kern = dict(family=1, theta=1.0, length=0.1, nu=0.5)
+    gpu = P.CovarianceOperator(P.Grid(nx, ny), P.KernelSpec(**kern))
+    orc = O.CovarianceOperator(nx, ny, **kern)
+    assert (gpu.mx, gpu.my) == (orc.mx, orc.my) and 1024 in (gpu.mx, gpu.my)
+    X = O.gaussian_matrix(nx * ny, ncols, 5, 1)
+    Yg = gpu.apply(X if ncols > 1 else X[:, 0]).reshape(nx * ny, -1)
+    Yo = np.stack([orc.apply(X[:, j]) for j in range(ncols)], axis=1)
+    assert rel_err(Yg, Yo) < 1e-12
+
+
+@pytest.mark.parametrize("name,ncols", [("c4", 1), ("c4", 9), ("c2", 1), ("c2", 9)])
+def test_register_resident_tori_match_oracle(name, ncols):
+    """The register-resident transforms: 512² tori (8³ radix-8) and the c4 1024² torus
+    (2·8³: a register radix-2 pass, three radix-8 exchanges), single vector (the step's
+    Γ(Hᵀz)) and batched (≥ 8 columns: the offline Γ·X), against the oracle's FFTW restatement."""
+    w = W.CONFIGS[name]
+    kern = dict(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    gpu = P.CovarianceOperator(P.Grid(w.n, w.n), P.KernelSpec(**kern))
+    orc = O.CovarianceOperator(w.n, w.n, **kern)
+    assert (gpu.mx, gpu.my) == (orc.mx, orc.my)
+    X = O.gaussian_matrix(w.N, ncols, 17, 3)
+    Yg = gpu.apply(X if ncols > 1 else X[:, 0])
+    Yo = np.stack([orc.apply(X[:, j]) for j in range(ncols)], axis=1)
+    assert rel_err(Yg.reshape(w.N, -1), Yo) < 1e-12
