@@ -142,6 +142,8 @@ def phase_work(w, r, fft_flops, nnz, uq_count=-1, fft_split=None):
     mean_upd = ("hbm", w_bytes + 24.0 * N + 16.0 * N * cnt)
     # U pass: U in, v out, the step's r-vectors (+ diag Σ out, draws in, xp out)
     u_pass = 8.0 * N * r + 8.0 * N + 16.0 * r + (0.0 if uq_count < 0 else 8.0 * N + 16.0 * N * cnt + 8.0 * r * cnt)
+    if uq_count >= 0:  # k_mean_uq: U, t and mean in; mean, diag Σ and the realizations out
+        mean_upd = ("hbm", 8.0 * N * r + 32.0 * N + 16.0 * N * cnt + 8.0 * r * cnt + 16.0 * r)
     return {
         "residual": ("hbm", 12.0 * nnz + 4.0 * (m + 1) + 8.0 * N + 16.0 * m),
         "capacitance": ("tensor", 1.0 * m * r * (r + 1)),  # symmetric Eᵀ·diag·E (lower half)
@@ -434,6 +436,9 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     sp_ms = ga.elapsed_time(gb) / reps
     sp_bytes = 12 * h.nnz + 4 * (h.rows + 1) + 8 * (w.N + w.m) * l
+    sp_l2_bytes = 8.0 * h.nnz * l  # every nonzero reads one 8·l-byte X row (served from L2)
+    l2_peak = C.c_double()
+    check(L.fkb_l2_peak(32, C.byref(l2_peak)))
     # W-block products of the offline GHEP on the DMMA path (lowrank.hpp:53-106, :197-205):
     # the Γ-metric Gram Ȳᵀ(ΓȲ) (N×l)ᵀ(N×l) and the basis rotation U = Q·S (N×l)(l×k)
     wprod = {}
@@ -522,8 +527,10 @@ def run_ours(args, rank, world, local_rank):
                     "flops_per_column": fcol, "peak_tflops": fp64_peak},
         "spmm": {"gbs": sp_bytes / (sp_ms * 1e-3) / 1e9, "frac": sp_bytes / (sp_ms * 1e-3) / 1e9 / hbm,
                  "columns": l, "us": sp_ms * 1e3, "bytes": sp_bytes, "layout": "row-major X (N×l), Y (m×l)",
-                 "note": "each nonzero streams an 8·l-byte X row from L2: bound by the L2 bandwidth cap, "
-                         "L2→SM traffic = 8·nnz·l bytes"},
+                 "l2_gbs": sp_l2_bytes / (sp_ms * 1e-3) / 1e9, "l2_peak_gbs": l2_peak.value,
+                 "l2_frac": sp_l2_bytes / (sp_ms * 1e-3) / 1e9 / l2_peak.value,
+                 "note": "each nonzero streams an 8·l-byte X row from L2: L2→SM traffic = 8·nnz·l bytes, "
+                         "l2_frac against the measured L2→SM read bandwidth (fkb_l2_peak, 32 MB buffer)"},
         "w_products": {**{kk: {**v, "frac": v["tflops"] / fp64_peak} for kk, v in wprod.items()},
                        "shapes": f"gram: ({w.N}x{l})^T({w.N}x{l}); basis: ({w.N}x{l})({l}x{k})",
                        "kernels": "k_gram (split-K DMMA, 16-byte cp.async), k_gemm (DMMA)"},

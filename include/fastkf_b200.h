@@ -145,7 +145,9 @@ int fkb_lowrank_uq(fkb_cov* c, long long n, int r, double alpha, const double* d
 
 /* The GHEP's W-block products on the DMMA path (device pointers, column-major, on `stream`):
  * which 0 — Gram C (p×q) = AᵀB, A n×p, B n×q (Ȳᵀ(ΓȲ), lowrank.hpp:53-106 block form);
- * which 1 — C (n×q) = A (n×p)·B (p×q) (U = Q·S, Ū = Q̄·S, lowrank.hpp:197-205). */
+ * which 1 — C (n×q) = A (n×p)·B (p×q) (U = Q·S, Ū = Q̄·S, lowrank.hpp:197-205);
+ * which 2 — symmetric Gram C (p×p) = AᵀA, both triangles (the per-step capacitance kernel
+ *           k_gram_sym, fast_filter.hpp:100-108 in Woodbury form; q must equal p, B unused). */
 int fkb_dense_product(int which, long long n, int p, int q, const double* dA, const double* dB, double* dC,
                       void* stream);
 
@@ -236,6 +238,8 @@ int fkb_cap_pcg_test(int n, const double* K, const double* b, double* x, int* it
 
 /* measured FP64 peak of this GPU (mode 0: DFMA pipe, 1: DMMA tensor path), TFLOP/s */
 int fkb_fp64_peak(int mode, double* tflops);
+/* measured L2→SM read bandwidth (GB/s) over an L2-resident buffer of mbytes MB */
+int fkb_l2_peak(int mbytes, double* gbs);
 int fkb_set_device(int device);  /* cudaSetDevice for this library's runtime */
 int fkb_profiler(int on);        /* cudaProfilerStart/Stop (ncu --profile-from-start off) */
 

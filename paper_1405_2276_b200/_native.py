@@ -101,6 +101,7 @@ SIGNATURES = {
     "fkb_filter_graph_timing": (_i, [_p, _i]),
     "fkb_filter_graph_phase_times": (_i, [_p, _dp, C.c_char_p, _i, _PI]),
     "fkb_fp64_peak": (_i, [_i, _PD]),
+    "fkb_l2_peak": (_i, [_i, _PD]),
     "fkb_chol_solve_small": (_i, [_i, _dp, _dp, _dp, _dp, np.ctypeslib.ndpointer(dtype=np.uint64)]),
     "fkb_cap_pcg_test": (_i, [_i, _dp, _dp, _dp, _PI, np.ctypeslib.ndpointer(dtype=np.uint64)]),
     "fkb_set_device": (_i, [_i]),

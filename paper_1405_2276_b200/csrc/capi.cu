@@ -516,7 +516,15 @@ int fkb_dense_product(int which, long long n, int p, int q, const double* dA, co
         static fkb::DBuf<double> ws;
         if (which == 0) fkb::gram_tn(n, p, q, dA, dB, dC, ws, s);
         else if (which == 1) fkb::tall_times_small(n, p, q, dA, dB, dC, s);
-        else throw std::invalid_argument("dense_product: which must be 0 (AᵀB) or 1 (A·B)");
+        else if (which == 2) {  // symmetric Gram AᵀA (n×p A, both triangles): the capacitance kernel
+            if (q != p) throw std::invalid_argument("dense_product: the symmetric Gram needs q == p");
+            fkb::GemmArgs g;
+            g.M = p; g.N = p; g.K = int(n);
+            g.A = dA; g.lda = n; g.transA = 1;
+            g.B = dA; g.ldb = n;
+            g.C = dC; g.ldc = p;
+            fkb::gram_sym(g, s);
+        } else throw std::invalid_argument("dense_product: which must be 0 (AᵀB), 1 (A·B) or 2 (AᵀA)");
     });
 }
 int fkb_ghep_run(fkb_cov* c, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,

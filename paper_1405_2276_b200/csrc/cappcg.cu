@@ -161,13 +161,100 @@ __device__ __forceinline__ void fused_rhs(PcgShared& sh, const PcgRhs& ra, int r
     }
 }
 
+// sh.q[c] = sqd_j · Σ_b parts[b·n + j] for this CTA's rows j = r0 + c (the rotate-in kernel's
+// per-CTA partials of Eᵀ(Λ_M⁻¹r̃)): warp w sums parts b ≡ w (mod 16), lane l column r0 + l
+// (+32), 16 loads in flight per lane; the 16 warp sums are then added in warp order
+// (deterministic).
+__device__ __forceinline__ void parts_rhs(PcgShared& sh, const PcgRhs& ra, int n, int r0, int r1) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = PC_T / 32;
+    __shared__ double part[NW][32];
+    for (int c0 = 0; c0 < r1 - r0; c0 += 32) {
+        const int c = c0 + lane;
+        const bool on = r0 + c < r1;
+        double acc = 0.0;
+        for (int b0 = warp; b0 < ra.nparts; b0 += NW * 16) {
+            double v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int b = b0 + q * NW;
+                v[q] = (on && b < ra.nparts) ? __ldcg(ra.parts + (long long)b * n + r0 + c) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc += v[q];
+        }
+        part[warp][lane] = acc;
+        __syncthreads();
+        if (tid < 32 && on) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) v += part[w][lane];
+            sh.q[c] = __ldg(ra.sqd + r0 + c) * v;
+        }
+        __syncthreads();
+    }
+}
+
+// The filter step's Woodbury tail (PcgTail): x (all n entries) is in xs on every CTA.
+// s̃ rows split over the cluster, a warp per 4 rows with 32 loads in flight per lane; then each
+// CTA commits d for the capacitance rows it owns and CTA 0 commits α.
+__device__ __forceinline__ void woodbury_tail(const PcgTail& tl, const double* xs, double* ys, int n, int crank,
+                                              bool own, int row, double x, bool zero) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int j = tid; j < n; j += PC_T) ys[j] = zero ? 0.0 : __ldg(tl.sqd + j) * xs[j];
+    __syncthreads();
+    const int mb = (tl.m + PC_CL - 1) / PC_CL;
+    const int i0 = min(tl.m, crank * mb), i1 = min(tl.m, i0 + mb);
+    for (int ib = i0 + warp * 4; ib < i1; ib += (PC_T / 32) * 4) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int jb = 0; jb < n; jb += 32 * 8) {
+            double e[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int j = jb + lane + 32 * c;
+                    e[q][c] = (ib + q < i1 && j < n) ? __ldcg(tl.Erow + (long long)(ib + q) * n + j) : 0.0;
+                }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int j = jb + lane + 32 * c;
+                const double yv = j < n ? ys[j] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = fma(e[q][c], yv, acc[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        if (lane < 4 && ib + lane < i1) {
+            const int i = ib + lane;
+            const double a = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+            tl.st[i] = __ldg(tl.wsq + i) * (__ldg(tl.rt + i) + a);
+        }
+    }
+    const double alpha = tl.alpha_dev[1];
+    if (own) {
+        const double dj = tl.d[row], l = tl.lam[row], c = alpha - dj;
+        tl.dc[row] = zero ? 0.0 : __ldg(tl.sqd + row) * x;
+        const double dn = (dj + alpha * l * c) / (1.0 + l * c);
+        tl.d[row] = dn;
+        if (tl.hout[1]) reinterpret_cast<double*>(tl.hout[1])[row] = dn;
+    }
+    if (crank == 0 && tid == 0) tl.alpha_dev[0] = alpha;
+}
+
 template <int KR>
 __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, long long ld, int n,
                                                  double* __restrict__ u, double* __restrict__ work,
                                                  int* __restrict__ fallback, int maxit, double tol, int kstage,
-                                                 unsigned long long* __restrict__ ts, double vtol, PcgRhs ra) {
+                                                 unsigned long long* __restrict__ ts, double vtol, PcgRhs ra,
+                                                 PcgTail tl) {
     __shared__ PcgShared sh;
     extern __shared__ double Ks[];  // this CTA's columns of K (rb × n) when kstage
+    // a programmatic dependent (the step's k_woodbury_st_pdl) may start staging its operands now;
+    // it waits for this grid's completion before reading x
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const bool stamp = ts && blockIdx.x == 0 && threadIdx.x == 0;
     if (stamp) ts[0] = gtimer();
     cg::cluster_group cl = cg::this_cluster();
@@ -210,6 +297,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         for (int e = n + tid; e < 16 * KR; e += PC_T) sh.v[0][e] = sh.v[1][e] = 0.0;
     __syncthreads();  // mbarrier initialized before anyone waits on it
     if (ra.E) fused_rhs(sh, ra, r0, r1);  // overlaps the K staging copy
+    else if (ra.parts) parts_rhs(sh, ra, n, r0, r1);
     // Pipelined Jacobi-PCG (Ghysels–Vanroose): the matvec n = K·m and the reductions
     // γ = rᵀu, δ = wᵀu of the same iteration are independent, so one cluster exchange per
     // iteration carries both: owners push m into every CTA and every CTA pushes its
@@ -226,7 +314,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         const double kii = K[row + (long long)row * ld];
         nonpos = kii > 0.0 ? 0.0 : 1.0;
         dinv = 1.0 / kii;
-        if (ra.E) {
+        if (ra.E || ra.parts) {
             r = sh.q[tid];
             u[row] = r;  // the Cholesky fallback's right-hand side
         } else {
@@ -464,6 +552,13 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
         if (own) u[row] = x;
     } else if (crank == 0 && tid == 0) {
         *fallback = 1;
+        if (tl.st || tl.retry_only) atomicCAS(tl.info, 0, kInfoRetry);
+    }
+    // Woodbury tail: the residual check left x (all n entries) in sh.v[(it + 1) & 1] of every
+    // CTA; it == 0 means u = 0, x = 0.  *info is uniform here (set only by earlier kernels).
+    if (tl.st && done && *reinterpret_cast<volatile int*>(tl.info) == 0) {
+        const int xb = (it + 1) & 1;
+        woodbury_tail(tl, sh.v[xb], sh.v[xb ^ 1], n, crank, own, row, x, it == 0);
     }
     if (crank == 0 && tid == 0) work[n] = double(it);  // iteration count (diagnostics)
     if (stamp) ts[63] = gtimer();
@@ -472,9 +567,10 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
 static bool g_pcg_attr = false;
 
 void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int* fallback, cudaStream_t s, int maxit,
-             double tol, unsigned long long* ts, double vtol, PcgRhs rhs) {
+             double tol, unsigned long long* ts, double vtol, PcgRhs rhs, PcgTail tail) {
     if (n <= 0) return;
     if (n > PC_MAXN) throw std::invalid_argument("cap_pcg: n exceeds 1024");
+    if (tail.st && !(vtol > 0.0)) throw std::invalid_argument("cap_pcg: the Woodbury tail needs the residual check");
     const int rb = (n + PC_CL - 1) / PC_CL;
     const size_t stage = sizeof(double) * size_t(rb) * n;
     const int kstage = stage <= 190 * 1024 ? 1 : 0;  // K columns resident in shared memory
@@ -498,11 +594,11 @@ void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int*
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (kstage && n <= 16 * 20)
-        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<20>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs));
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<20>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs, tail));
     else if (kstage && n <= 16 * 32)
-        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<32>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs));
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<32>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs, tail));
     else
-        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<0>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs));
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, k_cap_pcg<0>, K, ld, n, u, work, fallback, maxit, tol, kstage, ts, vtol, rhs, tail));
     count_launch();
 }
 

@@ -230,6 +230,41 @@ __global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double*
     if (lane == 0) st[i] = wsq[i] * (rt[i] + acc);
 }
 
+// The same product launched as a programmatic dependent of the PCG cluster: its CTAs become
+// resident while the 16-SM PCG runs and load their rows of E, Λ_M⁻¹ and r̃ (none depend on the
+// solve), then wait for the PCG grid (griddepcontrol.wait) and read only x.
+__global__ void __launch_bounds__(256) k_woodbury_st_pdl(int m, int r, const double* __restrict__ Erow,
+                                                        const double* __restrict__ sqd, const double* __restrict__ x,
+                                                        const double* __restrict__ wsq, const double* __restrict__ rt,
+                                                        double* __restrict__ st, EpiCtzD upd) {
+    if (blockIdx.x == gridDim.x - 1) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int j = threadIdx.x; j < r; j += blockDim.x) upd(j, x[j], sqd[j]);
+        return;
+    }
+    const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const bool on = i < m;
+    const double* er = Erow + (long long)(on ? i : 0) * r;
+    constexpr int NQ = 16;  // r ≤ 512 held in registers across the wait
+    double e[NQ], sq[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int j = lane + 32 * q;
+        e[q] = (on && j < r) ? er[j] : 0.0;
+        sq[q] = j < r ? __ldg(sqd + j) : 0.0;
+    }
+    const double wi = on ? wsq[i] : 0.0, ri = on ? rt[i] : 0.0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int j = lane + 32 * q;
+        acc = fma(e[q], j < r ? sq[q] * x[j] : 0.0, acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (on && lane == 0) st[i] = wi * (ri + acc);
+}
+
 // d'_i = (d_i + αλ_i(α − d_i)) / (1 + λ_i(α − d_i))  (fast_filter.hpp:118-123); commits α
 __global__ void k_d_update(int r, double* __restrict__ d, const double* __restrict__ lam, double* alpha_dev,
                            const int* __restrict__ info) {
@@ -303,74 +338,143 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
 // `count` conditional realizations after every step): per row i of the column-major U,
 //   mean_i ← (mean_i + α·t_i) − Σ_j U_ij dc_j                      (fast_filter.hpp:114-116)
 //   var_i = αθ − Σ_j d_j U_ij²,  x_s,i = mean_i + √α(z_s,i − Σ_j U_ij Σ₋_j (Ūᵀz_s)_j)
-// with α, d already updated for this step (α_dev[1]; d by the Woodbury epilogue), one thread
-// per row and 8 coalesced column loads in flight.  The failure flag gates every write, as
+// with α, d already updated for this step (α_dev[1]; d by the Woodbury epilogue).  Each thread
+// owns R rows 128 apart (a warp reads 256 B of a column per load, 8·R loads in flight); the
+// per-column constants (dc_j, d_j and the CNT projections) sit in shared memory as one record
+// per column, read with 16-byte broadcasts and reused over the R rows — the shared-memory
+// issue rate, not HBM, bounded the one-row version.  The failure flag gates every write, as
 // EpiMean, and is published to the mapped host slot.
+template <int CNT, int R, int JB>
 __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const double* __restrict__ U,
                                                    const double* __restrict__ dc, const double* __restrict__ d,
                                                    const double* __restrict__ alpha_dev, double theta,
-                                                   const double* __restrict__ t, double* __restrict__ mean, int count,
+                                                   const double* __restrict__ t, double* __restrict__ mean,
                                                    const double* __restrict__ Z, const double* __restrict__ proj,
                                                    double* __restrict__ X, double* __restrict__ var,
                                                    const int* __restrict__ info,
                                                    const unsigned long long* __restrict__ hout) {
-    extern __shared__ double sh[];
-    double* cs = sh;           // dc (r)
-    double* ds = sh + r;       // d  (r)
-    double* P = sh + 2 * r;    // Σ₋ ⊙ Ūᵀz_s (r × count)
+    constexpr int SW = (2 + CNT + 1) & ~1;  // record: dc, d, Σ₋⊙Ūᵀz_s (s < CNT), pad
+    extern __shared__ double2 rec2[];
+    double* rec = reinterpret_cast<double*>(rec2);
     const int bad = *info;
     if (blockIdx.x == 0 && threadIdx.x == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
     if (bad) return;
     const double alpha = alpha_dev[1];
-    for (int j = threadIdx.x; j < r; j += blockDim.x) {
-        cs[j] = dc[j];
-        ds[j] = d[j];
-        const double sm = 1.0 - sqrt(fmax(1.0 - d[j] / alpha, 0.0));  // uq.hpp:59-64
-        for (int s = 0; s < count; ++s) P[j * count + s] = sm * proj[j + (long long)s * r];
+    const int rp = (r + 15) / 16 * 16;
+    for (int j = threadIdx.x; j < rp; j += blockDim.x) {
+        double* q = rec + (long long)j * SW;
+        const bool in = j < r;
+        const double dj = in ? d[j] : 0.0;
+        q[0] = in ? dc[j] : 0.0;
+        q[1] = dj;
+        const double sm = in ? 1.0 - sqrt(fmax(1.0 - dj / alpha, 0.0)) : 0.0;  // uq.hpp:59-64
+#pragma unroll
+        for (int s = 0; s < CNT; ++s) q[2 + s] = in ? sm * proj[j + (long long)s * r] : 0.0;
+        if (SW > 2 + CNT) q[SW - 1] = 0.0;
     }
     __syncthreads();
     const double ra = sqrt(alpha);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double vm = 0.0, vs = 0.0;
-        double acc[8];
+    double* vo = hout[4] ? reinterpret_cast<double*>(hout[4]) : var;  // mapped host or device
+    double* xo = hout[3] ? reinterpret_cast<double*>(hout[3]) : X;
+    const long long span = (long long)blockDim.x * R;
+    for (long long i0 = blockIdx.x * span + threadIdx.x; i0 < n; i0 += (long long)gridDim.x * span) {
+        double vm[R], vs[R], acc[R][CNT > 0 ? CNT : 1];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) acc[s] = 0.0;
-        int j0 = 0;
-        for (; j0 + 16 <= r; j0 += 16) {  // 16 coalesced column loads in flight per thread
-            double u[16];
+        for (int q = 0; q < R; ++q) {
+            vm[q] = vs[q] = 0.0;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) u[q] = __ldcs(U + i + (long long)(j0 + q) * n);
+            for (int s = 0; s < CNT; ++s) acc[q][s] = 0.0;
+        }
+        for (int j0 = 0; j0 < r; j0 += JB) {
+            double u[R][JB];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int j = j0 + q;
-                vm = fma(u[q], cs[j], vm);
-                vs = fma(u[q] * u[q], ds[j], vs);
+            for (int q = 0; q < R; ++q) {
+                const long long i = i0 + q * (long long)blockDim.x;
 #pragma unroll
-                for (int s = 0; s < 8; ++s)
-                    if (s < count) acc[s] = fma(u[q], P[j * count + s], acc[s]);
+                for (int c = 0; c < JB; ++c)
+                    u[q][c] = (i < n && j0 + c < r) ? __ldcs(U + i + (long long)(j0 + c) * n) : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < JB; ++c) {
+                const double2* p = rec2 + (long long)(j0 + c) * (SW / 2);
+                const double2 cd = p[0];
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    vm[q] = fma(u[q][c], cd.x, vm[q]);
+                    vs[q] = fma(u[q][c] * u[q][c], cd.y, vs[q]);
+                }
+#pragma unroll
+                for (int s = 0; s + 1 < CNT; s += 2) {
+                    const double2 pp = p[1 + s / 2];
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        acc[q][s] = fma(u[q][c], pp.x, acc[q][s]);
+                        acc[q][s + 1] = fma(u[q][c], pp.y, acc[q][s + 1]);
+                    }
+                }
+                if constexpr (CNT & 1) {
+                    const double pl = p[1 + CNT / 2].x;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) acc[q][CNT - 1] = fma(u[q][c], pl, acc[q][CNT - 1]);
+                }
             }
         }
-        for (int j = j0; j < r; ++j) {
-            const double u = U[i + (long long)j * n];
-            vm = fma(u, cs[j], vm);
-            vs = fma(u * u, ds[j], vs);
 #pragma unroll
-            for (int s = 0; s < 8; ++s)
-                if (s < count) acc[s] = fma(u, P[j * count + s], acc[s]);
-        }
-        const double mi = (mean[i] + alpha * t[i]) - vm;
-        mean[i] = mi;
-        if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = mi;
-        double* vo = hout[4] ? reinterpret_cast<double*>(hout[4]) : var;  // mapped host or device
-        double* xo = hout[3] ? reinterpret_cast<double*>(hout[3]) : X;
-        if (vo) vo[i] = alpha * theta - vs;
+        for (int q = 0; q < R; ++q) {
+            const long long i = i0 + q * (long long)blockDim.x;
+            if (i >= n) continue;
+            const double mi = (mean[i] + alpha * t[i]) - vm[q];
+            mean[i] = mi;
+            if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = mi;
+            if (vo) vo[i] = alpha * theta - vs[q];
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
-            if (s < count) {
+            for (int s = 0; s < CNT; ++s) {
                 const double z = Z[i + (long long)s * n];
-                xo[i + (long long)s * n] = mi + (ra * z - ra * acc[s]);
+                xo[i + (long long)s * n] = mi + (ra * z - ra * acc[q][s]);
             }
+        }
     }
+}
+
+void launch_mean_uq(int count, long long n, int r, const double* U, const double* dc, const double* d,
+                    const double* alpha_dev, double theta, const double* t, double* mean, const double* Z,
+                    const double* proj, double* X, double* var, const int* info, const unsigned long long* hout,
+                    cudaStream_t s) {
+    // rows per thread × columns per batch (FKB_UQ_SHAPE 116 or 208; measured at c3: one row
+    // with 16 column loads in flight per batch is fastest)
+    static const int shape = [] {
+        const char* e = std::getenv("FKB_UQ_SHAPE");
+        return e ? std::atoi(e) : 116;
+    }();
+    auto go = [&](auto c) {
+        constexpr int CNT = decltype(c)::value;
+        constexpr int SW = (2 + CNT + 1) & ~1;
+        const size_t shm = sizeof(double) * size_t((r + 15) / 16 * 16) * SW;
+        auto launch = [&](auto kern, int R) {
+            static bool attr = false;
+            if (!attr) {
+                FKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                attr = true;
+            }
+            kern<<<ceil_div(n, 128 * R), 128, shm, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, Z, proj, X, var,
+                                                       info, hout);
+        };
+        if (shape == 208) launch(k_mean_uq<CNT, 2, 8>, 2);
+        else launch(k_mean_uq<CNT, 1, 16>, 1);
+    };
+    switch (count) {
+        case 0: go(std::integral_constant<int, 0>{}); break;
+        case 1: go(std::integral_constant<int, 1>{}); break;
+        case 2: go(std::integral_constant<int, 2>{}); break;
+        case 3: go(std::integral_constant<int, 3>{}); break;
+        case 4: go(std::integral_constant<int, 4>{}); break;
+        case 5: go(std::integral_constant<int, 5>{}); break;
+        case 6: go(std::integral_constant<int, 6>{}); break;
+        case 7: go(std::integral_constant<int, 7>{}); break;
+        default: go(std::integral_constant<int, 8>{}); break;
+    }
+    FKB_LAUNCH_CHECK();
+    count_launch();
 }
 
 // ghep_residual (lowrank.hpp:215-228) per pair j: ‖A u_j − λ_j Γ⁻¹u_j‖ / max(λ_j‖Γ⁻¹u_j‖, ε)
@@ -757,6 +861,7 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     pcgwork.alloc(size_t(std::max(r, 1)) + 2);
     dsnap.alloc(size_t(std::max(r, 1)));
     pcgflag.alloc(1);
+    parts.alloc(size_t(std::max(coldot_grid(m), 1)) * std::max(r, 1));
     if (std::getenv("FKB_PCG_STAMPS")) pcg_ts.alloc(64);
     {
         GemmArgs g;  // split-K workspace of the capacitance Gram
@@ -775,6 +880,10 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     if (const char* e = std::getenv("FKB_KFORK")) kfork = std::atoi(e);
     if (const char* e = std::getenv("FKB_UFORK")) ufork = std::atoi(e);
     if (const char* e = std::getenv("FKB_FUSE_RHS")) fuse_rhs = std::atoi(e) != 0;
+    // the PDL-launched s̃ kernel wins when the U pass runs beside the chain (rank ≤ 320, c2); at
+    // larger rank its early-resident CTAs crowd the next-K Gram, so the PCG cluster's tail does it
+    fused_chain = r <= 320 ? 2 : 1;
+    if (const char* e = std::getenv("FKB_FUSED_CHAIN")) fused_chain = std::atoi(e);
     if (const char* e = std::getenv("FKB_UPASS_GRID")) upass_per_sm = -std::atoi(e);  // total CTAs
     if (const char* e = std::getenv("FKB_UPASS_SIDE")) upass_side_mode = std::atoi(e);
     cvec.alloc(size_t(std::max(r, 1)));
@@ -901,6 +1010,7 @@ std::vector<std::pair<std::string, double>> Filter::phase_times(int reps) {
             acc[i - 1].second += ms / reps;
         }
         for (auto e : ev) cudaEventDestroy(e);
+        gt_last_par = par_next;  // the parity a rerun of this step would use
         par_next ^= 1;
         check_info();
         alpha += 1.0;
@@ -965,7 +1075,7 @@ void Filter::enqueue_step(const double* d_y) {
         k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
                                                theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq_c : nullptr,
                                                sqd_c, (solver == 1 && r > 0) ? dsnap.p : nullptr,
-                                               solver == 1 ? pcgflag.p : nullptr);
+                                               (solver == 1 && !exact) ? pcgflag.p : nullptr);
         FKB_LAUNCH_CHECK();
         count_launch();
     }
@@ -998,13 +1108,9 @@ void Filter::enqueue_step(const double* d_y) {
         cov->apply1(t.p, t.p);
         mark("gamma_apply");
         if (par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
-        const size_t shm = sizeof(double) * size_t(r) * (2 + std::max(uq_count, 1));
-        k_mean_uq<<<ceil_div(n, 128), 128, shm, s>>>(n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
-                                                     uq_count, uq_count ? draws.p : nullptr,
-                                                     uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
-                                                     hostout.p);
-        FKB_LAUNCH_CHECK();
-        count_launch();
+        launch_mean_uq(uq_count, n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
+                       uq_count ? draws.p : nullptr, uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
+                       hostout.p, s);
         if (solver == 1 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
         mark("mean_update");
         return;
@@ -1033,10 +1139,16 @@ void Filter::launch_u_pass(XL xl, cudaStream_t st, bool beside) {
 }
 
 // z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
+// Fused chain (default): rotate_in also leaves per-CTA partials of u = D^½Eᵀ(Λ_M⁻¹r̃); the PCG
+// cluster sums them, solves K x = u, verifies the true residual and, in its tail, forms
+// s̃ = Λ_M⁻¹(r̃ + E·D^½x) and commits d and α — three dependent launches instead of five.  A
+// solve that does not verify raises kInfoRetry: the step's state epilogues are gated off and
+// the host reruns it on the exact path (exact = true: column-dot RHS, cluster Cholesky,
+// k_woodbury_st), which also reproduces the reference's "singular" error.
 void Filter::enqueue_solve_woodbury() {
     // side branch: the NEXT step's Woodbury scalars and K into the other parity's buffers (they
-    // depend on α and d only); forked at kfork: 0 after cap_rhs (beside the 16-SM PCG cluster),
-    // 1 at the start of the step, 2 after the capacitance solve
+    // depend on α and d only); forked at kfork: 0 before the capacitance solve (beside the
+    // 16-SM PCG cluster), 1 at the start of the step, 2 after the capacitance solve
     auto fork_next_k = [&] {
         if (r <= 0) return;
         if (side() != s) {
@@ -1048,8 +1160,7 @@ void Filter::enqueue_solve_woodbury() {
         mark_on(side() != s ? s3 : s, "capacitance");
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join2, s3));
     };
-    // the U pass v = U·(D^½x) beside the rest of the chain (ufork 0: after the capacitance
-    // solve, 1: after k_woodbury_st)
+    // the U pass v = U·(D^½x) beside the rest of the chain
     auto fork_u = [&] {
         if (r <= 0 || !upass_side()) return;
         fork();
@@ -1058,36 +1169,74 @@ void Filter::enqueue_solve_woodbury() {
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
     };
     if (kfork == 1) fork_next_k();
-    launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
-    mark("rotate_in");
-    if (r > 0) {
-        // u = D^½·Eᵀ·Λ_M⁻¹·r̃: formed by the PCG kernel itself (fuse_rhs) or as column dots
-        PcgRhs rhs;
-        if (fuse_rhs) {
-            rhs.E = E.p; rhs.lde = m; rhs.m = m; rhs.wsq = wsq_c; rhs.rt = rt.p; rhs.sqd = sqd_c;
-        } else {
-            launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
-            mark("cap_rhs");
-        }
+    const bool fused = fused_chain && !exact && r > 0;
+    if (fused) {
+        // r̃ = Pᵀ(y − H·mean) and the partials of Eᵀ(Λ_M⁻¹r̃) in one pass
+        launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, CtaParts{Erow.p, r, wsq_c, parts.p});
+        mark("rotate_in");
         if (kfork == 0) fork_next_k();
-        // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap.
-        // ‖Kx − u‖ ≤ 1e-12‖u‖: the solve's error reaches the mean through U·D^½x at ~1e-12
-        // relative, three orders below the 1e-9 parity bar.  A converged x is re-checked
-        // against the true residual ‖u − Kx‖ ≤ 1e-11‖u‖ inside the kernel (the pipelined
-        // recursion can drift); a miss routes to the Cholesky.
-        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs);
-        chol_solve_small(r, K_c, r, ucap.p, rdg.p, info.p, s, nullptr, pcgflag.p);
+        PcgRhs rhs;
+        rhs.parts = parts.p; rhs.nparts = coldot_grid(m); rhs.sqd = sqd_c;
+        PcgTail tl;
+        const bool pdl = fused_chain == 2 && r <= 512;
+        tl.info = info.p;
+        tl.retry_only = pdl;
+        if (!pdl) {
+            tl.Erow = Erow.p; tl.m = m; tl.wsq = wsq_c; tl.rt = rt.p; tl.sqd = sqd_c; tl.st = st.p; tl.dc = cvec.p;
+            tl.d = d.p; tl.lam = lambda.p; tl.alpha_dev = alpha_dev.p; tl.hout = hostout.p;
+        }
+        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs, tl);
+        if (pdl) {  // s̃ and the d/α commit by a programmatic dependent (gated on the flag the PCG raises)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(std::max(1, ceil_div(m, 8)) + 1, 1, 1);
+            cfg.blockDim = dim3(256, 1, 1);
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            FKB_CUDA(cudaLaunchKernelEx(&cfg, k_woodbury_st_pdl, m, r, (const double*)Erow.p, (const double*)sqd_c,
+                                        (const double*)ucap.p, (const double*)wsq_c, (const double*)rt.p, st.p,
+                                        EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p}));
+            count_launch();
+        }
         mark("cap_solve");
         if (kfork == 2) fork_next_k();
-        if (ufork == 0) fork_u();
+        fork_u();
+    } else {
+        launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
+        mark("rotate_in");
+        if (r > 0) {
+            // u = D^½·Eᵀ·Λ_M⁻¹·r̃: formed by the PCG kernel itself (fuse_rhs) or as column dots
+            PcgRhs rhs;
+            if (fuse_rhs && !exact) {
+                rhs.E = E.p; rhs.lde = m; rhs.m = m; rhs.wsq = wsq_c; rhs.rt = rt.p; rhs.sqd = sqd_c;
+            } else {
+                launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
+                mark("cap_rhs");
+            }
+            if (kfork == 0) fork_next_k();
+            // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap.
+            // ‖Kx − u‖ ≤ 1e-12‖u‖: the solve's error reaches the mean through U·D^½x at ~1e-12
+            // relative, three orders below the 1e-9 parity bar.  A converged x is re-checked
+            // against the true residual ‖u − Kx‖ ≤ 1e-11‖u‖ inside the kernel (the pipelined
+            // recursion can drift); a miss routes to the Cholesky.  The exact rerun of a step
+            // goes to the Cholesky directly.
+            if (!exact) cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs);
+            chol_solve_small(r, K_c, r, ucap.p, rdg.p, info.p, s, nullptr, exact ? nullptr : pcgflag.p);
+            mark("cap_solve");
+            if (kfork == 2) fork_next_k();
+            if (ufork == 0) fork_u();
+        }
+        // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
+        k_woodbury_st<<<std::max(1, ceil_div(m, 8)) + 1, 256, 0, s>>>(
+            m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p});
+        FKB_LAUNCH_CHECK();
+        count_launch();
+        mark("woodbury_st");
+        if (ufork == 1) fork_u();
     }
-    // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
-    k_woodbury_st<<<std::max(1, ceil_div(m, 8)) + 1, 256, 0, s>>>(
-        m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p});
-    FKB_LAUNCH_CHECK();
-    count_launch();
-    mark("woodbury_st");
-    if (ufork == 1) fork_u();
     launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s);  // z = P·s̃ (rows of P)
     mark("rotate_out");
 }
@@ -1118,7 +1267,33 @@ void Filter::check_info() {
     int h = 0;
     FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FKB_CUDA(cudaStreamSynchronize(s));
+    if (h == kInfoRetry) {
+        rerun_exact(gt_last_par);
+        FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+    }
     if (h) fail_step("fkf_step: innovation system is singular");
+}
+
+// The step replayed with parity q left the state untouched because its capacitance PCG did not
+// verify (kInfoRetry): clear the flag and run the same step (observation in ybuf, the same
+// parity's K, wsq and sqd) eagerly on the exact path — cluster Cholesky, which reports a
+// non-positive-definite system exactly like the reference LLT (fast_filter.hpp:104-106).  The
+// side branch recomputes the next step's K as usual.
+void Filter::rerun_exact(int q) {
+    FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+    // this step's K, Λ_M⁻¹ and D^½ afresh from the committed α and d: inside an asynchronous
+    // batch the no-op steps behind the sticky flag have overwritten the parity buffers
+    if (solver == 1 && r > 0) enqueue_capacitance(s, 0, wsqb[q].p, sqdb[q].p, Kb[q].p);
+    select_parity(q);
+    exact = true;
+    try {
+        enqueue_step(ybuf.p);
+    } catch (...) {
+        exact = false;
+        throw;
+    }
+    exact = false;
 }
 
 // A failed step: clear the sticky device flag (so the next step can run), invalidate the
@@ -1221,17 +1396,24 @@ void Filter::step_uq_host(const double* h_y, uint64_t seed, int count, double* h
     else set_hostout(0, 0, 0);
     if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_y, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
     launch_step();
-    if (!zc) {
-        FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
-        if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+    auto outputs = [&] {
+        if (!zc) {
+            FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
+            if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        }
+        if (r > 0 && !zx) {
+            if (h_var) FKB_CUDA(cudaMemcpyAsync(h_var, uq_var.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+            if (h_x && count)
+                FKB_CUDA(cudaMemcpyAsync(h_x, uq_x.p, sizeof(double) * size_t(n) * count, cudaMemcpyDeviceToHost, s));
+        }
+        FKB_CUDA(cudaStreamSynchronize(s));
+    };
+    outputs();
+    if (*h_info == kInfoRetry) {  // the PCG did not verify: the exact rerun writes the outputs
+        rerun_exact(gt_last_par);
+        outputs();
     }
-    if (r > 0 && !zx) {
-        if (h_var) FKB_CUDA(cudaMemcpyAsync(h_var, uq_var.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
-        if (h_x && count)
-            FKB_CUDA(cudaMemcpyAsync(h_x, uq_x.p, sizeof(double) * size_t(n) * count, cudaMemcpyDeviceToHost, s));
-    }
-    FKB_CUDA(cudaStreamSynchronize(s));
     if (*h_info) fail_step("fkf_step: innovation system is singular");
     alpha += 1.0;
     ++step_no;
@@ -1256,12 +1438,19 @@ void Filter::step_host_state(const double* h_y, double* h_d, double* h_mean) {
     else set_hostout(0, 0, 0);
     if (m > 0) FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_y, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
     launch_step();
-    if (!zc) {
-        FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
-        if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+    auto outputs = [&] {
+        if (!zc) {
+            FKB_CUDA(cudaMemcpyAsync(h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d, d.p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, s));
+            if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean, mean.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        }
+        FKB_CUDA(cudaStreamSynchronize(s));
+    };
+    outputs();
+    if (*h_info == kInfoRetry) {  // the PCG did not verify: the exact rerun writes the outputs
+        rerun_exact(gt_last_par);
+        outputs();
     }
-    FKB_CUDA(cudaStreamSynchronize(s));
     if (*h_info) fail_step("fkf_step: innovation system is singular");
     alpha += 1.0;
     ++step_no;
@@ -1276,6 +1465,9 @@ void Filter::step_host(const double* h_y) {
 void Filter::steps_async(const double* d_ys, int nsteps, long long ldy) {
     // Device-resident observation sequence; one deferred singularity check at the end.
     set_hostout(0, 0, 0);
+    batch_ys = d_ys;
+    batch_ldy = ldy;
+    batch_par0 = par_next;
     for (int k = 0; k < nsteps; ++k) {
         FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_ys + (long long)k * ldy, sizeof(double) * size_t(m),
                                  cudaMemcpyDeviceToDevice, s));
@@ -1293,7 +1485,25 @@ void Filter::finish_async(int nsteps) {
     FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FKB_CUDA(cudaMemcpyAsync(&a, alpha_dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     FKB_CUDA(cudaStreamSynchronize(s));
-    const int done = int(std::lround(a - alpha));
+    int done = int(std::lround(a - alpha));
+    // a step whose PCG did not verify (and, through the sticky flag, every later step of the
+    // batch) changed nothing: rerun it on the exact path, then replay the rest of the batch
+    while (h == kInfoRetry && batch_ys && done < nsteps) {
+        const int par = (batch_par0 + done) & 1;
+        FKB_CUDA(cudaMemcpyAsync(ybuf.p, batch_ys + (long long)done * batch_ldy, sizeof(double) * size_t(m),
+                                 cudaMemcpyDeviceToDevice, s));
+        rerun_exact(par);
+        par_next = par ^ 1;
+        for (int k = done + 1; k < nsteps; ++k) {
+            FKB_CUDA(cudaMemcpyAsync(ybuf.p, batch_ys + (long long)k * batch_ldy, sizeof(double) * size_t(m),
+                                     cudaMemcpyDeviceToDevice, s));
+            launch_step();
+        }
+        FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaMemcpyAsync(&a, alpha_dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+        done = int(std::lround(a - alpha));
+    }
     alpha = a;
     step_no += done;
     if (done > 0) state_rank = r;

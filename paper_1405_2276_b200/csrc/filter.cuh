@@ -104,6 +104,16 @@ struct Filter {
     int kfork = 1;            // where the next-K side branch forks (FKB_KFORK, enqueue_solve_woodbury)
     int ufork = 1;            // where the U pass forks (FKB_UFORK)
     bool fuse_rhs = false;    // capacitance RHS formed inside the PCG kernel (FKB_FUSE_RHS; measured slower)
+    // fused chain (FKB_FUSED_CHAIN, default on): rotate_in → PCG (+ s̃ and the d/α commit) →
+    // rotate_out; exact = the eager rerun of a step whose PCG did not verify (kInfoRetry)
+    int fused_chain = 1;  // 0: unfused; 1: Woodbury tail in the PCG cluster; 2: k_woodbury_st PDL-launched after it
+    bool exact = false;
+    DBuf<double> parts;  // rotate_in's per-CTA partials of Eᵀ(Λ_M⁻¹r̃), coldot_grid(m) × r
+    void rerun_exact(int parity);
+    // the device observations of the last asynchronous batch (rerun of a failed step)
+    const double* batch_ys = nullptr;
+    long long batch_ldy = 0;
+    int batch_par0 = 0;
     template <class XL>
     void launch_u_pass(XL xl, cudaStream_t st, bool beside);
     // the U pass runs beside the main chain (side branch) when it is short enough to hide

@@ -182,14 +182,42 @@ inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long 
     count_launch();
 }
 
+// Optional CTA epilogue of k_coldot, run by the whole CTA once its CPC column values are known
+// (vals in shared memory): NoCta does nothing; CtaParts leaves this CTA's partial of the
+// capacitance right-hand side, parts[b·r + l] = Σ_c Erow[j0+c, l]·wsq_{j0+c}·vals_c, so the
+// rotate-in r̃ = Pᵀz and Eᵀ(Λ_M⁻¹r̃) share one pass (the PCG kernel sums the partials).
+struct NoCta {
+    static constexpr bool active = false;
+    __device__ __forceinline__ void operator()(int, int, const double*) const {}
+};
+struct CtaParts {
+    static constexpr bool active = true;
+    const double* Erow;  // m×r row-major
+    int r;
+    const double* wsq;
+    double* parts;  // gridDim.x × r
+    __device__ __forceinline__ void operator()(int j0, int nc, const double* vals) const {
+        double w[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) w[c] = c < nc ? __ldg(wsq + j0 + c) * vals[c] : 0.0;
+        for (int l = threadIdx.x; l < r; l += blockDim.x) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < nc) acc = fma(__ldg(Erow + (long long)(j0 + c) * r + l), w[c], acc);
+            parts[(long long)blockIdx.x * r + l] = acc;
+        }
+    }
+};
+
 // ---- single-launch column dots: out_j = epi(j, Σ_i A_ij·x_i) for column-major A (m×n).
 // A CTA owns CPC consecutive columns; each thread keeps its x values in registers (reused
 // over the CPC columns) and issues every load of a 2048-row chunk × CPC columns before the
 // first FMA, so a chunk costs one memory latency.  Fixed-order reductions (deterministic),
 // no split partials and no second kernel.
-template <class XL, class Epi, int CPC>
+template <class XL, class Epi, int CPC, class CE = NoCta>
 __global__ void __launch_bounds__(256, CPC == 4 ? 4 : 1) k_coldot(int m, int n, const double* __restrict__ A, long long lda, XL xl,
-                                               Epi epi) {
+                                               Epi epi, CE cepi = CE{}) {
     constexpr int EPT = CPC == 4 ? 4 : 8;  // CPC 4: ≤ 64 regs, 4 CTAs/SM, n = 2048 in one wave
     const int j0 = blockIdx.x * CPC;
     double acc[CPC];
@@ -217,25 +245,33 @@ __global__ void __launch_bounds__(256, CPC == 4 ? 4 : 1) k_coldot(int m, int n, 
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
     }
     __syncthreads();
+    __shared__ double colv[CPC];
     if (threadIdx.x < CPC && j0 + threadIdx.x < n) {
         double v = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
         epi(j0 + threadIdx.x, v);
+        colv[threadIdx.x] = v;
+    }
+    if constexpr (CE::active) {
+        __syncthreads();
+        cepi(j0, min(CPC, n - j0), colv);
     }
 }
 
-template <class XL, class Epi>
-inline void launch_coldot(int m, int n, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s) {
+inline int coldot_cpc(int n) { return n >= 8 * 296 ? 8 : n >= 4 * 296 ? 4 : n >= 2 * 296 ? 2 : 1; }
+inline int coldot_grid(int n) { return n <= 0 ? 0 : (n + coldot_cpc(n) - 1) / coldot_cpc(n); }
+
+template <class XL, class Epi, class CE = NoCta>
+inline void launch_coldot(int m, int n, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s,
+                          CE cepi = CE{}) {
     if (n <= 0) return;
-    if (n >= 8 * 296) {
-        k_coldot<XL, Epi, 8><<<(unsigned)((n + 7) / 8), 256, 0, s>>>(m, n, A, lda, xl, epi);
-    } else if (n >= 4 * 296) {
-        k_coldot<XL, Epi, 4><<<(unsigned)((n + 3) / 4), 256, 0, s>>>(m, n, A, lda, xl, epi);
-    } else if (n >= 2 * 296) {
-        k_coldot<XL, Epi, 2><<<(unsigned)((n + 1) / 2), 256, 0, s>>>(m, n, A, lda, xl, epi);
-    } else {
-        k_coldot<XL, Epi, 1><<<(unsigned)n, 256, 0, s>>>(m, n, A, lda, xl, epi);
+    const unsigned g = (unsigned)coldot_grid(n);
+    switch (coldot_cpc(n)) {
+        case 8: k_coldot<XL, Epi, 8, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
+        case 4: k_coldot<XL, Epi, 4, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
+        case 2: k_coldot<XL, Epi, 2, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
+        default: k_coldot<XL, Epi, 1, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
     }
     FKB_LAUNCH_CHECK();
     count_launch();

@@ -160,14 +160,23 @@ void spmm_rm(const DevCsr& A, const double* X, long long ldx, int ncols, double*
     // flight.  Measured at c2 (l = 320): long rows (rays, ~320 nonzeros) 128 columns per warp
     // with 16 nonzeros per batch; short rows (cells, ~10) 256 columns with 4.
     const bool longrows = double(A.nnz) / A.rows > 64.0;
-    const int Q = ncols <= 32 ? 1 : longrows ? 4 : 8;
+    static const int qu = [] {  // FKB_SPMM_QU (development sweeps): 10·Q + U-code for long rows
+        const char* e = std::getenv("FKB_SPMM_QU");
+        return e ? std::atoi(e) : 0;
+    }();
+    int Q = ncols <= 32 ? 1 : longrows ? 4 : 8, U = Q == 1 ? 8 : longrows ? 16 : 4;
+    if (longrows && ncols > 32 && qu) { Q = qu / 100; U = qu % 100; }
     const dim3 grid(ceil_div((long long)A.rows * 32, 256), ceil_div(ncols, 32 * Q));
-    if (Q == 1)
-        k_spmm_rm<1, 8><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
-    else if (Q == 4)
-        k_spmm_rm<4, 16><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
-    else
-        k_spmm_rm<8, 4><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
+    auto go = [&](auto kern) { kern<<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha); };
+    if (Q == 1) go(k_spmm_rm<1, 8>);
+    else if (Q == 2 && U == 8) go(k_spmm_rm<2, 8>);
+    else if (Q == 2 && U == 16) go(k_spmm_rm<2, 16>);
+    else if (Q == 2) go(k_spmm_rm<2, 32>);
+    else if (Q == 4 && U == 8) go(k_spmm_rm<4, 8>);
+    else if (Q == 4) go(k_spmm_rm<4, 16>);
+    else if (Q == 5 && U == 8) go(k_spmm_rm<5, 8>);
+    else if (Q == 5) go(k_spmm_rm<5, 4>);
+    else go(k_spmm_rm<8, 4>);
     FKB_LAUNCH_CHECK();
     count_launch();
 }

@@ -1,16 +1,15 @@
-# c2 bench line under a list of environment settings (one per argument, e.g. "FKB_FUSE_RHS=0")
+# c2 bench lines (device value, e2e, in-graph phases) under environment variants.
+#   bash scripts/env_sweep.sh TAG CONFIG "VAR=a VAR2=b" "VAR=c" ...
+tag=$1; cfg=$2; shift 2
 mkdir -p gpurun_out
-i=0
-for spec in "$@"; do
-  i=$((i+1))
-  env $spec timeout 300 python bench.py --no-cpu-baseline --no-widened ${BENCH_ARGS:-} > gpurun_out/env_$i.json 2>gpurun_out/env_$i.err
-  python - "$i" "$spec" <<'PY'
-import json, sys
+for v in "$@"; do
+  env $v timeout 300 python bench.py --config $cfg --no-cpu-baseline --no-widened > gpurun_out/sweep_$tag.json 2> gpurun_out/sweep_$tag.err
+  python -c "
+import json
 try:
-    d = json.load(open(f"gpurun_out/env_{sys.argv[1]}.json"))
-except Exception as e:
-    print(sys.argv[2], "FAILED", e); sys.exit()
-k = d["kernel_ms_in_graph"]
-print(f"[{sys.argv[2]}]", round(d["value"]), round(d["e2e"]["value"]), " ".join(f"{a}={1e3*b:.1f}" for a, b in k.items()))
-PY
+    d=json.loads(open('gpurun_out/sweep_$tag.json').read().strip().splitlines()[-1])
+    print('$cfg [$v]', round(d['value']), 'e2e', round(d['e2e']['value']), 'us', round(d['ms_per_step']*1e3,1), {k: round(v*1e3,1) for k,v in d.get('kernel_ms_in_graph',{}).items()}, flush=True)
+except Exception as e: print('$v', 'ERR', e)
+"
+  tail -1 gpurun_out/sweep_$tag.err
 done

@@ -8,11 +8,11 @@ timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.er
 timeout 600 python bench.py --config c3 --no-cpu-baseline --no-widened > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
 timeout 900 python bench.py --config c4 --no-cpu-baseline --no-widened --steps 20 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-python scripts/profile_step.py c2 > /dev/null 2>&1 && \
+python scripts/profile.py step c2 > /dev/null 2>&1 && \
 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-    --clock-control none --csv --log-file gpurun_out/launches_c2.csv python scripts/profile_step.py c2 > gpurun_out/ncu_launch.log 2>&1
+    --clock-control none --csv --log-file gpurun_out/launches_c2.csv python scripts/profile.py step c2 > gpurun_out/ncu_launch.log 2>&1
 python scripts/launch_summary.py gpurun_out/launches_c2.csv > gpurun_out/launches_c2.txt 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_gemv_rowmajor \
-    -o gpurun_out/step_gemv -f python scripts/profile_step.py c2 > gpurun_out/ncu_gemv.log 2>&1
+    -o gpurun_out/step_gemv -f python scripts/profile.py step c2 > gpurun_out/ncu_gemv.log 2>&1
 python scripts/ncu_summary.py gpurun_out/step_gemv.ncu-rep step_gemv > gpurun_out/step_gemv.txt 2>&1
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log

@@ -413,3 +413,73 @@ def test_ghep_residual_matches_dense():  # lowrank.hpp:215-228, test_lowrank.cpp
     assert res.shape == (ctx.rank(),)
     assert np.max(np.abs(res - want)) < 1e-7
     assert res.max() < 1e-7  # the reference's sketched bound (test_lowrank.cpp:167)
+
+
+def _c2_pair(monkeypatch, steps):
+    """Two c2 contexts built from the same inputs: the fused step chain (default) and the
+    unfused one (FKB_FUSED_CHAIN=0: separate RHS column dots, gated Cholesky, k_woodbury_st)."""
+    w, h, ys, s2 = workload_inputs("c2", steps)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), kern)
+    a = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    monkeypatch.setenv("FKB_FUSED_CHAIN", "0")
+    b = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    monkeypatch.delenv("FKB_FUSED_CHAIN")
+    return w, ys, a, b
+
+
+def test_fused_chain_matches_unfused_chain(monkeypatch):
+    """The fused rotate_in → PCG(+ s̃, d/α commit) chain and the five-launch chain compute the
+    same step (fast_filter.hpp:100-123): same α, d to 1e-14·α, mean to 1e-12."""
+    w, ys, a, b = _c2_pair(monkeypatch, 4)
+    for y in ys:
+        sa, sb = P.fkf_step(a, y), P.fkf_step(b, y)
+        assert sa["alpha"] == sb["alpha"] and sa["step"] == sb["step"]
+        assert np.max(np.abs(sa["d"] - sb["d"])) / sa["alpha"] < 1e-14
+        assert rel_err(sa["mean"], sb["mean"]) < 1e-12
+    assert a.cap_stats()[1] is False
+
+
+def test_unverified_pcg_reruns_exactly_in_async_batches():
+    """A step whose PCG does not verify (forced: cap 0) leaves the state untouched and is rerun
+    on the exact Cholesky path — also inside an asynchronous batch, where the later steps of
+    the batch (no-ops behind the sticky flag) are replayed after the rerun."""
+    from paper_1405_2276_b200._native import DeviceArray
+    w, ys, a = _c0_ctx()
+    _, _, b = _c0_ctx()
+    b.set_pcg_maxit(0)
+    Y = DeviceArray.from_host(np.stack(ys).ravel())
+    a.steps_async(Y.ptr, len(ys), w.m)
+    a.sync(len(ys))
+    b.steps_async(Y.ptr, len(ys), w.m)
+    b.sync(len(ys))
+    sa, sb = a.state(), b.state()
+    assert sa["alpha"] == sb["alpha"] and sa["step"] == sb["step"] == len(ys)
+    assert rel_err(sb["mean"], sa["mean"]) < 1e-12
+    assert np.max(np.abs(sb["d"] - sa["d"])) / sa["alpha"] < 1e-12
+    assert b.cap_stats()[1] is True
+
+
+def test_unverified_pcg_rerun_writes_mapped_outputs():
+    """fkb_fkf_step_state with page-locked buffers: the graph's gated epilogues skip the
+    unverified step and the exact rerun writes d and the mean through the mapped pointers."""
+    import ctypes as C
+    import torch
+    from paper_1405_2276_b200._native import lib
+    w, ys, a = _c0_ctx()
+    _, _, b = _c0_ctx()
+    b.set_pcg_maxit(0)
+    hd = torch.empty(max(b.rank(), 1), dtype=torch.float64).pin_memory()
+    hm = torch.empty(w.N, dtype=torch.float64).pin_memory()
+    for y in ys:
+        sa = P.fkf_step(a, y)
+        y = np.ascontiguousarray(y)
+        hd.fill_(np.nan)
+        hm.fill_(np.nan)
+        alpha = C.c_double()
+        assert lib().fkb_fkf_step_state(b._f, C.c_void_p(y.ctypes.data), len(y), C.byref(alpha),
+                                        C.c_void_p(hd.data_ptr()), C.c_void_p(hm.data_ptr())) == 0
+        assert alpha.value == sa["alpha"]
+        assert rel_err(hm.numpy(), sa["mean"]) < 1e-12
+        assert np.max(np.abs(hd.numpy()[: b.rank()] - sa["d"])) / sa["alpha"] < 1e-12
