@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* 
                                                       const double* __restrict__ theta, const double* __restrict__ d,
                                                       double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
                                                       double* __restrict__ dsnap, int* __restrict__ pcgflag) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // rotate_in may stage P now
     const int gid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const double alpha = alpha_dev[0] + 1.0;
     if (gid == 0) {
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(256) k_woodbury_st_pdl(int m, int r, const dou
                                                         const double* __restrict__ sqd, const double* __restrict__ x,
                                                         const double* __restrict__ wsq, const double* __restrict__ rt,
                                                         double* __restrict__ st, EpiCtzD upd) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // rotate_out may stage Pᵀ now
     if (blockIdx.x == gridDim.x - 1) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int j = threadIdx.x; j < r; j += blockDim.x) upd(j, x[j], sqd[j]);
@@ -330,6 +332,81 @@ __global__ void __launch_bounds__(256) k_uq(long long n, int r, const double* __
             if (s < count) {
                 const double z = Z[i + (long long)s * n];
                 X[i + (long long)s * n] = alpha == 0.0 ? mi : mi + (ra * z - ra * acc[s]);
+            }
+    }
+}
+
+// The step's U pass fused with the UQ of the new state (c3-style workloads: diag Σ and
+// `count` conditional realizations after every step): per row i of the column-major U,
+//   mean_i ← (mean_i + α·t_i) − Σ_j U_ij dc_j                      (fast_filter.hpp:114-116)
+//   var_i = αθ − Σ_j d_j U_ij²,  x_s,i = mean_i + √α(z_s,i − Σ_j U_ij Σ₋_j (Ūᵀz_s)_j)
+// with α, d already updated for this step (α_dev[1]; d by the Woodbury epilogue), one thread
+// per row and 16 coalesced column loads in flight (the default shape; k_mean_uq below holds
+// the shared-memory-record variants).  The failure flag gates every write, as EpiMean, and is
+// published to the mapped host slot.
+__global__ void __launch_bounds__(128, 3) k_mean_uq1(long long n, int r, const double* __restrict__ U,
+                                                   const double* __restrict__ dc, const double* __restrict__ d,
+                                                   const double* __restrict__ alpha_dev, double theta,
+                                                   const double* __restrict__ t, double* __restrict__ mean, int count,
+                                                   const double* __restrict__ Z, const double* __restrict__ proj,
+                                                   double* __restrict__ X, double* __restrict__ var,
+                                                   const int* __restrict__ info,
+                                                   const unsigned long long* __restrict__ hout) {
+    extern __shared__ double sh[];
+    double* cs = sh;           // dc (r)
+    double* ds = sh + r;       // d  (r)
+    double* P = sh + 2 * r;    // Σ₋ ⊙ Ūᵀz_s (r × count)
+    const int bad = *info;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+    if (bad) return;
+    const double alpha = alpha_dev[1];
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        cs[j] = dc[j];
+        ds[j] = d[j];
+        const double sm = 1.0 - sqrt(fmax(1.0 - d[j] / alpha, 0.0));  // uq.hpp:59-64
+        for (int s = 0; s < count; ++s) P[j * count + s] = sm * proj[j + (long long)s * r];
+    }
+    __syncthreads();
+    const double ra = sqrt(alpha);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double vm = 0.0, vs = 0.0;
+        double acc[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[s] = 0.0;
+        int j0 = 0;
+        for (; j0 + 16 <= r; j0 += 16) {  // 16 coalesced column loads in flight per thread
+            double u[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) u[q] = __ldcs(U + i + (long long)(j0 + q) * n);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int j = j0 + q;
+                vm = fma(u[q], cs[j], vm);
+                vs = fma(u[q] * u[q], ds[j], vs);
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    if (s < count) acc[s] = fma(u[q], P[j * count + s], acc[s]);
+            }
+        }
+        for (int j = j0; j < r; ++j) {
+            const double u = U[i + (long long)j * n];
+            vm = fma(u, cs[j], vm);
+            vs = fma(u * u, ds[j], vs);
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+                if (s < count) acc[s] = fma(u, P[j * count + s], acc[s]);
+        }
+        const double mi = (mean[i] + alpha * t[i]) - vm;
+        mean[i] = mi;
+        if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = mi;
+        double* vo = hout[4] ? reinterpret_cast<double*>(hout[4]) : var;  // mapped host or device
+        double* xo = hout[3] ? reinterpret_cast<double*>(hout[3]) : X;
+        if (vo) vo[i] = alpha * theta - vs;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if (s < count) {
+                const double z = Z[i + (long long)s * n];
+                xo[i + (long long)s * n] = mi + (ra * z - ra * acc[s]);
             }
     }
 }
@@ -440,11 +517,12 @@ void launch_mean_uq(int count, long long n, int r, const double* U, const double
                     const double* alpha_dev, double theta, const double* t, double* mean, const double* Z,
                     const double* proj, double* X, double* var, const int* info, const unsigned long long* hout,
                     cudaStream_t s) {
-    // rows per thread × columns per batch (FKB_UQ_SHAPE 116 or 208; measured at c3: one row
-    // with 16 column loads in flight per batch is fastest)
+    // FKB_UQ_SHAPE: 0 (default) k_mean_uq1 — one row per thread, separate constant arrays;
+    // 116 / 208 — shared-memory records, 1 row × 16 or 2 rows × 8 columns per batch (c3, in
+    // graph: 64 / 80 / 68 µs)
     static const int shape = [] {
         const char* e = std::getenv("FKB_UQ_SHAPE");
-        return e ? std::atoi(e) : 116;
+        return e ? std::atoi(e) : 0;
     }();
     auto go = [&](auto c) {
         constexpr int CNT = decltype(c)::value;
@@ -460,7 +538,12 @@ void launch_mean_uq(int count, long long n, int r, const double* U, const double
                                                        info, hout);
         };
         if (shape == 208) launch(k_mean_uq<CNT, 2, 8>, 2);
-        else launch(k_mean_uq<CNT, 1, 16>, 1);
+        else if (shape == 116) launch(k_mean_uq<CNT, 1, 16>, 1);
+        else {
+            const size_t shm1 = sizeof(double) * size_t(r) * (2 + std::max(count, 1));
+            k_mean_uq1<<<ceil_div(n, 128), 128, shm1, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, count, Z, proj,
+                                                           X, var, info, hout);
+        }
     };
     switch (count) {
         case 0: go(std::integral_constant<int, 0>{}); break;
@@ -884,6 +967,8 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     // larger rank its early-resident CTAs crowd the next-K Gram, so the PCG cluster's tail does it
     fused_chain = r <= 320 ? 2 : 1;
     if (const char* e = std::getenv("FKB_FUSED_CHAIN")) fused_chain = std::atoi(e);
+    pdl_mask = 3;  // rotate_in / rotate_out stage their first chunk of P / Pᵀ before the wait
+    if (const char* e = std::getenv("FKB_PDL")) pdl_mask = std::atoi(e);
     if (const char* e = std::getenv("FKB_UPASS_GRID")) upass_per_sm = -std::atoi(e);  // total CTAs
     if (const char* e = std::getenv("FKB_UPASS_SIDE")) upass_side_mode = std::atoi(e);
     cvec.alloc(size_t(std::max(r, 1)));
@@ -1172,7 +1257,8 @@ void Filter::enqueue_solve_woodbury() {
     const bool fused = fused_chain && !exact && r > 0;
     if (fused) {
         // r̃ = Pᵀ(y − H·mean) and the partials of Eᵀ(Λ_M⁻¹r̃) in one pass
-        launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, CtaParts{Erow.p, r, wsq_c, parts.p});
+        launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, CtaParts{Erow.p, r, wsq_c, parts.p},
+                      (pdl_mask & 1) != 0);
         mark("rotate_in");
         if (kfork == 0) fork_next_k();
         PcgRhs rhs;
@@ -1237,7 +1323,8 @@ void Filter::enqueue_solve_woodbury() {
         mark("woodbury_st");
         if (ufork == 1) fork_u();
     }
-    launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s);  // z = P·s̃ (rows of P)
+    launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s, NoCta{},  // z = P·s̃ (rows of P)
+                  fused && fused_chain == 2 && r <= 512 && (pdl_mask & 2));
     mark("rotate_out");
 }
 

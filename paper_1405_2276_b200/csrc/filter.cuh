@@ -108,6 +108,7 @@ struct Filter {
     // rotate_out; exact = the eager rerun of a step whose PCG did not verify (kInfoRetry)
     int fused_chain = 1;  // 0: unfused; 1: Woodbury tail in the PCG cluster; 2: k_woodbury_st PDL-launched after it
     bool exact = false;
+    int pdl_mask = 0;  // FKB_PDL: 1 rotate_in after the residual, 2 rotate_out after k_woodbury_st_pdl
     DBuf<double> parts;  // rotate_in's per-CTA partials of Eᵀ(Λ_M⁻¹r̃), coldot_grid(m) × r
     void rerun_exact(int parity);
     // the device observations of the last asynchronous batch (rerun of a failed step)

@@ -215,7 +215,7 @@ struct CtaParts {
 // over the CPC columns) and issues every load of a 2048-row chunk × CPC columns before the
 // first FMA, so a chunk costs one memory latency.  Fixed-order reductions (deterministic),
 // no split partials and no second kernel.
-template <class XL, class Epi, int CPC, class CE = NoCta>
+template <class XL, class Epi, int CPC, class CE = NoCta, bool PDL = false>
 __global__ void __launch_bounds__(256, CPC == 4 ? 4 : 1) k_coldot(int m, int n, const double* __restrict__ A, long long lda, XL xl,
                                                Epi epi, CE cepi = CE{}) {
     constexpr int EPT = CPC == 4 ? 4 : 8;  // CPC 4: ≤ 64 regs, 4 CTAs/SM, n = 2048 in one wave
@@ -223,19 +223,40 @@ __global__ void __launch_bounds__(256, CPC == 4 ? 4 : 1) k_coldot(int m, int n, 
     double acc[CPC];
 #pragma unroll
     for (int c = 0; c < CPC; ++c) acc[c] = 0.0;
-    for (int i0 = 0; i0 < m; i0 += 256 * EPT) {
-        double xv[EPT], e[CPC][EPT];
+    auto chunk = [&](int i0, const double (&e)[CPC][EPT]) {
+        double xv[EPT];
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
             const int i = i0 + threadIdx.x + 256 * q;
             xv[q] = i < m ? xl(i) : 0.0;
-#pragma unroll
-            for (int c = 0; c < CPC; ++c) e[c][q] = (i < m && j0 + c < n) ? A[i + (long long)(j0 + c) * lda] : 0.0;
         }
 #pragma unroll
         for (int c = 0; c < CPC; ++c)
 #pragma unroll
             for (int q = 0; q < EPT; ++q) acc[c] = fma(e[c][q], xv[q], acc[c]);
+    };
+    auto load = [&](int i0, double (&e)[CPC][EPT]) {
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int i = i0 + threadIdx.x + 256 * q;
+#pragma unroll
+            for (int c = 0; c < CPC; ++c) e[c][q] = (i < m && j0 + c < n) ? A[i + (long long)(j0 + c) * lda] : 0.0;
+        }
+    };
+    int istart = 0;
+    if constexpr (PDL) {
+        // programmatic dependent launch: the first chunk of A does not depend on the producer
+        // kernel, so it is in flight before waiting for that kernel's x
+        double e[CPC][EPT];
+        load(0, e);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        chunk(0, e);
+        istart = 256 * EPT;
+    }
+    for (int i0 = istart; i0 < m; i0 += 256 * EPT) {
+        double e[CPC][EPT];
+        load(i0, e);  // every load of the chunk (and x's) before the first FMA
+        chunk(i0, e);
     }
     __shared__ double red[8][CPC];
 #pragma unroll
@@ -264,14 +285,30 @@ inline int coldot_grid(int n) { return n <= 0 ? 0 : (n + coldot_cpc(n) - 1) / co
 
 template <class XL, class Epi, class CE = NoCta>
 inline void launch_coldot(int m, int n, const double* A, long long lda, XL xl, Epi epi, cudaStream_t s,
-                          CE cepi = CE{}) {
+                          CE cepi = CE{}, bool pdl = false) {
     if (n <= 0) return;
     const unsigned g = (unsigned)coldot_grid(n);
+    auto go = [&](auto kplain, auto kpdl) {
+        if (!pdl) {
+            kplain<<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi);
+            return;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g, 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        FKB_CUDA(cudaLaunchKernelEx(&cfg, kpdl, m, n, A, lda, xl, epi, cepi));
+    };
     switch (coldot_cpc(n)) {
-        case 8: k_coldot<XL, Epi, 8, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
-        case 4: k_coldot<XL, Epi, 4, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
-        case 2: k_coldot<XL, Epi, 2, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
-        default: k_coldot<XL, Epi, 1, CE><<<g, 256, 0, s>>>(m, n, A, lda, xl, epi, cepi); break;
+        case 8: go(k_coldot<XL, Epi, 8, CE, false>, k_coldot<XL, Epi, 8, CE, true>); break;
+        case 4: go(k_coldot<XL, Epi, 4, CE, false>, k_coldot<XL, Epi, 4, CE, true>); break;
+        case 2: go(k_coldot<XL, Epi, 2, CE, false>, k_coldot<XL, Epi, 2, CE, true>); break;
+        default: go(k_coldot<XL, Epi, 1, CE, false>, k_coldot<XL, Epi, 1, CE, true>); break;
     }
     FKB_LAUNCH_CHECK();
     count_launch();

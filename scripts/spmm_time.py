@@ -22,14 +22,15 @@ X = torch.randn(w.N, l, dtype=torch.float64, device="cuda")
 Z = torch.empty(w.m, l, dtype=torch.float64, device="cuda")
 ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+st = torch.cuda.ExternalStream(ctx.stream)  # the library's stream
 out = {}
 for which, src, dst in ((0, X, Z), (1, Z, X)):
     ctx.spmm_rm_device(which, ptr(src), l, ptr(dst))
     torch.cuda.synchronize()
-    a.record()
+    a.record(st)
     for _ in range(10):
         ctx.spmm_rm_device(which, ptr(src), l, ptr(dst))
-    b.record()
+    b.record(st)
     torch.cuda.synchronize()
     out[which] = a.elapsed_time(b) / 10
 pk = C.c_double()
