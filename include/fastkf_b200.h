@@ -102,6 +102,17 @@ int fkb_fkf_step(fkb_filter* f, const double* y, long long ylen);
 /* one step from host y AND the new state (α, d (r), mean (N)) in one round trip — the reference's
  * fkf_step returns the new LowRankState by value (fast_filter.hpp:84-125); d/mean may be null */
 int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* alpha, double* d, double* mean);
+/* nsteps fkf_steps over host observations (row t at ys + t·ldy) with every step's new state
+ * returned: alphas[t], d row t (ld ldd ≥ r), mean row t (ld ldm ≥ N) — the driver's step loop
+ * (driver.hpp:283-300) as one call; each step's outputs leave the GPU while the next step runs
+ * (page-locked host arrays overlap best).  Outputs may be null.  A singular step raises (status
+ * 2) naming it; the steps before it are committed and their outputs valid. */
+int fkb_fkf_run(fkb_filter* f, const double* ys, int nsteps, long long ldy, double* alphas, double* d, long long ldd,
+                double* mean, long long ldm);
+/* the same with each new state's diag Σ (var row t, N) and `count` ≤ 8 FFT-mode realizations
+ * (x: N×count block per step at x + t·N·count) from the fused U pass (uq.hpp:16-23, 86-112) */
+int fkb_fkf_run_uq(fkb_filter* f, const double* ys, int nsteps, long long ldy, uint64_t seed, int count, double* x,
+                   double* var, double* alphas, double* d, long long ldd, double* mean, long long ldm);
 int fkb_fkf_step_device(fkb_filter* f, const double* d_y);
 /* one step plus the UQ of the new state — diag Σ (var, N) and `count` ≤ 8 conditional
  * realizations (x, N×count; RealizationPropagator draws (seed, s/2), uq.hpp:86-112) — from ONE

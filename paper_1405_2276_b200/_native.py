@@ -73,6 +73,8 @@ SIGNATURES = {
     "fkb_filter_get": (_i, [_p, _i, _dp]),
     "fkb_fkf_step": (_i, [_p, _p, _ll]),
     "fkb_fkf_step_state": (_i, [_p, _p, _ll, _p, _p, _p]),
+    "fkb_fkf_run": (_i, [_p, _p, _i, _ll, _p, _p, _ll, _p, _ll]),
+    "fkb_fkf_run_uq": (_i, [_p, _p, _i, _ll, C.c_uint64, _i, _p, _p, _p, _p, _ll, _p, _ll]),
     "fkb_fkf_step_device": (_i, [_p, _p]),
     "fkb_fkf_steps_async": (_i, [_p, _p, _i, _ll]),
     "fkb_fkf_sync": (_i, [_p, _i]),

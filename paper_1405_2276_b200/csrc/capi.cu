@@ -344,6 +344,32 @@ int fkb_fkf_step_state(fkb_filter* f, const double* y, long long ylen, double* a
         if (alpha) *alpha = F.alpha;
     });
 }
+int fkb_fkf_run(fkb_filter* f, const double* ys, int nsteps, long long ldy, double* alphas, double* d, long long ldd,
+                double* mean, long long ldm) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (nsteps < 0) throw std::invalid_argument("fkf_run: negative step count");
+        if (nsteps > 0) need(ys, "ys");
+        if (ldy < F.m || (d && ldd < F.r) || (mean && ldm < F.n))
+            throw std::invalid_argument("fkf_run: leading dimension smaller than the vector length");
+        F.run_host(ys, nsteps, ldy, alphas, d, ldd, mean, ldm);
+    });
+}
+int fkb_fkf_run_uq(fkb_filter* f, const double* ys, int nsteps, long long ldy, uint64_t seed, int count, double* x,
+                   double* var, double* alphas, double* d, long long ldd, double* mean, long long ldm) {
+    return guarded([&] {
+        need(f, "filter");
+        auto& F = *f->f;
+        if (nsteps < 0) throw std::invalid_argument("fkf_run: negative step count");
+        if (count < 0 || count > 8) throw std::invalid_argument("fkf_run: realization count must be in [0, 8]");
+        if (nsteps > 0) need(ys, "ys");
+        if (ldy < F.m || (d && ldd < F.r) || (mean && ldm < F.n))
+            throw std::invalid_argument("fkf_run: leading dimension smaller than the vector length");
+        if (F.r == 0) throw std::invalid_argument("fkf_run: the fused UQ batch needs a rank > 0 state");
+        F.run_host(ys, nsteps, ldy, alphas, d, ldd, mean, ldm, count, seed, x, var);
+    });
+}
 int fkb_fkf_step_device(fkb_filter* f, const double* d_y) {
     return guarded([&] {
         need(f, "filter");

@@ -974,8 +974,9 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
     info.alloc(1);
-    hostout.alloc(5);
+    hostout.alloc(10);  // [5q .. 5q+4]: the slots the parity-q step graph reads
     FKB_CUDA(cudaMemset(hostout.p, 0, hostout.bytes()));
+    select_parity(0);
     flags.alloc(size_t(2 * ceil_div(std::max(m, 1), 64) + 2));
     reset();
 }
@@ -986,7 +987,13 @@ Filter::~Filter() {
     if (s) cudaStreamSynchronize(s);
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
+    if (cs) cudaStreamSynchronize(cs);
     drop_graphs();
+    for (int q = 0; q < 2; ++q) {
+        if (ev_done[q]) cudaEventDestroy(ev_done[q]);
+        if (ev_copied[q]) cudaEventDestroy(ev_copied[q]);
+    }
+    if (cs) cudaStreamDestroy(cs);
     if (h_info) cudaFreeHost(h_info);
     if (h_hostout) cudaFreeHost(h_hostout);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -1175,7 +1182,7 @@ void Filter::enqueue_step(const double* d_y) {
     const bool fused_uq = uq_count >= 0 && r > 0;
     if (r > 0 && solver == 0) {
         fork();
-        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p}, side());
+        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hout_c}, side());
         mark_on(side(), "ctz_d_update");
         if (upass_side()) {
             launch_u_pass(XPlain{cvec.p}, side(), true);
@@ -1195,7 +1202,7 @@ void Filter::enqueue_step(const double* d_y) {
         if (par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
         launch_mean_uq(uq_count, n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
                        uq_count ? draws.p : nullptr, uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
-                       hostout.p, s);
+                       hout_c, s);
         if (solver == 1 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
         mark("mean_update");
         return;
@@ -1209,7 +1216,7 @@ void Filter::enqueue_step(const double* d_y) {
         else launch_u_pass(XProd{sqd_c, ucap.p}, s, false);
         mark("u_pass");
     }
-    cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hostout.p});
+    cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hout_c});
     if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
@@ -1269,7 +1276,7 @@ void Filter::enqueue_solve_woodbury() {
         tl.retry_only = pdl;
         if (!pdl) {
             tl.Erow = Erow.p; tl.m = m; tl.wsq = wsq_c; tl.rt = rt.p; tl.sqd = sqd_c; tl.st = st.p; tl.dc = cvec.p;
-            tl.d = d.p; tl.lam = lambda.p; tl.alpha_dev = alpha_dev.p; tl.hout = hostout.p;
+            tl.d = d.p; tl.lam = lambda.p; tl.alpha_dev = alpha_dev.p; tl.hout = hout_c;
         }
         cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs, tl);
         if (pdl) {  // s̃ and the d/α commit by a programmatic dependent (gated on the flag the PCG raises)
@@ -1284,7 +1291,7 @@ void Filter::enqueue_solve_woodbury() {
             cfg.numAttrs = 1;
             FKB_CUDA(cudaLaunchKernelEx(&cfg, k_woodbury_st_pdl, m, r, (const double*)Erow.p, (const double*)sqd_c,
                                         (const double*)ucap.p, (const double*)wsq_c, (const double*)rt.p, st.p,
-                                        EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p}));
+                                        EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hout_c}));
             count_launch();
         }
         mark("cap_solve");
@@ -1317,7 +1324,7 @@ void Filter::enqueue_solve_woodbury() {
         }
         // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
         k_woodbury_st<<<std::max(1, ceil_div(m, 8)) + 1, 256, 0, s>>>(
-            m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hostout.p});
+            m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hout_c});
         FKB_LAUNCH_CHECK();
         count_launch();
         mark("woodbury_st");
@@ -1459,14 +1466,123 @@ static unsigned long long mapped_host(const void* p) {
 
 void Filter::set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi, unsigned long long hx,
                          unsigned long long hv) {
-    const unsigned long long want[5] = {hm, hd, hi, hx, hv};
-    if (std::equal(want, want + 5, hostout_cache)) return;
+    const unsigned long long want[10] = {hm, hd, hi, hx, hv, hm, hd, hi, hx, hv};  // both parities
+    set_hostout_all(want);
+}
+void Filter::set_hostout_all(const unsigned long long (&want)[10]) {
+    if (std::equal(want, want + 10, hostout_cache)) return;
     if (!h_hostout)
-        FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_hostout), 5 * sizeof(unsigned long long),
+        FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_hostout), 10 * sizeof(unsigned long long),
                                cudaHostAllocDefault));
     FKB_CUDA(cudaStreamSynchronize(s));  // the staging slots may still feed an earlier copy
-    for (int i = 0; i < 5; ++i) h_hostout[i] = hostout_cache[i] = want[i];
-    FKB_CUDA(cudaMemcpyAsync(hostout.p, h_hostout, 5 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < 10; ++i) h_hostout[i] = hostout_cache[i] = want[i];
+    FKB_CUDA(cudaMemcpyAsync(hostout.p, h_hostout, 10 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+}
+
+// nsteps steps from host observations with every step's new state (and, count ≥ 0, its diag Σ
+// and `count` realizations) returned in host arrays — the reference driver's loop
+// (driver.hpp:283-300) as one call.  Each step's graph writes its outputs into per-parity
+// device snapshots (the hostout slots of that parity); a copy stream moves them to the host
+// while the next step runs, and step t+2 (same parity) waits only for step t's copies.  The
+// observation of step t is copied host → ybuf on the main stream right before its graph.
+// Failures as finish_async (kInfoRetry steps rerun exactly, "singular" names the step).
+void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_alpha, double* h_d, long long ldd,
+                      double* h_mean, long long ldm, int count, uint64_t seed, double* h_x, double* h_var) {
+    if (nsteps <= 0) return;
+    const bool uq = count >= 0 && r > 0;
+    set_step_uq(uq, seed, uq ? count : 0);
+    if (!cs) {
+        FKB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int q = 0; q < 2; ++q) {
+            FKB_CUDA(cudaEventCreateWithFlags(&ev_done[q], cudaEventDisableTiming));
+            FKB_CUDA(cudaEventCreateWithFlags(&ev_copied[q], cudaEventDisableTiming));
+        }
+    }
+    const int cnt = uq ? count : 0;
+    for (int q = 0; q < 2; ++q) {
+        snap_mean[q].ensure(size_t(n));
+        snap_d[q].ensure(size_t(std::max(r, 1)));
+        if (uq) {
+            snap_x[q].ensure(size_t(n) * std::max(cnt, 1));
+            snap_v[q].ensure(size_t(n));
+        }
+    }
+    auto u = [](const void* p) { return reinterpret_cast<unsigned long long>(p); };
+    unsigned long long want[10];
+    for (int q = 0; q < 2; ++q) {
+        want[5 * q + 0] = u(snap_mean[q].p);
+        want[5 * q + 1] = r > 0 ? u(snap_d[q].p) : 0;
+        want[5 * q + 2] = 0;
+        want[5 * q + 3] = uq && cnt ? u(snap_x[q].p) : 0;
+        want[5 * q + 4] = uq ? u(snap_v[q].p) : 0;
+    }
+    set_hostout_all(want);
+    const double alpha0 = alpha;
+    const int par0 = par_next;
+    auto copy_out = [&](int q, int t, cudaStream_t st) {  // step t's snapshot (parity q) → host rows
+        if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean + t * ldm, snap_mean[q].p, sizeof(double) * size_t(n),
+                                             cudaMemcpyDeviceToHost, st));
+        if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d + t * ldd, snap_d[q].p, sizeof(double) * size_t(r),
+                                                   cudaMemcpyDeviceToHost, st));
+        if (uq && h_var) FKB_CUDA(cudaMemcpyAsync(h_var + (long long)t * n, snap_v[q].p, sizeof(double) * size_t(n),
+                                                  cudaMemcpyDeviceToHost, st));
+        if (uq && cnt && h_x)
+            FKB_CUDA(cudaMemcpyAsync(h_x + (long long)t * n * cnt, snap_x[q].p, sizeof(double) * size_t(n) * cnt,
+                                     cudaMemcpyDeviceToHost, st));
+    };
+    for (int t = 0; t < nsteps; ++t) {
+        const int q = par_next;
+        if (t >= 2) FKB_CUDA(cudaStreamWaitEvent(s, ev_copied[q], 0));  // step t−2's copies are done
+        if (m > 0)
+            FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_ys + t * ldy, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+        launch_step();
+        FKB_CUDA(cudaEventRecord(ev_done[q], s));
+        FKB_CUDA(cudaStreamWaitEvent(cs, ev_done[q], 0));
+        copy_out(q, t, cs);
+        FKB_CUDA(cudaEventRecord(ev_copied[q], cs));
+    }
+    FKB_CUDA(cudaStreamSynchronize(cs));
+    int h = 0;
+    double a = 0.0;
+    FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaMemcpyAsync(&a, alpha_dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    FKB_CUDA(cudaStreamSynchronize(s));
+    int done = int(std::lround(a - alpha0));
+    // a step whose PCG did not verify (and every later step, behind the sticky flag) changed
+    // nothing: rerun it exactly, then the rest one by one, each with its outputs
+    for (int t = done; h == kInfoRetry && t < nsteps; ++t) {
+        const int q = (par0 + t) & 1;
+        if (m > 0)
+            FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_ys + t * ldy, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+        if (t == done) {
+            rerun_exact(q);
+            par_next = q ^ 1;
+        } else {
+            launch_step();
+        }
+        copy_out(q, t, s);
+        FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+        if (h == 0) ++done;
+        else if (h == kInfoRetry) {  // rerun this one exactly too
+            rerun_exact(q);
+            par_next = q ^ 1;
+            copy_out(q, t, s);
+            FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            FKB_CUDA(cudaStreamSynchronize(s));
+            if (h == 0) ++done;
+        }
+        if (h && h != kInfoRetry) break;
+    }
+    set_hostout(0, 0, 0);
+    alpha = alpha0 + done;
+    step_no += done;
+    if (done > 0) state_rank = r;
+    if (h_alpha)
+        for (int t = 0; t < done; ++t) h_alpha[t] = alpha0 + t + 1;
+    if (h)
+        fail_step("fkf_step: innovation system is singular (step " + std::to_string(done + 1) + " of " +
+                  std::to_string(nsteps) + " in the batch)");
 }
 
 // step + fused UQ from host y: page-locked x/var buffers are written by the fused U pass

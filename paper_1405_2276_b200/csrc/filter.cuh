@@ -89,6 +89,7 @@ struct Filter {
     double *wsq_n = nullptr, *sqd_n = nullptr, *K_n = nullptr;  // next step's
     int par_next = 0;  // parity of the next step to run
     void select_parity(int p) {
+        hout_c = hostout.p + 5 * p;
         wsq_c = wsqb[p].p; sqd_c = sqdb[p].p; K_c = Kb[p].p;
         wsq_n = wsqb[p ^ 1].p; sqd_n = sqdb[p ^ 1].p; K_n = Kb[p ^ 1].p;
     }
@@ -174,7 +175,16 @@ struct Filter {
     // mapped host outputs of the step graph: [0] mean, [1] d, [2] failure flag (0 = none)
     DBuf<unsigned long long> hostout;
     // [3] realizations, [4] diag Σ of the fused step + UQ
-    unsigned long long hostout_cache[5] = {0, 0, 0, 0, 0};
+    unsigned long long hostout_cache[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long* hout_c = nullptr;  // the slots of the parity being enqueued
+    void set_hostout_all(const unsigned long long (&want)[10]);
+    // pipelined host batch (run_host): per-parity device snapshots of the outputs, a copy stream
+    DBuf<double> snap_mean[2], snap_d[2], snap_x[2], snap_v[2];
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+    void run_host(const double* h_ys, int nsteps, long long ldy, double* h_alpha, double* h_d, long long ldd,
+                  double* h_mean, long long ldm, int count = -1, uint64_t seed = 0, double* h_x = nullptr,
+                  double* h_var = nullptr);
     unsigned long long* h_hostout = nullptr;
     void set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi, unsigned long long hx = 0,
                      unsigned long long hv = 0);

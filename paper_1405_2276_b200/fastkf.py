@@ -311,6 +311,22 @@ class FkfContext:
         y = np.ascontiguousarray(y, dtype=np.float64)
         check(lib().fkb_fkf_step(self._f, ptr(y), len(y)))
 
+    def run(self, ys, count=None, seed=0):
+        """len(ys) steps in one call with every step's new state (fkb_fkf_run; with count: the fused
+        diag Σ and `count` realizations too, fkb_fkf_run_uq).  Returns dict(alpha (n,), d (n, r),
+        mean (n, N)[, var (n, N), x (n, count, N)])."""
+        Y = np.ascontiguousarray(np.atleast_2d(np.asarray(ys, dtype=np.float64)))
+        ns = Y.shape[0]
+        r = max(self.r, 1)
+        al, d, mean = np.zeros(max(ns, 1)), np.zeros((max(ns, 1), r)), np.zeros((max(ns, 1), self.n))
+        if count is None:
+            check(lib().fkb_fkf_run(self._f, ptr(Y), ns, Y.shape[1], ptr(al), ptr(d), r, ptr(mean), self.n))
+            return dict(alpha=al[:ns], d=d[:ns, : self.r], mean=mean[:ns])
+        x, var = np.zeros((max(ns, 1), max(count, 1), self.n)), np.zeros((max(ns, 1), self.n))
+        check(lib().fkb_fkf_run_uq(self._f, ptr(Y), ns, Y.shape[1], int(seed), int(count), ptr(x), ptr(var), ptr(al),
+                                   ptr(d), r, ptr(mean), self.n))
+        return dict(alpha=al[:ns], d=d[:ns, : self.r], mean=mean[:ns], var=var[:ns], x=x[:ns, :count])
+
     def step_device(self, d_y):
         check(lib().fkb_fkf_step_device(self._f, d_y))
 

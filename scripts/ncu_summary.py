@@ -17,6 +17,19 @@ hdr = rows[0]
 ix = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Section Name", "Metric Name", "Metric Value", "Metric Unit")}
 rr = list(csv.reader(io.StringIO(raw)))
 rh = rr[0]
+# pipe utilisation and traffic counters quoted in DESIGN.md / the bench line
+EXTRA = ("TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+         "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+         "SM_C.TriageCompute.smsp__pipe_tensor_subpipe_dmma_cycles_active.avg",
+         "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors.sum", "lts__t_bytes.sum",
+         "sm__cycles_elapsed.avg")
+extra = {}
+for r in rr[2:]:
+    d = dict(zip(rh, r))
+    if "ID" in d:
+        extra[d["ID"]] = [(k, d[k], rr[1][rh.index(k)]) for k in EXTRA if k in d and d[k] != ""]
 dram = {}
 for r in rr[2:]:
     d = dict(zip(rh, r))
@@ -36,4 +49,6 @@ for r in rows[1:]:
         if cur in dram:
             rd, wr, unit = dram[cur]
             print(f"  [raw] dram__bytes_read.sum + dram__bytes_write.sum: {rd:.4g} + {wr:.4g} {unit}")
+        for k, v, u in extra.get(cur, []):
+            print(f"  [raw] {k}: {v} {u}")
     print(f"  [{r[ix['Section Name']]}] {r[ix['Metric Name']]}: {r[ix['Metric Value']]} {r[ix['Metric Unit']]}")

@@ -5,7 +5,8 @@
 Each mode runs its warm-up outside, then the region of interest between
 cudaProfilerStart/Stop, so `ncu --profile-from-start off …` captures exactly that region:
 
-  step   one fkf_step (plus the realizations when the config draws them) after 3 warm steps
+  step   one fkf_step after 3 warm steps (the fused step + diag Σ + realizations when the
+         config draws them, as bench.py runs it)
   init   fkf_init (spectrum, GHEP, G = HΓHᵀ and its eigendecomposition)
   wprod  the GHEP's W-block products at the config's sizes: the Γ-metric Gram Ȳᵀ(ΓȲ)
          (k_gram), U = Q·S (k_gemm) and the symmetric capacitance Gram (k_gram_sym)
@@ -54,12 +55,18 @@ if mode in ("step", "init", "spmm"):
         ctx.steps_async(dys.ptr, 3, w.m)
         ctx.sync(3)
 
-        def one():
-            ctx.steps_async(dys.ptr, 1, w.m)
-            if w.variance_each_step or w.realizations_per_step:
-                X = DeviceArray(w.N * 8)
-                V = DeviceArray(w.N)
-                ctx.realizations_device(w.sample_seed, w.realizations_per_step, X.ptr, V.ptr)
+        uq = bool(w.variance_each_step or w.realizations_per_step)
+        X, V = DeviceArray(w.N * 8), DeviceArray(w.N)
+        cnt = int(w.realizations_per_step or 0)
+
+        def one():  # the step as bench.py runs it: fused step + UQ when the config draws UQ
+            if uq:
+                ctx.step_uq_device(dys.ptr, w.sample_seed, cnt, X.ptr, V.ptr)
+            else:
+                ctx.steps_async(dys.ptr, 1, w.m)
+        if uq:
+            for _ in range(3):
+                one()
         region(one)
         ctx.sync(1)
     else:

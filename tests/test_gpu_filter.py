@@ -483,3 +483,61 @@ def test_unverified_pcg_rerun_writes_mapped_outputs():
         assert alpha.value == sa["alpha"]
         assert rel_err(hm.numpy(), sa["mean"]) < 1e-12
         assert np.max(np.abs(hd.numpy()[: b.rank()] - sa["d"])) / sa["alpha"] < 1e-12
+
+
+@pytest.mark.parametrize("name", ["c0", "c2"])
+def test_run_batch_matches_step_loop(name):
+    """fkb_fkf_run (the driver's step loop in one call, each step's state copied out while the
+    next step runs) returns exactly the states of fkf_step called step by step."""
+    w, h, ys, s2 = workload_inputs(name, 5)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), kern)
+    a = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    b = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    ref = [P.fkf_step(a, y) for y in ys]
+    out = b.run(np.stack(ys))
+    for t, st in enumerate(ref):
+        assert out["alpha"][t] == st["alpha"]
+        assert np.array_equal(out["d"][t], st["d"]) and np.array_equal(out["mean"][t], st["mean"])
+    sb = b.state()
+    assert sb["step"] == len(ys) and sb["alpha"] == ref[-1]["alpha"]
+    assert np.array_equal(sb["mean"], ref[-1]["mean"])
+    # a second batch continues from the committed state
+    out2 = b.run(np.stack(ys[:2]))
+    st2 = P.fkf_step(a, ys[0])
+    assert np.array_equal(out2["mean"][0], st2["mean"])
+
+
+def test_run_uq_batch_matches_step_uq():
+    """fkb_fkf_run_uq ≡ fkb_fkf_step_uq per step: new state, diag Σ and realizations (c0)."""
+    w, h, ys, s2 = workload_inputs("c0", 4)
+    kern = P.KernelSpec(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), kern)
+    a = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    b = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    out = b.run(np.stack(ys), count=3, seed=77)
+    for t, y in enumerate(ys):
+        st, x, var = a.step_uq(y, 77, 3)
+        assert np.array_equal(out["mean"][t], st["mean"]) and np.array_equal(out["d"][t], st["d"])
+        assert np.array_equal(out["var"][t], var)
+        assert np.array_equal(out["x"][t], x.T)
+
+
+def test_run_batch_reruns_unverified_and_raises_singular():
+    """Forced PCG give-up inside a host batch: every step is rerun exactly and the outputs match
+    the step loop; a singular step raises naming it and commits the steps before it."""
+    w, ys, a = _c0_ctx()
+    _, _, b = _c0_ctx()
+    b.set_pcg_maxit(0)
+    ref = [P.fkf_step(a, y) for y in ys]
+    out = b.run(np.stack(ys))
+    for t, st in enumerate(ref):
+        assert out["alpha"][t] == st["alpha"]
+        assert rel_err(out["mean"][t], st["mean"]) < 1e-12
+    st = b.state()
+    b.set_state(st["alpha"], np.full(b.rank(), 50.0 * st["alpha"]), st["mean"], st["step"])
+    with pytest.raises(RuntimeError, match=r"singular \(step 1 of"):
+        b.run(np.stack(ys[:2]))
+    assert b.state()["alpha"] == st["alpha"]
