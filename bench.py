@@ -423,7 +423,7 @@ def run_ours(args, rank, world, local_rank):
         else:
             check(L.fkb_fkf_run(ctx._f, p(run_y), nst, w.m, p(run_a), p(run_d), max(r, 1), p(run_mean), w.N))
 
-    run_batch(args.warmup)
+    run_batch(max(args.warmup, K))  # warm-up: the same batch shape (workspaces sized, graphs captured)
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         flush.zero_()

@@ -28,7 +28,7 @@ def _compile(src: str, verbose: bool) -> str:
     if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
         return out
     cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", out]
-    if src == "host_linalg.cpp":  # the host eigensolver's column sweeps run on OpenMP threads
+    if src in ("host_linalg.cpp", "filter.cu"):  # host eigensolver sweeps, Gram inverse square roots: OpenMP
         cmd += ["-Xcompiler", "-fopenmp"]
     if src.endswith(".cu") and verbose:
         cmd += ["-Xptxas", "-v"]

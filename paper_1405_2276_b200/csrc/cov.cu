@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
     const double* __restrict__ acc_coef = UPD ? upd.coef : nullptr;
     const int* __restrict__ gate = upd.gate;
     const double* __restrict__ sub = upd.sub;
+    if (UPD && upd.ycnt && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *upd.ycnt += 1;  // next batch row
     double* hm = nullptr;
     if (acc_coef && upd.hout) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && upd.hout[2])

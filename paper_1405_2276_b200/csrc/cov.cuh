@@ -23,6 +23,7 @@ struct MeanUpd {
     const int* gate = nullptr;
     const double* sub = nullptr;
     const unsigned long long* hout = nullptr;
+    long long* ycnt = nullptr;  // incremented once per step (the host batch's observation row)
 };
 
 struct Cov {

@@ -97,11 +97,12 @@ __global__ void k_transpose(long long n, int r, const double* __restrict__ in, d
 // asynchronous batch is a no-op (its epilogues are gated on it) until the host clears it.
 __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* __restrict__ rp,
                                                       const int* __restrict__ ci, const double* __restrict__ hv,
-                                                      const double* __restrict__ mean, const double* __restrict__ y,
+                                                      const double* __restrict__ mean, const double* y,
                                                       double* __restrict__ z, double* alpha_dev,
                                                       const double* __restrict__ theta, const double* __restrict__ d,
                                                       double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
-                                                      double* __restrict__ dsnap, int* __restrict__ pcgflag) {
+                                                      double* __restrict__ dsnap, int* __restrict__ pcgflag,
+                                                      const long long* __restrict__ ysrc) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // rotate_in may stage P now
     const int gid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const double alpha = alpha_dev[0] + 1.0;
@@ -117,6 +118,10 @@ __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* 
     }
     const int row = gid >> 5, lane = threadIdx.x & 31;
     if (row >= m) return;
+    // the observation: y, or (ysrc set) row ysrc[2] of the block at ysrc[0] with ld ysrc[1] —
+    // the host batch (Filter::run_host) uploads all its observations once and the step's last
+    // kernel advances ysrc[2]
+    if (ysrc) y = reinterpret_cast<const double*>(ysrc[0]) + ysrc[2] * ysrc[1];
     const int e0 = rp[row], e1 = rp[row + 1];
     double s = 0.0;
     for (int eb = e0; eb < e1; eb += 32 * 16) {
@@ -351,13 +356,17 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq1(long long n, int r, const d
                                                    const double* __restrict__ Z, const double* __restrict__ proj,
                                                    double* __restrict__ X, double* __restrict__ var,
                                                    const int* __restrict__ info,
-                                                   const unsigned long long* __restrict__ hout) {
+                                                   const unsigned long long* __restrict__ hout,
+                                                   long long* __restrict__ ycnt) {
     extern __shared__ double sh[];
     double* cs = sh;           // dc (r)
     double* ds = sh + r;       // d  (r)
     double* P = sh + 2 * r;    // Σ₋ ⊙ Ūᵀz_s (r × count)
     const int bad = *info;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+        if (ycnt) *ycnt += 1;  // the host batch's next observation row (see k_step_residual)
+    }
     if (bad) return;
     const double alpha = alpha_dev[1];
     for (int j = threadIdx.x; j < r; j += blockDim.x) {
@@ -429,12 +438,16 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const do
                                                    const double* __restrict__ Z, const double* __restrict__ proj,
                                                    double* __restrict__ X, double* __restrict__ var,
                                                    const int* __restrict__ info,
-                                                   const unsigned long long* __restrict__ hout) {
+                                                   const unsigned long long* __restrict__ hout,
+                                                   long long* __restrict__ ycnt) {
     constexpr int SW = (2 + CNT + 1) & ~1;  // record: dc, d, Σ₋⊙Ūᵀz_s (s < CNT), pad
     extern __shared__ double2 rec2[];
     double* rec = reinterpret_cast<double*>(rec2);
     const int bad = *info;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+        if (ycnt) *ycnt += 1;  // the host batch's next observation row (see k_step_residual)
+    }
     if (bad) return;
     const double alpha = alpha_dev[1];
     const int rp = (r + 15) / 16 * 16;
@@ -516,7 +529,7 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const do
 void launch_mean_uq(int count, long long n, int r, const double* U, const double* dc, const double* d,
                     const double* alpha_dev, double theta, const double* t, double* mean, const double* Z,
                     const double* proj, double* X, double* var, const int* info, const unsigned long long* hout,
-                    cudaStream_t s) {
+                    long long* ycnt, cudaStream_t s) {
     // FKB_UQ_SHAPE: 0 (default) k_mean_uq1 — one row per thread, separate constant arrays;
     // 116 / 208 — shared-memory records, 1 row × 16 or 2 rows × 8 columns per batch (c3, in
     // graph: 64 / 80 / 68 µs)
@@ -535,14 +548,14 @@ void launch_mean_uq(int count, long long n, int r, const double* U, const double
                 attr = true;
             }
             kern<<<ceil_div(n, 128 * R), 128, shm, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, Z, proj, X, var,
-                                                       info, hout);
+                                                       info, hout, ycnt);
         };
         if (shape == 208) launch(k_mean_uq<CNT, 2, 8>, 2);
         else if (shape == 116) launch(k_mean_uq<CNT, 1, 16>, 1);
         else {
             const size_t shm1 = sizeof(double) * size_t(r) * (2 + std::max(count, 1));
             k_mean_uq1<<<ceil_div(n, 128), 128, shm1, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, count, Z, proj,
-                                                           X, var, info, hout);
+                                                           X, var, info, hout, ycnt);
         }
     };
     switch (count) {
@@ -637,32 +650,44 @@ void tall_times_small(long long n, int p, int q, const double* A, const double* 
 // drop), ordered by ascending eigenvalue.  Both span the same columns when nothing is dropped.
 std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double tol, int& kept) {
     if (p > 0) {
-        std::vector<double> L(Gh);
-        auto at = [&](int i, int j) -> double& { return L[size_t(i) + size_t(j) * p]; };
+        // L held row-major (Lr[i·p + k] = L_ik) so every dot product below runs over contiguous
+        // memory; the rows of a column and the columns of the inverse are independent and run
+        // on the host threads (the arithmetic order per entry is fixed: bit-identical results)
+        std::vector<double> Lr(static_cast<size_t>(p) * p, 0.0);
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j <= i; ++j) Lr[size_t(i) * p + j] = Gh[size_t(i) + size_t(j) * p];
         double dmax = 0.0;
         for (int j = 0; j < p; ++j) dmax = std::max(dmax, Gh[size_t(j) + size_t(j) * p]);
         bool ok = dmax > 0.0;
         for (int j = 0; j < p && ok; ++j) {  // left-looking Cholesky on the lower triangle
-            double dj = at(j, j);
-            for (int k = 0; k < j; ++k) dj -= at(j, k) * at(j, k);
+            const double* lj = Lr.data() + size_t(j) * p;
+            double dj = lj[j];
+            for (int k = 0; k < j; ++k) dj -= lj[k] * lj[k];
             if (!(dj >= 1e-10 * dmax)) { ok = false; break; }
             const double ljj = std::sqrt(dj);
-            at(j, j) = ljj;
+            Lr[size_t(j) * p + j] = ljj;
+#pragma omp parallel for schedule(static) if (p - j > 64)
             for (int i = j + 1; i < p; ++i) {
-                double v = 0.5 * (at(i, j) + Gh[size_t(j) + size_t(i) * p]);  // symmetrized entry
-                for (int k = 0; k < j; ++k) v -= at(i, k) * at(j, k);
-                at(i, j) = v / ljj;
+                double* li = Lr.data() + size_t(i) * p;
+                double v = 0.5 * (li[j] + Gh[size_t(j) + size_t(i) * p]);  // symmetrized entry
+                for (int k = 0; k < j; ++k) v -= li[k] * lj[k];
+                li[j] = v / ljj;
             }
         }
         if (ok) {
-            // W = L⁻ᵀ (upper triangular): solve Lᵀ W = I column by column
+            // W = L⁻ᵀ (upper triangular): solve Lᵀ W = I column by column; Lc = L column-major
+            std::vector<double> Lc(static_cast<size_t>(p) * p);
+            for (int i = 0; i < p; ++i)
+                for (int k = 0; k <= i; ++k) Lc[size_t(i) + size_t(k) * p] = Lr[size_t(i) * p + k];
             std::vector<double> W(static_cast<size_t>(p) * p, 0.0);
+#pragma omp parallel for schedule(dynamic, 8)
             for (int c = 0; c < p; ++c) {
                 double* w = W.data() + size_t(c) * p;
                 for (int i = c; i >= 0; --i) {
+                    const double* li = Lc.data() + size_t(i) * p;  // column i of L
                     double v = i == c ? 1.0 : 0.0;
-                    for (int k = i + 1; k <= c; ++k) v -= at(k, i) * w[k];
-                    w[i] = v / at(i, i);
+                    for (int k = i + 1; k <= c; ++k) v -= li[k] * w[k];
+                    w[i] = v / li[i];
                 }
             }
             kept = p;
@@ -973,6 +998,8 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     if (const char* e = std::getenv("FKB_UPASS_SIDE")) upass_side_mode = std::atoi(e);
     cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
+    ysrc.alloc(3);
+    set_ysrc(ybuf.p, 0);
     info.alloc(1);
     hostout.alloc(10);  // [5q .. 5q+4]: the slots the parity-q step graph reads
     FKB_CUDA(cudaMemset(hostout.p, 0, hostout.bytes()));
@@ -996,6 +1023,7 @@ Filter::~Filter() {
     if (cs) cudaStreamDestroy(cs);
     if (h_info) cudaFreeHost(h_info);
     if (h_hostout) cudaFreeHost(h_hostout);
+    if (h_ysrc) cudaFreeHost(h_ysrc);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join2) cudaEventDestroy(ev_join2);
@@ -1167,7 +1195,7 @@ void Filter::enqueue_step(const double* d_y) {
         k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
                                                theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq_c : nullptr,
                                                sqd_c, (solver == 1 && r > 0) ? dsnap.p : nullptr,
-                                               (solver == 1 && !exact) ? pcgflag.p : nullptr);
+                                               (solver == 1 && !exact) ? pcgflag.p : nullptr, ysrc.p);
         FKB_LAUNCH_CHECK();
         count_launch();
     }
@@ -1202,7 +1230,7 @@ void Filter::enqueue_step(const double* d_y) {
         if (par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
         launch_mean_uq(uq_count, n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
                        uq_count ? draws.p : nullptr, uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
-                       hout_c, s);
+                       hout_c, ysrc.p + 2, s);
         if (solver == 1 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
         mark("mean_update");
         return;
@@ -1216,7 +1244,7 @@ void Filter::enqueue_step(const double* d_y) {
         else launch_u_pass(XProd{sqd_c, ucap.p}, s, false);
         mark("u_pass");
     }
-    cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hout_c});
+    cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hout_c, ysrc.p + 2});
     if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
     mark("mean_update");
 }
@@ -1464,6 +1492,22 @@ static unsigned long long mapped_host(const void* p) {
     return a.type == cudaMemoryTypeHost && a.devicePointer ? reinterpret_cast<unsigned long long>(a.devicePointer) : 0;
 }
 
+// Stream-ordered: the values come from a page-locked staging slot per (base, ld) pair that is
+// only rewritten after a stream synchronization.
+void Filter::set_ysrc(const double* base, long long ld) {
+    if (!h_ysrc) FKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_ysrc), 6 * sizeof(long long), cudaHostAllocDefault));
+    const long long b = static_cast<long long>(reinterpret_cast<uintptr_t>(base));
+    const int slot = ld == 0 ? 0 : 1;  // 0: the per-call buffer, 1: the host batch's block
+    long long* v = h_ysrc + 3 * slot;
+    if (v[0] != b || v[1] != ld) {
+        FKB_CUDA(cudaStreamSynchronize(s));  // an earlier copy may still read the slot
+        v[0] = b;
+        v[1] = ld;
+        v[2] = 0;
+    }
+    FKB_CUDA(cudaMemcpyAsync(ysrc.p, v, 3 * sizeof(long long), cudaMemcpyHostToDevice, s));
+}
+
 void Filter::set_hostout(unsigned long long hm, unsigned long long hd, unsigned long long hi, unsigned long long hx,
                          unsigned long long hv) {
     const unsigned long long want[10] = {hm, hd, hi, hx, hv, hm, hd, hi, hx, hv};  // both parities
@@ -1517,6 +1561,13 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
         want[5 * q + 4] = uq ? u(snap_v[q].p) : 0;
     }
     set_hostout_all(want);
+    // every step's observation uploaded once; the graphs read row ysrc[2] of the block
+    if (ys_dev.n < size_t(std::max(m, 1)) * nsteps)  // grown geometrically: repeated batches do not reallocate
+        ys_dev.ensure(std::max(size_t(std::max(m, 1)) * nsteps, 2 * ys_dev.n));
+    set_ysrc(ys_dev.p, m);
+    if (m > 0)
+        FKB_CUDA(cudaMemcpy2DAsync(ys_dev.p, sizeof(double) * size_t(m), h_ys, sizeof(double) * size_t(ldy),
+                                   sizeof(double) * size_t(m), size_t(nsteps), cudaMemcpyHostToDevice, s));
     const double alpha0 = alpha;
     const int par0 = par_next;
     auto copy_out = [&](int q, int t, cudaStream_t st) {  // step t's snapshot (parity q) → host rows
@@ -1530,18 +1581,45 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
             FKB_CUDA(cudaMemcpyAsync(h_x + (long long)t * n * cnt, snap_x[q].p, sizeof(double) * size_t(n) * cnt,
                                      cudaMemcpyDeviceToHost, st));
     };
+    // FKB_RUN_TRACE=1: per-step timing events (main stream before the input copy, after the
+    // graph; copy stream after the outputs), printed after the batch (diagnostics)
+    static const bool trace = std::getenv("FKB_RUN_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        FKB_CUDA(cudaEventCreate(&e));
+        FKB_CUDA(cudaEventRecord(e, st));
+        tev.push_back(e);
+    };
     for (int t = 0; t < nsteps; ++t) {
         const int q = par_next;
         if (t >= 2) FKB_CUDA(cudaStreamWaitEvent(s, ev_copied[q], 0));  // step t−2's copies are done
-        if (m > 0)
-            FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_ys + t * ldy, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+        tmark(s);
+        tmark(s);
         launch_step();
+        tmark(s);
         FKB_CUDA(cudaEventRecord(ev_done[q], s));
         FKB_CUDA(cudaStreamWaitEvent(cs, ev_done[q], 0));
         copy_out(q, t, cs);
+        tmark(cs);
         FKB_CUDA(cudaEventRecord(ev_copied[q], cs));
     }
     FKB_CUDA(cudaStreamSynchronize(cs));
+    set_ysrc(ybuf.p, 0);  // back to the per-call observation buffer (also for the reruns below)
+    if (trace) {
+        FKB_CUDA(cudaStreamSynchronize(s));
+        for (int t = 0; t + 1 < nsteps && t < 8; ++t) {
+            float a = 0, b = 0, c = 0, d2 = 0;
+            cudaEventElapsedTime(&a, tev[4 * t], tev[4 * t + 1]);
+            cudaEventElapsedTime(&b, tev[4 * t + 1], tev[4 * t + 2]);
+            cudaEventElapsedTime(&c, tev[4 * t + 2], tev[4 * t + 3]);
+            cudaEventElapsedTime(&d2, tev[4 * t], tev[4 * t + 4]);
+            std::fprintf(stderr, "[run] step %d: wait %.1f us, graph %.1f us, outputs done +%.1f us, step-to-step %.1f us\n",
+                         t, 1e3 * a, 1e3 * b, 1e3 * c, 1e3 * d2);
+        }
+        for (auto e : tev) cudaEventDestroy(e);
+    }
     int h = 0;
     double a = 0.0;
     FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1549,30 +1627,34 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
     FKB_CUDA(cudaStreamSynchronize(s));
     int done = int(std::lround(a - alpha0));
     // a step whose PCG did not verify (and every later step, behind the sticky flag) changed
-    // nothing: rerun it exactly, then the rest one by one, each with its outputs
-    for (int t = done; h == kInfoRetry && t < nsteps; ++t) {
-        const int q = (par0 + t) & 1;
-        if (m > 0)
-            FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_ys + t * ldy, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
-        if (t == done) {
-            rerun_exact(q);
-            par_next = q ^ 1;
-        } else {
-            launch_step();
-        }
-        copy_out(q, t, s);
-        FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        FKB_CUDA(cudaStreamSynchronize(s));
-        if (h == 0) ++done;
-        else if (h == kInfoRetry) {  // rerun this one exactly too
-            rerun_exact(q);
-            par_next = q ^ 1;
-            copy_out(q, t, s);
+    // nothing: rerun it exactly, then the rest one by one (each rerun exactly if it too does
+    // not verify), each with its outputs
+    if (h == kInfoRetry) {
+        h = 0;
+        for (int t = done; t < nsteps; ++t) {
+            const int q = (par0 + t) & 1;
+            if (m > 0)
+                FKB_CUDA(cudaMemcpyAsync(ybuf.p, h_ys + t * ldy, sizeof(double) * size_t(m), cudaMemcpyHostToDevice, s));
+            par_next = q;
+            if (t == done) {
+                rerun_exact(q);
+                par_next = q ^ 1;
+            } else {
+                launch_step();
+            }
             FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             FKB_CUDA(cudaStreamSynchronize(s));
-            if (h == 0) ++done;
+            if (h == kInfoRetry) {
+                rerun_exact(q);
+                par_next = q ^ 1;
+                FKB_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+                FKB_CUDA(cudaStreamSynchronize(s));
+            }
+            if (h) break;  // singular: raised below, the state stays at step t−1
+            copy_out(q, t, s);
+            FKB_CUDA(cudaStreamSynchronize(s));
+            ++done;
         }
-        if (h && h != kInfoRetry) break;
     }
     set_hostout(0, 0, 0);
     alpha = alpha0 + done;

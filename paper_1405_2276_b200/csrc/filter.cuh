@@ -162,6 +162,12 @@ struct Filter {
     DBuf<double> sig_minus;
 
     DBuf<double> ybuf;
+    // the step's observation source (k_step_residual): {base, ld, row}; per-call mode {ybuf, 0, ·},
+    // host batch {uploaded block, m, row advanced by the step's last kernel}
+    DBuf<long long> ysrc;
+    DBuf<double> ys_dev;
+    void set_ysrc(const double* base, long long ld);
+    long long* h_ysrc = nullptr;  // page-locked staging of the two ysrc configurations
     DBuf<double> host_out;  // staging for the host-buffer UQ calls
 
     Filter(Cov* cov, int m, int h_cols, const int* rowptr, const int* col, const double* val, double sigma2,

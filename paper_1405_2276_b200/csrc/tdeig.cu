@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <numeric>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -223,6 +224,69 @@ __global__ void __launch_bounds__(128) k_apply_rotations(int n, double* __restri
     }
 }
 
+// The same rotations with each thread's row of Q resident in shared memory (stride n + 1:
+// conflict-free column access across the rows of a warp) and the rotation stream staged
+// through shared memory a chunk of whole sweeps at a time (≤ RCH rotations; a sweep has at
+// most n − 1 ≤ 2047): the chunk's (c, s) are one coalesced load, and within a sweep a row's
+// next 8 elements are loaded before the 8 rotations that consume them (the carried DFMA chain
+// is then the only serial dependency) — one shared load and store per rotation.
+constexpr int RCH = 2048;
+__global__ void __launch_bounds__(64) k_apply_rotations_smem(int n, int rows, double* __restrict__ Q,
+                                                            const int* __restrict__ first, const int* __restrict__ cnt,
+                                                            const int* __restrict__ off, const double2* __restrict__ rot,
+                                                            int nchunk, const int* __restrict__ chunk_sw) {
+    extern __shared__ double qs[];  // qs[lr·(n+1) + c], then the staged chunk
+    const int k0 = blockIdx.x * rows, nr = min(rows, n - k0);
+    const int ld = n + 1;
+    double2* rc = reinterpret_cast<double2*>(qs + ((size_t(rows) * ld + 1) & ~size_t(1)));
+    for (long long e = threadIdx.x; e < (long long)nr * n; e += blockDim.x) {
+        const int lr = int(e % nr), c = int(e / nr);
+        qs[lr * ld + c] = Q[k0 + lr + (long long)c * n];
+    }
+    const int lr = threadIdx.x;
+    double* q = qs + lr * ld;
+    for (int ch = 0; ch < nchunk; ++ch) {
+        const int s0 = __ldg(chunk_sw + ch), s1 = __ldg(chunk_sw + ch + 1);
+        const int r0 = __ldg(off + s0), r1 = __ldg(off + s1 - 1) + __ldg(cnt + s1 - 1);
+        __syncthreads();  // the previous chunk is consumed (and, first time, Q is staged)
+        for (int e = threadIdx.x; e < r1 - r0; e += blockDim.x) rc[e] = __ldg(rot + r0 + e);
+        __syncthreads();
+        if (lr >= nr) continue;
+        for (int sw = s0; sw < s1; ++sw) {
+            const int i0 = __ldg(first + sw), c = __ldg(cnt + sw);
+            const double2* rs = rc + (__ldg(off + sw) - r0);
+            double carry = q[i0 + 1];
+            int t = 0;
+            for (; t + 8 <= c; t += 8) {
+                double qi[8];
+                double2 cs[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    qi[u] = q[i0 - t - u];
+                    cs[u] = rs[t + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    q[i0 - t - u + 1] = cs[u].y * qi[u] + cs[u].x * carry;
+                    carry = cs[u].x * qi[u] - cs[u].y * carry;
+                }
+            }
+            for (; t < c; ++t) {
+                const double2 cs = rs[t];
+                const double qi = q[i0 - t];
+                q[i0 - t + 1] = cs.y * qi + cs.x * carry;
+                carry = cs.x * qi - cs.y * carry;
+            }
+            q[i0 - c + 1] = carry;
+        }
+    }
+    __syncthreads();
+    for (long long e = threadIdx.x; e < (long long)nr * n; e += blockDim.x) {
+        const int r2 = int(e % nr), c = int(e / nr);
+        Q[k0 + r2 + (long long)c * n] = qs[r2 * ld + c];
+    }
+}
+
 __global__ void k_gather_cols(int n, const double* __restrict__ Q, const int* __restrict__ perm, double* __restrict__ Z) {
     const long long total = (long long)n * n;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
@@ -232,6 +296,18 @@ __global__ void k_gather_cols(int n, const double* __restrict__ Q, const int* __
 }
 
 void sym_eig_tridiag_device(int n, double* A, double* w_host, double* Z, cudaStream_t s) {
+    // FKB_CORE_EIG=jacobi: the device block-Jacobi solver (eig.cu) for the same contract
+    static const bool jac = [] {
+        const char* e = std::getenv("FKB_CORE_EIG");
+        return e && std::string(e) == "jacobi";
+    }();
+    if (jac && n > 0) {
+        DBuf<double> th{size_t(n)};
+        sym_eig_sorted_device(n, A, n, th.p, Z, s);
+        FKB_CUDA(cudaMemcpyAsync(w_host, th.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+        FKB_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     if (n <= 0) return;
     static const bool trace = std::getenv("FKB_TDEIG_TRACE") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
@@ -334,7 +410,38 @@ void sym_eig_tridiag_device(int n, double* A, double* w_host, double* Z, cudaStr
         FKB_CUDA(cudaMemcpyAsync(dc.p, cnt.data(), sizeof(int) * size_t(nsweep), cudaMemcpyHostToDevice, s));
         FKB_CUDA(cudaMemcpyAsync(doff.p, off.data(), sizeof(int) * size_t(nsweep), cudaMemcpyHostToDevice, s));
         FKB_CUDA(cudaMemcpyAsync(drot.p, rot.data(), sizeof(double2) * rot.size(), cudaMemcpyHostToDevice, s));
-        k_apply_rotations<<<ceil_div(n, 128), 128, 0, s>>>(n, Q.p, nsweep, df.p, dc.p, doff.p, drot.p);
+        // rows of Q resident in shared memory next to a staged chunk of whole sweeps (≤ 200 KB
+        // per CTA) unless n is too large for it
+        const size_t chunk_bytes = size_t(RCH) * sizeof(double2) + 16;
+        const int rows = int(std::min<long long>(64, (200LL * 1024 - (long long)chunk_bytes) / (8LL * (n + 1))));
+        static const bool smem_rot = std::getenv("FKB_TDEIG_L2ROT") == nullptr;
+        if (smem_rot && rows >= 4) {
+            std::vector<int> csw{0};  // chunk boundaries (sweep indices), ≤ RCH rotations each
+            int acc = 0;
+            for (int sw = 0; sw < nsweep; ++sw) {
+                if (acc + cnt[size_t(sw)] > RCH) {
+                    csw.push_back(sw);
+                    acc = 0;
+                }
+                acc += cnt[size_t(sw)];
+            }
+            csw.push_back(nsweep);
+            DBuf<int> dcsw(csw.size());
+            FKB_CUDA(cudaMemcpyAsync(dcsw.p, csw.data(), sizeof(int) * csw.size(), cudaMemcpyHostToDevice, s));
+            const size_t shm = sizeof(double) * ((size_t(rows) * (n + 1) + 1) & ~size_t(1)) + chunk_bytes;
+            static bool attr = false;
+            if (!attr) {
+                FKB_CUDA(cudaFuncSetAttribute(k_apply_rotations_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              210 * 1024));
+                attr = true;
+            }
+            k_apply_rotations_smem<<<ceil_div(n, rows), 64, shm, s>>>(n, rows, Q.p, df.p, dc.p, doff.p, drot.p,
+                                                                      int(csw.size()) - 1, dcsw.p);
+            FKB_LAUNCH_CHECK();
+            FKB_CUDA(cudaStreamSynchronize(s));  // dcsw goes out of scope
+        } else {
+            k_apply_rotations<<<ceil_div(n, 128), 128, 0, s>>>(n, Q.p, nsweep, df.p, dc.p, doff.p, drot.p);
+        }
         FKB_LAUNCH_CHECK();
         count_launch();
         FKB_CUDA(cudaStreamSynchronize(s));  // the rotation buffers go out of scope
