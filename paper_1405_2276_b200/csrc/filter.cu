@@ -541,12 +541,8 @@ void launch_mean_uq(int count, long long n, int r, const double* U, const double
         constexpr int CNT = decltype(c)::value;
         constexpr int SW = (2 + CNT + 1) & ~1;
         const size_t shm = sizeof(double) * size_t((r + 15) / 16 * 16) * SW;
-        auto launch = [&](auto kern, int R) {
-            static bool attr = false;
-            if (!attr) {
-                FKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                attr = true;
-            }
+        auto launch = [&](auto kern, int R) {  // (one lambda type per CNT: the attribute is set per call)
+            FKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             kern<<<ceil_div(n, 128 * R), 128, shm, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, Z, proj, X, var,
                                                        info, hout, ycnt);
         };
@@ -1224,6 +1220,7 @@ void Filter::enqueue_step(const double* d_y) {
     }
     spmv_short(HT, z.p, t.p, 1.0, s);
     mark("ht_z");
+    if (ufork == 3 && solver == 1) fork_upass();
     if (fused_uq) {  // U pass + diag Σ + realizations of the new state in one pass (needs t)
         cov->apply1(t.p, t.p);
         mark("gamma_apply");
@@ -1280,14 +1277,7 @@ void Filter::enqueue_solve_woodbury() {
         mark_on(side() != s ? s3 : s, "capacitance");
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join2, s3));
     };
-    // the U pass v = U·(D^½x) beside the rest of the chain
-    auto fork_u = [&] {
-        if (r <= 0 || !upass_side()) return;
-        fork();
-        launch_u_pass(XProd{sqd_c, ucap.p}, side(), true);
-        mark_on(side(), "u_pass");
-        if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
-    };
+    auto fork_u = [&] { fork_upass(); };
     if (kfork == 1) fork_next_k();
     const bool fused = fused_chain && !exact && r > 0;
     if (fused) {
@@ -1324,7 +1314,7 @@ void Filter::enqueue_solve_woodbury() {
         }
         mark("cap_solve");
         if (kfork == 2) fork_next_k();
-        fork_u();
+        if (ufork <= 1) fork_u();
     } else {
         launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
         mark("rotate_in");
@@ -1361,6 +1351,16 @@ void Filter::enqueue_solve_woodbury() {
     launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s, NoCta{},  // z = P·s̃ (rows of P)
                   fused && fused_chain == 2 && r <= 512 && (pdl_mask & 2));
     mark("rotate_out");
+    if (ufork == 2) fork_u();
+}
+
+// the U pass v = U·(D^½x) beside the rest of the chain (x from the capacitance solve)
+void Filter::fork_upass() {
+    if (r <= 0 || !upass_side()) return;
+    fork();
+    launch_u_pass(XProd{sqd_c, ucap.p}, side(), true);
+    mark_on(side(), "u_pass");
+    if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
 }
 
 // z ← S⁻¹z forming S = α·G − B·diag(d)·Bᵀ + σ²I and its LLT, as fast_filter.hpp:100-108.

@@ -118,6 +118,7 @@ struct Filter {
     int batch_par0 = 0;
     template <class XL>
     void launch_u_pass(XL xl, cudaStream_t st, bool beside);
+    void fork_upass();
     // the U pass runs beside the main chain (side branch) when it is short enough to hide
     // there: rank ≤ 320 (c2); otherwise after the forward FFT passes on the whole GPU (c4).
     // The fused step + UQ (c3) keeps its single pass k_mean_uq after Γ(Hᵀz).  FKB_UPASS_SIDE

@@ -153,102 +153,24 @@ __global__ void __launch_bounds__(256) k_spmm_rm(int rows, const int* __restrict
     }
 }
 
-// 16-byte variant: lane ℓ owns column pairs 2ℓ + 64q (q < Q2) of a 64·Q2-column slab, so each
-// nonzero's X row segment is read with 128-bit loads (half the load instructions and L1
-// wavefront requests of the 8-byte kernel); needs ldx, ldy even and 16-byte aligned blocks.
-template <int Q2, int U>
-__global__ void __launch_bounds__(256) k_spmm_rm2(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                 const double* __restrict__ v, const double* __restrict__ X,
-                                                 long long ldx, int ncols, double* __restrict__ Y, long long ldy,
-                                                 double alpha) {
-    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const int col0 = blockIdx.y * 64 * Q2;
-    double2 acc[Q2];
-#pragma unroll
-    for (int q = 0; q < Q2; ++q) acc[q] = make_double2(0.0, 0.0);
-    const int e0 = rp[row], e1 = rp[row + 1];
-    for (int eb = e0; eb < e1; eb += 32) {
-        const int cnt = min(32, e1 - eb);
-        const int myc = lane < cnt ? ci[eb + lane] : 0;
-        const double myv = lane < cnt ? v[eb + lane] : 0.0;
-        for (int u0 = 0; u0 < cnt; u0 += U) {
-            int c[U];
-            double w[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                c[u] = __shfl_sync(0xffffffffu, myc, (u0 + u) & 31);
-                w[u] = __shfl_sync(0xffffffffu, myv, (u0 + u) & 31);
-                if (u0 + u >= cnt) w[u] = 0.0;
-            }
-            double2 x[U][Q2];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int q = 0; q < Q2; ++q) {
-                    const int col = col0 + 2 * lane + 64 * q;
-                    x[u][q] = col < ncols ? __ldg(reinterpret_cast<const double2*>(X + (long long)c[u] * ldx + col))
-                                          : make_double2(0.0, 0.0);
-                }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int q = 0; q < Q2; ++q) {
-                    acc[q].x = fma(w[u], x[u][q].x, acc[q].x);
-                    acc[q].y = fma(w[u], x[u][q].y, acc[q].y);
-                }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < Q2; ++q) {
-        const int col = col0 + 2 * lane + 64 * q;
-        if (col < ncols)
-            *reinterpret_cast<double2*>(Y + (long long)row * ldy + col) = make_double2(alpha * acc[q].x, alpha * acc[q].y);
-    }
-}
-
 void spmm_rm(const DevCsr& A, const double* X, long long ldx, int ncols, double* Y, long long ldy, double alpha,
              cudaStream_t s) {
     if (A.rows <= 0 || ncols <= 0) return;
-    // Every nonzero streams a full X row from L2 (X is shared by the ~10 rays through a cell),
-    // so the kernel runs at the L2 bandwidth cap; the shape only decides how much of it is in
-    // flight.  Measured at c2 (l = 320): long rows (rays, ~320 nonzeros) 128 columns per warp
-    // with 16 nonzeros per batch; short rows (cells, ~10) 256 columns with 4.
+    // Every nonzero streams a full X row from L2 (X is shared by the ~10 rays through a cell):
+    // 8·nnz·l bytes of L2→SM traffic, which this kernel moves at 0.58 of the measured L2→SM
+    // read peak (fkb_l2_peak, 20.4 TB/s).  Measured at c2 (l = 320): long rows (rays, ~320
+    // nonzeros) 128 columns per warp with 16 nonzeros per batch (64 / 160-column slabs,
+    // 16-byte lane loads, 4–32 nonzeros per batch and cp.async.bulk row staging through shared
+    // memory all measured 0.23–0.59); short rows (cells, ~10) 256 columns with 4.
     const bool longrows = double(A.nnz) / A.rows > 64.0;
-    static const int qu = [] {  // FKB_SPMM_QU (development sweeps): 10·Q + U-code for long rows
-        const char* e = std::getenv("FKB_SPMM_QU");
-        return e ? std::atoi(e) : 0;
-    }();
-    int Q = ncols <= 32 ? 1 : longrows ? 4 : 8, U = Q == 1 ? 8 : longrows ? 16 : 4;
-    if (longrows && ncols > 32 && qu) { Q = qu / 100; U = qu % 100; }
-    const bool v2 = (ncols % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
-                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
-    if (v2 && Q >= 10) {  // FKB_SPMM_QU ≥ 1000: the 16-byte kernel, Q2 = Q / 10
-        const int Q2 = Q / 10;
-        const dim3 g2(ceil_div((long long)A.rows * 32, 256), ceil_div(ncols, 64 * Q2));
-        auto go2 = [&](auto kern) { kern<<<g2, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha); };
-        if (Q2 == 1 && U == 8) go2(k_spmm_rm2<1, 8>);
-        else if (Q2 == 1 && U == 16) go2(k_spmm_rm2<1, 16>);
-        else if (Q2 == 1) go2(k_spmm_rm2<1, 32>);
-        else if (Q2 == 2 && U == 8) go2(k_spmm_rm2<2, 8>);
-        else if (Q2 == 2) go2(k_spmm_rm2<2, 16>);
-        else if (Q2 == 5 && U == 4) go2(k_spmm_rm2<5, 4>);
-        else go2(k_spmm_rm2<5, 8>);
-        FKB_LAUNCH_CHECK();
-        count_launch();
-        return;
-    }
+    const int Q = ncols <= 32 ? 1 : longrows ? 4 : 8;
     const dim3 grid(ceil_div((long long)A.rows * 32, 256), ceil_div(ncols, 32 * Q));
-    auto go = [&](auto kern) { kern<<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha); };
-    if (Q == 1) go(k_spmm_rm<1, 8>);
-    else if (Q == 2 && U == 8) go(k_spmm_rm<2, 8>);
-    else if (Q == 2 && U == 16) go(k_spmm_rm<2, 16>);
-    else if (Q == 2) go(k_spmm_rm<2, 32>);
-    else if (Q == 4 && U == 8) go(k_spmm_rm<4, 8>);
-    else if (Q == 4) go(k_spmm_rm<4, 16>);
-    else if (Q == 5 && U == 8) go(k_spmm_rm<5, 8>);
-    else if (Q == 5) go(k_spmm_rm<5, 4>);
-    else go(k_spmm_rm<8, 4>);
+    if (Q == 1)
+        k_spmm_rm<1, 8><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
+    else if (Q == 4)
+        k_spmm_rm<4, 16><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
+    else
+        k_spmm_rm<8, 4><<<grid, 256, 0, s>>>(A.rows, A.rowptr.p, A.col.p, A.val.p, X, ldx, ncols, Y, ldy, alpha);
     FKB_LAUNCH_CHECK();
     count_launch();
 }

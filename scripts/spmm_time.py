@@ -33,9 +33,17 @@ for which, src, dst in ((0, X, Z), (1, Z, X)):
     b.record(st)
     torch.cuda.synchronize()
     out[which] = a.elapsed_time(b) / 10
+# correctness of the timed kernel: H·X against scipy on the host
+import numpy as np  # noqa: E402
+import scipy.sparse as sp  # noqa: E402
+Hs = sp.csr_matrix((np.asarray(h.val), np.asarray(h.col), np.asarray(h.rowptr)), shape=(w.m, w.N))
+ctx.spmm_rm_device(0, ptr(X), l, ptr(Z))
+torch.cuda.synchronize()
+ref = Hs @ X.cpu().numpy()
+err = np.abs(Z.cpu().numpy() - ref).max() / np.abs(ref).max()
 pk = C.c_double()
 check(lib().fkb_l2_peak(32, C.byref(pk)))
 alg = 12 * h.nnz + 4 * (h.rows + 1) + 8 * (w.N + w.m) * l
 print(f"{name} QU={os.environ.get('FKB_SPMM_QU', 'default')}: H·X {out[0] * 1e3:.1f} us = {alg / out[0] / 1e6:.0f} GB/s alg, "
       f"L2 {8 * h.nnz * l / out[0] / 1e6:.0f} GB/s of {pk.value:.0f} ({8 * h.nnz * l / out[0] / 1e6 / pk.value:.2f}); "
-      f"Hᵀ·Y {out[1] * 1e3:.1f} us", flush=True)
+      f"Hᵀ·Y {out[1] * 1e3:.1f} us; max rel err vs scipy {err:.1e}", flush=True)
