@@ -196,6 +196,18 @@ constexpr int kEpt = 8;
 constexpr int kRowPairs = 4;   // batched: 8 consecutive rows per CTA (128-byte W segments)
 constexpr int kRowPairs1 = 2;  // single vector: fewer, still-coalesced CTAs (measured best)  // transforms per CTA in the batched register-resident rows passes
 
+// Per-transform buffer stride of the register-resident rows passes with RP transforms per CTA:
+// the inverse pass maps lane t to (transform t % RP, index t / RP), so a quarter-warp's 16-byte
+// exchange accesses hit banks (p·stride + index) mod 8 — a stride ≡ 8/RP (mod 8) makes them
+// distinct (the bare NT + NT/8 + 1 ≡ 1 had 2-way conflicts for RP = 4: half of the pass's
+// shared-memory wavefronts).  The forward pass (one transform per warp) is unaffected.
+__host__ __device__ __forceinline__ int rows_bl(int n, int rp) {
+    const int b = n + n / 8 + 1;
+    if (rp <= 1 || rp >= 8) return b;
+    const int want = 8 / rp;
+    return b + ((want - b % 8) % 8 + 8) % 8;
+}
+
 // Shared layout of the single-transform kernels: twiddles | a | b.  NT > 0 (compile-time
 // power-of-two length): per-pass twiddle table and padded buffers (fft_block_p); NT = 0:
 // base table tw[0..n) and plain buffers (runtime schedule, fft_block).
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd_1(const double* __restrict__ x
         const int t = threadIdx.x, p = t / TPT, j = t % TPT;
         const int ix0 = blockIdx.x * 2 * RP;
         const int q0 = ix0 + 2 * p, q1 = q0 + 1;
-        const int bl = L::blen(my);
+        const int bl = rows_bl(my, RP);
         double2* ap = sm + p * bl;  // twiddles come from the global per-pass table (fft_reg)
         double2 v[8];
 #pragma unroll
@@ -388,7 +400,7 @@ __global__ void __launch_bounds__(256) k_rows_inv_1(const double2* __restrict__ 
         const int t = threadIdx.x, p = t % RP, j = t / RP;
         const int ix0 = blockIdx.x * 2 * RP;
         const int q0 = ix0 + 2 * p, q1 = q0 + 1;
-        const int bl = L::blen(my);
+        const int bl = rows_bl(my, RP);
         double2* ap = sm + p * bl;  // twiddles come from the global per-pass table (fft_reg)
         // mean-update operands loaded up front (independent of the transform, their latency
         // hides under it; loaded after the stores below they would serialize on aliasing)
@@ -829,7 +841,7 @@ static size_t smem_1(int n) {
 }
 // rows passes: register-resident lengths hold kRowPairs single buffers
 static size_t smem_rows(int n, int rp) {
-    if (n == 512 || n == 1024) return size_t(std::max(rp, 2)) * (n + n / 8 + 1) * sizeof(double2);
+    if (n == 512 || n == 1024) return size_t(std::max(rp, 2)) * rows_bl(n, rp) * sizeof(double2);
     return smem_1(n);
 }
 

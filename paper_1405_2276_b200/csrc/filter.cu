@@ -164,6 +164,43 @@ __global__ void k_woodbury_scalars(int m, int r, int mode, const double* __restr
     }
 }
 
+// Positive-definiteness certificate of the capacitance K (side branch, next to its Gram): by
+// Gershgorin, K is SPD if every row is strictly diagonally dominant — either as it stands or
+// after the symmetric Jacobi scaling D^{-½}KD^{-½} (unit diagonal).  *cert = 0 when either
+// test holds for every row, else 1; the step's PCG then gives up at once and the step is rerun
+// on the exact Cholesky path, so a K the Krylov space would not expose as indefinite still
+// gets the reference LLT's verdict (fast_filter.hpp:104-106).  One CTA; K is L2-resident.
+__global__ void __launch_bounds__(1024) k_cap_certificate(int r, const double* __restrict__ K, int* __restrict__ cert,
+                                                         int force_fail) {
+    extern __shared__ double rdiag[];  // 1/√K_jj
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        const double kjj = K[j + (long long)j * r];
+        rdiag[j] = kjj > 0.0 ? rsqrt(kjj) : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int failA = 0, failB = 0;
+    for (int i = warp; i < r; i += nw) {
+        const double* col = K + (long long)i * r;  // column i = row i (symmetric)
+        double sa = 0.0, sb = 0.0;
+        for (int j = lane; j < r; j += 32) {
+            if (j == i) continue;
+            const double a = fabs(col[j]);
+            sa += a;
+            sb += a * rdiag[j];
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        const double kii = col[i];
+        if (!(kii - sa > 0.0)) failA = 1;
+        if (!(rdiag[i] > 0.0) || !(1.0 - sb * rdiag[i] > 0.0)) failB = 1;
+    }
+    const int anyA = __syncthreads_or(failA), anyB = __syncthreads_or(failB);
+    if (threadIdx.x == 0) *cert = (force_fail || (anyA && anyB)) ? 1 : 0;
+}
+
 // u_j = sqd_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃); Λ_M⁻¹ and D^½
 // of this step were formed by the previous step's side branch)
 struct EpiScaleOut {
@@ -966,6 +1003,11 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     dsnap.alloc(size_t(std::max(r, 1)));
     pcgflag.alloc(1);
     parts.alloc(size_t(std::max(coldot_grid(m), 1)) * std::max(r, 1));
+    for (int q = 0; q < 2; ++q) {
+        certb[q].alloc(1);
+        FKB_CUDA(cudaMemset(certb[q].p, 0, sizeof(int)));
+    }
+    if (const char* e = std::getenv("FKB_CAP_CERT")) cert_force_fail = std::string(e) == "fail";
     if (std::getenv("FKB_PCG_STAMPS")) pcg_ts.alloc(64);
     {
         GemmArgs g;  // split-K workspace of the capacitance Gram
@@ -1176,6 +1218,10 @@ void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double
     g.C = K_o; g.ldc = r;
     g.diag_add = 1.0;
     gram_sym(g, b);  // full symmetric K (the PCG reads columns)
+    int* cert_o = K_o == Kb[0].p ? certb[0].p : certb[1].p;
+    k_cap_certificate<<<1, 1024, sizeof(double) * size_t(r), b>>>(r, K_o, cert_o, cert_force_fail ? 1 : 0);
+    FKB_LAUNCH_CHECK();
+    count_launch();
 }
 
 void Filter::prime_capacitance() {  // K, wsq, sqd of the next step (parity par_next), eagerly
@@ -1287,7 +1333,7 @@ void Filter::enqueue_solve_woodbury() {
         mark("rotate_in");
         if (kfork == 0) fork_next_k();
         PcgRhs rhs;
-        rhs.parts = parts.p; rhs.nparts = coldot_grid(m); rhs.sqd = sqd_c;
+        rhs.parts = parts.p; rhs.nparts = coldot_grid(m); rhs.sqd = sqd_c; rhs.cert = cert_c;
         PcgTail tl;
         const bool pdl = fused_chain == 2 && r <= 512;
         tl.info = info.p;
@@ -1321,6 +1367,7 @@ void Filter::enqueue_solve_woodbury() {
         if (r > 0) {
             // u = D^½·Eᵀ·Λ_M⁻¹·r̃: formed by the PCG kernel itself (fuse_rhs) or as column dots
             PcgRhs rhs;
+            rhs.cert = cert_c;
             if (fuse_rhs && !exact) {
                 rhs.E = E.p; rhs.lde = m; rhs.m = m; rhs.wsq = wsq_c; rhs.rt = rt.p; rhs.sqd = sqd_c;
             } else {

@@ -88,8 +88,12 @@ struct Filter {
     double *wsq_c = nullptr, *sqd_c = nullptr, *K_c = nullptr;  // this step's (capture-time)
     double *wsq_n = nullptr, *sqd_n = nullptr, *K_n = nullptr;  // next step's
     int par_next = 0;  // parity of the next step to run
+    DBuf<int> certb[2];          // K's positive-definiteness certificate per parity (k_cap_certificate)
+    const int* cert_c = nullptr;  // this step's
+    bool cert_force_fail = false; // FKB_CAP_CERT=fail: every step takes the exact path (tests)
     void select_parity(int p) {
         hout_c = hostout.p + 5 * p;
+        cert_c = certb[p].p;
         wsq_c = wsqb[p].p; sqd_c = sqdb[p].p; K_c = Kb[p].p;
         wsq_n = wsqb[p ^ 1].p; sqd_n = sqdb[p ^ 1].p; K_n = Kb[p ^ 1].p;
     }

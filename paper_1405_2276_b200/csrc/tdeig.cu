@@ -146,6 +146,141 @@ __global__ void __launch_bounds__(TD_T) k_tridiag(int n, double* __restrict__ A,
     }
 }
 
+// Cluster-resident tridiagonalization for n ≤ ~660: the 16 CTAs of one cluster hold A in shared
+// memory, column j in CTA j mod 16 (cyclic, so the shrinking trailing matrix stays balanced).
+// Step k: the owner of column k forms the reflector from its (already updated) column and
+// stores v into every CTA (DSMEM), cluster barrier; each CTA forms p_j = τ·(A₂₂v)_j for its
+// columns plus its partial of pᵀv and stores them into every CTA, cluster barrier; each CTA
+// applies A₂₂ −= v·wᵀ + w·vᵀ to its columns (w = p − ½τ(pᵀv)v, partials summed in CTA order:
+// bit-identical everywhere).  v/p buffers alternate by step parity.  Two cluster barriers per
+// step instead of two grid barriers and L2 round trips; A (with the v's below the subdiagonal,
+// as k_tridiag leaves it) is written back at the end.
+constexpr int TDC = 16;      // CTAs per cluster
+constexpr int TDC_T = 1024;  // threads per CTA
+__device__ __forceinline__ void dsmem_st(double* local, int rank, double v) {
+    unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local)), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+__global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDC_T) k_tridiag_cluster(
+    int n, double* __restrict__ A, double* __restrict__ d, double* __restrict__ e, double* __restrict__ tau) {
+    extern __shared__ double tsm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int crank = int(cl.block_rank());
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = TDC_T / 32;
+    const int ncl = (n - crank + TDC - 1) / TDC;  // columns owned: crank, crank + 16, …
+    const int ldc = n;
+    double* cols = tsm;                               // [ncl][n]
+    double* vb = cols + (size_t)((n + TDC - 1) / TDC) * ldc;  // [2][n]
+    double* pb = vb + 2 * n;                          // [2][n]
+    double* part = pb + 2 * n;                        // [2][TDC]
+    double* sc = part + 2 * TDC;                      // [4] τ of the step, per parity (+ pad)
+    for (long long q = tid; q < (long long)ncl * n; q += TDC_T) {
+        const int lc = int(q / n), i = int(q % n);
+        cols[(size_t)lc * ldc + i] = A[(long long)i + (long long)(crank + TDC * lc) * n];
+    }
+    __syncthreads();
+    // reflector of column k by warp 0 of its owner; v (len values) and τ to every CTA
+    auto reflector = [&](int k) {
+        const int o = k + 1, len = n - o, par = k & 1;
+        double* x = cols + (size_t)(k / TDC) * ldc + o;
+        if (warp == 0) {
+            double sig = 0.0;
+            for (int i = 1 + lane; i < len; i += 32) sig = fma(x[i], x[i], sig);
+            for (int s = 16; s > 0; s >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, s);
+            const double x0 = x[0];
+            double t = 0.0, beta = x0, v0 = 1.0;
+            if (sig != 0.0) {
+                const double mu = sqrt(x0 * x0 + sig);
+                beta = x0 <= 0.0 ? mu : -mu;
+                v0 = x0 - beta;
+                t = -v0 / beta;
+                for (int i = 1 + lane; i < len; i += 32) x[i] /= v0;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                d[k] = cols[(size_t)(k / TDC) * ldc + k];
+                e[k] = beta;
+                tau[k] = t;
+                x[0] = 1.0;
+                for (int c = 0; c < TDC; ++c) dsmem_st(&sc[par], c, t);
+            }
+        }
+        __syncthreads();
+        for (int q = tid; q < len * TDC; q += TDC_T) {  // v to every CTA (consecutive threads: one CTA, consecutive i)
+            const int c = q / len, i = q % len;
+            dsmem_st(&vb[par * n + o + i], c, x[i]);
+        }
+    };
+    if (n > 2 && crank == 0) reflector(0);
+    cl.sync();
+    for (int k = 0; k + 2 < n; ++k) {
+        const int o = k + 1, len = n - o, par = k & 1;
+        const double t = sc[par];
+        const double* v = vb + par * n;  // v_i at index i ≥ o
+        // p_j for owned columns j ≥ o, warp per column; partial pᵀv in CTA order
+        const int lc0 = (o - crank + TDC - 1) / TDC;  // first owned column ≥ o
+        double pv = 0.0;
+        if (t != 0.0) {
+            for (int lc = lc0 + warp; lc < ncl; lc += nw) {
+                const int j = crank + TDC * lc;
+                const double* col = cols + (size_t)lc * ldc;
+                double acc = 0.0, acc1 = 0.0;
+                int i = o + lane;
+                for (; i + 32 < n; i += 64) {
+                    acc = fma(col[i], v[i], acc);
+                    acc1 = fma(col[i + 32], v[i + 32], acc1);
+                }
+                if (i < n) acc = fma(col[i], v[i], acc);
+                acc += acc1;
+                for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+                acc *= t;
+                if (lane < TDC) dsmem_st(&pb[par * n + j], lane, acc);
+                pv = fma(acc, v[j], pv);
+            }
+        }
+        __shared__ double red[TDC_T / 32];
+        if (lane == 0) red[warp] = pv;
+        __syncthreads();
+        if (tid < TDC) {
+            double sacc = 0.0;
+            for (int w = 0; w < nw; ++w) sacc += red[w];
+            dsmem_st(&part[par * TDC + crank], tid, sacc);
+        }
+        cl.sync();  // p and the pᵀv partials everywhere
+        if (t != 0.0) {
+            double ptv = 0.0;
+            for (int c = 0; c < TDC; ++c) ptv += part[par * TDC + c];
+            const double h = 0.5 * t * ptv;
+            const double* p = pb + par * n;
+            for (int lc = lc0 + warp; lc < ncl; lc += nw) {
+                const int j = crank + TDC * lc;
+                double* col = cols + (size_t)lc * ldc;
+                const double vj = v[j], wj = p[j] - h * vj;
+                for (int i = o + lane; i < n; i += 32) col[i] -= v[i] * wj + (p[i] - h * v[i]) * vj;
+            }
+        }
+        __syncthreads();
+        if (k + 3 < n && (o % TDC) == crank) reflector(o);
+        cl.sync();  // the next reflector everywhere
+    }
+    if (crank == (n - 2 + TDC) % TDC && tid == 0 && n >= 2) {
+        d[n - 2] = cols[(size_t)((n - 2) / TDC) * ldc + n - 2];
+        e[n - 2] = cols[(size_t)((n - 2) / TDC) * ldc + n - 1];
+    }
+    if (crank == (n - 1) % TDC && tid == 0) {
+        d[n - 1] = cols[(size_t)((n - 1) / TDC) * ldc + n - 1];
+        e[n - 1] = 0.0;
+    }
+    for (long long q = tid; q < (long long)ncl * n; q += TDC_T) {
+        const int lc = int(q / n), i = int(q % n);
+        A[(long long)i + (long long)(crank + TDC * lc) * n] = cols[(size_t)lc * ldc + i];
+    }
+}
+static size_t tridiag_cluster_smem(int n) {
+    return sizeof(double) * (size_t((n + TDC - 1) / TDC) * n + 4 * size_t(n) + 2 * TDC + 4);
+}
+
 // Q = H₀H₁…H_{n−3} (column-major n×n), one warp per column held in registers (lane l owns
 // rows l, l+32, …): column j starts as e_j and meets the reflectors k = n−3 … 0 (only
 // k ≤ j−1 touch it); per reflector one pipelined read of v, a warp reduction, an axpy.
@@ -328,7 +463,19 @@ void sym_eig_tridiag_device(int n, double* A, double* w_host, double* Z, cudaStr
     const int grid = std::max(1, std::min(want, sms * std::max(per, 1)));
     DBuf<double> part{size_t(grid)};
     FKB_CUDA(cudaMemsetAsync(tau.p, 0, tau.bytes(), s));
-    {
+    static const bool cl_ok = std::getenv("FKB_TDEIG_GRID") == nullptr;
+    if (cl_ok && n >= 3 && tridiag_cluster_smem(n) <= 225 * 1024) {  // A resident in one 16-CTA cluster
+        static bool attr = false;
+        if (!attr) {
+            FKB_CUDA(cudaFuncSetAttribute((const void*)k_tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            FKB_CUDA(cudaFuncSetAttribute((const void*)k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          225 * 1024));
+            attr = true;
+        }
+        k_tridiag_cluster<<<TDC, TDC_T, tridiag_cluster_smem(n), s>>>(n, A, d.p, e.p, tau.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    } else {
         void* args[] = {&n, &A, &d.p, &e.p, &tau.p, &p.p, &part.p};
         FKB_CUDA(cudaLaunchCooperativeKernel((const void*)k_tridiag, dim3(grid), dim3(TD_T), args, 0, s));
         count_launch();

@@ -541,3 +541,18 @@ def test_run_batch_reruns_unverified_and_raises_singular():
     with pytest.raises(RuntimeError, match=r"singular \(step 1 of"):
         b.run(np.stack(ys[:2]))
     assert b.state()["alpha"] == st["alpha"]
+
+
+def test_uncertified_capacitance_takes_the_exact_path(monkeypatch):
+    """A capacitance K without the Gershgorin SPD certificate (forced: FKB_CAP_CERT=fail) is
+    never trusted to the PCG: every step reruns on the exact Cholesky path, same states."""
+    w, ys, a = _c0_ctx()
+    monkeypatch.setenv("FKB_CAP_CERT", "fail")
+    _, _, b = _c0_ctx()
+    monkeypatch.delenv("FKB_CAP_CERT")
+    for y in ys:
+        sa, sb = P.fkf_step(a, y), P.fkf_step(b, y)
+        assert sa["alpha"] == sb["alpha"]
+        assert rel_err(sb["mean"], sa["mean"]) < 1e-12
+        assert np.max(np.abs(sb["d"] - sa["d"])) / sa["alpha"] < 1e-12
+        assert b.cap_stats()[1] is True and a.cap_stats()[1] is False

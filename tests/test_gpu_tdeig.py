@@ -1,5 +1,6 @@
 """The GPU symmetric eigensolver of the GHEP core T and the add_low_rank core M (tdeig.cu:
-Householder tridiagonalization and Q on the GPU, QL rotations applied on the GPU), the
+Householder tridiagonalization (cluster-resident up to n ≈ 660, grid-wide beyond) and Q on the
+GPU, QL rotations applied on the GPU), the
 SelfAdjointEigenSolver calls of lowrank.hpp:193, :265-270, against numpy's eigh."""
 import numpy as np
 import pytest
@@ -9,7 +10,7 @@ from paper_1405_2276_b200 import fastkf as F
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 64, 320, 600])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 64, 320, 600, 640, 700])
 @pytest.mark.parametrize("graded", [False, True])
 def test_tridiag_eig_matches_eigh(n, graded):
     rng = np.random.default_rng(n + (1000 if graded else 0))
