@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     double nonpos = 0.0;  // K_ii ≤ 0: K (hence S) is not positive definite
     if (own) {
         const double kii = K[row + (long long)row * ld];
-        nonpos = (kii > 0.0 && !(ra.cert && *ra.cert)) ? 0.0 : 1.0;
+        nonpos = (kii > 0.0 && !(ra.cert && *ra.cert == 3)) ? 0.0 : 1.0;  // both Gershgorin tests failed
         dinv = 1.0 / kii;
         if (ra.E || ra.parts) {
             r = sh.q[tid];

@@ -24,7 +24,7 @@ struct PcgRhs {
     const double* sqd = nullptr;
     const double* parts = nullptr;
     int nparts = 0;
-    const int* cert = nullptr;  // ≠ 0: K is not certified SPD — give up at once (exact path decides)
+    const int* cert = nullptr;  // == 3: K is not certified SPD — give up at once (exact path decides)
 };
 // Optional tail (st set; needs vtol > 0): after a verified solve the cluster finishes the
 // filter step's Woodbury back-substitution and commit instead of a separate kernel:

@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* 
 __global__ void k_woodbury_scalars(int m, int r, int mode, const double* __restrict__ alpha_dev,
                                    const double* __restrict__ theta, const double* __restrict__ d,
                                    const double* __restrict__ lam, double sigma2, double* __restrict__ wsq,
-                                   double* __restrict__ sqd) {
+                                   double* __restrict__ sqd, int* __restrict__ cert) {
+    if (cert && blockIdx.x == 0 && threadIdx.x == 0) *cert = 0;  // k_cap_certificate ORs into it
     const double a_step = mode == 0 ? alpha_dev[0] + 1.0 : alpha_dev[1];
     const double alpha = mode == 0 ? a_step : a_step + 1.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
@@ -169,36 +170,35 @@ __global__ void k_woodbury_scalars(int m, int r, int mode, const double* __restr
 // after the symmetric Jacobi scaling D^{-½}KD^{-½} (unit diagonal).  *cert = 0 when either
 // test holds for every row, else 1; the step's PCG then gives up at once and the step is rerun
 // on the exact Cholesky path, so a K the Krylov space would not expose as indefinite still
-// gets the reference LLT's verdict (fast_filter.hpp:104-106).  One CTA; K is L2-resident.
-__global__ void __launch_bounds__(1024) k_cap_certificate(int r, const double* __restrict__ K, int* __restrict__ cert,
-                                                         int force_fail) {
+// gets the reference LLT's verdict (fast_filter.hpp:104-106).  A warp per row, failures
+// OR-ed into the flag (zeroed by k_woodbury_scalars earlier on the same branch); bit 0: the
+// unscaled test failed somewhere, bit 1: the scaled one — certified iff not both.
+__global__ void __launch_bounds__(256) k_cap_certificate(int r, const double* __restrict__ K, int* __restrict__ cert,
+                                                        int force_fail) {
     extern __shared__ double rdiag[];  // 1/√K_jj
     for (int j = threadIdx.x; j < r; j += blockDim.x) {
         const double kjj = K[j + (long long)j * r];
         rdiag[j] = kjj > 0.0 ? rsqrt(kjj) : 0.0;
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int failA = 0, failB = 0;
-    for (int i = warp; i < r; i += nw) {
-        const double* col = K + (long long)i * r;  // column i = row i (symmetric)
-        double sa = 0.0, sb = 0.0;
-        for (int j = lane; j < r; j += 32) {
-            if (j == i) continue;
-            const double a = fabs(col[j]);
-            sa += a;
-            sb += a * rdiag[j];
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            sa += __shfl_xor_sync(0xffffffffu, sa, o);
-            sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        }
-        const double kii = col[i];
-        if (!(kii - sa > 0.0)) failA = 1;
-        if (!(rdiag[i] > 0.0) || !(1.0 - sb * rdiag[i] > 0.0)) failB = 1;
+    const int lane = threadIdx.x & 31, i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= r) return;
+    const double* col = K + (long long)i * r;  // column i = row i (symmetric)
+    double sa = 0.0, sb = 0.0;
+    for (int j = lane; j < r; j += 32) {
+        const double a = j == i ? 0.0 : fabs(col[j]);
+        sa += a;
+        sb = fma(a, rdiag[j], sb);
     }
-    const int anyA = __syncthreads_or(failA), anyB = __syncthreads_or(failB);
-    if (threadIdx.x == 0) *cert = (force_fail || (anyA && anyB)) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (lane == 0) {
+        const double kii = col[i];
+        const int f = (!(kii - sa > 0.0) ? 1 : 0) | ((!(rdiag[i] > 0.0) || !(1.0 - sb * rdiag[i] > 0.0)) ? 2 : 0);
+        if (f || (force_fail && i == 0)) atomicOr(cert, force_fail ? 3 : f);
+    }
 }
 
 // u_j = sqd_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃); Λ_M⁻¹ and D^½
@@ -563,6 +563,110 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const do
     }
 }
 
+// The fused U pass + UQ on the FP64 tensor path: the per-row products with the count
+// projections, acc_s = Σ_j U_ij·(Σ₋⊙Ūᵀz_s)_j (s < 8), are an N×r by r×8 product — one DMMA
+// m8n8k4 per 8 rows × 4 columns of U — while U·dc and Σ_j d_j U_ij² ride along on the same
+// A-fragment registers (DFMA).  A warp owns 32 rows (four m-tiles); lane (g = lane/4,
+// q = lane%4) holds U[row 8t+g, col j0+q], i.e. 4 × 64-byte column segments per load
+// instruction; 4 k-steps (16 loads) in flight.  The B fragment (P[j0+q][g]), dc and d come
+// from shared memory (one LDS each per k-step).  Removes the per-element shared-memory
+// broadcasts that bounded k_mean_uq1.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256, 2) k_mean_uq_mma(long long n, int r, const double* __restrict__ U,
+                                                       const double* __restrict__ dc, const double* __restrict__ d,
+                                                       const double* __restrict__ alpha_dev, double theta,
+                                                       const double* __restrict__ t, double* __restrict__ mean,
+                                                       int count, const double* __restrict__ Z,
+                                                       const double* __restrict__ proj, double* __restrict__ X,
+                                                       double* __restrict__ var, const int* __restrict__ info,
+                                                       const unsigned long long* __restrict__ hout,
+                                                       long long* __restrict__ ycnt) {
+    extern __shared__ double msm[];
+    const int r4 = (r + 15) & ~15;  // k-steps of 4, unrolled by 4
+    double* Bt = msm;               // [r4][8]
+    double* dcs = Bt + (size_t)r4 * 8;
+    double* ds = dcs + r4;
+    const int bad = *info;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
+        if (ycnt) *ycnt += 1;
+    }
+    if (bad) return;
+    const double alpha = alpha_dev[1];
+    for (int j = threadIdx.x; j < r4; j += blockDim.x) {
+        const bool in = j < r;
+        const double dj = in ? d[j] : 0.0;
+        dcs[j] = in ? dc[j] : 0.0;
+        ds[j] = dj;
+        const double sm = in ? 1.0 - sqrt(fmax(1.0 - dj / alpha, 0.0)) : 0.0;  // uq.hpp:59-64
+        for (int s2 = 0; s2 < 8; ++s2) Bt[j * 8 + s2] = (in && s2 < count) ? sm * proj[j + (long long)s2 * r] : 0.0;
+    }
+    __syncthreads();
+    const double ra = sqrt(alpha);
+    double* vo = hout[4] ? reinterpret_cast<double*>(hout[4]) : var;
+    double* xo = hout[3] ? reinterpret_cast<double*>(hout[3]) : X;
+    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const long long wstride = (long long)gridDim.x * (blockDim.x >> 5) * 32;
+    for (long long i0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; i0 < n; i0 += wstride) {
+        double acc[4][2], vm[4], vs[4];
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) acc[tt][0] = acc[tt][1] = vm[tt] = vs[tt] = 0.0;
+        bool rin[4];
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) rin[tt] = i0 + 8 * tt + g < n;
+        for (int j0 = 0; j0 < r4; j0 += 16) {
+            double a[4][4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int j = j0 + 4 * kk + q;
+#pragma unroll
+                for (int tt = 0; tt < 4; ++tt)
+                    a[kk][tt] = (j < r && rin[tt]) ? __ldcs(U + (long long)j * n + i0 + 8 * tt + g) : 0.0;
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int j = j0 + 4 * kk + q;
+                const double b = Bt[(j0 + 4 * kk + q) * 8 + g];
+                const double cj = dcs[j], dj = ds[j];
+#pragma unroll
+                for (int tt = 0; tt < 4; ++tt) {
+                    dmma884(acc[tt][0], acc[tt][1], a[kk][tt], b);
+                    vm[tt] = fma(a[kk][tt], cj, vm[tt]);
+                    vs[tt] = fma(a[kk][tt] * a[kk][tt], dj, vs[tt]);
+                }
+            }
+        }
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+            // the row's four column classes q: fixed butterfly (same sum in all four lanes)
+            vm[tt] += __shfl_xor_sync(0xffffffffu, vm[tt], 1);
+            vm[tt] += __shfl_xor_sync(0xffffffffu, vm[tt], 2);
+            vs[tt] += __shfl_xor_sync(0xffffffffu, vs[tt], 1);
+            vs[tt] += __shfl_xor_sync(0xffffffffu, vs[tt], 2);
+            if (!rin[tt]) continue;
+            const long long i = i0 + 8 * tt + g;
+            const double mi = (mean[i] + alpha * t[i]) - vm[tt];
+            if (q == 0) {
+                mean[i] = mi;
+                if (hout[0]) reinterpret_cast<double*>(hout[0])[i] = mi;
+                if (vo) vo[i] = alpha * theta - vs[tt];
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int s2 = 2 * q + h;
+                if (s2 < count) {
+                    const double z = Z[i + (long long)s2 * n];
+                    xo[i + (long long)s2 * n] = mi + (ra * z - ra * acc[tt][h]);
+                }
+            }
+        }
+    }
+}
+
 void launch_mean_uq(int count, long long n, int r, const double* U, const double* dc, const double* d,
                     const double* alpha_dev, double theta, const double* t, double* mean, const double* Z,
                     const double* proj, double* X, double* var, const int* info, const unsigned long long* hout,
@@ -583,7 +687,18 @@ void launch_mean_uq(int count, long long n, int r, const double* U, const double
             kern<<<ceil_div(n, 128 * R), 128, shm, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, Z, proj, X, var,
                                                        info, hout, ycnt);
         };
-        if (shape == 208) launch(k_mean_uq<CNT, 2, 8>, 2);
+        if (shape == 9) {  // the DMMA pass (k_mean_uq_mma)
+            const int r16 = (r + 15) & ~15;
+            const size_t shm9 = sizeof(double) * size_t(r16) * 10;
+            FKB_CUDA(cudaFuncSetAttribute(k_mean_uq_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            int dev = 0, sms = 0;
+            FKB_CUDA(cudaGetDevice(&dev));
+            FKB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            const long long warps = (n + 31) / 32;
+            const int grid = int(std::min<long long>((warps + 7) / 8, 2LL * sms));
+            k_mean_uq_mma<<<grid, 256, shm9, s>>>(n, r, U, dc, d, alpha_dev, theta, t, mean, count, Z, proj, X, var,
+                                                  info, hout, ycnt);
+        } else if (shape == 208) launch(k_mean_uq<CNT, 2, 8>, 2);
         else if (shape == 116) launch(k_mean_uq<CNT, 1, 16>, 1);
         else {
             const size_t shm1 = sizeof(double) * size_t(r) * (2 + std::max(count, 1));
@@ -1205,7 +1320,8 @@ void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double
     // mode 1 (inside the step graph) reads the snapshot of the committed d taken by the step's
     // first kernel: the step's own epilogue commits the new d concurrently with this branch
     k_woodbury_scalars<<<std::max(1, std::min(ceil_div(std::max(m, r), 256), 148)), 256, 0, b>>>(
-        m, r, mode, alpha_dev.p, theta.p, mode == 1 ? dsnap.p : d.p, lambda.p, sigma2, wsq_o, sqd_o);
+        m, r, mode, alpha_dev.p, theta.p, mode == 1 ? dsnap.p : d.p, lambda.p, sigma2, wsq_o, sqd_o,
+        K_o == Kb[0].p ? certb[0].p : certb[1].p);
     FKB_LAUNCH_CHECK();
     count_launch();
     GemmArgs g;  // K = I − D^½·Eᵀ·Λ_M⁻¹·E·D^½
@@ -1219,7 +1335,7 @@ void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double
     g.diag_add = 1.0;
     gram_sym(g, b);  // full symmetric K (the PCG reads columns)
     int* cert_o = K_o == Kb[0].p ? certb[0].p : certb[1].p;
-    k_cap_certificate<<<1, 1024, sizeof(double) * size_t(r), b>>>(r, K_o, cert_o, cert_force_fail ? 1 : 0);
+    k_cap_certificate<<<ceil_div(r, 8), 256, sizeof(double) * size_t(r), b>>>(r, K_o, cert_o, cert_force_fail ? 1 : 0);
     FKB_LAUNCH_CHECK();
     count_launch();
 }
