@@ -201,6 +201,25 @@ __global__ void __launch_bounds__(256) k_cap_certificate(int r, const double* __
     }
 }
 
+// Second-chance certificate: a K that fails both Gershgorin tests (c1 has such steps) is
+// factored — a copy, the PCG needs K intact — by the cluster Cholesky on the side branch; a
+// clean factorization certifies it.  Idle (early exit) whenever Gershgorin succeeded.
+__global__ void k_cert_prepare(int r, const double* __restrict__ K, double* __restrict__ Kc, const int* __restrict__ cert,
+                               int* __restrict__ gate, int* __restrict__ cinfo) {
+    const bool run = *cert == 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *gate = run ? 1 : 0;
+        *cinfo = 0;
+    }
+    if (!run) return;
+    const long long total = (long long)r * r;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        Kc[e] = K[e];
+}
+__global__ void k_cert_finish(int* __restrict__ cert, const int* __restrict__ gate, const int* __restrict__ cinfo) {
+    if (*gate && *cinfo == 0) *cert = 0;
+}
+
 // u_j = sqd_j · v  (capacitance right-hand side from the column dot Eᵀ(Λ_M⁻¹ r̃); Λ_M⁻¹ and D^½
 // of this step were formed by the previous step's side branch)
 struct EpiScaleOut {
@@ -671,12 +690,12 @@ void launch_mean_uq(int count, long long n, int r, const double* U, const double
                     const double* alpha_dev, double theta, const double* t, double* mean, const double* Z,
                     const double* proj, double* X, double* var, const int* info, const unsigned long long* hout,
                     long long* ycnt, cudaStream_t s) {
-    // FKB_UQ_SHAPE: 0 (default) k_mean_uq1 — one row per thread, separate constant arrays;
-    // 116 / 208 — shared-memory records, 1 row × 16 or 2 rows × 8 columns per batch (c3, in
-    // graph: 64 / 80 / 68 µs)
+    // FKB_UQ_SHAPE: 9 (default) k_mean_uq_mma — the projections on DMMA; 0 k_mean_uq1 — one
+    // row per thread, separate constant arrays; 116 / 208 — shared-memory records, 1 row × 16
+    // or 2 rows × 8 columns per batch (c3, in graph: 53 / 64 / 80 / 68 µs)
     static const int shape = [] {
         const char* e = std::getenv("FKB_UQ_SHAPE");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 9;
     }();
     auto go = [&](auto c) {
         constexpr int CNT = decltype(c)::value;
@@ -1122,6 +1141,14 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
         certb[q].alloc(1);
         FKB_CUDA(cudaMemset(certb[q].p, 0, sizeof(int)));
     }
+    if (r > 0 && r <= 640) {
+        Kchk.alloc(size_t(r) * r);
+        bchk.alloc(size_t(r));
+        FKB_CUDA(cudaMemset(bchk.p, 0, bchk.bytes()));
+        rdg2.alloc(std::max<size_t>(chol_solve_scratch(r), 1));
+        cgate.alloc(2);
+        FKB_CUDA(cudaMemset(cgate.p, 0, cgate.bytes()));
+    }
     if (const char* e = std::getenv("FKB_CAP_CERT")) cert_force_fail = std::string(e) == "fail";
     if (std::getenv("FKB_PCG_STAMPS")) pcg_ts.alloc(64);
     {
@@ -1338,6 +1365,15 @@ void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double
     k_cap_certificate<<<ceil_div(r, 8), 256, sizeof(double) * size_t(r), b>>>(r, K_o, cert_o, cert_force_fail ? 1 : 0);
     FKB_LAUNCH_CHECK();
     count_launch();
+    if (r <= 640 && !cert_force_fail) {  // the cluster Cholesky's staging limit
+        k_cert_prepare<<<std::min(ceil_div((long long)r * r, 256), 296), 256, 0, b>>>(r, K_o, Kchk.p, cert_o, cgate.p,
+                                                                                      cgate.p + 1);
+        FKB_LAUNCH_CHECK();
+        chol_solve_small(r, Kchk.p, r, bchk.p, rdg2.p, cgate.p + 1, b, nullptr, cgate.p);
+        k_cert_finish<<<1, 1, 0, b>>>(cert_o, cgate.p, cgate.p + 1);
+        FKB_LAUNCH_CHECK();
+        count_launch(2);
+    }
 }
 
 void Filter::prime_capacitance() {  // K, wsq, sqd of the next step (parity par_next), eagerly

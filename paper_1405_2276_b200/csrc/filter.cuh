@@ -89,6 +89,8 @@ struct Filter {
     double *wsq_n = nullptr, *sqd_n = nullptr, *K_n = nullptr;  // next step's
     int par_next = 0;  // parity of the next step to run
     DBuf<int> certb[2];          // K's positive-definiteness certificate per parity (k_cap_certificate)
+    DBuf<double> Kchk, bchk, rdg2;  // the side branch's Cholesky certificate of a K Gershgorin cannot certify
+    DBuf<int> cgate;             // [gate, info] of that factorization
     const int* cert_c = nullptr;  // this step's
     bool cert_force_fail = false; // FKB_CAP_CERT=fail: every step takes the exact path (tests)
     void select_parity(int p) {
