@@ -826,14 +826,22 @@ std::vector<double> gram_inv_sqrt(int p, const std::vector<double>& Gh, double t
         double dmax = 0.0;
         for (int j = 0; j < p; ++j) dmax = std::max(dmax, Gh[size_t(j) + size_t(j) * p]);
         bool ok = dmax > 0.0;
-        for (int j = 0; j < p && ok; ++j) {  // left-looking Cholesky on the lower triangle
+        // left-looking Cholesky on the lower triangle; one parallel region (a fork/join per
+        // column cost more than the column's work): the pivot in `single`, the rows in `for`
+#pragma omp parallel if (p > 64)
+        for (int j = 0; j < p; ++j) {
+#pragma omp single
+            {
+                const double* lj = Lr.data() + size_t(j) * p;
+                double dj = ok ? lj[j] : 0.0;
+                for (int k = 0; k < j; ++k) dj -= lj[k] * lj[k];
+                if (!(dj >= 1e-10 * dmax)) ok = false;
+                else Lr[size_t(j) * p + j] = std::sqrt(dj);
+            }  // implicit barrier: every thread sees ok and L_jj
+            if (!ok) break;
             const double* lj = Lr.data() + size_t(j) * p;
-            double dj = lj[j];
-            for (int k = 0; k < j; ++k) dj -= lj[k] * lj[k];
-            if (!(dj >= 1e-10 * dmax)) { ok = false; break; }
-            const double ljj = std::sqrt(dj);
-            Lr[size_t(j) * p + j] = ljj;
-#pragma omp parallel for schedule(static) if (p - j > 64)
+            const double ljj = lj[j];
+#pragma omp for schedule(static)
             for (int i = j + 1; i < p; ++i) {
                 double* li = Lr.data() + size_t(i) * p;
                 double v = 0.5 * (li[j] + Gh[size_t(j) + size_t(i) * p]);  // symmetrized entry
