@@ -50,5 +50,22 @@ int main(int argc, char** argv) {
     if (std::abs(trace_criterion(s3, cov) - trace_criterion(s3, cctx)) > 1e-12 * std::abs(trace_criterion(s3, cctx)))
         return 9;
     std::printf("edit ok\n");
+    // the driver's loop as one call (extension fkf_run) ≡ fkf_step step by step
+    Matrix ys(h.rows(), 2);
+    for (Index i = 0; i < h.rows(); ++i) {
+        ys(i, 0) = y[i];
+        ys(i, 1) = 0.5 * y[i];
+    }
+    Vector y2(h.rows());
+    for (Index i = 0; i < h.rows(); ++i) y2[i] = 0.5 * y[i];
+    const LowRankState r1 = fkf_step(s3, ctx, y), r2 = fkf_step(r1, ctx, y2);
+    const std::vector<LowRankState> run = fkf_run(s3, ctx, ys);
+    if (run.size() != 2 || run[1].mean.v != r2.mean.v || run[1].d.v != r2.d.v || run[1].alpha != r2.alpha ||
+        run[0].mean.v != r1.mean.v || run[1].step != r2.step)
+        return 10;
+    const LowRankState r3 = fkf_step(run[1], ctx, y);  // continues from the mirrored state
+    const LowRankState r4 = fkf_step(r2, ctx, y);
+    if (r3.mean.v != r4.mean.v) return 11;
+    std::printf("run ok\n");
     return 0;
 }

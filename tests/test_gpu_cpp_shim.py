@@ -46,6 +46,7 @@ def test_cpp_shim_matches_oracle(tmp_path):
         assert abs(float(hdr[5]) - of.trace_criterion()) <= 1e-9 * abs(of.trace_criterion())
         assert abs(float(hdr[7]) - of.relative_entropy()) <= 1e-9 * abs(of.relative_entropy())
     assert out[i].strip() == "edit ok"
+    assert out[i + 1].strip() == "run ok"  # fkf_run (the driver loop in one call) ≡ fkf_step × 2
 
 
 def _compile_fekf(tmp_path):
