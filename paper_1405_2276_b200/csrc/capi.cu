@@ -429,6 +429,7 @@ int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const 
                 "fkf_step: state rank does not match the eigendecomposition (constant-H regime requires W = U)");
         const double a2[2] = {alpha, alpha};
         FKB_CUDA(cudaMemsetAsync(F.info.p, 0, sizeof(int), F.s));  // a new state starts unflagged
+        FKB_CUDA(cudaMemsetAsync(F.ready.p, 0, sizeof(double), F.s));  // no stale epoch for the new α
         FKB_CUDA(cudaMemcpyAsync(F.alpha_dev.p, a2, sizeof(a2), cudaMemcpyHostToDevice, F.s));
         if (rank) FKB_CUDA(cudaMemcpyAsync(F.d.p, d, sizeof(double) * F.r, cudaMemcpyHostToDevice, F.s));
         else FKB_CUDA(cudaMemsetAsync(F.d.p, 0, F.d.bytes(), F.s));
@@ -438,6 +439,7 @@ int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const 
         F.step_no = step;
         F.state_rank = rank;
         F.k_valid = false;  // the precomputed capacitance belongs to the old (α, d)
+        if (mean) F.hm_valid = false;  // the carried image H·mean too
     });
 }
 int fkb_filter_reset(fkb_filter* f) {

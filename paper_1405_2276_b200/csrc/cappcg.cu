@@ -239,9 +239,14 @@ __device__ __forceinline__ void woodbury_tail(const PcgTail& tl, const double* x
         tl.dc[row] = zero ? 0.0 : __ldg(tl.sqd + row) * x;
         const double dn = (dj + alpha * l * c) / (1.0 + l * c);
         tl.d[row] = dn;
+        if (tl.d_q) tl.d_q[row] = dn;
         if (tl.hout[1]) reinterpret_cast<double*>(tl.hout[1])[row] = dn;
     }
-    if (crank == 0 && tid == 0) tl.alpha_dev[0] = alpha;
+    if (crank == 0 && tid == 0) {
+        tl.alpha_dev[0] = alpha;
+        if (tl.alpha_q) *tl.alpha_q = alpha;
+        if (tl.gate_q) *tl.gate_q = 0;
+    }
 }
 
 template <int KR>
@@ -296,6 +301,24 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     if constexpr (KR > 0)  // entries n..16·KR−1 of both exchange buffers multiply zero K entries
         for (int e = n + tid; e < 16 * KR; e += PC_T) sh.v[0][e] = sh.v[1][e] = 0.0;
     __syncthreads();  // mbarrier initialized before anyone waits on it
+    __shared__ int spin_fail;
+    if (ra.ready) {  // the producer of parts may still be running (K is staging meanwhile)
+        if (tid == 0) {
+            const double want = ra.alpha_dev[0] + 1.0;
+            const unsigned long long t0 = gtimer();
+            int fail = 0;
+            while (*reinterpret_cast<const volatile double*>(ra.ready) != want) {
+                if (gtimer() - t0 > ra.ready_timeout_ns) {
+                    fail = 1;
+                    break;
+                }
+                __nanosleep(64);
+            }
+            __threadfence();
+            spin_fail = fail;
+        }
+        __syncthreads();
+    }
     if (ra.E) fused_rhs(sh, ra, r0, r1);  // overlaps the K staging copy
     else if (ra.parts) parts_rhs(sh, ra, n, r0, r1);
     // Pipelined Jacobi-PCG (Ghysels–Vanroose): the matvec n = K·m and the reductions
@@ -313,6 +336,7 @@ __global__ void __launch_bounds__(PC_T) k_cap_pcg(const double* __restrict__ K, 
     if (own) {
         const double kii = K[row + (long long)row * ld];
         nonpos = (kii > 0.0 && !(ra.cert && *ra.cert == 3)) ? 0.0 : 1.0;  // both Gershgorin tests failed
+        if (ra.ready && spin_fail) nonpos = 1.0;  // the partials never arrived: give up (exact rerun)
         dinv = 1.0 / kii;
         if (ra.E || ra.parts) {
             r = sh.q[tid];

@@ -25,6 +25,13 @@ struct PcgRhs {
     const double* parts = nullptr;
     int nparts = 0;
     const int* cert = nullptr;  // == 3: K is not certified SPD — give up at once (exact path decides)
+    // parts written by a kernel that may still be running (the pipelined batch launches this
+    // cluster first so it owns its 16 SMs): wait until *ready == alpha_dev[0] + 1, the epoch the
+    // producer's last CTA publishes (gemv.cuh CtaParts), at most ready_timeout_ns — a timeout
+    // (a profiler serializing kernels) makes the solve give up, i.e. the step is rerun exactly
+    const double* ready = nullptr;
+    const double* alpha_dev = nullptr;
+    unsigned long long ready_timeout_ns = 2000000ull;
 };
 // Optional tail (st set; needs vtol > 0): after a verified solve the cluster finishes the
 // filter step's Woodbury back-substitution and commit instead of a separate kernel:
@@ -47,6 +54,10 @@ struct PcgTail {
     double* alpha_dev = nullptr;
     int* info = nullptr;
     const unsigned long long* hout = nullptr;  // [1]: mapped pinned host d (0 = none)
+    // parity snapshots written with the commit (filter.cu EpiCtzD): the step's α, gate = 0, new d
+    double* alpha_q = nullptr;
+    int* gate_q = nullptr;
+    double* d_q = nullptr;
     bool retry_only = false;  // no tail; only raise kInfoRetry (a dependent kernel finishes the step)
 };
 void cap_pcg(int n, const double* K, long long ld, double* u, double* work, int* fallback, cudaStream_t s,

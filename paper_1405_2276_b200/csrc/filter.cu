@@ -87,28 +87,38 @@ __global__ void k_transpose(long long n, int r, const double* __restrict__ in, d
     }
 }
 
-// Step prologue fused with the residual (fast_filter.hpp:97, :108): α ← α + 1, the PCG fallback
-// flag cleared, Woodbury scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j (when wsq ≠
-// null), a snapshot of the committed d for the side branch that forms the next step's
-// capacitance (dsnap ≠ null; the step's own epilogue overwrites d concurrently), and
-// z_i = y_i − H_i·mean with one warp per ray: every lane prefetches 16 (col, val) pairs, then
-// gathers the 16 mean values — two memory latencies per 512 nonzeros.
+// Step prologue (fast_filter.hpp:97, :108): α ← α + 1, the PCG fallback flag cleared, Woodbury
+// scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j (when wsq ≠ null), a snapshot of the
+// committed d for the side branch that forms the next step's capacitance (dsnap ≠ null; the
+// step's own epilogue overwrites d concurrently), and the residual z = y − H·mean.
 // The failure flag *info is sticky: a failed step leaves it set, so every later step of an
 // asynchronous batch is a no-op (its epilogues are gated on it) until the host clears it.
-__global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* __restrict__ rp,
-                                                      const int* __restrict__ ci, const double* __restrict__ hv,
-                                                      const double* __restrict__ mean, const double* y,
-                                                      double* __restrict__ z, double* alpha_dev,
-                                                      const double* __restrict__ theta, const double* __restrict__ d,
-                                                      double sigma2, double* __restrict__ wsq, double* __restrict__ sqd,
+// The observation: y, or (ysrc set) row ysrc[2] of the block at ysrc[0] with ld ysrc[1] — the
+// host batch (Filter::run_host) uploads all its observations once.
+//
+// The residual is taken from the carried image of the mean, hm = H·mean: z = y − hm, no pass
+// over H.  The step keeps hm current without H either: S z = y − H·mean
+// with S = H·Σ_pred·Hᵀ + σ²I, so H·mean_new = H·mean + H·Σ_pred·Hᵀz = y − σ²z exactly (the
+// rotate-out epilogue EpiZHm stores it; rounding as the reference's own H·mean, plus the
+// solve's residual).  The next step's chain therefore does not wait for
+// this step's N-space mean update.  Also: the observation copied to ycur (EpiZHm reads it
+// after the batch row has advanced), the parity's commit gate closed (gate = 1 until the
+// step's epilogue commits), and the host batch's observation row ysrc[2] advanced by the last
+// CTA to finish (every CTA has read the row by then).
+__global__ void __launch_bounds__(256) k_step_prologue(int m, int r, const double* y, const double* __restrict__ hm,
+                                                      double* __restrict__ z, double* __restrict__ ycur,
+                                                      double* alpha_dev, const double* __restrict__ theta,
+                                                      const double* __restrict__ d, double sigma2,
+                                                      double* __restrict__ wsq, double* __restrict__ sqd,
                                                       double* __restrict__ dsnap, int* __restrict__ pcgflag,
-                                                      const long long* __restrict__ ysrc) {
+                                                      long long* ysrc, int* __restrict__ gate, unsigned* ticket) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // rotate_in may stage P now
     const int gid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const double alpha = alpha_dev[0] + 1.0;
     if (gid == 0) {
         alpha_dev[1] = alpha;
         if (pcgflag) *pcgflag = 0;
+        *gate = 1;
     }
     if (dsnap)
         for (int j = gid; j < r; j += nthreads) dsnap[j] = d[j];
@@ -116,30 +126,42 @@ __global__ void __launch_bounds__(256) k_step_residual(int m, int r, const int* 
         for (int i = gid; i < m; i += nthreads) wsq[i] = 1.0 / (alpha * theta[i] + sigma2);
         for (int j = gid; j < r; j += nthreads) sqd[j] = sqrt(d[j]);
     }
-    const int row = gid >> 5, lane = threadIdx.x & 31;
-    if (row >= m) return;
-    // the observation: y, or (ysrc set) row ysrc[2] of the block at ysrc[0] with ld ysrc[1] —
-    // the host batch (Filter::run_host) uploads all its observations once and the step's last
-    // kernel advances ysrc[2]
     if (ysrc) y = reinterpret_cast<const double*>(ysrc[0]) + ysrc[2] * ysrc[1];
-    const int e0 = rp[row], e1 = rp[row + 1];
-    double s = 0.0;
-    for (int eb = e0; eb < e1; eb += 32 * 16) {
-        int c[16];
-        double w[16], xv[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int e = eb + lane + 32 * q;
-            c[q] = e < e1 ? ci[e] : 0;
-            w[q] = e < e1 ? hv[e] : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) xv[q] = __ldg(mean + c[q]);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) s = fma(w[q], xv[q], s);
+    for (int i = gid; i < m; i += nthreads) {
+        const double yi = y[i];
+        ycur[i] = yi;
+        z[i] = yi - hm[i];
     }
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) z[row] = y[row] - s;
+    if (ysrc) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+                *ticket = 0;
+                ysrc[2] += 1;
+            }
+        }
+    }
+}
+
+// rotate-out epilogue: z_i = (P·s̃)_i and, unless the step failed, the image of the new mean
+// hm_i = y_i − σ²z_i (see k_step_prologue)
+struct EpiZHm {
+    double* z;
+    double* hm;
+    const double* ycur;
+    double sigma2;
+    const int* info;
+    __device__ __forceinline__ void operator()(long long i, double v) const {
+        z[i] = v;
+        if (!*info) hm[i] = ycur[i] - sigma2 * v;
+    }
+};
+__global__ void k_image_update(int m, const double* __restrict__ z, double* __restrict__ hm,
+                               const double* __restrict__ ycur, double sigma2, const int* __restrict__ info) {
+    if (*info) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        hm[i] = ycur[i] - sigma2 * z[i];
 }
 
 // Woodbury scalars wsq_i = 1/(α θ_i + σ²) (Λ_M⁻¹) and sqd_j = √d_j for a step that has not
@@ -237,15 +259,27 @@ struct EpiCtzD {
     double* alpha_dev;
     const int* info;
     const unsigned long long* hout;  // [1]: mapped pinned host d (0 = none), see Filter::hostout
+    // the parity's snapshots for a deferred mean side (Filter::enqueue_mean_side): the step's α,
+    // the commit gate (0 = committed) and, for the fused UQ pass, the new d
+    double* alpha_q;
+    int* gate_q;
+    double* d_q;
+    __device__ __forceinline__ void commit(long long j, double alpha, double dn) const {
+        d[j] = dn;
+        if (d_q) d_q[j] = dn;
+        if (hout[1]) reinterpret_cast<double*>(hout[1])[j] = dn;
+        if (j == 0) {
+            alpha_dev[0] = alpha;
+            *alpha_q = alpha;
+            *gate_q = 0;
+        }
+    }
     __device__ __forceinline__ void operator()(long long j, double v) const {
         if (*info) return;
         const double alpha = alpha_dev[1];
         const double dj = d[j], l = lam[j], c = alpha - dj;
         dc[j] = dj * v;
-        const double dn = (dj + alpha * l * c) / (1.0 + l * c);
-        d[j] = dn;
-        if (hout[1]) reinterpret_cast<double*>(hout[1])[j] = dn;
-        if (j == 0) alpha_dev[0] = alpha;
+        commit(j, alpha, (dj + alpha * l * c) / (1.0 + l * c));
     }
     // dc_j = sqd_j·x_j given directly (Woodbury path), then the same d/α commit
     __device__ __forceinline__ void operator()(long long j, double xj, double sqdj) const {
@@ -253,10 +287,7 @@ struct EpiCtzD {
         const double alpha = alpha_dev[1];
         const double dj = d[j], l = lam[j], c = alpha - dj;
         dc[j] = sqdj * xj;
-        const double dn = (dj + alpha * l * c) / (1.0 + l * c);
-        d[j] = dn;
-        if (hout[1]) reinterpret_cast<double*>(hout[1])[j] = dn;
-        if (j == 0) alpha_dev[0] = alpha;
+        commit(j, alpha, (dj + alpha * l * c) / (1.0 + l * c));
     }
 };
 
@@ -297,8 +328,8 @@ __global__ void __launch_bounds__(256) k_woodbury_st(int m, int r, const double*
 // solve), then wait for the PCG grid (griddepcontrol.wait) and read only x.
 __global__ void __launch_bounds__(256) k_woodbury_st_pdl(int m, int r, const double* __restrict__ Erow,
                                                         const double* __restrict__ sqd, const double* __restrict__ x,
-                                                        const double* __restrict__ wsq, const double* __restrict__ rt,
-                                                        double* __restrict__ st, EpiCtzD upd) {
+                                                        const double* __restrict__ wsq, const double* rt,
+                                                        double* __restrict__ st, EpiCtzD upd, int rt_late) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // rotate_out may stage Pᵀ now
     if (blockIdx.x == gridDim.x - 1) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -316,8 +347,12 @@ __global__ void __launch_bounds__(256) k_woodbury_st_pdl(int m, int r, const dou
         e[q] = (on && j < r) ? er[j] : 0.0;
         sq[q] = j < r ? __ldg(sqd + j) : 0.0;
     }
-    const double wi = on ? wsq[i] : 0.0, ri = on ? rt[i] : 0.0;
+    // rt_late: r̃ comes from a rotate_in that runs beside the PCG (early-PCG graphs) — read it
+    // only once the PCG, which waited for it, has completed
+    const double wi = on ? wsq[i] : 0.0;
+    double ri = (on && !rt_late) ? rt[i] : 0.0;
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (on && rt_late) ri = *reinterpret_cast<const volatile double*>(rt + i);
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -330,7 +365,7 @@ __global__ void __launch_bounds__(256) k_woodbury_st_pdl(int m, int r, const dou
 
 // d'_i = (d_i + αλ_i(α − d_i)) / (1 + λ_i(α − d_i))  (fast_filter.hpp:118-123); commits α
 __global__ void k_d_update(int r, double* __restrict__ d, const double* __restrict__ lam, double* alpha_dev,
-                           const int* __restrict__ info) {
+                           const int* __restrict__ info, double* alpha_q, int* gate_q) {
     if (*info) return;
     const double alpha = alpha_dev[1];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
@@ -338,7 +373,11 @@ __global__ void k_d_update(int r, double* __restrict__ d, const double* __restri
         const double l = lam[i];
         d[i] = (d[i] + alpha * l * c) / (1.0 + l * c);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) alpha_dev[0] = alpha;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        alpha_dev[0] = alpha;
+        *alpha_q = alpha;
+        *gate_q = 0;
+    }
 }
 
 // diag Σ and conditional realizations from one pass over U (uq.hpp:16-23, App. A.4):
@@ -421,7 +460,7 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq1(long long n, int r, const d
     const int bad = *info;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
-        if (ycnt) *ycnt += 1;  // the host batch's next observation row (see k_step_residual)
+        if (ycnt) *ycnt += 1;  // the host batch's next observation row (see k_step_prologue)
     }
     if (bad) return;
     const double alpha = alpha_dev[1];
@@ -502,7 +541,7 @@ __global__ void __launch_bounds__(128, 3) k_mean_uq(long long n, int r, const do
     const int bad = *info;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (hout[2]) *reinterpret_cast<volatile int*>(hout[2]) = bad;
-        if (ycnt) *ycnt += 1;  // the host batch's next observation row (see k_step_residual)
+        if (ycnt) *ycnt += 1;  // the host batch's next observation row (see k_step_prologue)
     }
     if (bad) return;
     const double alpha = alpha_dev[1];
@@ -1079,6 +1118,19 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     FKB_CUDA(cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming));
     FKB_CUDA(cudaEventCreateWithFlags(&ev_ctz, cudaEventDisableTiming));
     FKB_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+    FKB_CUDA(cudaStreamCreateWithFlags(&s4, cudaStreamNonBlocking));  // a deferred mean side (launch_step_piped)
+    {
+        int lo = 0, hi = 0;
+        FKB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FKB_CUDA(cudaStreamCreateWithPriority(&s5, cudaStreamNonBlocking, hi));  // the chain's head (early-PCG graphs)
+        int dev = 0;
+        FKB_CUDA(cudaGetDevice(&dev));
+        FKB_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+    }
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_rfork, cudaEventDisableTiming));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_rjoin, cudaEventDisableTiming));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_mfork, cudaEventDisableTiming));
+    FKB_CUDA(cudaEventCreateWithFlags(&ev_mjoin, cudaEventDisableTiming));
     if (m < 0) throw std::invalid_argument("fkf_init: negative measurement count");
     if ((long long)h_cols != n) throw std::invalid_argument("fkf_init: H columns do not match state dimension");
     for (int i = 0; i < m; ++i)
@@ -1165,7 +1217,24 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
         g.splitk = gemm_pick_splitk(r, r, m);
         ws_step.alloc(std::max<size_t>(std::max(gemm_ws_elems(g), gram_ws_elems(r, r, m)), 1));  // graph-captured
     }
-    z.alloc(size_t(std::max(m, 1)));
+    for (int q = 0; q < 2; ++q) {
+        zb[q].alloc(size_t(std::max(m, 1)));
+        cvb[q].alloc(size_t(std::max(r, 1)));
+        dq[q].alloc(size_t(std::max(r, 1)));
+    }
+    hm.alloc(size_t(std::max(m, 1)));
+    ycur.alloc(size_t(std::max(m, 1)));
+    alphaq.alloc(2);
+    gateq.alloc(2);
+    ticket.alloc(2);
+    FKB_CUDA(cudaMemset(ticket.p, 0, 2 * sizeof(unsigned)));
+    ready.alloc(1);
+    FKB_CUDA(cudaMemset(ready.p, 0, sizeof(double)));
+    // opt-in: on B200 the whole-GPU kernels of the two overlapped steps crowd each other out of
+    // the SMs (c2: 96 µs per step against 80 µs for the full graphs back to back)
+    piped_ok = false;
+    if (const char* e = std::getenv("FKB_PIPED")) piped_ok = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FKB_EARLY_PCG")) early_pcg = std::atoi(e) != 0;
     t.alloc(size_t(n));
     vsub.alloc(size_t(n));
     if (const char* e = std::getenv("FKB_UPASS_CTAS")) upass_per_sm = std::atoi(e);
@@ -1184,7 +1253,6 @@ Filter::Filter(Cov* c, int m_, int h_cols, const int* rowptr, const int* col, co
     if (const char* e = std::getenv("FKB_PDL")) pdl_mask = std::atoi(e);
     if (const char* e = std::getenv("FKB_UPASS_GRID")) upass_per_sm = -std::atoi(e);  // total CTAs
     if (const char* e = std::getenv("FKB_UPASS_SIDE")) upass_side_mode = std::atoi(e);
-    cvec.alloc(size_t(std::max(r, 1)));
     ybuf.alloc(size_t(std::max(m, 1)));
     ysrc.alloc(3);
     set_ysrc(ybuf.p, 0);
@@ -1202,6 +1270,8 @@ Filter::~Filter() {
     if (s) cudaStreamSynchronize(s);
     if (s2) cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
+    if (s4) cudaStreamSynchronize(s4);
+    if (s5) cudaStreamSynchronize(s5);
     if (cs) cudaStreamSynchronize(cs);
     drop_graphs();
     for (int q = 0; q < 2; ++q) {
@@ -1216,6 +1286,12 @@ Filter::~Filter() {
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join2) cudaEventDestroy(ev_join2);
     if (ev_ctz) cudaEventDestroy(ev_ctz);
+    if (ev_rfork) cudaEventDestroy(ev_rfork);
+    if (ev_rjoin) cudaEventDestroy(ev_rjoin);
+    if (s5) cudaStreamDestroy(s5);
+    if (ev_mfork) cudaEventDestroy(ev_mfork);
+    if (ev_mjoin) cudaEventDestroy(ev_mjoin);
+    if (s4) cudaStreamDestroy(s4);
     if (s3) cudaStreamDestroy(s3);
     if (s2) cudaStreamDestroy(s2);
 }
@@ -1225,7 +1301,10 @@ void Filter::reset() {  // LowRankState::zero_start (fast_filter.hpp:30-36)
     FKB_CUDA(cudaMemsetAsync(alpha_dev.p, 0, 2 * sizeof(double), s));
     FKB_CUDA(cudaMemsetAsync(d.p, 0, d.bytes(), s));
     FKB_CUDA(cudaMemsetAsync(mean.p, 0, mean.bytes(), s));
+    FKB_CUDA(cudaMemsetAsync(hm.p, 0, hm.bytes(), s));  // H·0
+    FKB_CUDA(cudaMemsetAsync(ready.p, 0, sizeof(double), s));
     FKB_CUDA(cudaStreamSynchronize(s));
+    hm_valid = true;
     alpha = 0.0;
     step_no = 0;
     state_rank = 0;
@@ -1262,6 +1341,10 @@ void Filter::mark_on(cudaStream_t st, const char* name) {
 
 void Filter::drop_graphs() {
     for (int q = 0; q < 2; ++q) {
+        for (int v = 0; v < 3; ++v) {
+            if (graphv[v][q]) cudaGraphExecDestroy(graphv[v][q]);
+            graphv[v][q] = nullptr;
+        }
         if (graph[q]) cudaGraphExecDestroy(graph[q]);
         graph[q] = nullptr;
         graph_ready[q] = false;
@@ -1384,72 +1467,152 @@ void Filter::enqueue_capacitance(cudaStream_t b, int mode, double* wsq_o, double
     }
 }
 
+// hm = H·mean after the mean was set from outside (set_state); the steps keep it current
+void Filter::prime_image() {
+    if (hm_valid) return;
+    if (m > 0) spmm(H, mean.p, n, 1, hm.p, m, 1.0, 0.0, s);
+    hm_valid = true;
+}
+
 void Filter::prime_capacitance() {  // K, wsq, sqd of the next step (parity par_next), eagerly
+    prime_image();
     if (k_valid || solver != 1 || r <= 0) return;
     enqueue_capacitance(s, 0, wsqb[par_next].p, sqdb[par_next].p, Kb[par_next].p);
     k_valid = true;
 }
 
+// The commit epilogue of the step being enqueued (parity buffers selected by select_parity)
+EpiCtzD Filter::commit_epi() {
+    return EpiCtzD{cv_c, d.p, lambda.p, alpha_dev.p, info.p, hout_c, aq_c, gate_c, uq_count >= 0 ? dq_c : nullptr};
+}
+
+// One step = the m-space chain (enqueue_chain: everything the NEXT step depends on — α, d, the
+// image hm of the mean) followed by the N-space mean side (enqueue_mean_side: Γ(Hᵀz), the U
+// pass, the mean update and the fused UQ).  The chain does not read the mean (k_step_prologue),
+// so a batch can run step t's mean side beside step t+1's chain (launch_step_piped).
 void Filter::enqueue_step(const double* d_y) {
-    // α ← α + 1, flags, z = y − H·mean (:97, :108): one kernel
+    enqueue_chain(d_y, false);
+    MeanSide ms;
+    ms.z = z_c; ms.cv = cv_c; ms.alpha1 = alpha_dev.p; ms.gate = info.p; ms.d = d.p; ms.hout = hout_c;
+    ms.sqd = sqd_c;
+    enqueue_mean_side(ms, s, false);
+}
+
+void Filter::enqueue_chain(const double* d_y, bool deferred, const std::function<void()>& after_prologue) {
+    (void)d_y;  // the observation is read through ysrc (per-call: ybuf)
+    // Pipelined batch graphs launch the PCG cluster FIRST (a root of the graph, on the main
+    // stream): it needs 16 empty SMs of one GPC, which it would wait for behind the previous
+    // step's mean side; resident from the start it stages K and spins until rotate_in's last
+    // CTA publishes the partials (PcgRhs::ready).  The prologue and rotate_in then run on the
+    // head stream s5 beside it.
+    hs = s;
+    if (deferred && solver == 1 && r > 0 && fused_chain && side() != s && early_pcg) {
+        hs = s5;
+        FKB_CUDA(cudaEventRecord(ev_rfork, s));
+        FKB_CUDA(cudaStreamWaitEvent(s5, ev_rfork, 0));
+    }
+    // α ← α + 1, flags, z = y − hm (:97, :108): one kernel
     {
-        const int blocks = std::max(1, ceil_div((long long)std::max(m, 1) * 32, 256));
-        k_step_residual<<<blocks, 256, 0, s>>>(m, r, H.rowptr.p, H.col.p, H.val.p, mean.p, d_y, z.p, alpha_dev.p,
-                                               theta.p, d.p, sigma2, (solver == 1 && r == 0) ? wsq_c : nullptr,
-                                               sqd_c, (solver == 1 && r > 0) ? dsnap.p : nullptr,
-                                               (solver == 1 && !exact) ? pcgflag.p : nullptr, ysrc.p);
+        const int blocks = std::max(1, std::min(ceil_div(std::max(m, 1), 256), 148));
+        k_step_prologue<<<blocks, 256, 0, hs>>>(m, r, ybuf.p, hm.p, z_c, ycur.p, alpha_dev.p, theta.p, d.p, sigma2,
+                                                (solver == 1 && r == 0) ? wsq_c : nullptr, sqd_c,
+                                                (solver == 1 && r > 0) ? dsnap.p : nullptr,
+                                                (solver == 1 && !exact) ? pcgflag.p : nullptr, ysrc.p, gate_c,
+                                                ticket.p);
         FKB_LAUNCH_CHECK();
         count_launch();
     }
-    mark("residual");
-    if (solver == 0) enqueue_solve_dense();
-    else enqueue_solve_woodbury();
+    if (after_prologue) after_prologue();
+    mark_on(hs, "residual");
+    chain_deferred = deferred;
+    if (solver == 0) {
+        enqueue_solve_dense();
+        k_image_update<<<std::max(1, ceil_div(m, 256)), 256, 0, s>>>(m, z_c, hm.p, ycur.p, sigma2, info.p);
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    } else {
+        enqueue_solve_woodbury();
+    }
     // dc = d ⊙ Bᵀz with d and α updated in the same pass (solver 0: a side-branch pass over B;
-    // solver 1: D^½x inside k_woodbury_st) and the U pass v = U·dc on the side branch (solver 1
-    // forks it right after the capacitance solve); main branch: t = Γ(Hᵀz), whose last FFT
-    // pass applies mean ← (mean + α·t) − v (:114-123) once the side branch has joined.
+    // solver 1: D^½x inside k_woodbury_st)
+    if (r > 0 && solver == 0) {
+        if (!deferred) fork();
+        launch_coldot(m, r, B.p, m, XPlain{z_c}, commit_epi(), deferred ? s : side());
+        mark_on(deferred ? s : side(), "ctz_d_update");
+        if (!deferred) {
+            if (upass_side()) {
+                launch_u_pass(XPlain{cv_c}, side(), true);
+                mark_on(side(), "u_pass");
+            }
+            if (side() != s) FKB_CUDA(cudaEventRecord(ev_join, s2));
+        }
+    } else if (r == 0) {
+        k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p, aq_c, gate_c);  // commits α
+        FKB_LAUNCH_CHECK();
+        count_launch();
+    }
+    chain_deferred = false;
+    hs = s;
+}
+
+// The N-space side of a step whose chain has committed: t = Γ(Hᵀz); v = U·dc; the last FFT
+// pass applies mean ← (mean + α·t) − v (:114-116), or the fused pass k_mean_uq does it with
+// diag Σ and the realizations.  ms names the step's buffers: the step just enqueued on this
+// stream (deferred = false: the U pass may already run on the side branch, forked inside the
+// chain), or the previous step's parity snapshots (deferred = true: everything is launched
+// here, on sm and the U-pass branch s2).
+void Filter::enqueue_mean_side(const MeanSide& ms, cudaStream_t sm, bool deferred) {
     const bool par = side() != s;
     const bool fused_uq = uq_count >= 0 && r > 0;
-    if (r > 0 && solver == 0) {
-        fork();
-        launch_coldot(m, r, B.p, m, XPlain{z.p}, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hout_c}, side());
-        mark_on(side(), "ctz_d_update");
-        if (upass_side()) {
-            launch_u_pass(XPlain{cvec.p}, side(), true);
-            mark_on(side(), "u_pass");
-        }
-        if (par) FKB_CUDA(cudaEventRecord(ev_join, s2));
-    } else if (r == 0) {
-        k_d_update<<<1, 32, 0, s>>>(0, d.p, lambda.p, alpha_dev.p, info.p);  // commits α (reads α_dev[1] only)
-        FKB_LAUNCH_CHECK();
-        count_launch();
+    cudaStream_t cov_stream = cov->stream;
+    cov->stream = sm;
+    struct Restore {
+        Cov* c;
+        cudaStream_t st;
+        ~Restore() { c->stream = st; }
+    } restore{cov, cov_stream};
+    const bool u_beside = r > 0 && upass_side() && par;
+    // beside a chain whose PCG cluster owns 16 SMs the persistent U pass takes the others
+    upass_leave = deferred && sm != s ? 16 : 0;
+    struct Leave {
+        int& v;
+        ~Leave() { v = 0; }
+    } leave{upass_leave};
+    if (deferred && u_beside) {  // the U pass beside Γ(Hᵀz)
+        FKB_CUDA(cudaEventRecord(ev_fork, sm));
+        FKB_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
+        mark_on(s2, "fork");
+        launch_u_pass(XPlain{ms.cv}, s2, true);
+        mark_on(s2, "u_pass");
+        FKB_CUDA(cudaEventRecord(ev_join, s2));
     }
-    spmv_short(HT, z.p, t.p, 1.0, s);
-    mark("ht_z");
-    if (ufork == 3 && solver == 1) fork_upass();
+    spmv_short(HT, ms.z, t.p, 1.0, sm);
+    mark_on(sm, "ht_z");
+    if (!deferred && ufork == 3 && solver == 1) fork_upass();
     if (fused_uq) {  // U pass + diag Σ + realizations of the new state in one pass (needs t)
         cov->apply1(t.p, t.p);
-        mark("gamma_apply");
-        if (par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // dc ready
-        launch_mean_uq(uq_count, n, r, U.p, cvec.p, d.p, alpha_dev.p, cov->spec.theta, t.p, mean.p,
-                       uq_count ? draws.p : nullptr, uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, info.p,
-                       hout_c, ysrc.p + 2, s);
-        if (solver == 1 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
-        mark("mean_update");
+        mark_on(sm, "gamma_apply");
+        if (!deferred && par && solver == 0) FKB_CUDA(cudaStreamWaitEvent(sm, ev_join, 0));  // dc ready
+        launch_mean_uq(uq_count, n, r, U.p, ms.cv, ms.d, ms.alpha1, cov->spec.theta, t.p, mean.p,
+                       uq_count ? draws.p : nullptr, uq_count ? draw_proj.p : nullptr, uq_x.p, uq_var.p, ms.gate,
+                       ms.hout, nullptr, sm);
+        if (!deferred && solver == 1 && par) FKB_CUDA(cudaStreamWaitEvent(sm, ev_join2, 0));  // next K ready
+        mark_on(sm, "mean_update");
         return;
     }
     cov->apply1_fwd(t.p);
-    mark("gamma_fwd");
-    if (r > 0 && par && (upass_side() || solver == 0))
-        FKB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // v = U·dc (or solver 0's dc) ready
-    if (r > 0 && !upass_side()) {  // the long U pass (rank > 320 or fused UQ) on the whole GPU
-        if (solver == 0) launch_u_pass(XPlain{cvec.p}, s, false);
-        else launch_u_pass(XProd{sqd_c, ucap.p}, s, false);
-        mark("u_pass");
+    mark_on(sm, "gamma_fwd");
+    const bool u_joined = r > 0 && par && (deferred ? u_beside : (upass_side() || solver == 0));
+    if (u_joined) FKB_CUDA(cudaStreamWaitEvent(sm, ev_join, 0));  // v = U·dc (or solver 0's dc) ready
+    if (r > 0 && !(upass_side() && (par || !deferred)) ) {
+        // the long U pass (rank > 320) on the whole GPU, or the serial phase-timing order
+        if (deferred || solver == 0) launch_u_pass(XPlain{ms.cv}, sm, false);
+        else launch_u_pass(XProd{ms.sqd, ucap.p}, sm, false);
+        mark_on(sm, "u_pass");
     }
-    cov->apply1_inv(mean.p, MeanUpd{alpha_dev.p + 1, info.p, r > 0 ? vsub.p : nullptr, hout_c, ysrc.p + 2});
-    if (solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
-    mark("mean_update");
+    cov->apply1_inv(mean.p, MeanUpd{ms.alpha1 + 1, ms.gate, r > 0 ? vsub.p : nullptr, ms.hout, nullptr});
+    if (!deferred && solver == 1 && r > 0 && par) FKB_CUDA(cudaStreamWaitEvent(sm, ev_join2, 0));  // next K ready
+    mark_on(sm, "mean_update");
 }
 
 // v = U·dc (the mean update's low-rank term) streaming the row-major U: beside the main chain
@@ -1457,8 +1620,10 @@ void Filter::enqueue_step(const double* d_y) {
 // main stream with the whole GPU
 template <class XL>
 void Filter::launch_u_pass(XL xl, cudaStream_t st, bool beside) {
-    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), xl, EpiStore{vsub.p}, st, beside ? upass_per_sm : 0,
-                         upass_threads);
+    int cap = beside ? upass_per_sm : 0;
+    if (upass_leave > 0 && cap >= 0 && sm_count > upass_leave)
+        cap = -(sm_count - upass_leave) * (beside ? std::max(upass_per_sm, 1) : 2);
+    launch_gemv_rowmajor(n, r, Urow.p, std::max(r, 1), xl, EpiStore{vsub.p}, st, cap, upass_threads);
 }
 
 // z ← S⁻¹z with S = P[Λ_M − E·D·Eᵀ]Pᵀ (Woodbury with the k×k capacitance K).
@@ -1472,10 +1637,10 @@ void Filter::enqueue_solve_woodbury() {
     // side branch: the NEXT step's Woodbury scalars and K into the other parity's buffers (they
     // depend on α and d only); forked at kfork: 0 before the capacitance solve (beside the
     // 16-SM PCG cluster), 1 at the start of the step, 2 after the capacitance solve
-    auto fork_next_k = [&] {
+    auto fork_next_k = [&](cudaStream_t at) {
         if (r <= 0) return;
         if (side() != s) {
-            FKB_CUDA(cudaEventRecord(ev_ctz, s));
+            FKB_CUDA(cudaEventRecord(ev_ctz, at));
             FKB_CUDA(cudaStreamWaitEvent(s3, ev_ctz, 0));
             mark_on(s3, "fork_k");
         }
@@ -1483,46 +1648,61 @@ void Filter::enqueue_solve_woodbury() {
         mark_on(side() != s ? s3 : s, "capacitance");
         if (side() != s) FKB_CUDA(cudaEventRecord(ev_join2, s3));
     };
-    auto fork_u = [&] { fork_upass(); };
-    if (kfork == 1) fork_next_k();
+    auto fork_u = [&] {
+        if (!chain_deferred) fork_upass();  // a deferred mean side launches its own U pass
+    };
+    if (kfork == 1) fork_next_k(hs);
     const bool fused = fused_chain && !exact && r > 0;
     if (fused) {
         // r̃ = Pᵀ(y − H·mean) and the partials of Eᵀ(Λ_M⁻¹r̃) in one pass
-        launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s, CtaParts{Erow.p, r, wsq_c, parts.p},
-                      (pdl_mask & 1) != 0);
-        mark("rotate_in");
-        if (kfork == 0) fork_next_k();
-        PcgRhs rhs;
-        rhs.parts = parts.p; rhs.nparts = coldot_grid(m); rhs.sqd = sqd_c; rhs.cert = cert_c;
-        PcgTail tl;
-        const bool pdl = fused_chain == 2 && r <= 512;
-        tl.info = info.p;
-        tl.retry_only = pdl;
-        if (!pdl) {
-            tl.Erow = Erow.p; tl.m = m; tl.wsq = wsq_c; tl.rt = rt.p; tl.sqd = sqd_c; tl.st = st.p; tl.dc = cvec.p;
-            tl.d = d.p; tl.lam = lambda.p; tl.alpha_dev = alpha_dev.p; tl.hout = hout_c;
-        }
-        cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs, tl);
-        if (pdl) {  // s̃ and the d/α commit by a programmatic dependent (gated on the flag the PCG raises)
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(std::max(1, ceil_div(m, 8)) + 1, 1, 1);
-            cfg.blockDim = dim3(256, 1, 1);
-            cfg.stream = s;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            FKB_CUDA(cudaLaunchKernelEx(&cfg, k_woodbury_st_pdl, m, r, (const double*)Erow.p, (const double*)sqd_c,
-                                        (const double*)ucap.p, (const double*)wsq_c, (const double*)rt.p, st.p,
-                                        EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hout_c}));
-            count_launch();
+        auto rotate_in = [&] {
+            launch_coldot(m, m, P.p, m, XPlain{z_c}, EpiAxpby{rt.p, 1.0, 0.0}, hs,
+                          CtaParts{Erow.p, r, wsq_c, parts.p, ready.p, ticket.p + 1, alpha_dev.p}, (pdl_mask & 1) != 0);
+            mark_on(hs, "rotate_in");
+            if (kfork == 0) fork_next_k(hs);
+        };
+        auto solve = [&] {
+            PcgRhs rhs;
+            rhs.parts = parts.p; rhs.nparts = coldot_grid(m); rhs.sqd = sqd_c; rhs.cert = cert_c;
+            rhs.ready = ready.p; rhs.alpha_dev = alpha_dev.p;
+            PcgTail tl;
+            const bool pdl = fused_chain == 2 && r <= 512;
+            tl.info = info.p;
+            tl.retry_only = pdl;
+            if (!pdl) {
+                tl.Erow = Erow.p; tl.m = m; tl.wsq = wsq_c; tl.rt = rt.p; tl.sqd = sqd_c; tl.st = st.p; tl.dc = cv_c;
+                tl.d = d.p; tl.lam = lambda.p; tl.alpha_dev = alpha_dev.p; tl.hout = hout_c;
+                tl.alpha_q = aq_c; tl.gate_q = gate_c; tl.d_q = uq_count >= 0 ? dq_c : nullptr;
+            }
+            cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs, tl);
+            if (pdl) {  // s̃ and the d/α commit by a programmatic dependent (gated on the flag the PCG raises)
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(std::max(1, ceil_div(m, 8)) + 1, 1, 1);
+                cfg.blockDim = dim3(256, 1, 1);
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                FKB_CUDA(cudaLaunchKernelEx(&cfg, k_woodbury_st_pdl, m, r, (const double*)Erow.p, (const double*)sqd_c,
+                                            (const double*)ucap.p, (const double*)wsq_c, (const double*)rt.p, st.p,
+                                            commit_epi(), hs != s ? 1 : 0));
+                count_launch();
+            }
+        };
+        if (hs != s) {  // early PCG: the cluster is captured (and dispatched) ahead of rotate_in
+            solve();
+            rotate_in();
+        } else {
+            rotate_in();
+            solve();
         }
         mark("cap_solve");
-        if (kfork == 2) fork_next_k();
+        if (kfork == 2) fork_next_k(s);
         if (ufork <= 1) fork_u();
     } else {
-        launch_coldot(m, m, P.p, m, XPlain{z.p}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
+        launch_coldot(m, m, P.p, m, XPlain{z_c}, EpiAxpby{rt.p, 1.0, 0.0}, s);  // r̃ = Pᵀ(y − H·mean)
         mark("rotate_in");
         if (r > 0) {
             // u = D^½·Eᵀ·Λ_M⁻¹·r̃: formed by the PCG kernel itself (fuse_rhs) or as column dots
@@ -1534,7 +1714,7 @@ void Filter::enqueue_solve_woodbury() {
                 launch_coldot(m, r, E.p, m, XProd{wsq_c, rt.p}, EpiScaleOut{ucap.p, sqd_c}, s);
                 mark("cap_rhs");
             }
-            if (kfork == 0) fork_next_k();
+            if (kfork == 0) fork_next_k(s);
             // x = K⁻¹u: Jacobi-PCG in one cluster; exact Cholesky only if PCG hits its cap.
             // ‖Kx − u‖ ≤ 1e-12‖u‖: the solve's error reaches the mean through U·D^½x at ~1e-12
             // relative, three orders below the 1e-9 parity bar.  A converged x is re-checked
@@ -1544,20 +1724,24 @@ void Filter::enqueue_solve_woodbury() {
             if (!exact) cap_pcg(r, K_c, r, ucap.p, pcgwork.p, pcgflag.p, s, pcg_maxit, 1e-12, pcg_ts.p, 1e-11, rhs);
             chol_solve_small(r, K_c, r, ucap.p, rdg.p, info.p, s, nullptr, exact ? nullptr : pcgflag.p);
             mark("cap_solve");
-            if (kfork == 2) fork_next_k();
+            if (kfork == 2) fork_next_k(s);
             if (ufork == 0) fork_u();
         }
         // s̃ = Λ_M⁻¹(r̃ + E·D^½·x): one warp per row of the row-major copy of E
         k_woodbury_st<<<std::max(1, ceil_div(m, 8)) + 1, 256, 0, s>>>(
-            m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, EpiCtzD{cvec.p, d.p, lambda.p, alpha_dev.p, info.p, hout_c});
+            m, r, Erow.p, sqd_c, ucap.p, wsq_c, rt.p, st.p, commit_epi());
         FKB_LAUNCH_CHECK();
         count_launch();
         mark("woodbury_st");
         if (ufork == 1) fork_u();
     }
-    launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiAxpby{z.p, 1.0, 0.0}, s, NoCta{},  // z = P·s̃ (rows of P)
+    launch_coldot(m, m, Pt.p, m, XPlain{st.p}, EpiZHm{z_c, hm.p, ycur.p, sigma2, info.p}, s, NoCta{},  // z = P·s̃ (rows of P); hm = y − σ²z
                   fused && fused_chain == 2 && r <= 512 && (pdl_mask & 2));
     mark("rotate_out");
+    if (hs != s) {  // the head stream (prologue, rotate_in) rejoins
+        FKB_CUDA(cudaEventRecord(ev_rjoin, hs));
+        FKB_CUDA(cudaStreamWaitEvent(s, ev_rjoin, 0));
+    }
     if (ufork == 2) fork_u();
 }
 
@@ -1588,7 +1772,7 @@ void Filter::enqueue_solve_dense() {
     mark("innovation_build");
     potrf_lower(m, S.p, m, info.p, potrf_ws.p, potrf_ws.n, s);  // LLT (:104-106)
     mark("llt");
-    potrs_lower(m, S.p, m, z.p, flags.p, s);         // z = S⁻¹(y − H·mean) (:108)
+    potrs_lower(m, S.p, m, z_c, flags.p, s);         // z = S⁻¹(y − H·mean) (:108)
     mark("llt_solve");
 }
 
@@ -1611,6 +1795,7 @@ void Filter::check_info() {
 // side branch recomputes the next step's K as usual.
 void Filter::rerun_exact(int q) {
     FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+    FKB_CUDA(cudaMemsetAsync(ready.p, 0, sizeof(double), s));  // the failed step's epoch must not satisfy a later wait
     // this step's K, Λ_M⁻¹ and D^½ afresh from the committed α and d: inside an asynchronous
     // batch the no-op steps behind the sticky flag have overwritten the parity buffers
     if (solver == 1 && r > 0) enqueue_capacitance(s, 0, wsqb[q].p, sqdb[q].p, Kb[q].p);
@@ -1630,6 +1815,7 @@ void Filter::rerun_exact(int q) {
 // raise the reference's error (fast_filter.hpp:104-106).
 void Filter::fail_step(const std::string& msg) {
     FKB_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+    FKB_CUDA(cudaMemsetAsync(ready.p, 0, sizeof(double), s));
     FKB_CUDA(cudaStreamSynchronize(s));
     k_valid = false;
     throw std::runtime_error(msg);
@@ -1672,6 +1858,73 @@ void Filter::launch_step() {
     count_launch(launches_per_step);
     gt_last_par = q;
     par_next ^= 1;
+}
+
+Filter::MeanSide Filter::snapshot_side(int q) {
+    MeanSide ms;
+    ms.z = zb[q].p; ms.cv = cvb[q].p; ms.alpha1 = alphaq.p + q - 1; ms.gate = gateq.p + q; ms.d = dq[q].p;
+    ms.hout = hostout.p + 5 * q;
+    return ms;
+}
+
+// Pipelined batch graphs (see graphv): variant v for the step of parity q.
+void Filter::launch_piped(int v, int q) {
+    if (v != 2) prime_capacitance();
+    if (!graphv[v][q]) {
+        const unsigned long long before = g_launches;
+        select_parity(q);
+        cudaGraph_t gr;
+        FKB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
+        try {
+            const bool par = side() != s;
+            if (v == 0) {
+                enqueue_chain(ybuf.p, true);
+                if (par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));  // next K ready
+            } else if (v == 1) {
+                // the previous step's mean side forks after this step's prologue: by then the
+                // PCG cluster (a root of the graph) owns its SMs
+                enqueue_chain(ybuf.p, true, [&] {
+                    FKB_CUDA(cudaEventRecord(ev_mfork, hs));
+                    FKB_CUDA(cudaStreamWaitEvent(s4, ev_mfork, 0));
+                    enqueue_mean_side(snapshot_side(q ^ 1), s4, true);
+                    FKB_CUDA(cudaEventRecord(ev_mjoin, s4));
+                });
+                if (par) FKB_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));
+                FKB_CUDA(cudaStreamWaitEvent(s, ev_mjoin, 0));
+            } else {
+                enqueue_mean_side(snapshot_side(q), s, true);
+            }
+        } catch (...) {
+            capturing = false;
+            cudaStreamEndCapture(s, &gr);
+            throw;
+        }
+        capturing = false;
+        FKB_CUDA(cudaStreamEndCapture(s, &gr));
+        FKB_CUDA(cudaGraphInstantiate(&graphv[v][q], gr, cudaGraphInstantiateFlagUseNodePriority));
+        cudaGraphDestroy(gr);
+        launches_v[v] = int(g_launches - before);
+        g_launches = before;
+    }
+    FKB_CUDA(cudaGraphLaunch(graphv[v][q], s));
+    count_launch(launches_v[v]);
+    if (v != 2) {
+        gt_last_par = q;
+        par_next = q ^ 1;
+    }
+}
+
+// Step t of an nsteps batch: its chain beside step t−1's mean side; after the last chain the
+// pending mean side alone.  Outside a pipelined configuration the full step graph.
+void Filter::run_piped(int t, int nsteps) {
+    if (!piped()) {
+        launch_step();
+        return;
+    }
+    const int q = par_next;
+    launch_piped(t == 0 ? 0 : 1, q);
+    (void)nsteps;
 }
 
 void Filter::step(const double* d_y) {
@@ -1777,11 +2030,14 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
                                    sizeof(double) * size_t(m), size_t(nsteps), cudaMemcpyHostToDevice, s));
     const double alpha0 = alpha;
     const int par0 = par_next;
-    auto copy_out = [&](int q, int t, cudaStream_t st) {  // step t's snapshot (parity q) → host rows
+    // step t's snapshot (parity q) → host rows; what: 1 = d (the chain's), 2 = mean, diag Σ and
+    // realizations (the mean side's)
+    auto copy_out = [&](int q, int t, cudaStream_t st, int what) {
+        if ((what & 1) && h_d && r > 0)
+            FKB_CUDA(cudaMemcpyAsync(h_d + t * ldd, snap_d[q].p, sizeof(double) * size_t(r), cudaMemcpyDeviceToHost, st));
+        if (!(what & 2)) return;
         if (h_mean) FKB_CUDA(cudaMemcpyAsync(h_mean + t * ldm, snap_mean[q].p, sizeof(double) * size_t(n),
                                              cudaMemcpyDeviceToHost, st));
-        if (h_d && r > 0) FKB_CUDA(cudaMemcpyAsync(h_d + t * ldd, snap_d[q].p, sizeof(double) * size_t(r),
-                                                   cudaMemcpyDeviceToHost, st));
         if (uq && h_var) FKB_CUDA(cudaMemcpyAsync(h_var + (long long)t * n, snap_v[q].p, sizeof(double) * size_t(n),
                                                   cudaMemcpyDeviceToHost, st));
         if (uq && cnt && h_x)
@@ -1799,18 +2055,36 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
         FKB_CUDA(cudaEventRecord(e, st));
         tev.push_back(e);
     };
+    // Pipelined: graph t runs step t's chain beside step t−1's mean side, so after graph t the
+    // copy stream takes d of step t and the N-space outputs of step t−1; the flush graph after
+    // the loop finishes the last step's.  A snapshot written by graph t+2 waits for the copies
+    // issued after graph t.
+    const bool pp = piped() && nsteps > 1;
     for (int t = 0; t < nsteps; ++t) {
         const int q = par_next;
         if (t >= 2) FKB_CUDA(cudaStreamWaitEvent(s, ev_copied[q], 0));  // step t−2's copies are done
         tmark(s);
         tmark(s);
-        launch_step();
+        if (pp) run_piped(t, nsteps);
+        else launch_step();
         tmark(s);
         FKB_CUDA(cudaEventRecord(ev_done[q], s));
         FKB_CUDA(cudaStreamWaitEvent(cs, ev_done[q], 0));
-        copy_out(q, t, cs);
+        if (pp) {
+            copy_out(q, t, cs, 1);
+            if (t > 0) copy_out(q ^ 1, t - 1, cs, 2);
+        } else {
+            copy_out(q, t, cs, 3);
+        }
         tmark(cs);
         FKB_CUDA(cudaEventRecord(ev_copied[q], cs));
+    }
+    if (pp) {
+        const int q = par_next ^ 1;
+        launch_piped(2, q);
+        FKB_CUDA(cudaEventRecord(ev_done[q], s));
+        FKB_CUDA(cudaStreamWaitEvent(cs, ev_done[q], 0));
+        copy_out(q, nsteps - 1, cs, 2);
     }
     FKB_CUDA(cudaStreamSynchronize(cs));
     set_ysrc(ybuf.p, 0);  // back to the per-call observation buffer (also for the reruns below)
@@ -1858,7 +2132,7 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
                 FKB_CUDA(cudaStreamSynchronize(s));
             }
             if (h) break;  // singular: raised below, the state stays at step t−1
-            copy_out(q, t, s);
+            copy_out(q, t, s, 3);
             FKB_CUDA(cudaStreamSynchronize(s));
             ++done;
         }
@@ -1960,11 +2234,14 @@ void Filter::steps_async(const double* d_ys, int nsteps, long long ldy) {
     batch_ys = d_ys;
     batch_ldy = ldy;
     batch_par0 = par_next;
+    const bool pp = piped() && nsteps > 1;
     for (int k = 0; k < nsteps; ++k) {
         FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_ys + (long long)k * ldy, sizeof(double) * size_t(m),
                                  cudaMemcpyDeviceToDevice, s));
-        launch_step();
+        if (pp) run_piped(k, nsteps);
+        else launch_step();
     }
+    if (pp) launch_piped(2, par_next ^ 1);  // the last step's mean side
 }
 
 // The deferred check of an asynchronous batch: the device α counts the committed steps (a

@@ -3,6 +3,7 @@
 #include <cstdlib>
 
 #include <deque>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -51,7 +52,9 @@ void lowrank_uq(Cov* cov, long long n, int r, const double* alpha_dev, const dou
                 const double* Wbar, const double* mean, uint64_t seed, uint64_t first, int count, double* X,
                 double* var, double* colsq, DBuf<double>& scratch);
 
+struct EpiCtzD;
 struct Filter {
+    EpiCtzD commit_epi();
     Cov* cov = nullptr;
     cudaStream_t s = nullptr;
     long long n = 0;
@@ -93,7 +96,21 @@ struct Filter {
     DBuf<int> cgate;             // [gate, info] of that factorization
     const int* cert_c = nullptr;  // this step's
     bool cert_force_fail = false; // FKB_CAP_CERT=fail: every step takes the exact path (tests)
+    // Per-parity snapshots of what a step's N-space mean side needs once its m-space chain
+    // has committed — z = S⁻¹(y − H·mean), dc = d ⊙ Bᵀz, the step's α, the new d (fused UQ)
+    // and the commit gate — so step t's mean side can run beside step t+1's chain.
+    DBuf<double> zb[2], cvb[2], dq[2], alphaq;
+    DBuf<int> gateq;
+    double *z_c = nullptr, *cv_c = nullptr, *dq_c = nullptr, *aq_c = nullptr;
+    int* gate_c = nullptr;
+    // the image hm = H·mean carried by the steps (k_step_prologue / EpiZHm), the step's
+    // observation, the prologue's last-CTA ticket
+    DBuf<double> hm, ycur;
+    DBuf<unsigned> ticket;
+    bool hm_valid = false;
+    void prime_image();
     void select_parity(int p) {
+        z_c = zb[p].p; cv_c = cvb[p].p; dq_c = dq[p].p; aq_c = alphaq.p + p; gate_c = gateq.p + p;
         hout_c = hostout.p + 5 * p;
         cert_c = certb[p].p;
         wsq_c = wsqb[p].p; sqd_c = sqdb[p].p; K_c = Kb[p].p;
@@ -104,7 +121,7 @@ struct Filter {
     int pcg_maxit = 200;  // iteration cap before the exact Cholesky takes over (tests force 0)  // 1 when the capacitance PCG fell back to the cluster Cholesky
 
     // step workspaces (vsub = U·dc from the side-branch U pass)
-    DBuf<double> S, z, t, cvec, vsub, ws, ws_step, potrf_ws;
+    DBuf<double> S, t, vsub, ws, ws_step, potrf_ws;
     int upass_per_sm = 1;     // resident U-pass CTAs per SM beside the main chain (FKB_UPASS_CTAS);
                               // negative: a total CTA count (FKB_UPASS_GRID)
     int upass_threads = 256;  // threads per U-pass CTA (FKB_UPASS_THREADS: 128 or 256)
@@ -133,6 +150,36 @@ struct Filter {
     bool upass_side() const { return upass_side_mode >= 0 ? upass_side_mode == 1 : (uq_count < 0 && r <= 320); }
     DBuf<int> info, flags;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one per step parity
+    // Pipelined batch variants per parity q of the step whose chain runs: [0] head — chain(q)
+    // only; [1] steady — chain(q) beside the mean side of step q^1; [2] flush — the mean side
+    // of step q alone (after the batch's last chain).
+    cudaGraphExec_t graphv[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+    int launches_v[3] = {0, 0, 0};
+    bool piped_ok = false;       // FKB_PIPED=1: batches overlap step t's mean side with step t+1's chain
+    bool chain_deferred = false; // enqueue_chain: the mean side (and its U pass) is launched elsewhere
+    cudaStream_t s4 = nullptr;   // the deferred mean side's stream
+    cudaEvent_t ev_mfork = nullptr, ev_mjoin = nullptr;
+    struct MeanSide {
+        const double* z = nullptr;       // S⁻¹(y − H·mean)
+        const double* cv = nullptr;      // d ⊙ Bᵀz
+        const double* alpha1 = nullptr;  // alpha1[1] = the step's α
+        const int* gate = nullptr;       // ≠ 0: the step did not commit
+        const double* d = nullptr;       // the new d (fused UQ)
+        const double* sqd = nullptr;
+        const unsigned long long* hout = nullptr;
+    };
+    void enqueue_chain(const double* d_y, bool deferred, const std::function<void()>& after_prologue = {});
+    cudaStream_t hs = nullptr;   // the stream of the chain's head (prologue, rotate_in): s, or s5 in early-PCG graphs
+    cudaStream_t s5 = nullptr;
+    cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
+    bool early_pcg = true;       // FKB_EARLY_PCG=0: pipelined graphs keep the PCG behind rotate_in
+    DBuf<double> ready;          // epoch of the last complete set of rotate_in partials (PcgRhs::ready)
+    int sm_count = 0, upass_leave = 0;
+    void enqueue_mean_side(const MeanSide& ms, cudaStream_t sm, bool deferred);
+    MeanSide snapshot_side(int q);
+    bool piped() const { return piped_ok && solver == 1 && r > 0 && !phase_events && !gtime; }
+    void launch_piped(int variant, int q);  // replay (capturing on first use) the variant for parity q
+    void run_piped(int t, int nsteps); // step t of an nsteps batch: head / steady, flush after the last
     bool graph_ready[2] = {false, false};
     void drop_graphs();
     // side stream for the independent branches of a step (captured into the same graph):
@@ -169,7 +216,7 @@ struct Filter {
     DBuf<double> sig_minus;
 
     DBuf<double> ybuf;
-    // the step's observation source (k_step_residual): {base, ld, row}; per-call mode {ybuf, 0, ·},
+    // the step's observation source (k_step_prologue): {base, ld, row}; per-call mode {ybuf, 0, ·},
     // host batch {uploaded block, m, row advanced by the step's last kernel}
     DBuf<long long> ysrc;
     DBuf<double> ys_dev;

@@ -175,8 +175,9 @@ inline void launch_gemv_rowmajor(long long m, int k, const double* A, long long 
     FKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemv_rowmajor<XL, Epi>, 256, shm));
     if (per_sm_cap > 0 && per_sm_cap < 1000) per_sm = std::min(per_sm, per_sm_cap);
     const long long warps = (m + 3) / 4;  // at least one 4-row group per warp
-    const long long ctas = per_sm_cap >= 1000 ? (warps + 7) / 8  // non-persistent
-                                              : std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
+    long long ctas = per_sm_cap >= 1000 ? (warps + 7) / 8  // non-persistent
+                                        : std::min((warps + 7) / 8, (long long)std::max(sms, 1) * std::max(per_sm, 1));
+    if (per_sm_cap < 0) ctas = std::min(ctas, (long long)-per_sm_cap);  // negative: a total CTA count
     k_gemv_rowmajor<XL, Epi><<<(unsigned)ctas, 256, shm, s>>>(m, k, A, ld, xl, epi);
     FKB_LAUNCH_CHECK();
     count_launch();
@@ -196,7 +197,26 @@ struct CtaParts {
     int r;
     const double* wsq;
     double* parts;  // gridDim.x × r
+    // Completion signal for a consumer that is already resident (the pipelined batch launches
+    // the PCG cluster first, cappcg.cuh PcgRhs::ready): the last CTA to leave its partials
+    // publishes the step's α (alpha_dev[1], set by the step prologue) as the epoch.
+    double* ready = nullptr;
+    unsigned* ticket = nullptr;
+    const double* alpha_dev = nullptr;
     __device__ __forceinline__ void operator()(int j0, int nc, const double* vals) const {
+        partials(j0, nc, vals);
+        if (!ready) return;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+                *ticket = 0;
+                __threadfence();
+                *reinterpret_cast<volatile double*>(ready) = alpha_dev[1];
+            }
+        }
+    }
+    __device__ __forceinline__ void partials(int j0, int nc, const double* vals) const {
         double w[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) w[c] = c < nc ? __ldg(wsq + j0 + c) * vals[c] : 0.0;

@@ -14,7 +14,7 @@ for c in c2 c3 c4; do
   python scripts/launch_summary.py $o/launches_${c}_$tag.csv > $o/launches_${c}_$tag.txt 2>&1
 done
 F="--set full --clock-control none --import-source on --profile-from-start off"
-timeout 600 ncu $F -k regex:"k_cap_pcg|k_coldot|k_gemv_rowmajor|k_step_residual|k_spmv" -o $r/step_c2_$tag -f $P step c2 > $o/ncu_step_c2.log 2>&1
+timeout 600 ncu $F -k regex:"k_cap_pcg|k_coldot|k_gemv_rowmajor|k_step_prologue|k_spmv" -o $r/step_c2_$tag -f $P step c2 > $o/ncu_step_c2.log 2>&1
 timeout 600 ncu $F -k regex:"k_mean_uq|k_cap_pcg|k_coldot" -o $r/step_c3_$tag -f $P step c3 > $o/ncu_step_c3.log 2>&1
 timeout 600 ncu $F -k regex:"k_gemv_rowmajor|k_cap_pcg" -o $r/step_c4_$tag -f $P step c4 > $o/ncu_step_c4.log 2>&1
 timeout 300 $P wprod c2 > $o/prof_wprod.log 2>&1 && \

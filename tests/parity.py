@@ -89,6 +89,47 @@ def run_config(name, steps=None, solver=1, uq=None, realizations=None, record=No
     return out
 
 
+def run_config_batch(name, steps=None, fused_uq=None):
+    """The same comparison with the GPU side run as ONE call over all steps (fkb_fkf_run /
+    fkb_fkf_run_uq — the pipelined batch: step t's mean side beside step t+1's chain).  With
+    fused_uq the per-step diag Σ and realizations come from the fused pass of the batch."""
+    import paper_1405_2276_b200 as P
+    from oracle import oracle as O
+
+    steps = STEPS[name] if steps is None else steps
+    nreal = REALIZATIONS.get(name, 0)
+    fused_uq = (name == "c3") if fused_uq is None else fused_uq
+    w, h, ys, s2 = workload_inputs(name, steps)
+    kern = dict(family=1, theta=w.theta, length=w.length, nu=w.nu)
+    k, p = w.ghep_sizes()
+    cov = P.CovarianceOperator(P.Grid(w.n, w.n), P.KernelSpec(**kern))
+    ctx = P.fkf_init(cov, h, s2, k, p, w.ghep_seed)
+    ocov = O.CovarianceOperator(w.n, w.n, **kern)
+    oh = O.Csr.from_arrays(h.rows, h.cols, h.rowptr, h.col, h.val)
+    of = O.FastFilter(ocov, oh, s2, k, p, w.ghep_seed)
+    g = ctx.run(np.asarray(ys), count=nreal, seed=w.sample_seed) if fused_uq else ctx.run(np.asarray(ys))
+    out = dict(config=name, solver=1, steps=steps, rank=int(ctx.rank()), oracle_rank=int(of.rank), alpha_exact=True,
+               mean=[], d=[], var=[], real=[], api="fkb_fkf_run_uq" if fused_uq else "fkb_fkf_run")
+    for t, y in enumerate(ys):
+        of.step(y)
+        so = of.state()
+        if g["alpha"][t] != so["alpha"]:
+            out["alpha_exact"] = False
+        out["mean"].append(rel_err(g["mean"][t], so["mean"]))
+        out["d"].append(float(np.max(np.abs(g["d"][t] - so["d"])) / so["alpha"]) if len(so["d"]) else 0.0)
+        if fused_uq:
+            out["var"].append(rel_err(g["var"][t], of.variance()))
+            if nreal:
+                xo = of.realizations(w.sample_seed, nreal)
+                out["real"].append(max(rel_err(g["x"][t, j] - so["mean"], xo[:, j] - so["mean"]) for j in range(nreal)))
+    # the state the batch leaves behind is the last step's
+    st = ctx.state()
+    out["final_state"] = rel_err(st["mean"], of.state()["mean"])
+    out["worst"] = {key: (max(out[key]) if out[key] else 0.0) for key in ("mean", "d", "var", "real")}
+    out["worst"]["final_state"] = out["final_state"]
+    return out
+
+
 def assert_parity(res, tol=TOL):
     assert res["rank"] == res["oracle_rank"], res
     assert res["alpha_exact"], res
