@@ -130,6 +130,8 @@ int fkb_fkf_sync(fkb_filter* f, int nsteps);
 int fkb_filter_state(fkb_filter* f, double* alpha, int* step, int* rank, double* d, double* mean);
 int fkb_filter_set_state(fkb_filter* f, double alpha, int step, int rank, const double* d, const double* mean);
 int fkb_filter_reset(fkb_filter* f);
+/* read-only view of the device mean: the steps carry H*mean = y - sigma2*z beside it (fast_filter.hpp:108
+ * without the SpMV), so a new mean must go through fkb_filter_set_state */
 int fkb_filter_mean_device(fkb_filter* f, const double** d_mean);
 
 /* ---- UQ (uq.hpp:16-112) ---------------------------------------------------------- */

@@ -285,6 +285,31 @@ __global__ void __launch_bounds__(QT) k_gram(GemmArgs g, int kchunk, double* __r
 
 // C = epilogue(Aᵀ·diag(dA)·B) for k-contiguous A (K×M) and B (K×N); same GemmArgs semantics
 // as gemm() with transA = 1, transB = 0.  Requires K, lda, ldb even (16-byte chunks).
+// Split-K factor of the Gram: all tiles·s CTAs are resident at once (3 per SM: 74 KB of shared
+// memory each), so the launch takes as long as the busiest SM — ceil(tiles·s / SMs) CTAs of
+// K/s each.  Pick the s that minimizes that (ties: the smaller s, less reduction traffic):
+// l = 320 gives 25 tiles, where ceil(296/25) = 12 put three CTAs on four SMs and two on the
+// rest (SMs busy 66 % of the launch, profiles/round2_ncu_wprod_c2_v3.txt); s = 17 keeps every
+// SM within 4 % of the even split.
+static int gram_pick_splitk(long long tiles, int K) {
+    static const int sms = [] {
+        int dev = 0, n = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return std::max(n, 1);
+    }();
+    const long long smax = std::min<long long>(3LL * sms / std::max<long long>(tiles, 1), K / 128);
+    int best = 1;
+    double best_cost = 1e300;
+    for (long long sk = 1; sk <= std::max<long long>(smax, 1); ++sk) {
+        const double cost = double((tiles * sk + sms - 1) / sms) / double(sk);
+        if (cost < best_cost * (1.0 - 1e-9)) {
+            best_cost = cost;
+            best = int(sk);
+        }
+    }
+    return best;
+}
+
 void gram(const GemmArgs& g_in, double* ws, cudaStream_t s) {
     GemmArgs g = g_in;
     if (g.M <= 0 || g.N <= 0) return;
@@ -295,7 +320,7 @@ void gram(const GemmArgs& g_in, double* ws, cudaStream_t s) {
     if (!g.Cin) { g.Cin = g.C; g.ldcin = g.ldc; }
     const long long tiles = (long long)ceil_div(g.M, QB) * ceil_div(g.N, QB);
     int splitk = 1;
-    if (ws && tiles < 296) splitk = int(std::max<long long>(1, std::min<long long>((296 + tiles - 1) / tiles, g.K / 128)));
+    if (ws && tiles < 296) splitk = gram_pick_splitk(tiles, g.K);
     int kchunk = ((ceil_div(g.K, splitk) + QK - 1) / QK) * QK;
     splitk = ceil_div(g.K, kchunk);
     g.splitk = splitk;
@@ -457,7 +482,7 @@ void gram_sym(const GemmArgs& g_in, cudaStream_t s) {
 size_t gram_ws_elems(int M, int N, int K) {
     const long long tiles = (long long)ceil_div(M, QB) * ceil_div(N, QB);
     if (tiles <= 0 || tiles >= 296) return 0;
-    const long long s = std::max<long long>(1, std::min<long long>((296 + tiles - 1) / tiles, K / 128));
+    const long long s = gram_pick_splitk(tiles, K);
     return size_t(s + 1) * M * N;
 }
 

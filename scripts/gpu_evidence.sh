@@ -16,6 +16,6 @@ tail -3 gpurun_out/pytest_$tag.log; tail -2 gpurun_out/smoke_$tag.log
 for c in c2 c3 c4; do python -c "
 import json
 d=json.loads(open('gpurun_out/bench_${c}_$tag.json').read().strip().splitlines()[-1])
-print('$c', round(d['value']), 'e2e', round(d['e2e']['value']), 'per_call', round(d['e2e']['per_call']['value']), 'us', round(d['ms_per_step']*1e3,1), d['roofline']['kernel'], round(d['roofline']['frac'],3), d['clocks'])
+print('$c', round(d['value']), 'e2e', round(d['e2e']['value']), 'per_call', round(d['e2e']['per_call']['value']), 'us', round(d['ms_per_step']*1e3,1), 'lat_us', round(d['step_latency']['ms_per_step']*1e3,1), d['roofline']['kernel'], round(d['roofline']['frac'],3), d['clocks'])
 "; done
 cut -c1-400 gpurun_out/bench_ref_$tag.json
