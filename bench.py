@@ -145,7 +145,7 @@ def phase_work(w, r, fft_flops, nnz, uq_count=-1, fft_split=None):
     if uq_count >= 0:  # k_mean_uq: U, t and mean in; mean, diag Σ and the realizations out
         mean_upd = ("hbm", 8.0 * N * r + 32.0 * N + 16.0 * N * cnt + 8.0 * r * cnt + 16.0 * r)
     return {
-        "residual": ("hbm", 12.0 * nnz + 4.0 * (m + 1) + 8.0 * N + 16.0 * m),
+        "residual": ("hbm", 40.0 * m),  # y and the carried image H·mean in; z and the kept y out (no pass over H)
         "capacitance": ("tensor", 1.0 * m * r * (r + 1)),  # symmetric Eᵀ·diag·E (lower half)
         "rotate_in": ("hbm", 8.0 * m * m + 16.0 * m),
         "cap_rhs": ("hbm", 8.0 * m * r + 24.0 * m + 16.0 * r),
@@ -605,6 +605,12 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": head_launches,
         "roofline": roof,
         "roofline_side": roof_side,
+        "step_hbm": (lambda b: {"algorithmic_bytes": b, "achieved_gbs": b / (head_ms * 1e-3) / 1e9,
+                                "frac": b / (head_ms * 1e-3) / 1e9 / hbm, "peak_gbs": hbm,
+                                "note": "all HBM-bound phases of one step (their algorithmic bytes) over the "
+                                        "headline ms_per_step: how far the whole step is from streaming its "
+                                        "compulsory traffic at the measured HBM peak"})(
+            float(sum(work[kk][1] for kk in tsrc if kk in work and work[kk][0] == "hbm"))),
         "kernel_ms_in_graph": kernel_ms,
         "phases_ms_serial": phases,
         "gamma_x": {"tflops": gx_tf, "frac": gx_tf / fp64_peak, "columns": ncols, "ms": gx_ms,

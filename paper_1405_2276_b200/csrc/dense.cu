@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(QT) k_gram(GemmArgs g, int kchunk, double* __r
 // as gemm() with transA = 1, transB = 0.  Requires K, lda, ldb even (16-byte chunks).
 // Split-K factor of the Gram: all tiles·s CTAs are resident at once (3 per SM: 74 KB of shared
 // memory each), so the launch takes as long as the busiest SM — ceil(tiles·s / SMs) CTAs of
-// K/s each.  Pick the s that minimizes that (ties: the smaller s, less reduction traffic):
+// K/s each.  Pick the s that minimizes that (ties: the larger s — l = 420 ties at 1, 2 and 3
+// CTAs per SM, and one CTA per SM leaves the DMMA pipe waiting on shared-memory loads):
 // l = 320 gives 25 tiles, where ceil(296/25) = 12 put three CTAs on four SMs and two on the
 // rest (SMs busy 66 % of the launch, profiles/round2_ncu_wprod_c2_v3.txt); s = 17 keeps every
 // SM within 4 % of the even split.
@@ -302,7 +303,7 @@ static int gram_pick_splitk(long long tiles, int K) {
     double best_cost = 1e300;
     for (long long sk = 1; sk <= std::max<long long>(smax, 1); ++sk) {
         const double cost = double((tiles * sk + sms - 1) / sms) / double(sk);
-        if (cost < best_cost * (1.0 - 1e-9)) {
+        if (cost <= best_cost * (1.0 + 1e-9)) {  // ties: more CTAs per SM hide the DMMA latency better
             best_cost = cost;
             best = int(sk);
         }

@@ -44,7 +44,16 @@ int main(int argc, char** argv) {
     edited.alpha += 0.5;
     const LowRankState s2 = fkf_step(edited, ctx, y);
     const LowRankState s3 = fkf_step(state, ctx, y);
-    if (s3.mean.v != s1.mean.v || s3.d.v != s1.d.v || s3.alpha != s1.alpha) return 7;
+    // s1 continued the device chain (which carries H·mean = y − σ²z), s3 re-uploaded the state
+    // (H·mean recomputed): the same function of (state, y) up to rounding, d and α exactly
+    {
+        double num = 0.0, den = 0.0;
+        for (size_t i = 0; i < s1.mean.v.size(); ++i) {
+            num += (s3.mean.v[i] - s1.mean.v[i]) * (s3.mean.v[i] - s1.mean.v[i]);
+            den += s1.mean.v[i] * s1.mean.v[i];
+        }
+        if (!(num <= 1e-24 * den) || s3.d.v != s1.d.v || s3.alpha != s1.alpha) return 7;
+    }
     if (s2.mean.v == s1.mean.v || s2.alpha != state.alpha + 1.5) return 8;
     const FkfContext& cctx = ctx;  // const context, reference signatures
     if (std::abs(trace_criterion(s3, cov) - trace_criterion(s3, cctx)) > 1e-12 * std::abs(trace_criterion(s3, cctx)))
