@@ -46,14 +46,15 @@ int main(int argc, char** argv) {
     const LowRankState s3 = fkf_step(state, ctx, y);
     // s1 continued the device chain (which carries H·mean = y − σ²z), s3 re-uploaded the state
     // (H·mean recomputed): the same function of (state, y) up to rounding, d and α exactly
-    {
+    auto close = [](const Vector& a, const Vector& b) {
         double num = 0.0, den = 0.0;
-        for (size_t i = 0; i < s1.mean.v.size(); ++i) {
-            num += (s3.mean.v[i] - s1.mean.v[i]) * (s3.mean.v[i] - s1.mean.v[i]);
-            den += s1.mean.v[i] * s1.mean.v[i];
+        for (size_t i = 0; i < a.v.size(); ++i) {
+            num += (a.v[i] - b.v[i]) * (a.v[i] - b.v[i]);
+            den += b.v[i] * b.v[i];
         }
-        if (!(num <= 1e-24 * den) || s3.d.v != s1.d.v || s3.alpha != s1.alpha) return 7;
-    }
+        return a.v.size() == b.v.size() && num <= 1e-24 * den;
+    };
+    if (!close(s3.mean, s1.mean) || s3.d.v != s1.d.v || s3.alpha != s1.alpha) return 7;
     if (s2.mean.v == s1.mean.v || s2.alpha != state.alpha + 1.5) return 8;
     const FkfContext& cctx = ctx;  // const context, reference signatures
     if (std::abs(trace_criterion(s3, cov) - trace_criterion(s3, cctx)) > 1e-12 * std::abs(trace_criterion(s3, cctx)))
@@ -69,12 +70,12 @@ int main(int argc, char** argv) {
     for (Index i = 0; i < h.rows(); ++i) y2[i] = 0.5 * y[i];
     const LowRankState r1 = fkf_step(s3, ctx, y), r2 = fkf_step(r1, ctx, y2);
     const std::vector<LowRankState> run = fkf_run(s3, ctx, ys);
-    if (run.size() != 2 || run[1].mean.v != r2.mean.v || run[1].d.v != r2.d.v || run[1].alpha != r2.alpha ||
-        run[0].mean.v != r1.mean.v || run[1].step != r2.step)
+    if (run.size() != 2 || !close(run[1].mean, r2.mean) || run[1].d.v != r2.d.v || run[1].alpha != r2.alpha ||
+        !close(run[0].mean, r1.mean) || run[1].step != r2.step)
         return 10;
     const LowRankState r3 = fkf_step(run[1], ctx, y);  // continues from the mirrored state
     const LowRankState r4 = fkf_step(r2, ctx, y);
-    if (r3.mean.v != r4.mean.v) return 11;
+    if (!close(r3.mean, r4.mean)) return 11;
     std::printf("run ok\n");
     return 0;
 }
