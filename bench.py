@@ -176,6 +176,20 @@ def gamma_split(w, mx, my):
     return rows + cols, rows, 16.0 * nky * nx
 
 
+def workload_config(name, w, rank, nnz, uq, uq_count):
+    """The `config` object of the JSON line — the same for both arms (the driver compares them):
+    the workload and how the timed steps follow each other.  Arm-specific settings (solver,
+    torus, parallelism) are top-level keys of the line."""
+    flushed = "flushed between timed steps (256 MiB write + 256 MiB read sweep on the filter stream)"
+    mb = (8.0 * w.N * rank + 16.0 * w.m * w.m) / 1e6
+    b2b = (f"none between the timed steps: K steps back to back, each streaming ≈ 8·N·k + 16·m² = {mb:.0f} MB of "
+           + ("operands, more than the 126 MB L2" if mb > 126.0 else "operands (they fit the 126 MB L2)")
+           + "; flushed once before the timed region")
+    return {"workload": name, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": int(rank), "nnz_H": int(nnz),
+            "uq_per_step": (f"diag Σ + {uq_count} realizations" if uq else "none"),
+            "l2": flushed if uq else b2b}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -213,8 +227,9 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": k,
-                   "parallelism": "host cores"},
+        "config": workload_config(args.config, w, f.rank, len(val), bool(w.variance_each_step or w.realizations_per_step),
+                                  int(w.realizations_per_step or 0)),
+        "parallelism": "host cores",
         "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample,
                          "cpu_model": cpu_model(),
                          "note": "the oracle's line-by-line C++ restatement of the reference CPU path with OpenMP "
@@ -621,11 +636,9 @@ def run_ours(args, rank, world, local_rank):
         "metric": BASELINE_METRIC, "value": head_value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "grid": f"{w.n}x{w.n}", "N": w.N, "m": w.m, "rank": r,
-                   "torus": f"{cov.mx}x{cov.my}", "nnz_H": int(h.nnz), "solver": "woodbury-eig",
-                   "uq_per_step": (f"diag Σ + {uq_count} realizations" if uq else "none"),
-                   "l2": head_l2,
-                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
+        "config": workload_config(args.config, w, r, h.nnz, uq, uq_count),
+        "torus": f"{cov.mx}x{cov.my}", "solver": "woodbury-eig",
+        "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
         "clocks": clk.summary(),
         "e2e": e2e,
         "step_latency": latency,
