@@ -300,7 +300,18 @@ __global__ void __launch_bounds__(256, CPC == 4 ? 4 : 1) k_coldot(int m, int n, 
     }
 }
 
-inline int coldot_cpc(int n) { return n >= 8 * 296 ? 8 : n >= 4 * 296 ? 4 : n >= 2 * 296 ? 2 : 1; }
+inline int coldot_cpc(int n) {
+    static const int forced = [] {  // FKB_COLDOT_CPC: columns per CTA for every size (measurement)
+        const char* e = std::getenv("FKB_COLDOT_CPC");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+    }();
+    if (forced) return forced;
+    // 8 columns per CTA (≈ 180 registers, one CTA per SM, 3.5 waves at n = 4096) measured slower
+    // than 4 (≤ 64 registers, 4 CTAs per SM) at every size: c4 rotate_in 45 → 33 µs, rotate_out
+    // 33 → 27 µs (5.0 TB/s), step 351 → 332 µs
+    return n >= 4 * 296 ? 4 : n >= 2 * 296 ? 2 : 1;
+}
 inline int coldot_grid(int n) { return n <= 0 ? 0 : (n + coldot_cpc(n) - 1) / coldot_cpc(n); }
 
 template <class XL, class Epi, class CE = NoCta>
