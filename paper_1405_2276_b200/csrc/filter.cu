@@ -1915,17 +1915,9 @@ void Filter::launch_piped(int v, int q) {
     }
 }
 
-// Step t of an nsteps batch: its chain beside step t−1's mean side; after the last chain the
-// pending mean side alone.  Outside a pipelined configuration the full step graph.
-void Filter::run_piped(int t, int nsteps) {
-    if (!piped()) {
-        launch_step();
-        return;
-    }
-    const int q = par_next;
-    launch_piped(t == 0 ? 0 : 1, q);
-    (void)nsteps;
-}
+// Step t of a pipelined batch: the head graph (chain only), then the steady graph (the chain
+// beside step t−1's mean side); the caller flushes the last mean side with launch_piped(2, ·).
+void Filter::run_piped(int t) { launch_piped(t == 0 ? 0 : 1, par_next); }
 
 void Filter::step(const double* d_y) {
     set_hostout(0, 0, 0);
@@ -2065,7 +2057,7 @@ void Filter::run_host(const double* h_ys, int nsteps, long long ldy, double* h_a
         if (t >= 2) FKB_CUDA(cudaStreamWaitEvent(s, ev_copied[q], 0));  // step t−2's copies are done
         tmark(s);
         tmark(s);
-        if (pp) run_piped(t, nsteps);
+        if (pp) run_piped(t);
         else launch_step();
         tmark(s);
         FKB_CUDA(cudaEventRecord(ev_done[q], s));
@@ -2243,7 +2235,7 @@ void Filter::steps_async(const double* d_ys, int nsteps, long long ldy) {
         if (!block)
             FKB_CUDA(cudaMemcpyAsync(ybuf.p, d_ys + (long long)k * ldy, sizeof(double) * size_t(m),
                                      cudaMemcpyDeviceToDevice, s));
-        if (pp) run_piped(k, nsteps);
+        if (pp) run_piped(k);
         else launch_step();
     }
     if (pp) launch_piped(2, par_next ^ 1);  // the last step's mean side

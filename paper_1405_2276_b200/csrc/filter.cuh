@@ -179,7 +179,7 @@ struct Filter {
     MeanSide snapshot_side(int q);
     bool piped() const { return piped_ok && solver == 1 && r > 0 && !phase_events && !gtime; }
     void launch_piped(int variant, int q);  // replay (capturing on first use) the variant for parity q
-    void run_piped(int t, int nsteps); // step t of an nsteps batch: head / steady, flush after the last
+    void run_piped(int t);       // step t of a pipelined batch: head (t = 0) or steady graph
     bool graph_ready[2] = {false, false};
     void drop_graphs();
     // side stream for the independent branches of a step (captured into the same graph):
